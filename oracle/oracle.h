@@ -1,0 +1,126 @@
+/*
+ * oracle.h — CPU ORACLE for the LGA docking hot path.  TEST INFRASTRUCTURE ONLY.
+ *
+ * Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / --impl
+ * reference leg may load this library.  The product path (libdock.so and the
+ * paper_2203_02096_b200 package) never includes, links or calls it, and shares
+ * no code, header, table or helper with it.
+ *
+ * Plain, slow, double-precision C written from the method statement:
+ *   PAPER.md:64-66 (§II-A) — grid "reaction field", ligand particle model with
+ *     self-interactions (H-bond, vdW, desolvation), GA with crossover and
+ *     fitness selection, Lamarckian local search on a random sample each
+ *     generation, Solis-Wets optimiser, independent runs of 150 individuals,
+ *     degrees of freedom = translation + orientation + rotatable bonds;
+ *   PAPER.md:92-101 (§IV-A, Listing 1) — sum_evals reduction over individuals;
+ *   PAPER.md:135-136 (§IV-B) — torsion rotations applied in a fixed order;
+ *   and, where the paper is silent, the readings D1-D11 of SURVEY.md §8(c),
+ *   restated in DESIGN.md §3 (each function cites the reading it follows).
+ *
+ * Parity status of every function is listed in DESIGN.md §3.  The multi-
+ * generation trajectory of or_dock_run is "parity unpinned" (chaotic after the
+ * first near-tie, SURVEY.md §8(c) "Unpinned" (i)); its building blocks are each
+ * pinned by tests/test_oracle_*.py.
+ */
+#ifndef DOCK_ORACLE_H
+#define DOCK_ORACLE_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define OR_MAX_ATOMS 256
+#define OR_MAX_TORS 32
+#define OR_MAX_GENES (6 + OR_MAX_TORS)
+
+/* A docking problem: receptor grid + per-type parameters + preprocessed ligand. */
+typedef struct {
+    int nx, ny, nz;            /* grid nodes per axis */
+    double spacing;            /* Å */
+    double origin[3];          /* position of node (0,0,0) */
+    int n_types;               /* maps: n_types type maps, then E, then D */
+    const float *maps;         /* [(n_types+2)][nz][ny][nx], node (i,j,k) at i + nx*(j + ny*k) */
+    const double *tR, *teps, *tS, *tV;   /* per-type R, eps, S, V [n_types] (D5) */
+    const int *trole;          /* per-type H-bond role 0 none, 1 donor, 2 acceptor */
+    int N;                     /* atoms */
+    const int *type;           /* [N] index into the grid's type list */
+    const double *q;           /* [N] charges */
+    const double *X;           /* [N*3] reference coordinates */
+    int T;                     /* torsions (D1 order) */
+    const int *tor_a, *tor_b;  /* [T] axis atoms, a on the root side */
+    const unsigned char *moved;/* [T*N] 1 if atom moves with torsion k */
+    int P;                     /* intramolecular pairs */
+    const int *pairs;          /* [P*2] */
+} or_problem;
+
+typedef struct {
+    double p_tour, p_cross, p_mut, mut_trans, mut_angle;   /* D8 */
+    int ls_method;             /* 0 ADADELTA, 1 Solis-Wets */
+    double ls_rate;
+    int ls_max_iters;
+    double sw_rho, sw_rho_min, sw_expand, sw_contract;     /* D9 */
+    int sw_cons_succ, sw_cons_fail;
+    double ad_rho, ad_eps;     /* D10 */
+    int max_generations;
+} or_params;
+
+/* ---- D2: Philox4x32-10 and the stream layout ---- */
+void     or_philox4x32_10(const uint32_t ctr[4], const uint32_t key[2], uint32_t out[4]);
+uint32_t or_word(uint64_t seed, uint32_t ligand_id, uint32_t purpose, uint32_t slot,
+                 uint32_t gen, uint32_t run, uint32_t m);
+double   or_u01(uint32_t w);
+uint32_t or_below(uint32_t w, uint32_t n);
+
+/* ---- D1: topology (brute force).  Returns 0 ok, 1 input error. ---- */
+int or_topology(int N, int n_bonds, const int *bonds, const unsigned char *rotatable,
+                int *T_out, int *tor_a, int *tor_b, unsigned char *moved /*[32*N]*/,
+                int *depth /*[32]*/, int *P_out, int *pairs /*[cap*2]*/, int cap,
+                int *frag /*[N] nullable*/);
+
+/* ---- D3: genotype -> pose ---- */
+void or_pose(const or_problem *P, const double *genes, double *xyz);
+
+/* ---- D4: intermolecular (per atom and total) ---- */
+double or_inter_atom(const or_problem *P, int a, const double r[3], double grad[3]);
+double or_inter(const or_problem *P, const double *xyz, double *grad /*[N*3] nullable*/);
+/* ---- D5: intramolecular ---- */
+double or_pair_energy(const or_problem *P, int i, int j, double rho2_in, double *dE_drho2);
+double or_intra(const or_problem *P, const double *xyz, double *grad /*[N*3] nullable*/);
+/* ---- D6 + D7: total energy and genotype gradient ---- */
+double or_energy(const or_problem *P, const double *genes, double *ggrad /*[G] nullable*/,
+                 double *xyz /*[N*3] nullable*/, double *terms /*[2] inter,intra nullable*/);
+/* smallest distance, in grid units, of any atom coordinate to a cell/box face, and
+   smallest |rho2 - 1e-4| over pairs (both used to flag boundary poses). */
+void or_margins(const or_problem *P, const double *xyz, double *face_margin, double *clamp_margin);
+
+/* ---- D8: GA pieces ---- */
+int  or_elite(int pop, const double *E);
+void or_ga_slot(const or_params *pp, uint64_t seed, uint32_t ligand_id, uint32_t run,
+                uint32_t gen, uint32_t slot, int pop, int G, const double *old_genes,
+                const double *old_E, double *child, int *dbg /*[8] nullable*/);
+int  or_n_ls(double ls_rate, int pop);
+void or_ls_pick(uint64_t seed, uint32_t ligand_id, uint32_t run, uint32_t gen, int pop,
+                int n_ls, int *perm /*[pop]*/);
+
+/* ---- D9 / D10: local search.  objective: P != NULL -> docking energy of P,
+   else the bowl sum_j bowl[j] * x_j^2 (test objective for SPEC S:304 pins). ---- */
+void or_solis_wets(const or_problem *P, const double *bowl, int G, const or_params *pp,
+                   uint64_t seed, uint32_t ligand_id, uint32_t run, uint32_t gen, uint32_t slot,
+                   double *x, double *E, int64_t *evals);
+void or_adadelta(const or_problem *P, const double *bowl, int G, const or_params *pp,
+                 int iters, double *x, double *E, int64_t *evals);
+
+/* ---- D8 + D11: one full run ---- */
+int or_dock_run(const or_problem *P, const or_params *pp, int pop, int64_t max_evals,
+                uint64_t seed, uint32_t ligand_id, uint32_t run,
+                double *best_E, double *best_genes, int64_t *evals_used, int *generations,
+                double *final_E /*[pop] nullable*/);
+
+/* D11 / Listing 1: sum of per-individual evaluation counters. */
+int64_t or_sum_evals(int n, const int64_t *counters);
+
+#ifdef __cplusplus
+}
+#endif
+#endif
