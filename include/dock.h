@@ -1,0 +1,192 @@
+/*
+ * dock.h — C ABI of the B200-native LGA docking hot path (libdock.so).
+ *
+ * Method: arXiv 2203.02096 (MiniMDock), PAPER.md:64-66 [§II-A]: a flexible ligand is
+ * docked into a receptor given as a precomputed 3-D grid ("reaction field") by a
+ * Lamarckian genetic algorithm over `nruns` independent populations (150 individuals
+ * each in the paper) with a memetic local search on a random sample of every
+ * generation; the answer is the best pose over all runs.  Readings D1-D11 of the
+ * paper's silent points are in DESIGN.md §3.
+ *
+ * Conventions (all entry points):
+ *   units Å, radians, kcal/mol, elementary charge; arrays dense, row-major.
+ *   Pointers named h_* / plain are HOST memory, d_* are DEVICE memory of the context's
+ *   device.  Inputs are only read during the call (dock_init deep-copies and uploads
+ *   what the device needs); outputs are caller-allocated.  A context owns its device
+ *   memory until dock_free.  One context must not be used by two threads at once;
+ *   different contexts may be used concurrently.
+ *   Return codes (SPEC S:448 convention): DOCK_OK, DOCK_E_INPUT (caller error: NULL,
+ *   out-of-range index, non-finite value, bad topology, unsupported size),
+ *   DOCK_E_INTERNAL (CUDA error, out of memory, no device).  dock_last_error() names
+ *   the offending field / index.  There is no CPU fallback: without a usable CUDA
+ *   device every compute entry point returns DOCK_E_INTERNAL.
+ *
+ *   Genotype layout (D3): [tx, ty, tz, phi, theta, alpha, tau_1 .. tau_T], G = 6 + T,
+ *   torsions in dock_get_torsions() order.  Atom order at the ABI is always the
+ *   caller's; the device renumbers internally.
+ */
+#ifndef DOCK_H
+#define DOCK_H
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct dock_ctx dock_ctx;
+enum { DOCK_OK = 0, DOCK_E_INPUT = 1, DOCK_E_INTERNAL = 2 };
+enum { DOCK_LS_ADADELTA = 0, DOCK_LS_SOLIS_WETS = 1 };
+
+#define DOCK_MAX_ATOMS 256
+#define DOCK_MAX_TORSIONS 32
+#define DOCK_MAX_GENES (6 + DOCK_MAX_TORSIONS)
+
+/* Receptor grid maps ("reaction field ... three-dimensional grid").
+   maps holds n_types type maps, then the electrostatic map E, then the desolvation map D,
+   each nx*ny*nz floats with node (i,j,k) at i + nx*(j + ny*k).  origin = node (0,0,0). */
+typedef struct {
+    int32_t nx, ny, nz;          /* each >= 2 */
+    float spacing;               /* > 0 */
+    float origin[3];
+    int32_t n_types;             /* 1..16 */
+    const float *maps;           /* host, (n_types+2)*nx*ny*nz, finite */
+} dock_grids;
+
+/* Per-type ligand parameters, one per grid type map, in map order (D5; "hydrogen
+   bonding, van der Waals forces, and desolvation"). role: 0 none, 1 donor, 2 acceptor. */
+typedef struct {
+    float R, eps, S, V;
+    int32_t role;
+} dock_type_param;
+
+/* Ligand (atoms + rotatable bonds).  Torsions and the intra-
+   molecular pair list are derived by D1. */
+typedef struct {
+    int32_t n_atoms;             /* 1..256 */
+    const int32_t *type;         /* [n_atoms] index into the grid's type maps */
+    const float *charge;         /* [n_atoms] */
+    const float *xyz;            /* [n_atoms*3] reference coordinates */
+    int32_t n_bonds;
+    const int32_t *bonds;        /* [n_bonds*2] atom pairs; graph must be connected */
+    const uint8_t *rotatable;    /* [n_bonds] 1 = rotatable (must be a bridge); <= 32 */
+} dock_ligand;
+
+/* Search parameters (D8-D10). */
+typedef struct {
+    float p_tour, p_cross, p_mut, mut_trans, mut_angle;
+    int32_t ls_method;           /* DOCK_LS_ADADELTA or DOCK_LS_SOLIS_WETS */
+    float ls_rate;               /* fraction of the population locally searched */
+    int32_t ls_max_iters;
+    float sw_rho, sw_rho_min, sw_expand, sw_contract;
+    int32_t sw_cons_succ, sw_cons_fail;
+    float ad_rho, ad_eps;
+    int32_t max_generations;
+    int32_t device;              /* CUDA device ordinal */
+    int32_t l2_persist;          /* 1: pin the grid in L2 with an access-policy window */
+    int32_t gens_per_graph;      /* generations per CUDA-graph launch (>= 1) */
+    int32_t profile;             /* 1: CUDA events around every GA and LS launch (dock_kernel_stats) */
+} dock_params;
+
+/* Fills the defaults: p_tour .60, p_cross .80, p_mut .02, 2.0 Å / 0.523 rad, ADADELTA,
+   ls_rate 1.0, 300 iterations, SW 1.0/0.01/2/0.5/4/4, ADADELTA rho .8 eps 1e-2,
+   27000 generations, device 0, l2_persist 1, gens_per_graph 16. */
+int dock_params_default(dock_params *p);
+
+/* Built-in type table by name ("C","A","N","NA","O","OA","H","HD").
+   Returns DOCK_E_INPUT for an unknown name. */
+int dock_builtin_type_param(const char *name, dock_type_param *out);
+
+/* Preprocess the ligand (D1: torsion tree, DFS renumbering, pair list), pack the grid
+   into the device layout and upload both.  Validation errors -> DOCK_E_INPUT. */
+int dock_init(const dock_grids *grids, const dock_type_param *type_params,
+              const dock_ligand *ligand, const dock_params *params, dock_ctx **out);
+void dock_free(dock_ctx *ctx);
+const char *dock_last_error(const dock_ctx *ctx);   /* ctx may be NULL: last dock_init error */
+
+int dock_n_atoms(const dock_ctx *ctx);
+int dock_n_torsions(const dock_ctx *ctx);
+int dock_n_genes(const dock_ctx *ctx);
+int dock_n_pairs(const dock_ctx *ctx);
+
+/* Full docking (D8 + D11; "several full optimizations each with a starting
+   population of 150 ... The final solution is the best scoring pose out of all final
+   solutions over all runs").  Runs get global indices run_base .. run_base+num_runs-1
+   in the RNG counter (D2), so a run's result does not depend on how runs are split over
+   GPUs.  Outputs per run r (host): best_energy[r]; best_genotype[r*G]; best_xyz[r*N*3]
+   (caller atom order, may be NULL); evals_used[r] (may be NULL; >= max_evals, overshoot
+   < one generation); generations[r] (may be NULL).  Synchronous. */
+int dock_run(dock_ctx *ctx, int32_t pop_size, int32_t num_runs, int64_t max_evals,
+             uint64_t seed, float *best_energy, float *best_genotype, float *best_xyz,
+             int64_t *evals_used, int32_t *generations);
+int dock_run_ex(dock_ctx *ctx, int32_t pop_size, int32_t num_runs, int32_t run_base,
+                uint32_t ligand_id, int64_t max_evals, uint64_t seed,
+                float *best_energy, float *best_genotype, float *best_xyz,
+                int64_t *evals_used, int32_t *generations);
+/* Device-resident variant: outputs are DEVICE pointers, work is enqueued on `stream`
+   (a cudaStream_t, NULL = the context's own stream).  Returns after the last generation batch has
+   been enqueued and the termination flags were polled (it syncs on `stream` once per
+   gens_per_graph generations to read 4*num_runs bytes). */
+int dock_run_device(dock_ctx *ctx, int32_t pop_size, int32_t num_runs, int32_t run_base,
+                    uint32_t ligand_id, int64_t max_evals, uint64_t seed,
+                    float *d_best_energy, float *d_best_genotype, int64_t *d_evals_used,
+                    int32_t *d_generations, void *stream);
+
+/* ---------------- parity hooks (one per hot-path row) ---------------- */
+
+/* Energy (D4+D5+D6), optionally genotype gradient (D7) and pose (D3) of n genotypes.
+   genotypes [n*G]; energy [n]; grad [n*G] or NULL; xyz [n*N*3] (caller order) or NULL. */
+int dock_eval(dock_ctx *ctx, int32_t n, const float *genotypes, float *energy, float *grad,
+              float *xyz);
+int dock_eval_device(dock_ctx *ctx, int32_t n, const float *d_genotypes, float *d_energy,
+                     float *d_grad, float *d_xyz, void *stream);   /* stream NULL = legacy default */
+
+/* D1 on the host, without a device (runs the same preprocessing as dock_init):
+   *n_tors, axis [T*2] (a on the root side), moved [T*n_atoms], *n_pairs, pairs [P*2]
+   (lexicographic, caller indices).  pair_cap = capacity of `pairs` in pairs; returns
+   DOCK_E_INPUT if exceeded or the ligand is invalid (dock_last_error(NULL) says why). */
+int dock_topology(const dock_ligand *ligand, const dock_type_param *type_params, int32_t n_types,
+                  int32_t *n_tors, int32_t *axis, uint8_t *moved, int32_t *n_pairs, int32_t *pairs,
+                  int32_t pair_cap);
+
+/* D1 results in caller atom indices: pairs [P*2] lexicographic; torsion axes [T*2]
+   (a on the root side) and moved-set membership [T*N] in torsion order. */
+int dock_get_pairs(const dock_ctx *ctx, int32_t *pairs);
+int dock_get_torsions(const dock_ctx *ctx, int32_t *axis, uint8_t *moved);
+
+/* D2 on the device: raw Philox4x32-10 of n (counter, key) pairs [n*4], [n*2] -> [n*4];
+   and stream words m0..m0+n-1 of (seed, ligand_id, purpose, slot, gen, run). */
+int dock_philox(int32_t n, const uint32_t *ctr4, const uint32_t *key2, uint32_t *out4);
+int dock_stream_words(uint64_t seed, uint32_t ligand_id, uint32_t purpose, uint32_t slot,
+                      uint32_t gen, uint32_t run, uint32_t m0, int32_t n, uint32_t *out);
+
+/* D8 one GA generation of one run on an injected population (genes [pop*G], E [pop]):
+   new_genes [pop*G], new_E [pop] (offspring evaluated, slot 0 = elite copy),
+   debug [pop*8] = {A, B, crossover, c1, c2, mutation mask lo, hi, elite (slot 0)},
+   perm [pop] = LS pick order (first n_ls entries used). */
+int dock_ga_step(dock_ctx *ctx, uint64_t seed, uint32_t ligand_id, int32_t run, int32_t gen,
+                 int32_t pop, const float *old_genes, const float *old_E, float *new_genes,
+                 float *new_E, int32_t *debug, int32_t *perm);
+
+/* D9 / D10 local search of n individuals from injected genes / energies, in place.
+   slots[n] = population index of each (SW RNG slot); method per DOCK_LS_*; iters
+   overrides ls_max_iters; evals [n] receives the evaluation count. */
+int dock_ls_step(dock_ctx *ctx, int32_t method, int32_t n, int32_t iters, uint64_t seed,
+                 uint32_t ligand_id, int32_t run, int32_t gen, const int32_t *slots,
+                 float *genes, float *energy, int64_t *evals);
+
+/* Kernel-launch counter of this context (for the benchmark's gpu_launches claim). */
+int64_t dock_launch_count(const dock_ctx *ctx);
+
+/* With params.profile = 1: device time (ms, CUDA events on the launching stream) and
+   launch counts accumulated over the last dock_run* call, per kernel class
+   0 = k_ga (offspring), 1 = k_ls_* (local search), 2 = k_init.  Arrays of 3. */
+int dock_kernel_stats(const dock_ctx *ctx, double *ms, int64_t *launches);
+
+/* Bytes dock_init copied host -> device (packed grid + ligand block + atom map). */
+int64_t dock_upload_bytes(const dock_ctx *ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

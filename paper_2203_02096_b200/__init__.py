@@ -1,0 +1,318 @@
+"""Python binding of libdock.so (include/dock.h): argument marshalling only.
+
+Every step of the docking hot path (pose, grid interpolation, pair energy, gradient,
+ADADELTA / Solis-Wets, GA, Philox) runs in the sm_100a kernels of libdock.so.  There is
+no CPU fallback: importing this package fails loudly when the library is missing, and
+every compute call raises when no CUDA device is usable.  PyTorch is used only for
+device memory and streams (the *_device entry points accept torch CUDA tensors).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libdock.so")
+
+DOCK_OK, DOCK_E_INPUT, DOCK_E_INTERNAL = 0, 1, 2
+LS_ADADELTA, LS_SOLIS_WETS = 0, 1
+PURPOSE_INIT, PURPOSE_GA, PURPOSE_LS_PICK, PURPOSE_SW = 0, 1, 2, 3
+
+
+class DockError(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__(f"dock error {code}: {msg}")
+        self.code = code
+
+
+class Grids(C.Structure):
+    _fields_ = [("nx", C.c_int32), ("ny", C.c_int32), ("nz", C.c_int32), ("spacing", C.c_float),
+                ("origin", C.c_float * 3), ("n_types", C.c_int32), ("maps", C.POINTER(C.c_float))]
+
+
+class TypeParam(C.Structure):
+    _fields_ = [("R", C.c_float), ("eps", C.c_float), ("S", C.c_float), ("V", C.c_float), ("role", C.c_int32)]
+
+
+class Ligand(C.Structure):
+    _fields_ = [("n_atoms", C.c_int32), ("type", C.POINTER(C.c_int32)), ("charge", C.POINTER(C.c_float)),
+                ("xyz", C.POINTER(C.c_float)), ("n_bonds", C.c_int32), ("bonds", C.POINTER(C.c_int32)),
+                ("rotatable", C.POINTER(C.c_uint8))]
+
+
+class Params(C.Structure):
+    _fields_ = [("p_tour", C.c_float), ("p_cross", C.c_float), ("p_mut", C.c_float),
+                ("mut_trans", C.c_float), ("mut_angle", C.c_float), ("ls_method", C.c_int32),
+                ("ls_rate", C.c_float), ("ls_max_iters", C.c_int32), ("sw_rho", C.c_float),
+                ("sw_rho_min", C.c_float), ("sw_expand", C.c_float), ("sw_contract", C.c_float),
+                ("sw_cons_succ", C.c_int32), ("sw_cons_fail", C.c_int32), ("ad_rho", C.c_float),
+                ("ad_eps", C.c_float), ("max_generations", C.c_int32), ("device", C.c_int32),
+                ("l2_persist", C.c_int32), ("gens_per_graph", C.c_int32), ("profile", C.c_int32)]
+
+
+def _load():
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; "
+                          "g.build()'` (there is no CPU fallback)")
+    L = C.CDLL(LIB_PATH)
+    P, v = C.POINTER, C.c_void_p
+    i32, i64, u32, u64, f = C.c_int32, C.c_int64, C.c_uint32, C.c_uint64, C.c_float
+    sig = {
+        "dock_params_default": (i32, [P(Params)]),
+        "dock_builtin_type_param": (i32, [C.c_char_p, P(TypeParam)]),
+        "dock_init": (i32, [P(Grids), P(TypeParam), P(Ligand), P(Params), P(v)]),
+        "dock_free": (None, [v]),
+        "dock_last_error": (C.c_char_p, [v]),
+        "dock_n_atoms": (i32, [v]), "dock_n_torsions": (i32, [v]),
+        "dock_n_genes": (i32, [v]), "dock_n_pairs": (i32, [v]),
+        "dock_run": (i32, [v, i32, i32, i64, u64, P(f), P(f), P(f), P(i64), P(i32)]),
+        "dock_run_ex": (i32, [v, i32, i32, i32, u32, i64, u64, P(f), P(f), P(f), P(i64), P(i32)]),
+        "dock_run_device": (i32, [v, i32, i32, i32, u32, i64, u64, v, v, v, v, v]),
+        "dock_eval": (i32, [v, i32, P(f), P(f), P(f), P(f)]),
+        "dock_eval_device": (i32, [v, i32, v, v, v, v, v]),
+        "dock_get_pairs": (i32, [v, P(i32)]),
+        "dock_get_torsions": (i32, [v, P(i32), P(C.c_uint8)]),
+        "dock_philox": (i32, [i32, P(u32), P(u32), P(u32)]),
+        "dock_stream_words": (i32, [u64, u32, u32, u32, u32, u32, u32, i32, P(u32)]),
+        "dock_ga_step": (i32, [v, u64, u32, i32, i32, i32, P(f), P(f), P(f), P(f), P(i32), P(i32)]),
+        "dock_ls_step": (i32, [v, i32, i32, i32, u64, u32, i32, i32, P(i32), P(f), P(f), P(i64)]),
+        "dock_launch_count": (i64, [v]),
+        "dock_kernel_stats": (i32, [v, P(C.c_double), P(i64)]),
+        "dock_upload_bytes": (i64, [v]),
+        "dock_topology": (i32, [P(Ligand), P(TypeParam), i32, P(i32), P(i32), P(C.c_uint8), P(i32), P(i32), i32]),
+    }
+    for name, (res, args) in sig.items():
+        fn = getattr(L, name)
+        fn.restype = res
+        fn.argtypes = args
+    return L
+
+
+lib = _load()
+EXPORTED = ("dock_params_default", "dock_builtin_type_param", "dock_init", "dock_free", "dock_last_error",
+            "dock_n_atoms", "dock_n_torsions", "dock_n_genes", "dock_n_pairs", "dock_run", "dock_run_ex",
+            "dock_run_device", "dock_eval", "dock_eval_device", "dock_get_pairs", "dock_get_torsions",
+            "dock_philox", "dock_stream_words", "dock_ga_step", "dock_ls_step", "dock_launch_count",
+            "dock_topology", "dock_kernel_stats", "dock_upload_bytes")
+
+
+def topology(types, charges, xyz, bonds, rotatable, type_params, roles):
+    """D1 on the host (no device needed): (axis [T,2], moved [T,N], pairs [P,2])."""
+    t = np.ascontiguousarray(types, dtype=np.int32)
+    q = np.ascontiguousarray(charges, dtype=np.float32)
+    x = np.ascontiguousarray(xyz, dtype=np.float32).reshape(-1)
+    b = np.ascontiguousarray(bonds, dtype=np.int32).reshape(-1)
+    r = np.ascontiguousarray(rotatable, dtype=np.uint8)
+    tp = np.asarray(type_params, dtype=np.float32).reshape(-1, 4)
+    tarr = (TypeParam * tp.shape[0])()
+    for k in range(tp.shape[0]):
+        tarr[k] = TypeParam(*(float(v) for v in tp[k]), int(roles[k]))
+    lg = Ligand()
+    lg.n_atoms = t.shape[0]; lg.type = _ptr(t, C.c_int32); lg.charge = _ptr(q, C.c_float)
+    lg.xyz = _ptr(x, C.c_float); lg.n_bonds = b.shape[0] // 2
+    lg.bonds = _ptr(b, C.c_int32) if lg.n_bonds else None
+    lg.rotatable = _ptr(r, C.c_uint8) if lg.n_bonds else None
+    N = t.shape[0]
+    cap = max(1, N * (N - 1) // 2)
+    T = C.c_int32(0); Pn = C.c_int32(0)
+    axis = np.zeros(64, np.int32); moved = np.zeros(32 * N, np.uint8); pairs = np.zeros(2 * cap, np.int32)
+    _check(lib.dock_topology(C.byref(lg), tarr, tp.shape[0], C.byref(T), _ptr(axis, C.c_int32),
+                             _ptr(moved, C.c_uint8), C.byref(Pn), _ptr(pairs, C.c_int32), cap))
+    return (axis[: 2 * T.value].reshape(-1, 2), moved[: T.value * N].reshape(T.value, N),
+            pairs[: 2 * Pn.value].reshape(-1, 2))
+
+
+def _ptr(a, ct):
+    return a.ctypes.data_as(C.POINTER(ct)) if a is not None else None
+
+
+def _check(rc, ctx=None):
+    if rc != DOCK_OK:
+        msg = lib.dock_last_error(ctx)
+        raise DockError(rc, msg.decode() if msg else "")
+
+
+def params_default(**overrides) -> Params:
+    p = Params()
+    _check(lib.dock_params_default(C.byref(p)))
+    for k, val in overrides.items():
+        if not hasattr(p, k):
+            raise KeyError(k)
+        setattr(p, k, val)
+    return p
+
+
+def builtin_type_param(name: str) -> TypeParam:
+    t = TypeParam()
+    _check(lib.dock_builtin_type_param(name.encode(), C.byref(t)))
+    return t
+
+
+def philox(ctr, key):
+    """Raw Philox4x32-10 on the device: ctr [n,4] u32, key [n,2] u32 -> [n,4]."""
+    c = np.ascontiguousarray(ctr, dtype=np.uint32).reshape(-1, 4)
+    k = np.ascontiguousarray(key, dtype=np.uint32).reshape(-1, 2)
+    out = np.zeros_like(c)
+    _check(lib.dock_philox(c.shape[0], _ptr(c, C.c_uint32), _ptr(k, C.c_uint32), _ptr(out, C.c_uint32)))
+    return out
+
+
+def stream_words(seed, ligand_id, purpose, slot, gen, run, m0, n):
+    out = np.zeros(n, np.uint32)
+    _check(lib.dock_stream_words(seed, ligand_id, purpose, slot, gen, run, m0, n, _ptr(out, C.c_uint32)))
+    return out
+
+
+class Docker:
+    """One (device, receptor grid, ligand) docking context (dock_init ... dock_free)."""
+
+    def __init__(self, maps, n, spacing, origin, type_params, roles, types, charges, xyz, bonds,
+                 rotatable, params: Params | None = None, **overrides):
+        maps = np.ascontiguousarray(maps, dtype=np.float32).reshape(-1)
+        n = tuple(int(v) for v in n)
+        tp = np.asarray(type_params, dtype=np.float32).reshape(-1, 4)
+        roles = np.asarray(roles, dtype=np.int32).reshape(-1)
+        g = Grids()
+        g.nx, g.ny, g.nz = n
+        g.spacing = float(spacing)
+        for d in range(3):
+            g.origin[d] = float(origin[d])
+        g.n_types = tp.shape[0]
+        g.maps = _ptr(maps, C.c_float)
+        tarr = (TypeParam * tp.shape[0])()
+        for t in range(tp.shape[0]):
+            tarr[t] = TypeParam(*(float(x) for x in tp[t]), int(roles[t]))
+        self._types = np.ascontiguousarray(types, dtype=np.int32)
+        self._charges = np.ascontiguousarray(charges, dtype=np.float32)
+        self._xyz = np.ascontiguousarray(xyz, dtype=np.float32).reshape(-1)
+        self._bonds = np.ascontiguousarray(bonds, dtype=np.int32).reshape(-1)
+        self._rot = np.ascontiguousarray(rotatable, dtype=np.uint8)
+        lg = Ligand()
+        lg.n_atoms = self._types.shape[0]
+        lg.type = _ptr(self._types, C.c_int32)
+        lg.charge = _ptr(self._charges, C.c_float)
+        lg.xyz = _ptr(self._xyz, C.c_float)
+        lg.n_bonds = self._bonds.shape[0] // 2
+        lg.bonds = _ptr(self._bonds, C.c_int32) if lg.n_bonds else None
+        lg.rotatable = _ptr(self._rot, C.c_uint8) if lg.n_bonds else None
+        if params is None:
+            params = params_default(**overrides)
+        else:
+            for k, val in overrides.items():
+                setattr(params, k, val)
+        self.params = params
+        self._ctx = C.c_void_p()
+        _check(lib.dock_init(C.byref(g), tarr, C.byref(lg), C.byref(params), C.byref(self._ctx)))
+        self.N = lib.dock_n_atoms(self._ctx)
+        self.T = lib.dock_n_torsions(self._ctx)
+        self.G = lib.dock_n_genes(self._ctx)
+        self.P = lib.dock_n_pairs(self._ctx)
+
+    @classmethod
+    def from_inputs(cls, grid, lig, params: Params | None = None, **overrides):
+        """Duck-typed constructor: grid has maps/n/spacing/origin/type_params(); lig has
+        types/charges/xyz/bonds/rotatable (e.g. gen.synth objects)."""
+        tp, roles = grid.type_params()
+        return cls(grid.maps, grid.n, grid.spacing, grid.origin, tp, roles, lig.types, lig.charges,
+                   lig.xyz, lig.bonds, lig.rotatable, params=params, **overrides)
+
+    def close(self):
+        if getattr(self, "_ctx", None) and self._ctx.value:
+            lib.dock_free(self._ctx)
+            self._ctx = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _chk(self, rc):
+        _check(rc, self._ctx)
+
+    @property
+    def launches(self) -> int:
+        return int(lib.dock_launch_count(self._ctx))
+
+    @property
+    def upload_bytes(self) -> int:
+        return int(lib.dock_upload_bytes(self._ctx))
+
+    def kernel_stats(self):
+        """(ms[3], launches[3]) for kernel classes (k_ga, k_ls_*, k_init) of the last run
+        (needs profile=1)."""
+        ms = np.zeros(3, np.float64); n = np.zeros(3, np.int64)
+        self._chk(lib.dock_kernel_stats(self._ctx, _ptr(ms, C.c_double), _ptr(n, C.c_int64)))
+        return ms, n
+
+    # ---- D1 ----
+    def pairs(self):
+        out = np.zeros(max(1, 2 * self.P), np.int32)
+        self._chk(lib.dock_get_pairs(self._ctx, _ptr(out, C.c_int32)))
+        return out[: 2 * self.P].reshape(-1, 2)
+
+    def torsions(self):
+        axis = np.zeros(max(1, 2 * self.T), np.int32)
+        moved = np.zeros(max(1, self.T * self.N), np.uint8)
+        self._chk(lib.dock_get_torsions(self._ctx, _ptr(axis, C.c_int32), _ptr(moved, C.c_uint8)))
+        return axis[: 2 * self.T].reshape(-1, 2), moved[: self.T * self.N].reshape(self.T, self.N)
+
+    # ---- D3-D7 ----
+    def eval(self, genotypes, grad=False, xyz=False):
+        x = np.ascontiguousarray(genotypes, dtype=np.float32).reshape(-1, self.G)
+        n = x.shape[0]
+        E = np.zeros(n, np.float32)
+        gr = np.zeros((n, self.G), np.float32) if grad else None
+        xy = np.zeros((n, self.N, 3), np.float32) if xyz else None
+        self._chk(lib.dock_eval(self._ctx, n, _ptr(x, C.c_float), _ptr(E, C.c_float), _ptr(gr, C.c_float),
+                                _ptr(xy, C.c_float)))
+        return E, gr, xy
+
+    def eval_device(self, genotypes, energy, grad=None, xyz=None, stream=0):
+        """torch CUDA tensors (float32, contiguous); stream = torch.cuda.Stream.cuda_stream or 0."""
+        n = genotypes.shape[0]
+        self._chk(lib.dock_eval_device(self._ctx, n, genotypes.data_ptr(), energy.data_ptr(),
+                                       grad.data_ptr() if grad is not None else None,
+                                       xyz.data_ptr() if xyz is not None else None, stream or None))
+
+    # ---- D8-D11 ----
+    def run(self, pop, runs, max_evals, seed, run_base=0, ligand_id=0, xyz=True):
+        bE = np.zeros(runs, np.float32)
+        bG = np.zeros((runs, self.G), np.float32)
+        bX = np.zeros((runs, self.N, 3), np.float32) if xyz else None
+        ev = np.zeros(runs, np.int64)
+        gens = np.zeros(runs, np.int32)
+        self._chk(lib.dock_run_ex(self._ctx, pop, runs, run_base, ligand_id, max_evals, seed,
+                                  _ptr(bE, C.c_float), _ptr(bG, C.c_float), _ptr(bX, C.c_float),
+                                  _ptr(ev, C.c_int64), _ptr(gens, C.c_int32)))
+        return dict(best_E=bE, best_genes=bG, best_xyz=bX, evals=ev, generations=gens)
+
+    def run_device(self, pop, runs, max_evals, seed, best_E, best_genes, evals=None, gens=None,
+                   run_base=0, ligand_id=0, stream=0):
+        self._chk(lib.dock_run_device(self._ctx, pop, runs, run_base, ligand_id, max_evals, seed,
+                                      best_E.data_ptr(), best_genes.data_ptr(),
+                                      evals.data_ptr() if evals is not None else None,
+                                      gens.data_ptr() if gens is not None else None, stream or None))
+
+    def ga_step(self, seed, ligand_id, run, gen, old_genes, old_E):
+        og = np.ascontiguousarray(old_genes, dtype=np.float32)
+        oE = np.ascontiguousarray(old_E, dtype=np.float32)
+        pop = og.shape[0]
+        ng = np.zeros_like(og); nE = np.zeros_like(oE)
+        dbg = np.zeros((pop, 8), np.int32); perm = np.zeros(pop, np.int32)
+        self._chk(lib.dock_ga_step(self._ctx, seed, ligand_id, run, gen, pop, _ptr(og, C.c_float),
+                                   _ptr(oE, C.c_float), _ptr(ng, C.c_float), _ptr(nE, C.c_float),
+                                   _ptr(dbg, C.c_int32), _ptr(perm, C.c_int32)))
+        return ng, nE, dbg, perm
+
+    def ls_step(self, method, genes, energy, iters, seed=0, ligand_id=0, run=0, gen=1, slots=None):
+        g = np.ascontiguousarray(genes, dtype=np.float32).reshape(-1, self.G).copy()
+        E = np.ascontiguousarray(energy, dtype=np.float32).copy()
+        n = g.shape[0]
+        sl = np.ascontiguousarray(slots if slots is not None else np.arange(n), dtype=np.int32)
+        ev = np.zeros(n, np.int64)
+        self._chk(lib.dock_ls_step(self._ctx, method, n, iters, seed, ligand_id, run, gen, _ptr(sl, C.c_int32),
+                                   _ptr(g, C.c_float), _ptr(E, C.c_float), _ptr(ev, C.c_int64)))
+        return g, E, ev

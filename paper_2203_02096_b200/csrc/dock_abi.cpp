@@ -1,0 +1,561 @@
+// dock_abi.cpp — the C ABI (include/dock.h) and the per-device engine.
+//
+// The engine keeps the whole search on the device: populations, per-run counters and the
+// LS sample live in HBM; one generation = k_ga -> k_ls_* -> k_gen_end, captured as a
+// CUDA graph of `gens_per_graph` generations and relaunched until every run has met its
+// evaluation budget (D8.5).  The host reads 16 bytes per run per graph launch to
+// decide termination; finished runs turn their kernels into no-ops.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <climits>
+#include <cmath>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/dock.h"
+#include "kernels.cuh"
+#include "prep.h"
+
+struct dock_ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    dk::Prepared prep;
+    dk::LigDev lig{};
+    dk::GridDev grid{};
+    dock_params params{};
+    float4 *d_maps = nullptr;
+    size_t maps_bytes = 0;
+    uint8_t *d_blob = nullptr;
+    int *d_dfs2orig = nullptr;
+    int cap_runs = 0, cap_pop = 0;
+    float *d_genes = nullptr, *d_E = nullptr;
+    dk::RunState *d_state = nullptr;
+    int *d_perm = nullptr, *d_ls_evals = nullptr;
+    dk::RunState *h_state = nullptr;
+    int h_state_cap = 0;
+    std::string err;
+    long long launches = 0;
+    double prof_ms[3] = {0, 0, 0};
+    long long prof_n[3] = {0, 0, 0};
+    std::vector<cudaEvent_t> events;   // profiling: 3 per captured generation + 2 for init
+};
+
+namespace {
+
+thread_local std::string g_init_error;
+
+#define CK(call)                                                                          \
+    do {                                                                                  \
+        cudaError_t e_ = (call);                                                          \
+        if (e_ != cudaSuccess) {                                                          \
+            c->err = std::string(#call) + ": " + cudaGetErrorString(e_);                  \
+            return DOCK_E_INTERNAL;                                                       \
+        }                                                                                 \
+    } while (0)
+
+int input_error(dock_ctx *c, const std::string &m) {
+    if (c) c->err = m;
+    return DOCK_E_INPUT;
+}
+
+bool prob_ok(float p) { return std::isfinite(p) && p >= 0.f && p <= 1.f; }
+
+int validate_params(const dock_params &p, std::string *err) {
+    if (!prob_ok(p.p_tour) || !prob_ok(p.p_cross) || !prob_ok(p.p_mut)) { *err = "params: probabilities must be in [0,1]"; return DOCK_E_INPUT; }
+    if (!std::isfinite(p.mut_trans) || !std::isfinite(p.mut_angle) || p.mut_trans < 0 || p.mut_angle < 0) { *err = "params.mut_*: must be finite, >= 0"; return DOCK_E_INPUT; }
+    if (p.ls_method != DOCK_LS_ADADELTA && p.ls_method != DOCK_LS_SOLIS_WETS) { *err = "params.ls_method: 0 or 1"; return DOCK_E_INPUT; }
+    if (!prob_ok(p.ls_rate)) { *err = "params.ls_rate: must be in [0,1]"; return DOCK_E_INPUT; }
+    if (p.ls_max_iters < 0) { *err = "params.ls_max_iters: must be >= 0"; return DOCK_E_INPUT; }
+    if (!(p.sw_rho > 0) || !(p.sw_rho_min > 0) || !(p.sw_expand > 0) || !(p.sw_contract > 0) || p.sw_cons_succ < 1 || p.sw_cons_fail < 1) { *err = "params.sw_*: must be positive"; return DOCK_E_INPUT; }
+    if (!(p.ad_rho >= 0 && p.ad_rho < 1) || !(p.ad_eps > 0)) { *err = "params.ad_rho in [0,1), ad_eps > 0"; return DOCK_E_INPUT; }
+    if (p.max_generations < 0) { *err = "params.max_generations: must be >= 0"; return DOCK_E_INPUT; }
+    if (p.gens_per_graph < 1 || p.gens_per_graph > 4096) { *err = "params.gens_per_graph: 1..4096"; return DOCK_E_INPUT; }
+    return DOCK_OK;
+}
+
+// n_ls = ceil(ls_rate * pop - 1e-4) clamped to [0, pop] (DESIGN.md §3 reading 16a).
+int n_ls_of(float ls_rate, int pop) {
+    int n = (int)std::ceil((double)ls_rate * (double)pop - 1e-4);
+    return std::max(0, std::min(pop, n));
+}
+
+dk::SearchDev make_search(const dock_ctx *c, int pop, int runs, int run_base, uint32_t ligand_id, int64_t max_evals,
+                          uint64_t seed) {
+    const dock_params &p = c->params;
+    dk::SearchDev s{};
+    s.p_tour = p.p_tour; s.p_cross = p.p_cross; s.p_mut = p.p_mut;
+    s.mut_trans = p.mut_trans; s.mut_angle = p.mut_angle;
+    s.ls_method = p.ls_method; s.ls_iters = p.ls_max_iters; s.n_ls = n_ls_of(p.ls_rate, pop);
+    s.sw_rho = p.sw_rho; s.sw_rho_min = p.sw_rho_min; s.sw_expand = p.sw_expand; s.sw_contract = p.sw_contract;
+    s.sw_cons_succ = p.sw_cons_succ; s.sw_cons_fail = p.sw_cons_fail;
+    s.ad_rho = p.ad_rho; s.ad_eps = p.ad_eps;
+    s.max_generations = p.max_generations;
+    s.max_evals = max_evals;
+    s.pop = pop; s.runs = runs; s.run_base = run_base;
+    const uint64_t k = seed + (uint64_t)ligand_id * 0x9E3779B97F4A7C15ull;   // D2 key
+    s.key0 = (uint32_t)k; s.key1 = (uint32_t)(k >> 32);
+    return s;
+}
+
+dk::PopDev pop_of(const dock_ctx *c) {
+    dk::PopDev d;
+    d.genes = c->d_genes; d.E = c->d_E; d.state = c->d_state; d.perm = c->d_perm; d.ls_evals = c->d_ls_evals;
+    return d;
+}
+
+int ensure_buffers(dock_ctx *c, int runs, int pop) {
+    if (runs <= c->cap_runs && pop <= c->cap_pop) return DOCK_OK;
+    const int R = std::max(runs, c->cap_runs), P = std::max(pop, c->cap_pop);
+    cudaFree(c->d_genes); cudaFree(c->d_E); cudaFree(c->d_state); cudaFree(c->d_perm); cudaFree(c->d_ls_evals);
+    c->d_genes = nullptr; c->d_E = nullptr; c->d_state = nullptr; c->d_perm = nullptr; c->d_ls_evals = nullptr;
+    c->cap_runs = c->cap_pop = 0;
+    const size_t G = (size_t)c->prep.G;
+    CK(cudaMalloc(&c->d_genes, 2 * (size_t)R * P * G * sizeof(float)));
+    CK(cudaMalloc(&c->d_E, 2 * (size_t)R * P * sizeof(float)));
+    CK(cudaMalloc(&c->d_state, (size_t)R * sizeof(dk::RunState)));
+    CK(cudaMalloc(&c->d_perm, (size_t)R * P * sizeof(int)));
+    CK(cudaMalloc(&c->d_ls_evals, (size_t)R * P * sizeof(int)));
+    if (R > c->h_state_cap) {
+        if (c->h_state) cudaFreeHost(c->h_state);
+        c->h_state = nullptr;
+        CK(cudaMallocHost(&c->h_state, (size_t)R * sizeof(dk::RunState)));
+        c->h_state_cap = R;
+    }
+    c->cap_runs = R; c->cap_pop = P;
+    return DOCK_OK;
+}
+
+int check_run_args(dock_ctx *c, int pop, int runs, int run_base, int64_t max_evals) {
+    if (pop < 2 || pop > 4096) return input_error(c, "pop_size: must be in 2..4096");
+    if (runs < 1) return input_error(c, "num_runs: must be >= 1");
+    if (run_base < 0) return input_error(c, "run_base: must be >= 0");
+    if (max_evals < pop) return input_error(c, "max_evals: must be >= pop_size");
+    return DOCK_OK;
+}
+
+struct DevBuf {
+    void *p = nullptr;
+    ~DevBuf() { if (p) cudaFree(p); }
+};
+
+}  // namespace
+
+extern "C" {
+
+int dock_params_default(dock_params *p) {
+    if (!p) return DOCK_E_INPUT;
+    std::memset(p, 0, sizeof(*p));
+    p->p_tour = 0.60f; p->p_cross = 0.80f; p->p_mut = 0.02f; p->mut_trans = 2.0f; p->mut_angle = 0.523f;
+    p->ls_method = DOCK_LS_ADADELTA; p->ls_rate = 1.0f; p->ls_max_iters = 300;
+    p->sw_rho = 1.0f; p->sw_rho_min = 0.01f; p->sw_expand = 2.0f; p->sw_contract = 0.5f;
+    p->sw_cons_succ = 4; p->sw_cons_fail = 4;
+    p->ad_rho = 0.8f; p->ad_eps = 1e-2f;
+    p->max_generations = 27000;
+    p->device = 0; p->l2_persist = 1; p->gens_per_graph = 16;
+    return DOCK_OK;
+}
+
+int dock_builtin_type_param(const char *name, dock_type_param *out) {
+    static const struct { const char *n; dock_type_param t; } table[] = {
+        {"C", {4.00f, 0.150f, -0.00143f, 33.5103f, 0}}, {"A", {4.00f, 0.150f, -0.00052f, 33.5103f, 0}},
+        {"N", {3.50f, 0.160f, -0.00162f, 22.4493f, 0}}, {"NA", {3.50f, 0.160f, -0.00162f, 22.4493f, 2}},
+        {"O", {3.20f, 0.200f, -0.00251f, 17.1573f, 0}}, {"OA", {3.20f, 0.200f, -0.00251f, 17.1573f, 2}},
+        {"H", {2.00f, 0.020f, 0.00051f, 0.0f, 0}},      {"HD", {2.00f, 0.020f, 0.00051f, 0.0f, 1}},
+    };
+    if (!name || !out) return DOCK_E_INPUT;
+    for (const auto &e : table)
+        if (std::strcmp(e.n, name) == 0) { *out = e.t; return DOCK_OK; }
+    return DOCK_E_INPUT;
+}
+
+int dock_init(const dock_grids *grids, const dock_type_param *type_params, const dock_ligand *ligand,
+              const dock_params *params, dock_ctx **out) {
+    if (!out) { g_init_error = "out: NULL"; return DOCK_E_INPUT; }
+    *out = nullptr;
+    dock_params p;
+    if (params) p = *params; else dock_params_default(&p);
+    std::string err;
+    if (validate_params(p, &err) != DOCK_OK) { g_init_error = err; return DOCK_E_INPUT; }
+    std::vector<float4> packed;
+    if (dk::pack_grid(grids, &packed, &err) != DOCK_OK) { g_init_error = err; return DOCK_E_INPUT; }
+    auto *c = new dock_ctx();
+    c->params = p;
+    if (dk::prepare_ligand(ligand, type_params, grids->n_types, &c->prep, &err) != DOCK_OK) {
+        g_init_error = err; delete c; return DOCK_E_INPUT;
+    }
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev < 1) {
+        cudaGetLastError();
+        g_init_error = "no CUDA device (this library has no CPU fallback)"; delete c; return DOCK_E_INTERNAL;
+    }
+    if (p.device < 0 || p.device >= ndev) { g_init_error = "params.device: no such CUDA device"; delete c; return DOCK_E_INPUT; }
+    c->device = p.device;
+    auto bail = [&](int rc) { g_init_error = c->err; dock_free(c); return rc; };
+    if (cudaSetDevice(c->device) != cudaSuccess) { c->err = "cudaSetDevice failed"; return bail(DOCK_E_INTERNAL); }
+    if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess) { c->err = "cudaStreamCreate failed"; return bail(DOCK_E_INTERNAL); }
+    if (dk::setup_kernel_attributes() != cudaSuccess) { c->err = "cudaFuncSetAttribute failed (is this an sm_100 device?)"; return bail(DOCK_E_INTERNAL); }
+    c->maps_bytes = packed.size() * sizeof(float4);
+    if (cudaMalloc(&c->d_maps, c->maps_bytes) != cudaSuccess ||
+        cudaMemcpy(c->d_maps, packed.data(), c->maps_bytes, cudaMemcpyHostToDevice) != cudaSuccess ||
+        cudaMalloc(&c->d_blob, c->prep.blob.size()) != cudaSuccess ||
+        cudaMemcpy(c->d_blob, c->prep.blob.data(), c->prep.blob.size(), cudaMemcpyHostToDevice) != cudaSuccess ||
+        cudaMalloc(&c->d_dfs2orig, sizeof(int) * c->prep.N) != cudaSuccess ||
+        cudaMemcpy(c->d_dfs2orig, c->prep.dfs2orig.data(), sizeof(int) * c->prep.N, cudaMemcpyHostToDevice) != cudaSuccess) {
+        c->err = "device allocation/upload failed";
+        return bail(DOCK_E_INTERNAL);
+    }
+    c->lig = c->prep.layout;
+    c->lig.blob = c->d_blob;
+    dk::GridDev &g = c->grid;
+    g.maps = c->d_maps;
+    g.nx = grids->nx; g.ny = grids->ny; g.nz = grids->nz; g.n_types = grids->n_types;
+    g.ox = grids->origin[0]; g.oy = grids->origin[1]; g.oz = grids->origin[2];
+    g.s = grids->spacing; g.inv_s = 1.0f / grids->spacing;
+    g.hx = g.ox + (float)(g.nx - 1) * g.s; g.hy = g.oy + (float)(g.ny - 1) * g.s; g.hz = g.oz + (float)(g.nz - 1) * g.s;
+    if (p.l2_persist) {
+        // NS: "Grid maps live in HBM with L2-persistence windows".
+        cudaDeviceProp prop;
+        if (cudaGetDeviceProperties(&prop, c->device) == cudaSuccess && prop.persistingL2CacheMaxSize > 0 &&
+            prop.accessPolicyMaxWindowSize > 0) {
+            const size_t win = std::min(c->maps_bytes, (size_t)prop.accessPolicyMaxWindowSize);
+            const size_t lim = std::min(win, (size_t)prop.persistingL2CacheMaxSize);
+            cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, lim);
+            cudaStreamAttrValue attr{};
+            attr.accessPolicyWindow.base_ptr = c->d_maps;
+            attr.accessPolicyWindow.num_bytes = win;
+            attr.accessPolicyWindow.hitRatio = (float)std::min(1.0, (double)lim / (double)win);
+            attr.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+            attr.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+            cudaStreamSetAttribute(c->stream, cudaStreamAttributeAccessPolicyWindow, &attr);
+        }
+        cudaGetLastError();   // the window is an optimisation: never fatal
+    }
+    *out = c;
+    return DOCK_OK;
+}
+
+void dock_free(dock_ctx *c) {
+    if (!c) return;
+    cudaSetDevice(c->device);
+    if (c->stream) cudaStreamSynchronize(c->stream);
+    cudaFree(c->d_maps); cudaFree(c->d_blob); cudaFree(c->d_dfs2orig);
+    cudaFree(c->d_genes); cudaFree(c->d_E); cudaFree(c->d_state); cudaFree(c->d_perm); cudaFree(c->d_ls_evals);
+    if (c->h_state) cudaFreeHost(c->h_state);
+    for (cudaEvent_t e : c->events) cudaEventDestroy(e);
+    if (c->stream) cudaStreamDestroy(c->stream);
+    cudaGetLastError();
+    delete c;
+}
+
+const char *dock_last_error(const dock_ctx *c) { return c ? c->err.c_str() : g_init_error.c_str(); }
+int dock_n_atoms(const dock_ctx *c) { return c ? c->prep.N : -1; }
+int dock_n_torsions(const dock_ctx *c) { return c ? c->prep.T : -1; }
+int dock_n_genes(const dock_ctx *c) { return c ? c->prep.G : -1; }
+int dock_n_pairs(const dock_ctx *c) { return c ? c->prep.P : -1; }
+int64_t dock_launch_count(const dock_ctx *c) { return c ? c->launches : -1; }
+
+int64_t dock_upload_bytes(const dock_ctx *c) {
+    return c ? (int64_t)(c->maps_bytes + c->prep.blob.size() + sizeof(int) * c->prep.N) : -1;
+}
+
+int dock_kernel_stats(const dock_ctx *c, double *ms, int64_t *launches) {
+    if (!c) return DOCK_E_INPUT;
+    for (int i = 0; i < 3; ++i) {
+        if (ms) ms[i] = c->prof_ms[i];
+        if (launches) launches[i] = c->prof_n[i];
+    }
+    return DOCK_OK;
+}
+
+int dock_run_device(dock_ctx *c, int32_t pop, int32_t runs, int32_t run_base, uint32_t ligand_id, int64_t max_evals,
+                    uint64_t seed, float *d_best_energy, float *d_best_genotype, int64_t *d_evals_used,
+                    int32_t *d_generations, void *stream) {
+    if (!c) return DOCK_E_INPUT;
+    if (int rc = check_run_args(c, pop, runs, run_base, max_evals)) return rc;
+    if (!d_best_energy || !d_best_genotype) return input_error(c, "d_best_energy/d_best_genotype: NULL");
+    CK(cudaSetDevice(c->device));
+    if (int rc = ensure_buffers(c, runs, pop)) return rc;
+    cudaStream_t s = stream ? (cudaStream_t)stream : c->stream;
+    const dk::SearchDev sp = make_search(c, pop, runs, run_base, ligand_id, max_evals, seed);
+    const dk::PopDev pd = pop_of(c);
+    const int K = c->params.gens_per_graph;
+    const bool prof = c->params.profile != 0;
+    for (int i = 0; i < 3; ++i) { c->prof_ms[i] = 0; c->prof_n[i] = 0; }
+    if (prof && (int)c->events.size() < 3 * K + 2) {
+        while ((int)c->events.size() < 3 * K + 2) {
+            cudaEvent_t ev;
+            CK(cudaEventCreate(&ev));
+            c->events.push_back(ev);
+        }
+    }
+    cudaEvent_t *ev = c->events.data();
+    if (prof) CK(cudaEventRecord(ev[3 * K], s));
+    CK(dk::launch_init(c->lig, c->grid, sp, pd, s));
+    if (prof) CK(cudaEventRecord(ev[3 * K + 1], s));
+    c->launches += 1;
+    dk::LsArgs la{};
+    la.use_state = 1; la.n_per_run = sp.n_ls; la.iters = sp.ls_iters;
+    const bool do_ls = sp.n_ls > 0 && sp.ls_iters > 0;
+    // capture K generations once; the kernels read the generation from device state
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    CK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+    cudaError_t ce = cudaSuccess;
+    for (int k = 0; k < K && ce == cudaSuccess; ++k) {
+        if (prof) ce = cudaEventRecordWithFlags(ev[3 * k], s, cudaEventRecordExternal);
+        if (ce == cudaSuccess) ce = dk::launch_ga(c->lig, c->grid, sp, pd, nullptr, s);
+        if (ce == cudaSuccess && prof) ce = cudaEventRecordWithFlags(ev[3 * k + 1], s, cudaEventRecordExternal);
+        if (ce == cudaSuccess && do_ls) ce = dk::launch_ls(c->lig, c->grid, sp, pd, la, runs * sp.n_ls, s);
+        if (ce == cudaSuccess && prof) ce = cudaEventRecordWithFlags(ev[3 * k + 2], s, cudaEventRecordExternal);
+        if (ce == cudaSuccess) ce = dk::launch_gen_end(sp, pd, s);
+    }
+    cudaError_t ee = cudaStreamEndCapture(s, &graph);
+    if (ce != cudaSuccess || ee != cudaSuccess) {
+        if (graph) cudaGraphDestroy(graph);
+        c->err = std::string("graph capture: ") + cudaGetErrorString(ce != cudaSuccess ? ce : ee);
+        return DOCK_E_INTERNAL;
+    }
+    if (cudaGraphInstantiate(&exec, graph, 0) != cudaSuccess) {
+        cudaGraphDestroy(graph);
+        c->err = "cudaGraphInstantiate failed";
+        return DOCK_E_INTERNAL;
+    }
+    const int per_graph = K * (do_ls ? 3 : 2);
+    const long long max_batches = (long long)c->params.max_generations / K + 2;
+    int rc = DOCK_OK;
+    for (long long b = 0; b < max_batches; ++b) {
+        cudaError_t e = cudaGraphLaunch(exec, s);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(c->h_state, c->d_state, sizeof(dk::RunState) * runs, cudaMemcpyDeviceToHost, s);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+        if (e != cudaSuccess) { c->err = std::string("generation batch: ") + cudaGetErrorString(e); rc = DOCK_E_INTERNAL; break; }
+        c->launches += per_graph;
+        if (prof) {
+            float t;
+            cudaError_t pe = cudaSuccess;
+            if (b == 0 && (pe = cudaEventElapsedTime(&t, ev[3 * K], ev[3 * K + 1])) == cudaSuccess) { c->prof_ms[2] += t; c->prof_n[2] += 1; }
+            for (int k = 0; k < K && pe == cudaSuccess; ++k) {
+                if ((pe = cudaEventElapsedTime(&t, ev[3 * k], ev[3 * k + 1])) == cudaSuccess) { c->prof_ms[0] += t; c->prof_n[0] += 1; }
+                if (pe == cudaSuccess && do_ls && (pe = cudaEventElapsedTime(&t, ev[3 * k + 1], ev[3 * k + 2])) == cudaSuccess) { c->prof_ms[1] += t; c->prof_n[1] += 1; }
+            }
+            if (pe != cudaSuccess) {
+                c->err = std::string("profiling (ignored): cudaEventElapsedTime: ") + cudaGetErrorString(pe);
+                cudaGetLastError();
+                c->prof_n[0] = c->prof_n[1] = -1;
+            }
+        }
+        bool any = false;
+        for (int r = 0; r < runs && !any; ++r)
+            any = c->h_state[r].evals < max_evals && c->h_state[r].gen < c->params.max_generations;
+        if (!any) break;
+    }
+    cudaGraphExecDestroy(exec);
+    cudaGraphDestroy(graph);
+    if (rc != DOCK_OK) return rc;
+    CK(dk::launch_best(c->lig, sp, pd, d_best_energy, d_best_genotype, (long long *)d_evals_used, d_generations, s));
+    c->launches += 1;
+    return DOCK_OK;
+}
+
+int dock_run_ex(dock_ctx *c, int32_t pop, int32_t runs, int32_t run_base, uint32_t ligand_id, int64_t max_evals,
+                uint64_t seed, float *best_energy, float *best_genotype, float *best_xyz, int64_t *evals_used,
+                int32_t *generations) {
+    if (!c) return DOCK_E_INPUT;
+    if (int rc = check_run_args(c, pop, runs, run_base, max_evals)) return rc;
+    if (!best_energy || !best_genotype) return input_error(c, "best_energy/best_genotype: NULL");
+    CK(cudaSetDevice(c->device));
+    const int G = c->prep.G, N = c->prep.N;
+    DevBuf bE, bG, bEv, bGen, bX, bE2;
+    CK(cudaMalloc(&bE.p, sizeof(float) * runs));
+    CK(cudaMalloc(&bG.p, sizeof(float) * runs * G));
+    CK(cudaMalloc(&bEv.p, sizeof(int64_t) * runs));
+    CK(cudaMalloc(&bGen.p, sizeof(int32_t) * runs));
+    int rc = dock_run_device(c, pop, runs, run_base, ligand_id, max_evals, seed, (float *)bE.p, (float *)bG.p,
+                             (int64_t *)bEv.p, (int32_t *)bGen.p, c->stream);
+    if (rc != DOCK_OK) return rc;
+    if (best_xyz) {
+        CK(cudaMalloc(&bX.p, sizeof(float) * runs * N * 3));
+        CK(cudaMalloc(&bE2.p, sizeof(float) * runs));
+        CK(dk::launch_eval(c->lig, c->grid, runs, (const float *)bG.p, (float *)bE2.p, nullptr, (float *)bX.p,
+                           c->d_dfs2orig, c->stream));
+        c->launches += 1;
+        CK(cudaMemcpyAsync(best_xyz, bX.p, sizeof(float) * runs * N * 3, cudaMemcpyDeviceToHost, c->stream));
+    }
+    CK(cudaMemcpyAsync(best_energy, bE.p, sizeof(float) * runs, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaMemcpyAsync(best_genotype, bG.p, sizeof(float) * runs * G, cudaMemcpyDeviceToHost, c->stream));
+    if (evals_used) CK(cudaMemcpyAsync(evals_used, bEv.p, sizeof(int64_t) * runs, cudaMemcpyDeviceToHost, c->stream));
+    if (generations) CK(cudaMemcpyAsync(generations, bGen.p, sizeof(int32_t) * runs, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    return DOCK_OK;
+}
+
+int dock_run(dock_ctx *c, int32_t pop, int32_t runs, int64_t max_evals, uint64_t seed, float *best_energy,
+             float *best_genotype, float *best_xyz, int64_t *evals_used, int32_t *generations) {
+    return dock_run_ex(c, pop, runs, 0, 0u, max_evals, seed, best_energy, best_genotype, best_xyz, evals_used,
+                       generations);
+}
+
+int dock_eval_device(dock_ctx *c, int32_t n, const float *d_genotypes, float *d_energy, float *d_grad, float *d_xyz,
+                     void *stream) {
+    if (!c) return DOCK_E_INPUT;
+    if (n < 0) return input_error(c, "n: must be >= 0");
+    if (n > 0 && (!d_genotypes || !d_energy)) return input_error(c, "d_genotypes/d_energy: NULL");
+    CK(cudaSetDevice(c->device));
+    CK(dk::launch_eval(c->lig, c->grid, n, d_genotypes, d_energy, d_grad, d_xyz, c->d_dfs2orig, (cudaStream_t)stream));
+    c->launches += 1;
+    return DOCK_OK;
+}
+
+int dock_eval(dock_ctx *c, int32_t n, const float *genotypes, float *energy, float *grad, float *xyz) {
+    if (!c) return DOCK_E_INPUT;
+    if (n < 0) return input_error(c, "n: must be >= 0");
+    if (n == 0) return DOCK_OK;
+    if (!genotypes || !energy) return input_error(c, "genotypes/energy: NULL");
+    for (long long i = 0; i < (long long)n * c->prep.G; ++i)
+        if (!std::isfinite(genotypes[i])) return input_error(c, "genotypes[" + std::to_string(i) + "]: non-finite");
+    CK(cudaSetDevice(c->device));
+    const int G = c->prep.G, N = c->prep.N;
+    DevBuf dg, dE, dgr, dx;
+    CK(cudaMalloc(&dg.p, sizeof(float) * n * G));
+    CK(cudaMalloc(&dE.p, sizeof(float) * n));
+    if (grad) CK(cudaMalloc(&dgr.p, sizeof(float) * n * G));
+    if (xyz) CK(cudaMalloc(&dx.p, sizeof(float) * n * N * 3));
+    CK(cudaMemcpyAsync(dg.p, genotypes, sizeof(float) * n * G, cudaMemcpyHostToDevice, c->stream));
+    CK(dk::launch_eval(c->lig, c->grid, n, (const float *)dg.p, (float *)dE.p, (float *)dgr.p, (float *)dx.p,
+                       c->d_dfs2orig, c->stream));
+    c->launches += 1;
+    CK(cudaMemcpyAsync(energy, dE.p, sizeof(float) * n, cudaMemcpyDeviceToHost, c->stream));
+    if (grad) CK(cudaMemcpyAsync(grad, dgr.p, sizeof(float) * n * G, cudaMemcpyDeviceToHost, c->stream));
+    if (xyz) CK(cudaMemcpyAsync(xyz, dx.p, sizeof(float) * n * N * 3, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    return DOCK_OK;
+}
+
+int dock_topology(const dock_ligand *ligand, const dock_type_param *type_params, int32_t n_types, int32_t *n_tors,
+                  int32_t *axis, uint8_t *moved, int32_t *n_pairs, int32_t *pairs, int32_t pair_cap) {
+    dk::Prepared p;
+    std::string err;
+    if (dk::prepare_ligand(ligand, type_params, n_types, &p, &err) != DOCK_OK) { g_init_error = err; return DOCK_E_INPUT; }
+    if (n_tors) *n_tors = p.T;
+    if (n_pairs) *n_pairs = p.P;
+    for (int k = 0; k < p.T; ++k)
+        if (axis) { axis[2 * k] = p.tor_a[k]; axis[2 * k + 1] = p.tor_b[k]; }
+    if (moved) std::copy(p.moved.begin(), p.moved.end(), moved);
+    if (pairs) {
+        if (p.P > pair_cap) { g_init_error = "pair_cap: too small"; return DOCK_E_INPUT; }
+        std::copy(p.pairs.begin(), p.pairs.end(), pairs);
+    }
+    return DOCK_OK;
+}
+
+int dock_get_pairs(const dock_ctx *c, int32_t *pairs) {
+    if (!c || !pairs) return DOCK_E_INPUT;
+    std::copy(c->prep.pairs.begin(), c->prep.pairs.end(), pairs);
+    return DOCK_OK;
+}
+
+int dock_get_torsions(const dock_ctx *c, int32_t *axis, uint8_t *moved) {
+    if (!c) return DOCK_E_INPUT;
+    for (int k = 0; k < c->prep.T; ++k) {
+        if (axis) { axis[2 * k] = c->prep.tor_a[k]; axis[2 * k + 1] = c->prep.tor_b[k]; }
+    }
+    if (moved) std::copy(c->prep.moved.begin(), c->prep.moved.end(), moved);
+    return DOCK_OK;
+}
+
+int dock_philox(int32_t n, const uint32_t *ctr4, const uint32_t *key2, uint32_t *out4) {
+    if (n < 0 || (n > 0 && (!ctr4 || !key2 || !out4))) return DOCK_E_INPUT;
+    if (n == 0) return DOCK_OK;
+    dock_ctx tmp;
+    dock_ctx *c = &tmp;
+    DevBuf dc, dk_, dout;
+    CK(cudaMalloc(&dc.p, 16 * (size_t)n));
+    CK(cudaMalloc(&dk_.p, 8 * (size_t)n));
+    CK(cudaMalloc(&dout.p, 16 * (size_t)n));
+    CK(cudaMemcpy(dc.p, ctr4, 16 * (size_t)n, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(dk_.p, key2, 8 * (size_t)n, cudaMemcpyHostToDevice));
+    CK(dk::launch_philox(n, (const uint32_t *)dc.p, (const uint32_t *)dk_.p, (uint32_t *)dout.p, nullptr));
+    CK(cudaMemcpy(out4, dout.p, 16 * (size_t)n, cudaMemcpyDeviceToHost));
+    return DOCK_OK;
+}
+
+int dock_stream_words(uint64_t seed, uint32_t ligand_id, uint32_t purpose, uint32_t slot, uint32_t gen, uint32_t run,
+                      uint32_t m0, int32_t n, uint32_t *out) {
+    if (n < 0 || (n > 0 && !out) || purpose > 255 || slot >= (1u << 24)) return DOCK_E_INPUT;
+    if (n == 0) return DOCK_OK;
+    dock_ctx tmp;
+    dock_ctx *c = &tmp;
+    const uint64_t k = seed + (uint64_t)ligand_id * 0x9E3779B97F4A7C15ull;
+    DevBuf d;
+    CK(cudaMalloc(&d.p, 4 * (size_t)n));
+    CK(dk::launch_stream_words((uint32_t)k, (uint32_t)(k >> 32), purpose, slot, gen, run, m0, n, (uint32_t *)d.p, nullptr));
+    CK(cudaMemcpy(out, d.p, 4 * (size_t)n, cudaMemcpyDeviceToHost));
+    return DOCK_OK;
+}
+
+int dock_ga_step(dock_ctx *c, uint64_t seed, uint32_t ligand_id, int32_t run, int32_t gen, int32_t pop,
+                 const float *old_genes, const float *old_E, float *new_genes, float *new_E, int32_t *debug,
+                 int32_t *perm) {
+    if (!c) return DOCK_E_INPUT;
+    if (pop < 2 || pop > 4096) return input_error(c, "pop: must be in 2..4096");
+    if (gen < 1 || run < 0) return input_error(c, "gen >= 1 and run >= 0 required");
+    if (!old_genes || !old_E || !new_genes || !new_E) return input_error(c, "ga_step buffers: NULL");
+    CK(cudaSetDevice(c->device));
+    if (int rc = ensure_buffers(c, 1, pop)) return rc;
+    const int G = c->prep.G;
+    dk::SearchDev sp = make_search(c, pop, 1, run, ligand_id, LLONG_MAX, seed);
+    sp.max_generations = INT_MAX;
+    const dk::PopDev pd = pop_of(c);
+    const int cur = (gen - 1) & 1, nxt = gen & 1;
+    dk::RunState st{0, gen - 1, 0};
+    DevBuf ddbg;
+    CK(cudaMalloc(&ddbg.p, sizeof(int) * 8 * pop));
+    CK(cudaMemcpyAsync(c->d_genes + (size_t)cur * 1 * pop * G, old_genes, sizeof(float) * pop * G, cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemcpyAsync(c->d_E + (size_t)cur * pop, old_E, sizeof(float) * pop, cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemcpyAsync(c->d_state, &st, sizeof(st), cudaMemcpyHostToDevice, c->stream));
+    CK(dk::launch_ga(c->lig, c->grid, sp, pd, (int *)ddbg.p, c->stream));
+    c->launches += 1;
+    CK(cudaMemcpyAsync(new_genes, c->d_genes + (size_t)nxt * pop * G, sizeof(float) * pop * G, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaMemcpyAsync(new_E, c->d_E + (size_t)nxt * pop, sizeof(float) * pop, cudaMemcpyDeviceToHost, c->stream));
+    if (debug) CK(cudaMemcpyAsync(debug, ddbg.p, sizeof(int) * 8 * pop, cudaMemcpyDeviceToHost, c->stream));
+    if (perm) CK(cudaMemcpyAsync(perm, c->d_perm, sizeof(int) * pop, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    return DOCK_OK;
+}
+
+int dock_ls_step(dock_ctx *c, int32_t method, int32_t n, int32_t iters, uint64_t seed, uint32_t ligand_id,
+                 int32_t run, int32_t gen, const int32_t *slots, float *genes, float *energy, int64_t *evals) {
+    if (!c) return DOCK_E_INPUT;
+    if (method != DOCK_LS_ADADELTA && method != DOCK_LS_SOLIS_WETS) return input_error(c, "method: 0 or 1");
+    if (n < 0 || iters < 0) return input_error(c, "n, iters: must be >= 0");
+    if (n == 0) return DOCK_OK;
+    if (!slots || !genes || !energy) return input_error(c, "ls_step buffers: NULL");
+    CK(cudaSetDevice(c->device));
+    const int G = c->prep.G;
+    dk::SearchDev sp = make_search(c, 2, 1, run, ligand_id, LLONG_MAX, seed);
+    sp.ls_method = method;
+    DevBuf dg, dE, dev, dsl;
+    CK(cudaMalloc(&dg.p, sizeof(float) * n * G));
+    CK(cudaMalloc(&dE.p, sizeof(float) * n));
+    CK(cudaMalloc(&dev.p, sizeof(int) * n));
+    CK(cudaMalloc(&dsl.p, sizeof(int) * n));
+    CK(cudaMemcpyAsync(dg.p, genes, sizeof(float) * n * G, cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemcpyAsync(dE.p, energy, sizeof(float) * n, cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemcpyAsync(dsl.p, slots, sizeof(int) * n, cudaMemcpyHostToDevice, c->stream));
+    dk::LsArgs la{};
+    la.use_state = 0; la.n_per_run = n; la.iters = iters;
+    la.genes = (float *)dg.p; la.E = (float *)dE.p; la.evals = (int *)dev.p; la.rng_slot = (const int *)dsl.p;
+    la.gen = gen; la.run = run;
+    CK(dk::launch_ls(c->lig, c->grid, sp, pop_of(c), la, n, c->stream));
+    c->launches += 1;
+    std::vector<int> ev(n);
+    CK(cudaMemcpyAsync(genes, dg.p, sizeof(float) * n * G, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaMemcpyAsync(energy, dE.p, sizeof(float) * n, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaMemcpyAsync(ev.data(), dev.p, sizeof(int) * n, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    if (evals) for (int i = 0; i < n; ++i) evals[i] = ev[i];
+    return DOCK_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,75 @@
+// dock_internal.h — device-side data layout shared by the host engine and the kernels.
+//
+// Per-ligand constant block ("cData", PAPER.md:92 [§IV-A]: "the structure cData is
+// accessed to obtain the required information for each member of a population"):
+// one contiguous device buffer, staged into shared memory by every CTA.  Atoms are
+// renumbered in DFS preorder from the root fragment so that every torsion's moved
+// set is one contiguous atom range (D1).
+#pragma once
+#include <stdint.h>
+#include <vector_functions.h>
+#include <vector_types.h>
+
+namespace dk {
+
+constexpr int kMaxAtoms = 256;
+constexpr int kMaxTors = 32;
+constexpr int kMaxGenes = 6 + kMaxTors;
+
+enum Purpose : uint32_t { kInit = 0, kGA = 1, kLsPick = 2, kSW = 3 };   // D2 counter purposes
+
+struct LigDev {
+    int N, T, G, P;
+    int n_levels;                 // number of torsion depth levels
+    int lvl_start[kMaxTors + 1];  // torsions of level l: [lvl_start[l], lvl_start[l+1])
+    int blob_bytes;               // multiple of 16
+    // byte offsets inside the blob (all 16-byte aligned)
+    int off_lvl;      // int[kMaxTors+1] copy of lvl_start (read from shared memory)
+    int off_p;        // float4[N]  body coordinates p = X - c (x,y,z), charge q in .w
+    int off_par;      // float4[N]  R/2, sqrt(eps), S, V
+    int off_meta;     // int[N]     type | role << 8 | (deep + 1) << 16
+    int off_tA;       // float4[T]  torsion axis origin A = p[a_k]
+    int off_tU;       // float4[T]  unit axis u = (p[b_k] - p[a_k]) / |.|
+    int off_tmeta;    // int4[T]    parent torsion (-1 root), a (dfs), b (dfs), lo | hi << 16
+    int off_pairs;    // uint32[P]  i | j << 8 | hb << 16   (dfs indices, i < j)
+    int off_csr_off;  // int[N+1]   per-atom incidence offsets into csr_nbr
+    int off_csr_nbr;  // uint16[2P] j | hb << 8
+    const uint8_t *blob;          // device pointer
+};
+
+struct GridDev {
+    const float4 *maps;           // [n_types][nz][ny][nx] = {M_type, M_E, M_D, 0}
+    int nx, ny, nz, n_types;
+    float ox, oy, oz;             // origin
+    float s, inv_s;               // spacing and its reciprocal
+    float hx, hy, hz;             // upper box faces o + (n-1) s
+};
+
+struct RunState {                 // per run, device resident
+    long long evals;              // D11 sum_evals
+    int gen;                      // generations completed
+    int pad;
+};
+
+struct SearchDev {
+    float p_tour, p_cross, p_mut, mut_trans, mut_angle;
+    int ls_method, ls_iters, n_ls;
+    float sw_rho, sw_rho_min, sw_expand, sw_contract;
+    int sw_cons_succ, sw_cons_fail;
+    float ad_rho, ad_eps;
+    int max_generations;
+    long long max_evals;
+    int pop, runs, run_base;
+    uint32_t key0, key1;          // Philox key from (seed, ligand_id) (D2)
+};
+
+// Population buffers (double-buffered by generation parity).
+struct PopDev {
+    float *genes;                 // [2][runs][pop][G]
+    float *E;                     // [2][runs][pop]
+    RunState *state;              // [runs]
+    int *perm;                    // [runs][pop] LS pick order
+    int *ls_evals;                // [runs][pop] per-LS evaluation counts
+};
+
+}  // namespace dk

@@ -1,0 +1,657 @@
+// kernels.cu — sm_100a kernels of the LGA docking hot path.
+//
+//   k_init        a2   population init from Philox INIT words + energy (D8 gen 0)
+//   k_ga          a9   elitism, tournaments, two-point crossover, mutation, offspring
+//                      energy (D8); slot-0 group also draws the LS sample (a10)
+//   k_ls_adadelta a7   fused persistent ADADELTA local search, energy + gradient every
+//                      iteration, best tracking, Lamarckian writeback (D10)
+//   k_ls_sw       a8   Solis-Wets; for small ligands both trial points x+b+d and x-b-d
+//                      are scored at once by the two half-warps (speculative; the eval
+//                      count still follows D9's sequential definition)
+//   k_gen_end     a10  sum_evals (int64 warp reduction) + generation counter
+//   k_best        a10  best-of-run argmin (lowest index on ties)
+//   k_eval             parity hook / pose output: batched energy (+gradient, +pose)
+//   k_philox, k_stream_words   parity hooks for D2
+//
+// Every kernel stages the per-ligand block ("cData") into shared memory; one lane
+// group (16 or 32 lanes) handles one individual ("each local optimization occurs
+// independently"; NS "one CTA or warp-group handles each individual").
+#include <math.h>
+
+#include "kernels.cuh"
+#include "philox.cuh"
+#include "score.cuh"
+
+namespace dk {
+
+static inline __host__ __device__ int a16(int x) { return (x + 15) & ~15; }
+
+ScratchLayout scratch_layout(int N, int T, int G, bool grad, int extra) {
+    ScratchLayout s;
+    int o = 0;
+    s.off_r = o; o += a16(16 * N);
+    s.off_W = o; o += a16(48 * (T > 0 ? T : 1));
+    s.off_ts = o; if (grad) o += a16(32 * N);
+    s.off_genes = o; o += a16(4 * G);
+    s.off_grad = o; if (grad) o += a16(4 * G);
+    s.off_extra = o; o += a16(extra);
+    s.bytes = o;
+    return s;
+}
+
+GroupCfg pick_group(int N) {
+    GroupCfg c;
+    if (N <= 16) { c.W = 16; c.MAXC = 1; return c; }
+    c.W = 32;
+    c.MAXC = N <= 32 ? 1 : (N <= 64 ? 2 : (N <= 96 ? 3 : (N <= 128 ? 4 : 8)));
+    return c;
+}
+
+__device__ __forceinline__ LigSm stage_ligand(const LigDev &L, uint8_t *sm) {
+    const uint4 *src = reinterpret_cast<const uint4 *>(L.blob);
+    uint4 *dst = reinterpret_cast<uint4 *>(sm);
+    for (int i = threadIdx.x; i < L.blob_bytes / 16; i += blockDim.x) dst[i] = src[i];
+    __syncthreads();
+    LigSm v;
+    v.N = L.N; v.T = L.T; v.G = L.G; v.P = L.P; v.n_levels = L.n_levels;
+    v.lvl = reinterpret_cast<const int *>(sm + L.off_lvl);
+    v.p = reinterpret_cast<const float4 *>(sm + L.off_p);
+    v.par = reinterpret_cast<const float4 *>(sm + L.off_par);
+    v.meta = reinterpret_cast<const int *>(sm + L.off_meta);
+    v.tA = reinterpret_cast<const float4 *>(sm + L.off_tA);
+    v.tU = reinterpret_cast<const float4 *>(sm + L.off_tU);
+    v.tmeta = reinterpret_cast<const int4 *>(sm + L.off_tmeta);
+    v.pairs = reinterpret_cast<const uint32_t *>(sm + L.off_pairs);
+    v.csr_off = reinterpret_cast<const int *>(sm + L.off_csr_off);
+    v.csr_nbr = reinterpret_cast<const uint16_t *>(sm + L.off_csr_nbr);
+    return v;
+}
+
+__device__ __forceinline__ Scratch scratch_at(uint8_t *base, const ScratchLayout &SL) {
+    Scratch s;
+    s.r = reinterpret_cast<float4 *>(base + SL.off_r);
+    s.W = reinterpret_cast<float4 *>(base + SL.off_W);
+    s.ts = reinterpret_cast<float4 *>(base + SL.off_ts);
+    s.genes = reinterpret_cast<float *>(base + SL.off_genes);
+    s.grad = reinterpret_cast<float *>(base + SL.off_grad);
+    return s;
+}
+
+__device__ __forceinline__ bool run_active(const RunState &st, const SearchDev &sp) {
+    return st.evals < sp.max_evals && st.gen < sp.max_generations;   // D8.5, checked per generation
+}
+
+__device__ __forceinline__ float nan_inf(float v) { return isnan(v) ? INFINITY : v; }
+
+// ---------------------------------------------------------------------------
+// k_eval: batched energy (+ gradient, + pose) of given genotypes.
+// ---------------------------------------------------------------------------
+template <int W, int MAXC, bool GRAD>
+__global__ void __launch_bounds__(256) k_eval(const LigDev L, const GridDev g, const ScratchLayout SL,
+                                              int n, const float *__restrict__ genes, float *E,
+                                              float *grad, float *xyz, const int *__restrict__ dfs2orig) {
+    extern __shared__ uint4 smem_u4[];
+    uint8_t *sm = reinterpret_cast<uint8_t *>(smem_u4);
+    const LigSm Ls = stage_ligand(L, sm);
+    const int gl = threadIdx.x / W, sub = threadIdx.x % W;
+    const int gi = blockIdx.x * (blockDim.x / W) + gl;
+    if (gi >= n) return;
+    const Scratch S = scratch_at(sm + L.blob_bytes + gl * SL.bytes, SL);
+    const unsigned mask = group_mask<W>();
+    const int G = L.G;
+    for (int j = sub; j < G; j += W) S.genes[j] = genes[(size_t)gi * G + j];
+    __syncwarp(mask);
+    const float e = eval_group<W, MAXC, GRAD>(Ls, g, S, sub, mask);
+    if (sub == 0) E[gi] = e;
+    if (GRAD && grad)
+        for (int j = sub; j < G; j += W) grad[(size_t)gi * G + j] = S.grad[j];
+    if (xyz) {
+        for (int a = sub; a < L.N; a += W) {
+            const float4 r = S.r[a];
+            float *o = xyz + ((size_t)gi * L.N + dfs2orig[a]) * 3;
+            o[0] = r.x; o[1] = r.y; o[2] = r.z;
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// k_init: generation 0 (D8): t uniform in the box, angles 2*pi*u01; evaluate.
+// ---------------------------------------------------------------------------
+template <int W, int MAXC>
+__global__ void __launch_bounds__(256) k_init(const LigDev L, const GridDev g, const ScratchLayout SL,
+                                              const SearchDev sp, const PopDev pop) {
+    extern __shared__ uint4 smem_u4[];
+    uint8_t *sm = reinterpret_cast<uint8_t *>(smem_u4);
+    const LigSm Ls = stage_ligand(L, sm);
+    const int gl = threadIdx.x / W, sub = threadIdx.x % W;
+    const int gi = blockIdx.x * (blockDim.x / W) + gl;
+    if (gi >= sp.runs * sp.pop) return;
+    const int r = gi / sp.pop, k = gi % sp.pop, G = L.G;
+    const Scratch S = scratch_at(sm + L.blob_bytes + gl * SL.bytes, SL);
+    const unsigned mask = group_mask<W>();
+    const uint2 key = make_uint2(sp.key0, sp.key1);
+    const uint32_t run_g = (uint32_t)(sp.run_base + r);
+    float *row = pop.genes + ((size_t)r * sp.pop + k) * G;          // buffer 0 (generation 0)
+    for (int j = sub; j < G; j += W) {
+        const float u = u01(stream_word(key, kInit, (uint32_t)k, 0u, run_g, (uint32_t)j));
+        float v;
+        if (j == 0) v = g.ox + u * (g.hx - g.ox);
+        else if (j == 1) v = g.oy + u * (g.hy - g.oy);
+        else if (j == 2) v = g.oz + u * (g.hz - g.oz);
+        else v = 6.28318530717958647692f * u;
+        S.genes[j] = v;
+        row[j] = v;
+    }
+    __syncwarp(mask);
+    const float e = eval_group<W, MAXC, false>(Ls, g, S, sub, mask);
+    if (sub == 0) {
+        pop.E[(size_t)r * sp.pop + k] = e;
+        if (k == 0) { pop.state[r].evals = sp.pop; pop.state[r].gen = 0; }
+    }
+}
+
+// D8 tournament between two distinct candidates (ties -> lower index, NaN = +inf).
+__device__ __forceinline__ int tournament(const float *E, int pop, uint32_t wa, uint32_t wb, uint32_t wc,
+                                          float p_tour) {
+    const int i = (int)below(wa, (uint32_t)pop);
+    int j = (int)below(wb, (uint32_t)(pop - 1));
+    if (j >= i) j += 1;
+    const float ei = nan_inf(E[i]), ej = nan_inf(E[j]);
+    const int better = (ei < ej || (ei == ej && i < j)) ? i : j;
+    const int other = better == i ? j : i;
+    return u01(wc) < p_tour ? better : other;
+}
+
+// ---------------------------------------------------------------------------
+// k_ga: one generation of the GA for every (run, slot) (D8).
+// ---------------------------------------------------------------------------
+template <int W, int MAXC>
+__global__ void __launch_bounds__(256) k_ga(const LigDev L, const GridDev g, const ScratchLayout SL,
+                                            const SearchDev sp, const PopDev pop, int *dbg) {
+    extern __shared__ uint4 smem_u4[];
+    uint8_t *sm = reinterpret_cast<uint8_t *>(smem_u4);
+    const int gl = threadIdx.x / W, sub = threadIdx.x % W;
+    const int gi = blockIdx.x * (blockDim.x / W) + gl;
+    const int P = sp.pop, G = L.G;
+    bool act = false;
+    RunState st;
+    const int r = gi / P;
+    if (gi < sp.runs * P) { st = pop.state[r]; act = run_active(st, sp); }
+    if (!__syncthreads_or(act)) return;            // finished runs cost one state read
+    const LigSm Ls = stage_ligand(L, sm);
+    if (!act) return;
+    const int k = gi % P;
+    const uint32_t gen = (uint32_t)st.gen + 1u;
+    const int cur = st.gen & 1, nxt = gen & 1;
+    const float *oldG = pop.genes + ((size_t)cur * sp.runs + r) * P * G;
+    const float *oldE = pop.E + ((size_t)cur * sp.runs + r) * P;
+    float *newG = pop.genes + ((size_t)nxt * sp.runs + r) * P * G;
+    float *newE = pop.E + ((size_t)nxt * sp.runs + r) * P;
+    const Scratch S = scratch_at(sm + L.blob_bytes + gl * SL.bytes, SL);
+    const unsigned mask = group_mask<W>();
+    const uint2 key = make_uint2(sp.key0, sp.key1);
+    const uint32_t run_g = (uint32_t)(sp.run_base + r);
+
+    if (k == 0) {
+        // elitism: argmin, NaN = +inf, ties -> lowest index; copied without re-evaluation
+        float bv = INFINITY;
+        int bi = 0x7fffffff;
+        for (int i = sub; i < P; i += W) {
+            const float v = nan_inf(oldE[i]);
+            if (v < bv || (v == bv && i < bi)) { bv = v; bi = i; }
+        }
+#pragma unroll
+        for (int m = W / 2; m >= 1; m >>= 1) {
+            const float ov = __shfl_xor_sync(mask, bv, m, W);
+            const int oi = __shfl_xor_sync(mask, bi, m, W);
+            if (ov < bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; }
+        }
+        for (int j = sub; j < G; j += W) newG[j] = oldG[(size_t)bi * G + j];
+        if (sub == 0) newE[0] = oldE[bi];
+        // local-search sample: partial Fisher-Yates over the new population (D8.3)
+        int *perm = reinterpret_cast<int *>(sm + L.blob_bytes + gl * SL.bytes + SL.off_extra);
+        for (int i = sub; i < P; i += W) perm[i] = i;
+        __syncwarp(mask);
+        if (sub == 0) {
+            uint4 blk = make_uint4(0, 0, 0, 0);
+            for (int s = 0; s < sp.n_ls; ++s) {
+                if ((s & 3) == 0) blk = stream_block(key, kLsPick, 0u, gen, run_g, (uint32_t)(s >> 2));
+                const int j = s + (int)below(lane_of(blk, s & 3), (uint32_t)(P - s));
+                const int t = perm[s]; perm[s] = perm[j]; perm[j] = t;
+            }
+        }
+        __syncwarp(mask);
+        for (int s = sub; s < P; s += W) pop.perm[(size_t)r * P + s] = perm[s];
+        if (dbg && sub == 0) {
+            int *d = dbg + (size_t)gi * 8;
+            d[0] = bi; d[1] = bi; d[2] = 0; d[3] = 0; d[4] = 0; d[5] = 0; d[6] = 0; d[7] = bi;
+        }
+        return;
+    }
+    // slot k >= 1: words 0..8 from the first three Philox blocks
+    const uint4 b0 = stream_block(key, kGA, (uint32_t)k, gen, run_g, 0u);
+    const uint4 b1 = stream_block(key, kGA, (uint32_t)k, gen, run_g, 1u);
+    const uint4 b2 = stream_block(key, kGA, (uint32_t)k, gen, run_g, 2u);
+    const int A = tournament(oldE, P, b0.x, b0.y, b0.z, sp.p_tour);
+    const int B = tournament(oldE, P, b0.w, b1.x, b1.y, sp.p_tour);
+    const bool cross = u01(b1.z) < sp.p_cross;
+    int c1 = 0, c2 = 0;
+    if (cross) {
+        c1 = (int)below(b1.w, (uint32_t)(G + 1));
+        c2 = (int)below(b2.x, (uint32_t)(G + 1));
+        if (c2 < c1) { const int t = c1; c1 = c2; c2 = t; }
+    }
+    unsigned long long mbits = 0ull;
+    for (int j = sub; j < G; j += W) {
+        const uint32_t m = 9u + 2u * (uint32_t)j;                 // mutation coin; delta = m + 1
+        const uint4 bc = stream_block(key, kGA, (uint32_t)k, gen, run_g, m >> 2);
+        const uint32_t wc = lane_of(bc, m & 3);
+        const uint32_t md = m + 1u;
+        const uint32_t wd = ((md >> 2) == (m >> 2)) ? lane_of(bc, md & 3)
+                                                    : lane_of(stream_block(key, kGA, (uint32_t)k, gen, run_g, md >> 2), md & 3);
+        float v = (cross && c1 <= j && j < c2) ? oldG[(size_t)B * G + j] : oldG[(size_t)A * G + j];
+        if (u01(wc) < sp.p_mut) {
+            const float mag = j < 3 ? sp.mut_trans : sp.mut_angle;
+            v += (2.0f * u01(wd) - 1.0f) * mag;
+            mbits |= 1ull << j;
+        }
+        S.genes[j] = v;
+    }
+    __syncwarp(mask);
+    const float e = eval_group<W, MAXC, false>(Ls, g, S, sub, mask);
+    for (int j = sub; j < G; j += W) newG[(size_t)k * G + j] = S.genes[j];
+    if (sub == 0) newE[k] = e;
+    if (dbg) {
+#pragma unroll
+        for (int m = W / 2; m >= 1; m >>= 1) mbits |= __shfl_xor_sync(mask, mbits, m, W);
+        if (sub == 0) {
+            int *d = dbg + (size_t)gi * 8;
+            d[0] = A; d[1] = B; d[2] = cross ? 1 : 0; d[3] = c1; d[4] = c2;
+            d[5] = (int)(uint32_t)mbits; d[6] = (int)(uint32_t)(mbits >> 32); d[7] = -1;
+        }
+    }
+}
+
+// Resolve the row a local-search group works on (engine or hook mode).
+struct LsTarget {
+    bool act;
+    float *row;
+    float *E;
+    int *evals;
+    uint32_t slot, gen, run_g;
+};
+
+__device__ __forceinline__ LsTarget ls_target(const SearchDev &sp, const PopDev &pop, const LsArgs &a, int gi,
+                                              int G) {
+    LsTarget t;
+    t.act = false;
+    if (a.use_state) {
+        if (gi >= sp.runs * a.n_per_run) return t;
+        const int r = gi / a.n_per_run, s = gi % a.n_per_run;
+        const RunState st = pop.state[r];
+        if (!run_active(st, sp)) return t;
+        const int gen = st.gen + 1, nxt = gen & 1;
+        const int i = pop.perm[(size_t)r * sp.pop + s];
+        t.row = pop.genes + (((size_t)nxt * sp.runs + r) * sp.pop + i) * G;
+        t.E = pop.E + ((size_t)nxt * sp.runs + r) * sp.pop + i;
+        t.evals = pop.ls_evals + (size_t)r * sp.pop + s;
+        t.slot = (uint32_t)i; t.gen = (uint32_t)gen; t.run_g = (uint32_t)(sp.run_base + r);
+        t.act = true;
+    } else {
+        if (gi >= a.n_per_run) return t;
+        t.row = a.genes + (size_t)gi * G;
+        t.E = a.E + gi;
+        t.evals = a.evals + gi;
+        t.slot = (uint32_t)a.rng_slot[gi]; t.gen = (uint32_t)a.gen; t.run_g = (uint32_t)a.run;
+        t.act = true;
+    }
+    return t;
+}
+
+// ---------------------------------------------------------------------------
+// k_ls_adadelta: max_iters x (energy + gradient, ADADELTA step), best tracking (D10).
+// ---------------------------------------------------------------------------
+template <int W, int MAXC>
+__global__ void __launch_bounds__(256) k_ls_adadelta(const LigDev L, const GridDev g, const ScratchLayout SL,
+                                                     const SearchDev sp, const PopDev pop, const LsArgs a) {
+    extern __shared__ uint4 smem_u4[];
+    uint8_t *sm = reinterpret_cast<uint8_t *>(smem_u4);
+    const int gl = threadIdx.x / W, sub = threadIdx.x % W;
+    const int gi = blockIdx.x * (blockDim.x / W) + gl;
+    const int G = L.G;
+    const LsTarget t = ls_target(sp, pop, a, gi, G);
+    if (!__syncthreads_or(t.act)) return;
+    const LigSm Ls = stage_ligand(L, sm);
+    if (!t.act) return;
+    const Scratch S = scratch_at(sm + L.blob_bytes + gl * SL.bytes, SL);
+    const unsigned mask = group_mask<W>();
+    constexpr int NSET = (kMaxGenes + W - 1) / W;
+    float x[NSET], sg[NSET], sd[NSET], bx[NSET];
+#pragma unroll
+    for (int s = 0; s < NSET; ++s) {
+        const int j = sub + W * s;
+        x[s] = j < G ? t.row[j] : 0.0f;
+        bx[s] = x[s]; sg[s] = 0.0f; sd[s] = 0.0f;
+        if (j < G) S.genes[j] = x[s];
+    }
+    float Ebest = *t.E;
+    const float rho = sp.ad_rho, eps = sp.ad_eps;
+    __syncwarp(mask);
+    for (int it = 0; it < a.iters; ++it) {
+        const float E = eval_group<W, MAXC, true>(Ls, g, S, sub, mask);
+        if (E < Ebest) {
+            Ebest = E;
+#pragma unroll
+            for (int s = 0; s < NSET; ++s) bx[s] = x[s];
+        }
+#pragma unroll
+        for (int s = 0; s < NSET; ++s) {
+            const int j = sub + W * s;
+            if (j < G) {
+                const float gj = S.grad[j];
+                sg[s] = rho * sg[s] + (1.0f - rho) * gj * gj;
+                const float dx = -sqrtf(sd[s] + eps) * rsqrtf(sg[s] + eps) * gj;
+                sd[s] = rho * sd[s] + (1.0f - rho) * dx * dx;
+                x[s] += dx;
+                S.genes[j] = x[s];
+            }
+        }
+        __syncwarp(mask);
+    }
+#pragma unroll
+    for (int s = 0; s < NSET; ++s) {
+        const int j = sub + W * s;
+        if (j < G) t.row[j] = bx[s];
+    }
+    if (sub == 0) { *t.E = Ebest; *t.evals = a.iters; }
+}
+
+// ---------------------------------------------------------------------------
+// k_ls_sw: Solis-Wets (D9; P:64 citing Solis & Wets 1981).  One warp per individual.
+// W <= 16: the two half-warps score x+b+d and x-b-d concurrently.
+// ---------------------------------------------------------------------------
+template <int W, int MAXC>
+__global__ void __launch_bounds__(256) k_ls_sw(const LigDev L, const GridDev g, const ScratchLayout SL,
+                                               const SearchDev sp, const PopDev pop, const LsArgs a) {
+    constexpr int NG = (W <= 16) ? 2 : 1;
+    extern __shared__ uint4 smem_u4[];
+    uint8_t *sm = reinterpret_cast<uint8_t *>(smem_u4);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int grp = lane / W, sub = lane % W;
+    const int wi = blockIdx.x * (blockDim.x >> 5) + warp;
+    const int G = L.G;
+    const LsTarget t = ls_target(sp, pop, a, wi, G);
+    if (!__syncthreads_or(t.act)) return;
+    const LigSm Ls = stage_ligand(L, sm);
+    if (!t.act) return;
+    uint8_t *wbase = sm + L.blob_bytes + (size_t)warp * NG * SL.bytes;
+    const Scratch S0 = scratch_at(wbase, SL);
+    const Scratch S1 = scratch_at(wbase + (NG - 1) * SL.bytes, SL);
+    const Scratch Sg = grp == 0 ? S0 : S1;
+    const unsigned gmask = group_mask<W>();
+    const uint2 key = make_uint2(sp.key0, sp.key1);
+    constexpr int NSET = (kMaxGenes + 31) / 32;
+    float x[NSET], b[NSET], d[NSET], c1[NSET], c2[NSET];
+#pragma unroll
+    for (int s = 0; s < NSET; ++s) {
+        const int j = lane + 32 * s;
+        x[s] = j < G ? t.row[j] : 0.0f;
+        b[s] = 0.0f; d[s] = 0.0f; c1[s] = 0.0f; c2[s] = 0.0f;
+    }
+    float Ex = *t.E;
+    float rho = sp.sw_rho;
+    int succ = 0, fail = 0, ne = 0;
+    for (int it = 0; it < a.iters; ++it) {
+        if (rho < sp.sw_rho_min) break;
+#pragma unroll
+        for (int s = 0; s < NSET; ++s) {
+            const int j = lane + 32 * s;
+            if (j < G) {
+                const uint32_t m = 2u * (uint32_t)G * (uint32_t)it + 2u * (uint32_t)j;   // m even: m, m+1 share a block
+                const uint4 blk = stream_block(key, kSW, t.slot, t.gen, t.run_g, m >> 2);
+                const uint32_t w1 = lane_of(blk, m & 3), w2 = lane_of(blk, (m + 1) & 3);
+                d[s] = rho * ((u01(w1) - 0.5f) + (u01(w2) - 0.5f));   // exact: triangular on (-rho, rho)
+                c1[s] = x[s] + b[s] + d[s];
+                c2[s] = x[s] - b[s] - d[s];
+                S0.genes[j] = c1[s];
+                if (NG == 2) S1.genes[j] = c2[s];
+            }
+        }
+        __syncwarp();
+        float E1, E2 = 0.0f;
+        if (NG == 2) {
+            const float e = eval_group<W, MAXC, false>(Ls, g, Sg, sub, gmask);
+            E1 = __shfl_sync(0xffffffffu, e, 0);
+            E2 = __shfl_sync(0xffffffffu, e, W);
+        } else {
+            E1 = eval_group<W, MAXC, false>(Ls, g, S0, sub, gmask);
+        }
+        ++ne;
+        if (E1 < Ex) {
+#pragma unroll
+            for (int s = 0; s < NSET; ++s) { x[s] = c1[s]; b[s] = 0.2f * b[s] + 0.4f * d[s]; }
+            Ex = E1; ++succ; fail = 0;
+        } else {
+            if (NG == 1) {
+                __syncwarp();
+#pragma unroll
+                for (int s = 0; s < NSET; ++s) {
+                    const int j = lane + 32 * s;
+                    if (j < G) S0.genes[j] = c2[s];
+                }
+                __syncwarp();
+                E2 = eval_group<W, MAXC, false>(Ls, g, S0, sub, gmask);
+            }
+            ++ne;
+            if (E2 < Ex) {
+#pragma unroll
+                for (int s = 0; s < NSET; ++s) { x[s] = c2[s]; b[s] = b[s] - 0.4f * d[s]; }
+                Ex = E2; ++succ; fail = 0;
+            } else {
+#pragma unroll
+                for (int s = 0; s < NSET; ++s) b[s] = 0.5f * b[s];
+                ++fail; succ = 0;
+            }
+        }
+        if (succ >= sp.sw_cons_succ) { rho *= sp.sw_expand; succ = 0; }
+        if (fail >= sp.sw_cons_fail) { rho *= sp.sw_contract; fail = 0; }
+        __syncwarp();
+    }
+#pragma unroll
+    for (int s = 0; s < NSET; ++s) {
+        const int j = lane + 32 * s;
+        if (j < G) t.row[j] = x[s];
+    }
+    if (lane == 0) { *t.E = Ex; *t.evals = ne; }
+}
+
+// ---------------------------------------------------------------------------
+// k_gen_end: sum_evals (Listing 1: per-run reduction over the population's
+// evaluation counters with warp shuffles) and the generation counter.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_gen_end(const SearchDev sp, const PopDev pop) {
+    const int lane = threadIdx.x & 31;
+    const int r = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (r >= sp.runs) return;
+    const RunState st = pop.state[r];
+    if (!run_active(st, sp)) return;
+    long long s = 0;
+    for (int i = lane; i < sp.n_ls; i += 32) s += pop.ls_evals[(size_t)r * sp.pop + i];
+    s = gsum_ll<32>(s, 0xffffffffu);
+    if (lane == 0) {
+        pop.state[r].evals = st.evals + (long long)(sp.pop - 1) + s;   // offspring + local search
+        pop.state[r].gen = st.gen + 1;
+    }
+}
+
+// k_best: best of each run's final population (argmin, lowest index on ties).
+__global__ void __launch_bounds__(256) k_best(const int G, const SearchDev sp, const PopDev pop, float *bestE,
+                                              float *bestG, long long *evals, int *gens) {
+    const int lane = threadIdx.x & 31;
+    const int r = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (r >= sp.runs) return;
+    const RunState st = pop.state[r];
+    const int buf = st.gen & 1;
+    const float *E = pop.E + ((size_t)buf * sp.runs + r) * sp.pop;
+    float bv = INFINITY;
+    int bi = 0x7fffffff;
+    for (int i = lane; i < sp.pop; i += 32) {
+        const float v = nan_inf(E[i]);
+        if (v < bv || (v == bv && i < bi)) { bv = v; bi = i; }
+    }
+#pragma unroll
+    for (int m = 16; m >= 1; m >>= 1) {
+        const float ov = __shfl_xor_sync(0xffffffffu, bv, m);
+        const int oi = __shfl_xor_sync(0xffffffffu, bi, m);
+        if (ov < bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; }
+    }
+    const float *row = pop.genes + (((size_t)buf * sp.runs + r) * sp.pop + bi) * G;
+    for (int j = lane; j < G; j += 32) bestG[(size_t)r * G + j] = row[j];
+    if (lane == 0) {
+        bestE[r] = E[bi];
+        if (evals) evals[r] = st.evals;
+        if (gens) gens[r] = st.gen;
+    }
+}
+
+__global__ void k_philox(int n, const uint4 *ctr, const uint2 *key, uint4 *out) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) out[i] = philox4x32_10(ctr[i], key[i]);
+}
+
+__global__ void k_stream_words(uint2 key, uint32_t purpose, uint32_t slot, uint32_t gen, uint32_t run,
+                               uint32_t m0, int n, uint32_t *out) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) out[i] = stream_word(key, purpose, slot, gen, run, m0 + (uint32_t)i);
+}
+
+// ---------------------------------------------------------------------------
+// Launchers
+// ---------------------------------------------------------------------------
+#define DK_DISPATCH(cfg, ...)                                                \
+    do {                                                                     \
+        if ((cfg).W == 16) { constexpr int W = 16, MAXC = 1; __VA_ARGS__; }  \
+        else switch ((cfg).MAXC) {                                           \
+            case 1: { constexpr int W = 32, MAXC = 1; __VA_ARGS__; } break;  \
+            case 2: { constexpr int W = 32, MAXC = 2; __VA_ARGS__; } break;  \
+            case 3: { constexpr int W = 32, MAXC = 3; __VA_ARGS__; } break;  \
+            case 4: { constexpr int W = 32, MAXC = 4; __VA_ARGS__; } break;  \
+            default: { constexpr int W = 32, MAXC = 8; __VA_ARGS__; } break; \
+        }                                                                    \
+    } while (0)
+
+static constexpr int kThreads = 256;
+static constexpr int kSmemMax = 227 * 1024;
+
+template <typename K>
+static cudaError_t allow_smem(K kernel) {
+    return cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemMax);
+}
+
+cudaError_t setup_kernel_attributes() {
+    cudaError_t e = cudaSuccess;
+#define DK_ATTR(W, MAXC)                                                             \
+    if (e == cudaSuccess) e = allow_smem(k_eval<W, MAXC, false>);                    \
+    if (e == cudaSuccess) e = allow_smem(k_eval<W, MAXC, true>);                     \
+    if (e == cudaSuccess) e = allow_smem(k_init<W, MAXC>);                           \
+    if (e == cudaSuccess) e = allow_smem(k_ga<W, MAXC>);                             \
+    if (e == cudaSuccess) e = allow_smem(k_ls_adadelta<W, MAXC>);                    \
+    if (e == cudaSuccess) e = allow_smem(k_ls_sw<W, MAXC>);
+    DK_ATTR(16, 1) DK_ATTR(32, 1) DK_ATTR(32, 2) DK_ATTR(32, 3) DK_ATTR(32, 4) DK_ATTR(32, 8)
+#undef DK_ATTR
+    return e;
+}
+
+static inline int ceil_div(long long a, long long b) { return (int)((a + b - 1) / b); }
+
+cudaError_t launch_eval(const LigDev &L, const GridDev &g, int n, const float *genes, float *E, float *grad,
+                        float *xyz, const int *dfs2orig, cudaStream_t s) {
+    if (n <= 0) return cudaSuccess;
+    const GroupCfg cfg = pick_group(L.N);
+    const bool want_grad = grad != nullptr;
+    const ScratchLayout SL = scratch_layout(L.N, L.T, L.G, want_grad, 0);
+    const int groups = kThreads / cfg.W;
+    const size_t smem = (size_t)L.blob_bytes + (size_t)groups * SL.bytes;
+    if (smem > (size_t)kSmemMax) return cudaErrorInvalidConfiguration;
+    const int blocks = ceil_div(n, groups);
+    DK_DISPATCH(cfg, {
+        if (want_grad) k_eval<W, MAXC, true><<<blocks, kThreads, smem, s>>>(L, g, SL, n, genes, E, grad, xyz, dfs2orig);
+        else k_eval<W, MAXC, false><<<blocks, kThreads, smem, s>>>(L, g, SL, n, genes, E, grad, xyz, dfs2orig);
+    });
+    return cudaGetLastError();
+}
+
+cudaError_t launch_init(const LigDev &L, const GridDev &g, const SearchDev &sp, const PopDev &pop, cudaStream_t s) {
+    const GroupCfg cfg = pick_group(L.N);
+    const ScratchLayout SL = scratch_layout(L.N, L.T, L.G, false, 0);
+    const int groups = kThreads / cfg.W;
+    const size_t smem = (size_t)L.blob_bytes + (size_t)groups * SL.bytes;
+    if (smem > (size_t)kSmemMax) return cudaErrorInvalidConfiguration;
+    const int blocks = ceil_div((long long)sp.runs * sp.pop, groups);
+    DK_DISPATCH(cfg, { k_init<W, MAXC><<<blocks, kThreads, smem, s>>>(L, g, SL, sp, pop); });
+    return cudaGetLastError();
+}
+
+cudaError_t launch_ga(const LigDev &L, const GridDev &g, const SearchDev &sp, const PopDev &pop, int *dbg,
+                      cudaStream_t s) {
+    const GroupCfg cfg = pick_group(L.N);
+    const ScratchLayout SL = scratch_layout(L.N, L.T, L.G, false, 4 * sp.pop);
+    const int groups = kThreads / cfg.W;
+    const size_t smem = (size_t)L.blob_bytes + (size_t)groups * SL.bytes;
+    if (smem > (size_t)kSmemMax) return cudaErrorInvalidConfiguration;
+    const int blocks = ceil_div((long long)sp.runs * sp.pop, groups);
+    DK_DISPATCH(cfg, { k_ga<W, MAXC><<<blocks, kThreads, smem, s>>>(L, g, SL, sp, pop, dbg); });
+    return cudaGetLastError();
+}
+
+cudaError_t launch_ls(const LigDev &L, const GridDev &g, const SearchDev &sp, const PopDev &pop, const LsArgs &a,
+                      int n_total, cudaStream_t s) {
+    if (n_total <= 0) return cudaSuccess;
+    const GroupCfg cfg = pick_group(L.N);
+    if (sp.ls_method == 1) {
+        // Solis-Wets: one warp per individual; few individuals -> one warp per CTA so
+        // they spread over all SMs.
+        const ScratchLayout SL = scratch_layout(L.N, L.T, L.G, false, 0);
+        const int ng = cfg.W <= 16 ? 2 : 1;
+        const int warps = n_total >= 148 * 8 ? 8 : 1;
+        const size_t smem = (size_t)L.blob_bytes + (size_t)warps * ng * SL.bytes;
+        if (smem > (size_t)kSmemMax) return cudaErrorInvalidConfiguration;
+        const int blocks = ceil_div(n_total, warps);
+        DK_DISPATCH(cfg, { k_ls_sw<W, MAXC><<<blocks, warps * 32, smem, s>>>(L, g, SL, sp, pop, a); });
+    } else {
+        const ScratchLayout SL = scratch_layout(L.N, L.T, L.G, true, 0);
+        const int groups = kThreads / cfg.W;
+        const size_t smem = (size_t)L.blob_bytes + (size_t)groups * SL.bytes;
+        if (smem > (size_t)kSmemMax) return cudaErrorInvalidConfiguration;
+        const int blocks = ceil_div(n_total, groups);
+        DK_DISPATCH(cfg, { k_ls_adadelta<W, MAXC><<<blocks, kThreads, smem, s>>>(L, g, SL, sp, pop, a); });
+    }
+    return cudaGetLastError();
+}
+
+cudaError_t launch_gen_end(const SearchDev &sp, const PopDev &pop, cudaStream_t s) {
+    k_gen_end<<<ceil_div(sp.runs, kThreads / 32), kThreads, 0, s>>>(sp, pop);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_best(const LigDev &L, const SearchDev &sp, const PopDev &pop, float *bestE, float *bestG,
+                        long long *evals, int *gens, cudaStream_t s) {
+    k_best<<<ceil_div(sp.runs, kThreads / 32), kThreads, 0, s>>>(L.G, sp, pop, bestE, bestG, evals, gens);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_philox(int n, const uint32_t *ctr, const uint32_t *key, uint32_t *out, cudaStream_t s) {
+    if (n <= 0) return cudaSuccess;
+    k_philox<<<ceil_div(n, 128), 128, 0, s>>>(n, reinterpret_cast<const uint4 *>(ctr),
+                                              reinterpret_cast<const uint2 *>(key), reinterpret_cast<uint4 *>(out));
+    return cudaGetLastError();
+}
+
+cudaError_t launch_stream_words(uint32_t k0, uint32_t k1, uint32_t purpose, uint32_t slot, uint32_t gen, uint32_t run,
+                                uint32_t m0, int n, uint32_t *out, cudaStream_t s) {
+    if (n <= 0) return cudaSuccess;
+    k_stream_words<<<ceil_div(n, 128), 128, 0, s>>>(make_uint2(k0, k1), purpose, slot, gen, run, m0, n, out);
+    return cudaGetLastError();
+}
+
+}  // namespace dk

@@ -1,0 +1,52 @@
+// kernels.cuh — host-side launchers of the sm_100a kernels (implemented in kernels.cu).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "dock_internal.h"
+
+namespace dk {
+
+// Scratch layout of one lane group (bytes, 16-aligned offsets).
+struct ScratchLayout {
+    int off_r, off_W, off_ts, off_genes, off_grad, off_extra, bytes;
+};
+
+// Local-search launch arguments.  use_state = 1: engine mode (per-run state decides the
+// generation, buffers and the LS pick); 0: parity-hook mode on a plain [n][G] array.
+struct LsArgs {
+    int use_state;
+    int n_per_run;          // LS individuals per run
+    int iters;
+    float *genes;           // hook mode: [n][G]
+    float *E;               // hook mode: [n]
+    int *evals;             // hook mode: [n] evaluation counts (engine: PopDev.ls_evals)
+    const int *rng_slot;    // hook mode: [n] population index used as SW RNG slot
+    int gen, run;           // hook mode: generation and global run index
+};
+
+struct GroupCfg {
+    int W;      // lanes per individual (16 or 32)
+    int MAXC;   // atom chunks per lane (1, 2, 4, 8)
+};
+GroupCfg pick_group(int N);
+ScratchLayout scratch_layout(int N, int T, int G, bool grad, int extra_bytes);
+
+cudaError_t setup_kernel_attributes();
+
+cudaError_t launch_eval(const LigDev &L, const GridDev &g, int n, const float *genes, float *E,
+                        float *grad, float *xyz, const int *dfs2orig, cudaStream_t s);
+cudaError_t launch_init(const LigDev &L, const GridDev &g, const SearchDev &sp, const PopDev &pop,
+                        cudaStream_t s);
+cudaError_t launch_ga(const LigDev &L, const GridDev &g, const SearchDev &sp, const PopDev &pop,
+                      int *dbg, cudaStream_t s);
+cudaError_t launch_ls(const LigDev &L, const GridDev &g, const SearchDev &sp, const PopDev &pop,
+                      const LsArgs &a, int n_total, cudaStream_t s);
+cudaError_t launch_gen_end(const SearchDev &sp, const PopDev &pop, cudaStream_t s);
+cudaError_t launch_best(const LigDev &L, const SearchDev &sp, const PopDev &pop, float *bestE,
+                        float *bestG, long long *evals, int *gens, cudaStream_t s);
+cudaError_t launch_philox(int n, const uint32_t *ctr, const uint32_t *key, uint32_t *out, cudaStream_t s);
+cudaError_t launch_stream_words(uint32_t k0, uint32_t k1, uint32_t purpose, uint32_t slot, uint32_t gen,
+                                uint32_t run, uint32_t m0, int n, uint32_t *out, cudaStream_t s);
+
+}  // namespace dk

@@ -1,0 +1,313 @@
+// prep.cpp — ligand preprocessing (D1) and grid packing (row a11 of DESIGN.md §1).
+//
+// Written independently of the oracle (oracle/oracle.c does D1 by brute-force BFS with
+// edge removal).  Here: union-find for connectivity and rigid fragments, Tarjan's
+// low-link for bridges, a BFS tree from the root fragment to orient torsions, and a
+// DFS preorder renumbering that makes every moved set one contiguous atom range
+// (PAPER.md:135-136 [§IV-B]: rotations applied "in a particular order").
+#include "prep.h"
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <numeric>
+
+namespace dk {
+namespace {
+
+struct DSU {
+    std::vector<int> p;
+    explicit DSU(int n) : p(n) { std::iota(p.begin(), p.end(), 0); }
+    int find(int a) { while (p[a] != a) { p[a] = p[p[a]]; a = p[a]; } return a; }
+    void join(int a, int b) { a = find(a); b = find(b); if (a != b) p[std::max(a, b)] = std::min(a, b); }
+};
+
+inline int a16(int x) { return (x + 15) & ~15; }
+
+}  // namespace
+
+int prepare_ligand(const dock_ligand *l, const dock_type_param *tp, int n_types, Prepared *out, std::string *err) {
+    auto fail = [&](const std::string &m) { *err = m; return (int)DOCK_E_INPUT; };
+    if (!l) return fail("ligand: NULL");
+    const int N = l->n_atoms;
+    if (N < 1 || N > kMaxAtoms) return fail("ligand.n_atoms: must be in 1..256");
+    if (!l->type || !l->charge || !l->xyz) return fail("ligand.type/charge/xyz: NULL");
+    if (l->n_bonds < 0 || (l->n_bonds > 0 && !l->bonds)) return fail("ligand.bonds: NULL or negative count");
+    if (!tp || n_types < 1) return fail("type_params: NULL");
+    for (int t = 0; t < n_types; ++t) {
+        const dock_type_param &q = tp[t];
+        if (!std::isfinite(q.R) || !std::isfinite(q.eps) || !std::isfinite(q.S) || !std::isfinite(q.V) ||
+            q.R < 0.f || q.eps < 0.f || q.role < 0 || q.role > 2)
+            return fail("type_params[" + std::to_string(t) + "]: non-finite, negative or bad role");
+    }
+    for (int a = 0; a < N; ++a) {
+        if (l->type[a] < 0 || l->type[a] >= n_types)
+            return fail("ligand.type[" + std::to_string(a) + "]: no grid map for this type");
+        if (!std::isfinite(l->charge[a])) return fail("ligand.charge[" + std::to_string(a) + "]: non-finite");
+        for (int d = 0; d < 3; ++d)
+            if (!std::isfinite(l->xyz[3 * a + d])) return fail("ligand.xyz[" + std::to_string(a) + "]: non-finite");
+    }
+    // ---- bond graph ----
+    const int B = l->n_bonds;
+    std::vector<std::vector<std::pair<int, int>>> adj(N);   // (neighbour, edge id)
+    std::vector<uint8_t> seen((size_t)N * N, 0);
+    int nrot = 0;
+    for (int e = 0; e < B; ++e) {
+        const int x = l->bonds[2 * e], y = l->bonds[2 * e + 1];
+        const std::string tag = "ligand.bonds[" + std::to_string(e) + "]";
+        if (x < 0 || y < 0 || x >= N || y >= N) return fail(tag + ": atom index out of range");
+        if (x == y) return fail(tag + ": self bond");
+        if (seen[(size_t)x * N + y]) return fail(tag + ": duplicate bond");
+        seen[(size_t)x * N + y] = seen[(size_t)y * N + x] = 1;
+        adj[x].push_back({y, e});
+        adj[y].push_back({x, e});
+        if (l->rotatable && l->rotatable[e]) ++nrot;
+    }
+    if (nrot > kMaxTors) return fail("ligand.rotatable: more than 32 rotatable bonds");
+    for (auto &v : adj) std::sort(v.begin(), v.end());
+    auto is_rot = [&](int e) { return l->rotatable && l->rotatable[e] != 0; };
+    {
+        DSU all(N);
+        for (int e = 0; e < B; ++e) all.join(l->bonds[2 * e], l->bonds[2 * e + 1]);
+        for (int a = 1; a < N; ++a)
+            if (all.find(a) != all.find(0)) return fail("ligand.bonds: graph not connected (atom " + std::to_string(a) + ")");
+    }
+    // ---- bridges: Tarjan low-link, iterative ----
+    std::vector<uint8_t> bridge(B, 0);
+    {
+        std::vector<int> disc(N, -1), low(N, 0), pedge(N, -1), it(N, 0);
+        int timer = 0;
+        std::vector<int> st;
+        st.push_back(0); disc[0] = low[0] = timer++;
+        while (!st.empty()) {
+            const int v = st.back();
+            if (it[v] < (int)adj[v].size()) {
+                const auto [w, e] = adj[v][it[v]++];
+                if (e == pedge[v]) continue;
+                if (disc[w] < 0) {
+                    disc[w] = low[w] = timer++; pedge[w] = e; st.push_back(w);
+                } else {
+                    low[v] = std::min(low[v], disc[w]);
+                }
+            } else {
+                st.pop_back();
+                if (!st.empty()) {
+                    const int u = st.back();
+                    low[u] = std::min(low[u], low[v]);
+                    if (low[v] > disc[u]) bridge[pedge[v]] = 1;
+                }
+            }
+        }
+    }
+    for (int e = 0; e < B; ++e)
+        if (is_rot(e) && !bridge[e])
+            return fail("ligand.rotatable[" + std::to_string(e) + "]: rotatable bond lies in a ring");
+    // ---- rigid fragments and root (D1.2, D1.3) ----
+    DSU fr(N);
+    for (int e = 0; e < B; ++e) if (!is_rot(e)) fr.join(l->bonds[2 * e], l->bonds[2 * e + 1]);
+    std::vector<int> frag(N), fsize(N, 0);
+    for (int a = 0; a < N; ++a) { frag[a] = fr.find(a); fsize[frag[a]]++; }   // representative = min atom
+    int root_frag = frag[0];
+    for (int a = 0; a < N; ++a)
+        if (frag[a] == a && (fsize[a] > fsize[root_frag] || (fsize[a] == fsize[root_frag] && a < root_frag))) root_frag = a;
+    const int root_atom = root_frag;
+    // ---- BFS tree from the root: orient torsions, count rotatable bonds on the path ----
+    std::vector<int> bpar(N, -2), rotdepth(N, 0);
+    {
+        std::vector<int> q{root_atom};
+        bpar[root_atom] = -1;
+        for (size_t h = 0; h < q.size(); ++h) {
+            const int u = q[h];
+            for (auto [w, e] : adj[u])
+                if (bpar[w] == -2) { bpar[w] = u; rotdepth[w] = rotdepth[u] + (is_rot(e) ? 1 : 0); q.push_back(w); }
+        }
+    }
+    struct Tor { int a, b, depth; };
+    std::vector<Tor> tors;
+    for (int e = 0; e < B; ++e) {
+        if (!is_rot(e)) continue;
+        const int x = l->bonds[2 * e], y = l->bonds[2 * e + 1];
+        Tor t;
+        if (bpar[y] == x) { t.a = x; t.b = y; }
+        else if (bpar[x] == y) { t.a = y; t.b = x; }
+        else return fail("ligand.rotatable[" + std::to_string(e) + "]: not a tree edge (internal)");
+        t.depth = rotdepth[t.b];
+        tors.push_back(t);
+    }
+    std::sort(tors.begin(), tors.end(), [](const Tor &u, const Tor &v) {
+        if (u.depth != v.depth) return u.depth < v.depth;
+        if (u.a != v.a) return u.a < v.a;
+        return u.b < v.b;
+    });
+    const int T = (int)tors.size();
+    // ---- DFS preorder renumbering: subtree of b_k = far side of torsion k ----
+    std::vector<int> pos(N, -1), sub(N, 0), order;
+    {
+        std::vector<std::pair<int, int>> st{{root_atom, 0}};
+        pos[root_atom] = 0; order.push_back(root_atom);
+        while (!st.empty()) {
+            auto &[v, i] = st.back();
+            if (i < (int)adj[v].size()) {
+                const int w = adj[v][i++].first;
+                if (pos[w] < 0) { pos[w] = (int)order.size(); order.push_back(w); st.push_back({w, 0}); }
+            } else {
+                sub[v] = (int)order.size() - pos[v];
+                st.pop_back();
+            }
+        }
+    }
+    std::vector<int> lo(T), hi(T), parent(T, -1);
+    for (int k = 0; k < T; ++k) { lo[k] = pos[tors[k].b] + 1; hi[k] = pos[tors[k].b] + sub[tors[k].b]; }
+    for (int k = 0; k < T; ++k) {
+        const int pb = pos[tors[k].b];
+        for (int j = 0; j < T; ++j)
+            if (j != k && lo[j] <= pb && pb < hi[j] && (parent[k] < 0 || hi[j] - lo[j] < hi[parent[k]] - lo[parent[k]]))
+                parent[k] = j;
+        if (parent[k] >= 0 && tors[parent[k]].depth != tors[k].depth - 1)
+            return fail("ligand: torsion tree inconsistent (internal)");
+    }
+    std::vector<int> deep(N, -1);   // indexed by dfs position
+    for (int p = 0; p < N; ++p)
+        for (int k = 0; k < T; ++k)
+            if (lo[k] <= p && p < hi[k] && (deep[p] < 0 || hi[k] - lo[k] < hi[deep[p]] - lo[deep[p]])) deep[p] = k;
+    // ---- pairs (D1.6): i < j, more than 3 bonds apart, different rigid fragments ----
+    std::vector<int> pairs;
+    {
+        std::vector<int> mark(N, -1), depthv(N, 0);
+        for (int i = 0; i < N; ++i) {
+            std::vector<int> q{i};
+            mark[i] = i; depthv[i] = 0;
+            for (size_t h = 0; h < q.size(); ++h) {
+                const int u = q[h];
+                if (depthv[u] == 3) continue;
+                for (auto [w, e] : adj[u]) { (void)e; if (mark[w] != i) { mark[w] = i; depthv[w] = depthv[u] + 1; q.push_back(w); } }
+            }
+            for (int j = i + 1; j < N; ++j)
+                if (mark[j] != i && frag[i] != frag[j]) { pairs.push_back(i); pairs.push_back(j); }
+        }
+    }
+    const int P = (int)pairs.size() / 2;
+    if (P > 65535) return fail("ligand: more than 65535 intramolecular pairs");
+
+    // ---- outputs in caller order ----
+    Prepared &o = *out;
+    o.N = N; o.T = T; o.G = 6 + T; o.P = P;
+    o.tor_a.resize(T); o.tor_b.resize(T); o.tor_depth.resize(T);
+    o.moved.assign((size_t)T * N, 0);
+    for (int k = 0; k < T; ++k) {
+        o.tor_a[k] = tors[k].a; o.tor_b[k] = tors[k].b; o.tor_depth[k] = tors[k].depth;
+        for (int a = 0; a < N; ++a) o.moved[(size_t)k * N + a] = (pos[a] >= lo[k] && pos[a] < hi[k]) ? 1 : 0;
+    }
+    o.pairs = pairs;
+    o.dfs2orig = order;
+    o.orig2dfs = pos;
+
+    // ---- the constant block (DFS numbering) ----
+    LigDev &L = o.layout;
+    std::memset(&L, 0, sizeof(L));
+    L.N = N; L.T = T; L.G = 6 + T; L.P = P;
+    int off = 0;
+    L.off_lvl = off; off += a16(4 * (kMaxTors + 1));
+    L.off_p = off; off += 16 * N;
+    L.off_par = off; off += 16 * N;
+    L.off_meta = off; off += a16(4 * N);
+    L.off_tA = off; off += 16 * T;
+    L.off_tU = off; off += 16 * T;
+    L.off_tmeta = off; off += 16 * T;
+    L.off_pairs = off; off += a16(4 * P);
+    L.off_csr_off = off; off += a16(4 * (N + 1));
+    L.off_csr_nbr = off; off += a16(2 * 2 * P);
+    L.blob_bytes = a16(off);
+    o.blob.assign(L.blob_bytes, 0);
+    uint8_t *bl = o.blob.data();
+    // levels: torsions are sorted by depth, depth 1..D all present
+    int n_levels = 0;
+    for (int k = 0; k < T; ++k) n_levels = std::max(n_levels, tors[k].depth);
+    L.n_levels = n_levels;
+    int *lvl = reinterpret_cast<int *>(bl + L.off_lvl);
+    for (int d = 0; d <= kMaxTors; ++d) {
+        int s = 0;
+        while (s < T && tors[s].depth <= d) ++s;   // first torsion with depth > d
+        lvl[d] = s;
+        L.lvl_start[d] = s;
+    }
+    // body frame: c = centroid of the reference coordinates, computed in double (D1.8)
+    double c[3] = {0, 0, 0};
+    for (int a = 0; a < N; ++a) for (int d = 0; d < 3; ++d) c[d] += l->xyz[3 * a + d];
+    for (int d = 0; d < 3; ++d) c[d] /= N;
+    auto pref = [&](int a, int d) { return (double)l->xyz[3 * a + d] - c[d]; };
+    auto role_of = [&](int a) { return tp[l->type[a]].role; };
+    float4 *bp = reinterpret_cast<float4 *>(bl + L.off_p);
+    float4 *bprm = reinterpret_cast<float4 *>(bl + L.off_par);
+    int *bmeta = reinterpret_cast<int *>(bl + L.off_meta);
+    for (int p = 0; p < N; ++p) {
+        const int a = order[p];
+        const dock_type_param &q = tp[l->type[a]];
+        bp[p] = make_float4((float)pref(a, 0), (float)pref(a, 1), (float)pref(a, 2), l->charge[a]);
+        bprm[p] = make_float4(0.5f * q.R, (float)std::sqrt((double)q.eps), q.S, q.V);
+        bmeta[p] = (l->type[a] & 0xff) | ((q.role & 3) << 8) | ((deep[p] + 1) << 16);
+    }
+    float4 *tA = reinterpret_cast<float4 *>(bl + L.off_tA);
+    float4 *tU = reinterpret_cast<float4 *>(bl + L.off_tU);
+    int4 *tm = reinterpret_cast<int4 *>(bl + L.off_tmeta);
+    for (int k = 0; k < T; ++k) {
+        const int a = tors[k].a, b = tors[k].b;
+        double u[3], n = 0;
+        for (int d = 0; d < 3; ++d) { u[d] = pref(b, d) - pref(a, d); n += u[d] * u[d]; }
+        n = std::sqrt(n);
+        if (!(n > 0)) return fail("ligand.xyz: zero-length rotatable bond " + std::to_string(a) + "-" + std::to_string(b));
+        tA[k] = make_float4((float)pref(a, 0), (float)pref(a, 1), (float)pref(a, 2), 0.f);
+        tU[k] = make_float4((float)(u[0] / n), (float)(u[1] / n), (float)(u[2] / n), 0.f);
+        tm[k] = make_int4(parent[k], pos[a], pos[b], lo[k] | (hi[k] << 16));
+    }
+    auto hb_of = [&](int i, int j) {
+        const int ri = role_of(i), rj = role_of(j);
+        return (ri == 1 && rj == 2) || (ri == 2 && rj == 1);
+    };
+    uint32_t *bpairs = reinterpret_cast<uint32_t *>(bl + L.off_pairs);
+    std::vector<std::vector<std::pair<int, int>>> inc(N);   // dfs atom -> (dfs nbr, hb)
+    for (int q = 0; q < P; ++q) {
+        const int i = pairs[2 * q], j = pairs[2 * q + 1];
+        int di = pos[i], dj = pos[j];
+        if (di > dj) std::swap(di, dj);
+        const int hb = hb_of(i, j) ? 1 : 0;
+        bpairs[q] = (uint32_t)di | ((uint32_t)dj << 8) | ((uint32_t)hb << 16);
+        inc[di].push_back({dj, hb});
+        inc[dj].push_back({di, hb});
+    }
+    int *coff = reinterpret_cast<int *>(bl + L.off_csr_off);
+    uint16_t *cnb = reinterpret_cast<uint16_t *>(bl + L.off_csr_nbr);
+    int e = 0;
+    for (int p = 0; p < N; ++p) {
+        std::sort(inc[p].begin(), inc[p].end());
+        coff[p] = e;
+        for (auto [j, hb] : inc[p]) cnb[e++] = (uint16_t)(j | (hb << 8));
+    }
+    coff[N] = e;
+    return DOCK_OK;
+}
+
+int pack_grid(const dock_grids *g, std::vector<float4> *packed, std::string *err) {
+    auto fail = [&](const std::string &m) { *err = m; return (int)DOCK_E_INPUT; };
+    if (!g) return fail("grids: NULL");
+    if (g->nx < 2 || g->ny < 2 || g->nz < 2) return fail("grids.nx/ny/nz: each must be >= 2");
+    if (!(g->spacing > 0.f) || !std::isfinite(g->spacing)) return fail("grids.spacing: must be finite and > 0");
+    for (int d = 0; d < 3; ++d) if (!std::isfinite(g->origin[d])) return fail("grids.origin: non-finite");
+    if (g->n_types < 1 || g->n_types > 16) return fail("grids.n_types: must be in 1..16");
+    if (!g->maps) return fail("grids.maps: NULL");
+    const size_t n3 = (size_t)g->nx * g->ny * g->nz;
+    const size_t total = n3 * (size_t)(g->n_types + 2);
+    for (size_t i = 0; i < total; ++i)
+        if (!std::isfinite(g->maps[i]))
+            return fail("grids.maps[" + std::to_string(i / n3) + "][" + std::to_string(i % n3) + "]: non-finite");
+    packed->resize(n3 * g->n_types);
+    const float *E = g->maps + n3 * g->n_types, *D = E + n3;
+    for (int t = 0; t < g->n_types; ++t) {
+        const float *M = g->maps + n3 * t;
+        float4 *o = packed->data() + n3 * t;
+        for (size_t i = 0; i < n3; ++i) o[i] = make_float4(M[i], E[i], D[i], 0.f);
+    }
+    return DOCK_OK;
+}
+
+}  // namespace dk

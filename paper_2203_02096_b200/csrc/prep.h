@@ -1,0 +1,31 @@
+// prep.h — host-side preprocessing of a ligand and a receptor grid (row a11).
+#pragma once
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/dock.h"
+#include "dock_internal.h"
+
+namespace dk {
+
+struct Prepared {
+    int N = 0, T = 0, G = 0, P = 0;
+    // D1 results in caller atom order
+    std::vector<int> tor_a, tor_b, tor_depth;     // [T], torsion order (depth, a, b)
+    std::vector<uint8_t> moved;                   // [T*N]
+    std::vector<int> pairs;                       // [P*2] lexicographic, i < j
+    // device numbering
+    std::vector<int> dfs2orig, orig2dfs;          // [N]
+    LigDev layout;                                // offsets + sizes (blob pointer unset)
+    std::vector<uint8_t> blob;                    // the constant block, layout.blob_bytes
+};
+
+// D1 + blob assembly.  Returns DOCK_OK or DOCK_E_INPUT with `err` naming the field/index.
+int prepare_ligand(const dock_ligand *l, const dock_type_param *tp, int n_types, Prepared *out, std::string *err);
+
+// Grid validation and packing into one float4 {M_type, M_E, M_D, 0} per (type, node).
+int pack_grid(const dock_grids *g, std::vector<float4> *packed, std::string *err);
+
+}  // namespace dk
