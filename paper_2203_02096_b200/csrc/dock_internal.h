@@ -23,6 +23,7 @@ struct LigDev {
     int n_levels;                 // number of torsion depth levels
     int lvl_start[kMaxTors + 1];  // torsions of level l: [lvl_start[l], lvl_start[l+1])
     int blob_bytes;               // multiple of 16
+    int grad_bytes;               // prefix needed by the gradient kernels (no pair list / pair constants)
     // byte offsets inside the blob (all 16-byte aligned)
     int off_lvl;      // int[kMaxTors+1] copy of lvl_start (read from shared memory)
     int off_p;        // float4[N]  body coordinates p = X - c (x,y,z), charge q in .w
@@ -32,8 +33,9 @@ struct LigDev {
     int off_tU;       // float4[T]  unit axis u = (p[b_k] - p[a_k]) / |.|
     int off_tmeta;    // int4[T]    parent torsion (-1 root), a (dfs), b (dfs), lo | hi << 16
     int off_pairs;    // uint32[P]  i | j << 8 | hb << 16   (dfs indices, i < j)
-    int off_csr_off;  // int[N+1]   per-atom incidence offsets into csr_nbr
-    int off_csr_nbr;  // uint16[2P] j | hb << 8
+    int off_pprm;     // float4[P]  r_eq^2, eps_ij, S_iV_j + S_jV_i, 332.06363/4 q_i q_j
+    int off_mask;     // uint32[N][NW] pair-membership bit rows (dfs indices)
+    int NW;           // words per mask row = ceil(N / 32)
     const uint8_t *blob;          // device pointer
 };
 

@@ -47,13 +47,19 @@ GroupCfg pick_group(int N) {
     return c;
 }
 
-__device__ __forceinline__ LigSm stage_ligand(const LigDev &L, uint8_t *sm) {
+// Bytes of the ligand block a kernel stages: gradient kernels skip the pair list and the
+// pair constants of the energy-only path.
+static inline __host__ __device__ int staged_bytes(const LigDev &L, bool grad) {
+    return grad ? L.grad_bytes : L.blob_bytes;
+}
+
+__device__ __forceinline__ LigSm stage_ligand(const LigDev &L, uint8_t *sm, int bytes) {
     const uint4 *src = reinterpret_cast<const uint4 *>(L.blob);
     uint4 *dst = reinterpret_cast<uint4 *>(sm);
-    for (int i = threadIdx.x; i < L.blob_bytes / 16; i += blockDim.x) dst[i] = src[i];
+    for (int i = threadIdx.x; i < bytes / 16; i += blockDim.x) dst[i] = src[i];
     __syncthreads();
     LigSm v;
-    v.N = L.N; v.T = L.T; v.G = L.G; v.P = L.P; v.n_levels = L.n_levels;
+    v.N = L.N; v.T = L.T; v.G = L.G; v.P = L.P; v.NW = L.NW; v.n_levels = L.n_levels;
     v.lvl = reinterpret_cast<const int *>(sm + L.off_lvl);
     v.p = reinterpret_cast<const float4 *>(sm + L.off_p);
     v.par = reinterpret_cast<const float4 *>(sm + L.off_par);
@@ -62,8 +68,8 @@ __device__ __forceinline__ LigSm stage_ligand(const LigDev &L, uint8_t *sm) {
     v.tU = reinterpret_cast<const float4 *>(sm + L.off_tU);
     v.tmeta = reinterpret_cast<const int4 *>(sm + L.off_tmeta);
     v.pairs = reinterpret_cast<const uint32_t *>(sm + L.off_pairs);
-    v.csr_off = reinterpret_cast<const int *>(sm + L.off_csr_off);
-    v.csr_nbr = reinterpret_cast<const uint16_t *>(sm + L.off_csr_nbr);
+    v.pprm = reinterpret_cast<const float4 *>(sm + L.off_pprm);
+    v.mask = reinterpret_cast<const uint32_t *>(sm + L.off_mask);
     return v;
 }
 
@@ -92,11 +98,11 @@ __global__ void __launch_bounds__(256) k_eval(const LigDev L, const GridDev g, c
                                               float *grad, float *xyz, const int *__restrict__ dfs2orig) {
     extern __shared__ uint4 smem_u4[];
     uint8_t *sm = reinterpret_cast<uint8_t *>(smem_u4);
-    const LigSm Ls = stage_ligand(L, sm);
+    const LigSm Ls = stage_ligand(L, sm, staged_bytes(L, GRAD));
     const int gl = threadIdx.x / W, sub = threadIdx.x % W;
     const int gi = blockIdx.x * (blockDim.x / W) + gl;
     if (gi >= n) return;
-    const Scratch S = scratch_at(sm + L.blob_bytes + gl * SL.bytes, SL);
+    const Scratch S = scratch_at(sm + staged_bytes(L, GRAD) + gl * SL.bytes, SL);
     const unsigned mask = group_mask<W>();
     const int G = L.G;
     for (int j = sub; j < G; j += W) S.genes[j] = genes[(size_t)gi * G + j];
@@ -122,12 +128,12 @@ __global__ void __launch_bounds__(256) k_init(const LigDev L, const GridDev g, c
                                               const SearchDev sp, const PopDev pop) {
     extern __shared__ uint4 smem_u4[];
     uint8_t *sm = reinterpret_cast<uint8_t *>(smem_u4);
-    const LigSm Ls = stage_ligand(L, sm);
+    const LigSm Ls = stage_ligand(L, sm, staged_bytes(L, false));
     const int gl = threadIdx.x / W, sub = threadIdx.x % W;
     const int gi = blockIdx.x * (blockDim.x / W) + gl;
     if (gi >= sp.runs * sp.pop) return;
     const int r = gi / sp.pop, k = gi % sp.pop, G = L.G;
-    const Scratch S = scratch_at(sm + L.blob_bytes + gl * SL.bytes, SL);
+    const Scratch S = scratch_at(sm + staged_bytes(L, false) + gl * SL.bytes, SL);
     const unsigned mask = group_mask<W>();
     const uint2 key = make_uint2(sp.key0, sp.key1);
     const uint32_t run_g = (uint32_t)(sp.run_base + r);
@@ -178,7 +184,7 @@ __global__ void __launch_bounds__(256) k_ga(const LigDev L, const GridDev g, con
     const int r = gi / P;
     if (gi < sp.runs * P) { st = pop.state[r]; act = run_active(st, sp); }
     if (!__syncthreads_or(act)) return;            // finished runs cost one state read
-    const LigSm Ls = stage_ligand(L, sm);
+    const LigSm Ls = stage_ligand(L, sm, staged_bytes(L, false));
     if (!act) return;
     const int k = gi % P;
     const uint32_t gen = (uint32_t)st.gen + 1u;
@@ -187,7 +193,7 @@ __global__ void __launch_bounds__(256) k_ga(const LigDev L, const GridDev g, con
     const float *oldE = pop.E + ((size_t)cur * sp.runs + r) * P;
     float *newG = pop.genes + ((size_t)nxt * sp.runs + r) * P * G;
     float *newE = pop.E + ((size_t)nxt * sp.runs + r) * P;
-    const Scratch S = scratch_at(sm + L.blob_bytes + gl * SL.bytes, SL);
+    const Scratch S = scratch_at(sm + staged_bytes(L, false) + gl * SL.bytes, SL);
     const unsigned mask = group_mask<W>();
     const uint2 key = make_uint2(sp.key0, sp.key1);
     const uint32_t run_g = (uint32_t)(sp.run_base + r);
@@ -209,7 +215,7 @@ __global__ void __launch_bounds__(256) k_ga(const LigDev L, const GridDev g, con
         for (int j = sub; j < G; j += W) newG[j] = oldG[(size_t)bi * G + j];
         if (sub == 0) newE[0] = oldE[bi];
         // local-search sample: partial Fisher-Yates over the new population (D8.3)
-        int *perm = reinterpret_cast<int *>(sm + L.blob_bytes + gl * SL.bytes + SL.off_extra);
+        int *perm = reinterpret_cast<int *>(sm + staged_bytes(L, false) + gl * SL.bytes + SL.off_extra);
         for (int i = sub; i < P; i += W) perm[i] = i;
         __syncwarp(mask);
         if (sub == 0) {
@@ -321,9 +327,9 @@ __global__ void __launch_bounds__(256) k_ls_adadelta(const LigDev L, const GridD
     const int G = L.G;
     const LsTarget t = ls_target(sp, pop, a, gi, G);
     if (!__syncthreads_or(t.act)) return;
-    const LigSm Ls = stage_ligand(L, sm);
+    const LigSm Ls = stage_ligand(L, sm, staged_bytes(L, true));
     if (!t.act) return;
-    const Scratch S = scratch_at(sm + L.blob_bytes + gl * SL.bytes, SL);
+    const Scratch S = scratch_at(sm + staged_bytes(L, true) + gl * SL.bytes, SL);
     const unsigned mask = group_mask<W>();
     constexpr int NSET = (kMaxGenes + W - 1) / W;
     float x[NSET], sg[NSET], sd[NSET], bx[NSET];
@@ -382,9 +388,9 @@ __global__ void __launch_bounds__(256) k_ls_sw(const LigDev L, const GridDev g, 
     const int G = L.G;
     const LsTarget t = ls_target(sp, pop, a, wi, G);
     if (!__syncthreads_or(t.act)) return;
-    const LigSm Ls = stage_ligand(L, sm);
+    const LigSm Ls = stage_ligand(L, sm, staged_bytes(L, false));
     if (!t.act) return;
-    uint8_t *wbase = sm + L.blob_bytes + (size_t)warp * NG * SL.bytes;
+    uint8_t *wbase = sm + staged_bytes(L, false) + (size_t)warp * NG * SL.bytes;
     const Scratch S0 = scratch_at(wbase, SL);
     const Scratch S1 = scratch_at(wbase + (NG - 1) * SL.bytes, SL);
     const Scratch Sg = grp == 0 ? S0 : S1;
@@ -571,7 +577,7 @@ cudaError_t launch_eval(const LigDev &L, const GridDev &g, int n, const float *g
     const bool want_grad = grad != nullptr;
     const ScratchLayout SL = scratch_layout(L.N, L.T, L.G, want_grad, 0);
     const int groups = kThreads / cfg.W;
-    const size_t smem = (size_t)L.blob_bytes + (size_t)groups * SL.bytes;
+    const size_t smem = (size_t)staged_bytes(L, want_grad) + (size_t)groups * SL.bytes;
     if (smem > (size_t)kSmemMax) return cudaErrorInvalidConfiguration;
     const int blocks = ceil_div(n, groups);
     DK_DISPATCH(cfg, {
@@ -621,7 +627,7 @@ cudaError_t launch_ls(const LigDev &L, const GridDev &g, const SearchDev &sp, co
     } else {
         const ScratchLayout SL = scratch_layout(L.N, L.T, L.G, true, 0);
         const int groups = kThreads / cfg.W;
-        const size_t smem = (size_t)L.blob_bytes + (size_t)groups * SL.bytes;
+        const size_t smem = (size_t)staged_bytes(L, true) + (size_t)groups * SL.bytes;
         if (smem > (size_t)kSmemMax) return cudaErrorInvalidConfiguration;
         const int blocks = ceil_div(n_total, groups);
         DK_DISPATCH(cfg, { k_ls_adadelta<W, MAXC><<<blocks, kThreads, smem, s>>>(L, g, SL, sp, pop, a); });

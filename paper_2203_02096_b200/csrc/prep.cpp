@@ -214,9 +214,11 @@ int prepare_ligand(const dock_ligand *l, const dock_type_param *tp, int n_types,
     L.off_tA = off; off += 16 * T;
     L.off_tU = off; off += 16 * T;
     L.off_tmeta = off; off += 16 * T;
+    L.NW = (N + 31) / 32;
+    L.off_mask = off; off += a16(4 * N * L.NW);
+    L.grad_bytes = off;              // the gradient kernels stage only up to here
     L.off_pairs = off; off += a16(4 * P);
-    L.off_csr_off = off; off += a16(4 * (N + 1));
-    L.off_csr_nbr = off; off += a16(2 * 2 * P);
+    L.off_pprm = off; off += 16 * P;
     L.blob_bytes = a16(off);
     o.blob.assign(L.blob_bytes, 0);
     uint8_t *bl = o.blob.data();
@@ -265,25 +267,23 @@ int prepare_ligand(const dock_ligand *l, const dock_type_param *tp, int n_types,
         return (ri == 1 && rj == 2) || (ri == 2 && rj == 1);
     };
     uint32_t *bpairs = reinterpret_cast<uint32_t *>(bl + L.off_pairs);
-    std::vector<std::vector<std::pair<int, int>>> inc(N);   // dfs atom -> (dfs nbr, hb)
+    float4 *pprm = reinterpret_cast<float4 *>(bl + L.off_pprm);
+    uint32_t *bmask = reinterpret_cast<uint32_t *>(bl + L.off_mask);
     for (int q = 0; q < P; ++q) {
         const int i = pairs[2 * q], j = pairs[2 * q + 1];
         int di = pos[i], dj = pos[j];
         if (di > dj) std::swap(di, dj);
         const int hb = hb_of(i, j) ? 1 : 0;
         bpairs[q] = (uint32_t)di | ((uint32_t)dj << 8) | ((uint32_t)hb << 16);
-        inc[di].push_back({dj, hb});
-        inc[dj].push_back({di, hb});
+        // D5 pair constants for the energy-only path
+        const dock_type_param &ti = tp[l->type[i]], &tj = tp[l->type[j]];
+        const double req = 0.5 * ((double)ti.R + (double)tj.R);
+        pprm[q] = make_float4((float)(req * req), (float)std::sqrt((double)ti.eps * (double)tj.eps),
+                              (float)((double)ti.S * tj.V + (double)tj.S * ti.V),
+                              (float)(332.06363 / 4.0 * (double)l->charge[i] * (double)l->charge[j]));
+        bmask[di * L.NW + (dj >> 5)] |= 1u << (dj & 31);
+        bmask[dj * L.NW + (di >> 5)] |= 1u << (di & 31);
     }
-    int *coff = reinterpret_cast<int *>(bl + L.off_csr_off);
-    uint16_t *cnb = reinterpret_cast<uint16_t *>(bl + L.off_csr_nbr);
-    int e = 0;
-    for (int p = 0; p < N; ++p) {
-        std::sort(inc[p].begin(), inc[p].end());
-        coff[p] = e;
-        for (auto [j, hb] : inc[p]) cnb[e++] = (uint16_t)(j | (hb << 8));
-    }
-    coff[N] = e;
     return DOCK_OK;
 }
 

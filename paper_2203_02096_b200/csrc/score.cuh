@@ -2,11 +2,11 @@
 // the hot path, DESIGN.md §1/§5).
 //
 // One group of W lanes (W = 16 or 32) evaluates one genotype.  Lane `sub` owns atoms
-// a = sub + W*c (c < MAXC).  The ligand block (staged in shared memory per CTA) and a
-// small per-group scratch (pose coordinates, torsion composites, genes, gradient) are
-// the only memory besides the grid maps, which are read with float4 corner gathers
-// from L2/HBM.  All sums are fixed-order (butterfly shuffles, sequential per-lane
-// loops): no atomics, so results are bit-reproducible run to run.
+// a = sub + W*c (chunk c < MAXC).  The ligand block (staged in shared memory per CTA)
+// and a small per-group scratch (pose coordinates, torsion composites, genes, gradient)
+// are the only memory besides the grid maps, which are read with float4 corner gathers
+// from L2/HBM.  All sums are fixed-order (butterfly shuffles, fixed tile/step order):
+// no atomics, so results are bit-reproducible run to run.
 #pragma once
 #include <stdint.h>
 
@@ -14,14 +14,14 @@
 
 namespace dk {
 
-constexpr float kElec = 332.06363f;                         // D5
-constexpr float kInvTwoSigma2 = 1.0f / (2.0f * 3.6f * 3.6f);  // desolvation sigma 3.6 Å
-constexpr float kLog2e = 1.4426950408889634f;
-constexpr float kOut = 1e5f;                                  // D4.5 out-of-grid penalty
+constexpr float kElec4 = 332.06363f * 0.25f;                  // D5: 332.06363 / (4 rho^2)
+constexpr float kInvTwoSigma2 = 1.0f / (2.0f * 3.6f * 3.6f);    // desolvation sigma 3.6 Å
+constexpr float kExpScale = -kInvTwoSigma2 * 1.4426950408889634f;   // exp(-x/2s^2) = 2^(x*kExpScale)
+constexpr float kOut = 1e5f;                                    // D4.5 out-of-grid penalty
 
 // Shared-memory view of the staged ligand block.
 struct LigSm {
-    int N, T, G, P, n_levels;
+    int N, T, G, P, NW, n_levels;
     const int *lvl;               // [kMaxTors+1]
     const float4 *p;              // body coords + charge
     const float4 *par;            // R/2, sqrt eps, S, V
@@ -29,8 +29,8 @@ struct LigSm {
     const float4 *tA, *tU;
     const int4 *tmeta;            // parent, a, b, lo | hi<<16
     const uint32_t *pairs;        // i | j<<8 | hb<<16
-    const int *csr_off;
-    const uint16_t *csr_nbr;      // j | hb<<8
+    const float4 *pprm;           // per pair: r_eq^2, eps_ij, S_iV_j+S_jV_i, 332.06363/4 q_i q_j
+    const uint32_t *mask;         // [N][NW] pair-membership bit rows
 };
 
 // Per-group scratch in shared memory.
@@ -66,32 +66,52 @@ __device__ __forceinline__ long long gsum_ll(long long v, unsigned mask) {
     return v;
 }
 
-// D5 pair energy and dE/d(rho^2).
-template <bool GRAD>
-__device__ __forceinline__ float pair_energy(float rho2, float4 pi, float4 pj, float qq, bool hb,
-                                             float &dE) {
-    const bool clamped = rho2 < 1e-4f;                   // 0.01 Å clamp
+__device__ __forceinline__ float ex2_approx(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
+// sin/cos of an unwrapped angle: two-constant Cody-Waite reduction to [-pi, pi], then the
+// SFU (__sincosf, |err| < 4e-7 there).  Genes are never wrapped (D3), so the reduction
+// matters; beyond |x| = 1e5 the accurate library path is used.
+__device__ __forceinline__ void fast_sincos(float x, float &s, float &c) {
+    if (fabsf(x) < 1.0e5f) {
+        const float k = rintf(x * 0.15915494309189535f);
+        float r = fmaf(-k, 6.28318548202514648f, x);
+        r = fmaf(-k, -1.7484555314695172e-07f, r);
+        __sincosf(r, &s, &c);
+    } else {
+        sincosf(x, &s, &c);
+    }
+}
+
+// D5 pair energy from precomputed pair constants (energy-only path).
+__device__ __forceinline__ float pair_e_pre(float rho2, float4 pp, bool hb) {
+    rho2 = fmaxf(rho2, 1e-4f);                           // 0.01 Å clamp
+    const float inv = __fdividef(1.0f, rho2);
+    const float x2 = pp.x * inv, x4 = x2 * x2, x6 = x4 * x2, x12 = x6 * x6;
+    const float vdw = hb ? fmaf(5.0f, x12, -6.0f * (x6 * x4)) : fmaf(-2.0f, x6, x12);   // 12-10 / 12-6
+    return fmaf(pp.y, vdw, fmaf(pp.w, inv, pp.z * ex2_approx(rho2 * kExpScale)));
+}
+
+// D5 pair energy and dE/d(rho^2) from per-atom parameters (gradient path).
+__device__ __forceinline__ float pair_eg(float rho2, float4 pi, float qi, float4 pj, float qj, bool hb, float &dE) {
+    const bool clamped = rho2 < 1e-4f;
     rho2 = fmaxf(rho2, 1e-4f);
     const float inv = __fdividef(1.0f, rho2);
     const float req = pi.x + pj.x;                       // (R_i + R_j)/2
     const float eps = pi.y * pj.y;                       // sqrt(eps_i eps_j)
-    const float SV = pi.z * pj.w + pj.z * pi.w;          // S_i V_j + S_j V_i
-    const float x2 = req * req * inv;
-    const float x4 = x2 * x2;
-    const float x6 = x4 * x2;
-    const float x12 = x6 * x6;
-    const float xn = hb ? x6 * x4 : x6;                  // x^10 for H-bond pairs
-    const float c12 = hb ? 5.0f : 1.0f;
-    const float cn = hb ? 6.0f : 2.0f;
-    const float Evdw = eps * (c12 * x12 - cn * xn);
-    const float Eel = (0.25f * kElec) * qq * inv;        // eps(r) = 4r
-    const float Eds = SV * exp2f(-rho2 * (kInvTwoSigma2 * kLog2e));
-    if (GRAD) {
-        const float dn = hb ? 30.0f : 6.0f;
-        const float dv = -eps * inv * (6.0f * c12 * x12 - dn * xn);
-        const float dd = dv - Eel * inv - Eds * kInvTwoSigma2;
-        dE = clamped ? 0.0f : dd;
-    }
+    const float SV = fmaf(pi.z, pj.w, pj.z * pi.w);      // S_i V_j + S_j V_i
+    const float x2 = req * req * inv, x4 = x2 * x2, x6 = x4 * x2, x12 = x6 * x6;
+    const float xn = hb ? x6 * x4 : x6;
+    const float c12 = hb ? 5.0f : 1.0f, cn = hb ? 6.0f : 2.0f, dn = hb ? 30.0f : 6.0f;
+    const float Evdw = eps * fmaf(c12, x12, -cn * xn);
+    const float Eel = (kElec4 * qi * qj) * inv;          // eps(r) = 4r
+    const float Eds = SV * ex2_approx(rho2 * kExpScale);
+    const float dv = -eps * inv * fmaf(6.0f * c12, x12, -dn * xn);
+    const float d = fmaf(-Eel, inv, fmaf(-Eds, kInvTwoSigma2, dv));
+    dE = clamped ? 0.0f : d;
     return Evdw + Eel + Eds;
 }
 
@@ -113,20 +133,20 @@ __device__ __forceinline__ float inter_atom(const GridDev &g, int type, float q,
         const float aq = fabsf(q);
         // trilinear interpolation is linear in the map values: combine the three maps per
         // corner first (e = V(M_t) + q V(M_E) + |q| V(M_D) = V(M_t + q M_E + |q| M_D)).
-        const float c000 = m000.x + q * m000.y + aq * m000.z, c100 = m100.x + q * m100.y + aq * m100.z;
-        const float c010 = m010.x + q * m010.y + aq * m010.z, c110 = m110.x + q * m110.y + aq * m110.z;
-        const float c001 = m001.x + q * m001.y + aq * m001.z, c101 = m101.x + q * m101.y + aq * m101.z;
-        const float c011 = m011.x + q * m011.y + aq * m011.z, c111 = m111.x + q * m111.y + aq * m111.z;
+        const float c000 = fmaf(aq, m000.z, fmaf(q, m000.y, m000.x)), c100 = fmaf(aq, m100.z, fmaf(q, m100.y, m100.x));
+        const float c010 = fmaf(aq, m010.z, fmaf(q, m010.y, m010.x)), c110 = fmaf(aq, m110.z, fmaf(q, m110.y, m110.x));
+        const float c001 = fmaf(aq, m001.z, fmaf(q, m001.y, m001.x)), c101 = fmaf(aq, m101.z, fmaf(q, m101.y, m101.x));
+        const float c011 = fmaf(aq, m011.z, fmaf(q, m011.y, m011.x)), c111 = fmaf(aq, m111.z, fmaf(q, m111.y, m111.x));
         const float dx00 = c100 - c000, dx10 = c110 - c010, dx01 = c101 - c001, dx11 = c111 - c011;
-        const float a00 = c000 + fx * dx00, a10 = c010 + fx * dx10;
-        const float a01 = c001 + fx * dx01, a11 = c011 + fx * dx11;
+        const float a00 = fmaf(fx, dx00, c000), a10 = fmaf(fx, dx10, c010);
+        const float a01 = fmaf(fx, dx01, c001), a11 = fmaf(fx, dx11, c011);
         const float dy0 = a10 - a00, dy1 = a11 - a01;
-        const float b0 = a00 + fy * dy0, b1 = a01 + fy * dy1;
-        const float dxy0 = dx00 + fy * (dx10 - dx00), dxy1 = dx01 + fy * (dx11 - dx01);
-        gx = (dxy0 + fz * (dxy1 - dxy0)) * g.inv_s;
-        gy = (dy0 + fz * (dy1 - dy0)) * g.inv_s;
+        const float b0 = fmaf(fy, dy0, a00), b1 = fmaf(fy, dy1, a01);
+        const float dxy0 = fmaf(fy, dx10 - dx00, dx00), dxy1 = fmaf(fy, dx11 - dx01, dx01);
+        gx = fmaf(fz, dxy1 - dxy0, dxy0) * g.inv_s;
+        gy = fmaf(fz, dy1 - dy0, dy0) * g.inv_s;
         gz = (b1 - b0) * g.inv_s;
-        return b0 + fz * (b1 - b0);
+        return fmaf(fz, b1 - b0, b0);
     }
     const float cx = fminf(fmaxf(rx, g.ox), g.hx), cy = fminf(fmaxf(ry, g.oy), g.hy),
                 cz = fminf(fmaxf(rz, g.oz), g.hz);
@@ -137,6 +157,113 @@ __device__ __forceinline__ float inter_atom(const GridDev &g, int type, float q,
     return kOut * (1.0f + d);
 }
 
+// One D5 pair inside the gradient tiles: energy into e, force into the own-atom
+// accumulator (+dE d) and the partner accumulator (-dE d); the factor 2 of
+// dE/dr_i = 2 dE/drho2 (r_i - r_j) is applied once per atom at the end.
+__device__ __forceinline__ void tile_pair(bool on, float rxi, float ryi, float rzi, float4 pi, float qi, int rolei,
+                                          float4 rj, float4 pj, int rolej, float &e, float &gxi, float &gyi,
+                                          float &gzi, float &fx, float &fy, float &fz) {
+    const float dx = rxi - rj.x, dy = ryi - rj.y, dz = rzi - rj.z;
+    const float rho2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
+    float dE;
+    const float E = pair_eg(rho2, pi, qi, pj, rj.w, (rolei | rolej) == 3, dE);
+    dE = on ? dE : 0.0f;
+    e += on ? E : 0.0f;
+    gxi = fmaf(dE, dx, gxi); gyi = fmaf(dE, dy, gyi); gzi = fmaf(dE, dz, gzi);
+    fx = fmaf(-dE, dx, fx); fy = fmaf(-dE, dy, fy); fz = fmaf(-dE, dz, fz);
+}
+
+// Intramolecular energy and forces, every pair computed once, without atomics:
+//  * W x W tiles of atom chunks (I, J): at step s lane l pairs its atom I*W+l with
+//    J*W+((l+s) mod W); the partner's force accumulator travels with the partner (one
+//    lane shift per step) and returns to its owner after the tile.  Diagonal tiles use
+//    s = 1..W/2 (s = W/2 only for l < W/2), so each unordered pair appears once.
+//  * a short tail chunk (t atoms) is paired by broadcast: all lanes meet tail atom j at
+//    once and j's force is a butterfly sum.
+// Pair membership comes from bit rows (D1 pair list); fixed order -> deterministic.
+template <int W, int MAXC>
+__device__ __forceinline__ void intra_tiles(const LigSm &L, const Scratch &S, int sub, unsigned mask,
+                                            const float (&rx)[MAXC], const float (&ry)[MAXC], const float (&rz)[MAXC],
+                                            float (&gx)[MAXC], float (&gy)[MAXC], float (&gz)[MAXC], float &e) {
+    const int N = L.N;
+    const int Bf = N / W, t = N - Bf * W;
+    // cost model (issue slots): rotation of the tail as a padded chunk vs broadcast
+    const bool tail_rot = t > 0 && (W / 2 + Bf * W) * 53 < t * ((Bf + 1) * 50 + 3 * 5);
+    const int Bt = Bf + (tail_rot ? 1 : 0);
+    float4 pa[MAXC];
+    float qa[MAXC];
+    int ra[MAXC];
+    float hx[MAXC], hy[MAXC], hz[MAXC];   // pair-force sums (x 2 at the end)
+#pragma unroll
+    for (int c = 0; c < MAXC; ++c) {
+        const int a = sub + W * c;
+        const bool ok = a < N;
+        pa[c] = ok ? L.par[a] : make_float4(0.f, 0.f, 0.f, 0.f);
+        qa[c] = ok ? S.r[a].w : 0.0f;
+        ra[c] = ok ? (L.meta[a] >> 8) & 3 : 0;
+        hx[c] = hy[c] = hz[c] = 0.0f;
+    }
+#pragma unroll
+    for (int I = 0; I < MAXC; ++I) {
+        if (I >= Bt) break;
+#pragma unroll
+        for (int J = I; J < MAXC; ++J) {
+            if (J >= Bt) break;
+            const int aI = I * W + sub;
+            const int jb = J * W;
+            const uint32_t mw = aI < N ? (L.mask[aI * L.NW + (jb >> 5)] >> (jb & 31)) : 0u;
+            const int s0 = (I == J) ? 1 : 0, s1 = (I == J) ? W / 2 : W - 1;
+            float fx = 0.f, fy = 0.f, fz = 0.f;
+            for (int s = s0; s <= s1; ++s) {
+                const int jj = (sub + s) & (W - 1);
+                const int j = min(jb + jj, N - 1);
+                bool on = (mw >> jj) & 1u;
+                if (I == J && s == W / 2 && sub >= W / 2) on = false;
+                const float4 rj = S.r[j], pj = L.par[j];
+                const int rolej = (L.meta[j] >> 8) & 3;
+                tile_pair(on, rx[I], ry[I], rz[I], pa[I], qa[I], ra[I], rj, pj, rolej, e, hx[I], hy[I], hz[I], fx,
+                          fy, fz);
+                if (s < s1) {
+                    const int src = (sub + 1) & (W - 1);
+                    fx = __shfl_sync(mask, fx, src, W);
+                    fy = __shfl_sync(mask, fy, src, W);
+                    fz = __shfl_sync(mask, fz, src, W);
+                }
+            }
+            const int back = (sub - s1) & (W - 1);
+            fx = __shfl_sync(mask, fx, back, W);
+            fy = __shfl_sync(mask, fy, back, W);
+            fz = __shfl_sync(mask, fz, back, W);
+            hx[J] += fx; hy[J] += fy; hz[J] += fz;
+        }
+    }
+    if (t > 0 && !tail_rot) {
+        for (int k = 0; k < t; ++k) {
+            const int j = Bf * W + k;                       // uniform: shared-memory broadcast
+            const float4 rj = S.r[j], pj = L.par[j];
+            const int rolej = (L.meta[j] >> 8) & 3;
+            const uint32_t *mrow = L.mask + (size_t)j * L.NW;
+            float fx = 0.f, fy = 0.f, fz = 0.f;
+#pragma unroll
+            for (int I = 0; I < MAXC; ++I) {
+                if (I > Bf) break;
+                const int a = I * W + sub;
+                const bool on = (I < Bf || sub < k) && ((mrow[a >> 5] >> (a & 31)) & 1u);
+                tile_pair(on, rx[I], ry[I], rz[I], pa[I], qa[I], ra[I], rj, pj, rolej, e, hx[I], hy[I], hz[I], fx,
+                          fy, fz);
+            }
+            fx = gsum<W>(fx, mask); fy = gsum<W>(fy, mask); fz = gsum<W>(fz, mask);
+#pragma unroll
+            for (int c = 0; c < MAXC; ++c)
+                if (c == Bf && sub == k) { hx[c] += fx; hy[c] += fy; hz[c] += fz; }
+        }
+    }
+#pragma unroll
+    for (int c = 0; c < MAXC; ++c) {
+        gx[c] = fmaf(2.0f, hx[c], gx[c]); gy[c] = fmaf(2.0f, hy[c], gy[c]); gz[c] = fmaf(2.0f, hz[c], gz[c]);
+    }
+}
+
 // Energy (and genotype gradient into S.grad) of the genotype in S.genes.
 // Every lane of the group returns the same total energy.
 template <int W, int MAXC, bool GRAD>
@@ -144,9 +271,9 @@ __device__ float eval_group(const LigSm &L, const GridDev &grid, const Scratch &
     const float *x = S.genes;
     // ---- a3: orientation quaternion q = (cos a/2, sin(a/2) n) -> R(q) (D3) ----
     float sph, cph, sth, cth, sa, ca;
-    sincosf(x[3], &sph, &cph);
-    sincosf(x[4], &sth, &cth);
-    sincosf(0.5f * x[5], &sa, &ca);
+    fast_sincos(x[3], sph, cph);
+    fast_sincos(x[4], sth, cth);
+    fast_sincos(0.5f * x[5], sa, ca);
     const float nx = sth * cph, ny = sth * sph, nz = cth;
     const float qw = ca, qx = sa * nx, qy = sa * ny, qz = sa * nz;
     const float R00 = 1.f - 2.f * (qy * qy + qz * qz), R01 = 2.f * (qx * qy - qw * qz), R02 = 2.f * (qx * qz + qw * qy);
@@ -154,35 +281,51 @@ __device__ float eval_group(const LigSm &L, const GridDev &grid, const Scratch &
     const float R20 = 2.f * (qx * qz - qw * qy), R21 = 2.f * (qy * qz + qw * qx), R22 = 1.f - 2.f * (qx * qx + qy * qy);
     const float tx = x[0], ty = x[1], tz = x[2];
 
-    // ---- a3: torsion composites W_k = W_parent o Rot(u_k, tau_k) about A_k, level by level ----
+    // ---- a3: per-torsion local transform Rot(u_k, tau_k) about A_k (all torsions in
+    // parallel, lane-owned), then composites W_k = W_parent o local_k level by level ----
+    constexpr int KT = (kMaxTors + W - 1) / W;
+    float lr[KT][12];
+#pragma unroll
+    for (int tt = 0; tt < KT; ++tt) {
+        const int k = sub + W * tt;
+        if (k < L.T) {
+            float st, ct;
+            fast_sincos(x[6 + k], st, ct);
+            const float4 u = L.tU[k], A = L.tA[k];
+            const float oc = 1.0f - ct;
+            float *m = lr[tt];
+            m[0] = fmaf(oc * u.x, u.x, ct);     m[1] = fmaf(oc * u.x, u.y, -st * u.z); m[2] = fmaf(oc * u.x, u.z, st * u.y);
+            m[3] = fmaf(oc * u.y, u.x, st * u.z); m[4] = fmaf(oc * u.y, u.y, ct);    m[5] = fmaf(oc * u.y, u.z, -st * u.x);
+            m[6] = fmaf(oc * u.z, u.x, -st * u.y); m[7] = fmaf(oc * u.z, u.y, st * u.x); m[8] = fmaf(oc * u.z, u.z, ct);
+            m[9] = A.x - fmaf(m[0], A.x, fmaf(m[1], A.y, m[2] * A.z));
+            m[10] = A.y - fmaf(m[3], A.x, fmaf(m[4], A.y, m[5] * A.z));
+            m[11] = A.z - fmaf(m[6], A.x, fmaf(m[7], A.y, m[8] * A.z));
+        }
+    }
     for (int l = 0; l < L.n_levels; ++l) {
         const int k0 = L.lvl[l], k1 = L.lvl[l + 1];
-        for (int k = k0 + sub; k < k1; k += W) {
-            float st, ct;
-            sincosf(x[6 + k], &st, &ct);
-            const float4 u = L.tU[k], A = L.tA[k];
-            const int par = L.tmeta[k].x;
-            const float oc = 1.0f - ct;
-            const float k00 = ct + oc * u.x * u.x, k01 = oc * u.x * u.y - st * u.z, k02 = oc * u.x * u.z + st * u.y;
-            const float k10 = oc * u.y * u.x + st * u.z, k11 = ct + oc * u.y * u.y, k12 = oc * u.y * u.z - st * u.x;
-            const float k20 = oc * u.z * u.x - st * u.y, k21 = oc * u.z * u.y + st * u.x, k22 = ct + oc * u.z * u.z;
-            const float lx = A.x - (k00 * A.x + k01 * A.y + k02 * A.z);
-            const float ly = A.y - (k10 * A.x + k11 * A.y + k12 * A.z);
-            const float lz = A.z - (k20 * A.x + k21 * A.y + k22 * A.z);
-            float4 p0, p1, p2;
-            if (par < 0) {
-                p0 = make_float4(R00, R01, R02, tx);
-                p1 = make_float4(R10, R11, R12, ty);
-                p2 = make_float4(R20, R21, R22, tz);
-            } else {
-                p0 = S.W[3 * par]; p1 = S.W[3 * par + 1]; p2 = S.W[3 * par + 2];
+#pragma unroll
+        for (int tt = 0; tt < KT; ++tt) {
+            const int k = sub + W * tt;
+            if (k >= k0 && k < k1) {
+                const float *m = lr[tt];
+                const int par = L.tmeta[k].x;
+                float4 p0, p1, p2;
+                if (par < 0) {
+                    p0 = make_float4(R00, R01, R02, tx);
+                    p1 = make_float4(R10, R11, R12, ty);
+                    p2 = make_float4(R20, R21, R22, tz);
+                } else {
+                    p0 = S.W[3 * par]; p1 = S.W[3 * par + 1]; p2 = S.W[3 * par + 2];
+                }
+#define DK_ROW(P)                                                                                   \
+    make_float4(fmaf(P.x, m[0], fmaf(P.y, m[3], P.z * m[6])), fmaf(P.x, m[1], fmaf(P.y, m[4], P.z * m[7])), \
+                fmaf(P.x, m[2], fmaf(P.y, m[5], P.z * m[8])), fmaf(P.x, m[9], fmaf(P.y, m[10], fmaf(P.z, m[11], P.w))))
+                S.W[3 * k] = DK_ROW(p0);
+                S.W[3 * k + 1] = DK_ROW(p1);
+                S.W[3 * k + 2] = DK_ROW(p2);
+#undef DK_ROW
             }
-            S.W[3 * k] = make_float4(p0.x * k00 + p0.y * k10 + p0.z * k20, p0.x * k01 + p0.y * k11 + p0.z * k21,
-                                     p0.x * k02 + p0.y * k12 + p0.z * k22, p0.x * lx + p0.y * ly + p0.z * lz + p0.w);
-            S.W[3 * k + 1] = make_float4(p1.x * k00 + p1.y * k10 + p1.z * k20, p1.x * k01 + p1.y * k11 + p1.z * k21,
-                                         p1.x * k02 + p1.y * k12 + p1.z * k22, p1.x * lx + p1.y * ly + p1.z * lz + p1.w);
-            S.W[3 * k + 2] = make_float4(p2.x * k00 + p2.y * k10 + p2.z * k20, p2.x * k01 + p2.y * k11 + p2.z * k21,
-                                         p2.x * k02 + p2.y * k12 + p2.z * k22, p2.x * lx + p2.y * ly + p2.z * lz + p2.w);
         }
         __syncwarp(mask);
     }
@@ -199,14 +342,14 @@ __device__ float eval_group(const LigSm &L, const GridDev &grid, const Scratch &
             const int deep = (meta >> 16) - 1;
             const float4 p = L.p[a];
             if (deep < 0) {
-                rx[c] = R00 * p.x + R01 * p.y + R02 * p.z + tx;
-                ry[c] = R10 * p.x + R11 * p.y + R12 * p.z + ty;
-                rz[c] = R20 * p.x + R21 * p.y + R22 * p.z + tz;
+                rx[c] = fmaf(R00, p.x, fmaf(R01, p.y, fmaf(R02, p.z, tx)));
+                ry[c] = fmaf(R10, p.x, fmaf(R11, p.y, fmaf(R12, p.z, ty)));
+                rz[c] = fmaf(R20, p.x, fmaf(R21, p.y, fmaf(R22, p.z, tz)));
             } else {
                 const float4 w0 = S.W[3 * deep], w1 = S.W[3 * deep + 1], w2 = S.W[3 * deep + 2];
-                rx[c] = w0.x * p.x + w0.y * p.y + w0.z * p.z + w0.w;
-                ry[c] = w1.x * p.x + w1.y * p.y + w1.z * p.z + w1.w;
-                rz[c] = w2.x * p.x + w2.y * p.y + w2.z * p.z + w2.w;
+                rx[c] = fmaf(w0.x, p.x, fmaf(w0.y, p.y, fmaf(w0.z, p.z, w0.w)));
+                ry[c] = fmaf(w1.x, p.x, fmaf(w1.y, p.y, fmaf(w1.z, p.z, w1.w)));
+                rz[c] = fmaf(w2.x, p.x, fmaf(w2.y, p.y, fmaf(w2.z, p.z, w2.w)));
             }
             S.r[a] = make_float4(rx[c], ry[c], rz[c], p.w);
             e_part += inter_atom(grid, meta & 0xff, p.w, rx[c], ry[c], rz[c], gx[c], gy[c], gz[c]);
@@ -216,98 +359,75 @@ __device__ float eval_group(const LigSm &L, const GridDev &grid, const Scratch &
 
     // ---- a5: intramolecular pairs ----
     if constexpr (!GRAD) {
+#pragma unroll 4
         for (int q = sub; q < L.P; q += W) {
             const uint32_t w = L.pairs[q];
-            const int i = w & 0xff, j = (w >> 8) & 0xff;
-            const float4 ri = S.r[i], rj = S.r[j];
+            const float4 pp = L.pprm[q];
+            const float4 ri = S.r[w & 0xff], rj = S.r[(w >> 8) & 0xff];
             const float dx = ri.x - rj.x, dy = ri.y - rj.y, dz = ri.z - rj.z;
-            float dE;
-            e_part += pair_energy<false>(dx * dx + dy * dy + dz * dz, L.par[i], L.par[j], ri.w * rj.w,
-                                         (w >> 16) & 1, dE);
+            e_part += pair_e_pre(fmaf(dx, dx, fmaf(dy, dy, dz * dz)), pp, (w >> 16) & 1u);
         }
         return gsum<W>(e_part, mask);
     } else {
-    // gradient path: each lane owns its atoms' incidence lists (fixed order, no atomics);
-    // a pair's energy is counted by its lower-index owner only.
-#pragma unroll
-    for (int c = 0; c < MAXC; ++c) {
-        const int a = sub + W * c;
-        if (a < L.N) {
-            const float4 pa = L.par[a];
-            const float qa = L.p[a].w;
-            const int e0 = L.csr_off[a], e1 = L.csr_off[a + 1];
-            float fx = 0.f, fy = 0.f, fz = 0.f;
-            for (int e = e0; e < e1; ++e) {
-                const uint32_t nb = L.csr_nbr[e];
-                const int j = nb & 0xff;
-                const float4 rj = S.r[j];
-                const float dx = rx[c] - rj.x, dy = ry[c] - rj.y, dz = rz[c] - rj.z;
-                float dE;
-                const float E = pair_energy<true>(dx * dx + dy * dy + dz * dz, pa, L.par[j], qa * rj.w,
-                                                  (nb >> 8) & 1, dE);
-                if (a < j) e_part += E;
-                fx += dE * dx; fy += dE * dy; fz += dE * dz;
-            }
-            gx[c] += 2.0f * fx; gy[c] += 2.0f * fy; gz[c] += 2.0f * fz;
-        }
-    }
-    const float E = gsum<W>(e_part, mask);
+        intra_tiles<W, MAXC>(L, S, sub, mask, rx, ry, rz, gx, gy, gz, e_part);
+        const float E = gsum<W>(e_part, mask);
 
-    // ---- a6: back-projection to genotype space (D7) ----
-    float sgx = 0.f, sgy = 0.f, sgz = 0.f, Gx = 0.f, Gy = 0.f, Gz = 0.f;
+        // ---- a6: back-projection to genotype space (D7) ----
+        float sgx = 0.f, sgy = 0.f, sgz = 0.f, Gx = 0.f, Gy = 0.f, Gz = 0.f;
 #pragma unroll
-    for (int c = 0; c < MAXC; ++c) {
-        const int a = sub + W * c;
-        if (a < L.N) {
-            const float dx = rx[c] - tx, dy = ry[c] - ty, dz = rz[c] - tz;
-            const float cxp = dy * gz[c] - dz * gy[c], cyp = dz * gx[c] - dx * gz[c], czp = dx * gy[c] - dy * gx[c];
-            sgx += gx[c]; sgy += gy[c]; sgz += gz[c];
-            Gx += cxp; Gy += cyp; Gz += czp;
-            S.ts[2 * a] = make_float4(cxp, cyp, czp, 0.f);
-            S.ts[2 * a + 1] = make_float4(gx[c], gy[c], gz[c], 0.f);
+        for (int c = 0; c < MAXC; ++c) {
+            const int a = sub + W * c;
+            if (a < L.N) {
+                const float dx = rx[c] - tx, dy = ry[c] - ty, dz = rz[c] - tz;
+                const float cxp = fmaf(dy, gz[c], -dz * gy[c]), cyp = fmaf(dz, gx[c], -dx * gz[c]),
+                            czp = fmaf(dx, gy[c], -dy * gx[c]);
+                sgx += gx[c]; sgy += gy[c]; sgz += gz[c];
+                Gx += cxp; Gy += cyp; Gz += czp;
+                S.ts[2 * a] = make_float4(cxp, cyp, czp, 0.f);
+                S.ts[2 * a + 1] = make_float4(gx[c], gy[c], gz[c], 0.f);
+            }
         }
-    }
-    sgx = gsum<W>(sgx, mask); sgy = gsum<W>(sgy, mask); sgz = gsum<W>(sgz, mask);
-    Gx = gsum<W>(Gx, mask); Gy = gsum<W>(Gy, mask); Gz = gsum<W>(Gz, mask);
-    __syncwarp(mask);
-    // torsions: dE/dtau_k = w_k . sum_{a in moved(k)} (r_a - r_{a_k}) x g_a
-    for (int k = sub; k < L.T; k += W) {
-        const int4 tm = L.tmeta[k];
-        const int lo = tm.w & 0xffff, hi = tm.w >> 16;
-        float cx = 0.f, cy = 0.f, cz = 0.f, hx = 0.f, hy = 0.f, hz = 0.f;
-        for (int a = lo; a < hi; ++a) {
-            const float4 c4 = S.ts[2 * a], g4 = S.ts[2 * a + 1];
-            cx += c4.x; cy += c4.y; cz += c4.z;
-            hx += g4.x; hy += g4.y; hz += g4.z;
+        sgx = gsum<W>(sgx, mask); sgy = gsum<W>(sgy, mask); sgz = gsum<W>(sgz, mask);
+        Gx = gsum<W>(Gx, mask); Gy = gsum<W>(Gy, mask); Gz = gsum<W>(Gz, mask);
+        __syncwarp(mask);
+        // torsions: dE/dtau_k = w_k . sum_{a in moved(k)} (r_a - r_{a_k}) x g_a
+        for (int k = sub; k < L.T; k += W) {
+            const int4 tm = L.tmeta[k];
+            const int lo = tm.w & 0xffff, hi = tm.w >> 16;
+            float cx = 0.f, cy = 0.f, cz = 0.f, hx = 0.f, hy = 0.f, hz = 0.f;
+            for (int a = lo; a < hi; ++a) {
+                const float4 c4 = S.ts[2 * a], g4 = S.ts[2 * a + 1];
+                cx += c4.x; cy += c4.y; cz += c4.z;
+                hx += g4.x; hy += g4.y; hz += g4.z;
+            }
+            const float4 ra = S.r[tm.y], rb = S.r[tm.z];
+            const float dax = ra.x - tx, day = ra.y - ty, daz = ra.z - tz;
+            const float sx = cx - (day * hz - daz * hy), sy = cy - (daz * hx - dax * hz), sz = cz - (dax * hy - day * hx);
+            const float wx = rb.x - ra.x, wy = rb.y - ra.y, wz = rb.z - ra.z;
+            const float inw = rsqrtf(wx * wx + wy * wy + wz * wz);
+            S.grad[6 + k] = (wx * sx + wy * sy + wz * sz) * inw;
         }
-        const float4 ra = S.r[tm.y], rb = S.r[tm.z];
-        const float dax = ra.x - tx, day = ra.y - ty, daz = ra.z - tz;
-        const float sx = cx - (day * hz - daz * hy), sy = cy - (daz * hx - dax * hz), sz = cz - (dax * hy - day * hx);
-        float wx = rb.x - ra.x, wy = rb.y - ra.y, wz = rb.z - ra.z;
-        const float inw = rsqrtf(wx * wx + wy * wy + wz * wz);
-        S.grad[6 + k] = (wx * sx + wy * sy + wz * sz) * inw;
-    }
-    // translation and orientation: omega = adot n + sin(a) ndot + (1 - cos a) n x ndot
-    if (sub < 6) {
-        float v;
-        if (sub == 0) v = sgx;
-        else if (sub == 1) v = sgy;
-        else if (sub == 2) v = sgz;
-        else if (sub == 5) v = Gx * nx + Gy * ny + Gz * nz;
-        else {
-            const float sal = 2.0f * sa * ca, omc = 2.0f * sa * sa;   // sin(alpha), 1 - cos(alpha)
-            float dnx, dny, dnz;
-            if (sub == 3) { dnx = -sth * sph; dny = sth * cph; dnz = 0.0f; }
-            else { dnx = cth * cph; dny = cth * sph; dnz = -sth; }
-            const float wx = sal * dnx + omc * (ny * dnz - nz * dny);
-            const float wy = sal * dny + omc * (nz * dnx - nx * dnz);
-            const float wz = sal * dnz + omc * (nx * dny - ny * dnx);
-            v = Gx * wx + Gy * wy + Gz * wz;
+        // translation and orientation: omega = adot n + sin(a) ndot + (1 - cos a) n x ndot
+        if (sub < 6) {
+            float v;
+            if (sub == 0) v = sgx;
+            else if (sub == 1) v = sgy;
+            else if (sub == 2) v = sgz;
+            else if (sub == 5) v = Gx * nx + Gy * ny + Gz * nz;
+            else {
+                const float sal = 2.0f * sa * ca, omc = 2.0f * sa * sa;   // sin(alpha), 1 - cos(alpha)
+                float dnx, dny, dnz;
+                if (sub == 3) { dnx = -sth * sph; dny = sth * cph; dnz = 0.0f; }
+                else { dnx = cth * cph; dny = cth * sph; dnz = -sth; }
+                const float wx = sal * dnx + omc * (ny * dnz - nz * dny);
+                const float wy = sal * dny + omc * (nz * dnx - nx * dnz);
+                const float wz = sal * dnz + omc * (nx * dny - ny * dnx);
+                v = Gx * wx + Gy * wy + Gz * wz;
+            }
+            S.grad[sub] = v;
         }
-        S.grad[sub] = v;
-    }
-    __syncwarp(mask);
-    return E;
+        __syncwarp(mask);
+        return E;
     }
 }
 
