@@ -175,6 +175,47 @@ int dock_ls_step(dock_ctx *ctx, int32_t method, int32_t n, int32_t iters, uint64
                  uint32_t ligand_id, int32_t run, int32_t gen, const int32_t *slots,
                  float *genes, float *energy, int64_t *evals);
 
+/* ---------------- multi-ligand / multi-GPU screen ----------------
+   PAPER.md:34-38 [§I]: docking a ligand library is "a load balancing and dataflow
+   execution optimization problem"; runs (and ligands) are independent.
+   dock_screen docks n_ligands ligands against one receptor: host preprocessing (D1) on a
+   thread pool, longest-first order by the cost model 40 P + 133 N, one receptor upload
+   per device, `slots_per_device` ligands in flight per device (one stream each), one
+   worker thread per slot pulling the next ligand.  No collective: every ligand's result
+   is written to the caller's arrays by the worker that docked it.
+   Each ligand i is docked exactly as dock_run_ex(pop_size, num_runs, run_base 0,
+   ligand_id = ligand_ids ? ligand_ids[i] : i, max_evals, seed) would dock it, so results
+   are identical whatever the device count, slot count or order.
+   Outputs per ligand i (host, caller-allocated): best_energy[i] = min over runs (NaN if
+   status[i] != DOCK_OK); best_run[i] (lowest run on ties; may be NULL);
+   best_genotype[i*DOCK_MAX_GENES ..] (G genes, zero padded); evals_used[i] = sum over
+   runs (may be NULL); status[i] = DOCK_OK or DOCK_E_INPUT for a rejected ligand (the
+   screen continues; may be NULL); device_of[i] = CUDA device that docked it (may be NULL).
+   params->device is ignored (opts selects devices).  Returns DOCK_E_INPUT for bad shared
+   arguments, DOCK_E_INTERNAL on a CUDA error (dock_screen_last_error() says where). */
+typedef struct {
+    int32_t n_devices;           /* 0 = every visible device */
+    const int32_t *devices;      /* [n_devices] ordinals, or NULL for 0..n_devices-1 */
+    int32_t slots_per_device;    /* ligands in flight per device, 0 = 4 */
+    int32_t prep_threads;        /* host preprocessing threads, 0 = hardware concurrency */
+} dock_screen_opts;
+
+typedef struct {
+    double prep_ms;              /* wall time of the preprocessing pool */
+    double dock_ms;              /* wall time from first dispatch to last result */
+    int64_t total_evals;
+    int32_t n_failed;            /* ligands with status DOCK_E_INPUT */
+    int64_t launches;            /* kernel launches (graph nodes counted) */
+} dock_screen_stats;
+
+int dock_screen(const dock_grids *grids, const dock_type_param *type_params,
+                const dock_ligand *ligands, int32_t n_ligands, const uint32_t *ligand_ids,
+                const dock_params *params, const dock_screen_opts *opts, int32_t pop_size,
+                int32_t num_runs, int64_t max_evals, uint64_t seed, float *best_energy,
+                int32_t *best_run, float *best_genotype, int64_t *evals_used, int32_t *status,
+                int32_t *device_of, dock_screen_stats *stats);
+const char *dock_screen_last_error(void);
+
 /* Kernel-launch counter of this context (for the benchmark's gpu_launches claim). */
 int64_t dock_launch_count(const dock_ctx *ctx);
 

@@ -14,33 +14,7 @@
 #include <string>
 #include <vector>
 
-#include "../../include/dock.h"
-#include "kernels.cuh"
-#include "prep.h"
-
-struct dock_ctx {
-    int device = 0;
-    cudaStream_t stream = nullptr;
-    dk::Prepared prep;
-    dk::LigDev lig{};
-    dk::GridDev grid{};
-    dock_params params{};
-    float4 *d_maps = nullptr;
-    size_t maps_bytes = 0;
-    uint8_t *d_blob = nullptr;
-    int *d_dfs2orig = nullptr;
-    int cap_runs = 0, cap_pop = 0;
-    float *d_genes = nullptr, *d_E = nullptr;
-    dk::RunState *d_state = nullptr;
-    int *d_perm = nullptr, *d_ls_evals = nullptr;
-    dk::RunState *h_state = nullptr;
-    int h_state_cap = 0;
-    std::string err;
-    long long launches = 0;
-    double prof_ms[3] = {0, 0, 0};
-    long long prof_n[3] = {0, 0, 0};
-    std::vector<cudaEvent_t> events;   // profiling: 3 per captured generation + 2 for init
-};
+#include "engine.h"
 
 namespace {
 
@@ -58,21 +32,6 @@ thread_local std::string g_init_error;
 int input_error(dock_ctx *c, const std::string &m) {
     if (c) c->err = m;
     return DOCK_E_INPUT;
-}
-
-bool prob_ok(float p) { return std::isfinite(p) && p >= 0.f && p <= 1.f; }
-
-int validate_params(const dock_params &p, std::string *err) {
-    if (!prob_ok(p.p_tour) || !prob_ok(p.p_cross) || !prob_ok(p.p_mut)) { *err = "params: probabilities must be in [0,1]"; return DOCK_E_INPUT; }
-    if (!std::isfinite(p.mut_trans) || !std::isfinite(p.mut_angle) || p.mut_trans < 0 || p.mut_angle < 0) { *err = "params.mut_*: must be finite, >= 0"; return DOCK_E_INPUT; }
-    if (p.ls_method != DOCK_LS_ADADELTA && p.ls_method != DOCK_LS_SOLIS_WETS) { *err = "params.ls_method: 0 or 1"; return DOCK_E_INPUT; }
-    if (!prob_ok(p.ls_rate)) { *err = "params.ls_rate: must be in [0,1]"; return DOCK_E_INPUT; }
-    if (p.ls_max_iters < 0) { *err = "params.ls_max_iters: must be >= 0"; return DOCK_E_INPUT; }
-    if (!(p.sw_rho > 0) || !(p.sw_rho_min > 0) || !(p.sw_expand > 0) || !(p.sw_contract > 0) || p.sw_cons_succ < 1 || p.sw_cons_fail < 1) { *err = "params.sw_*: must be positive"; return DOCK_E_INPUT; }
-    if (!(p.ad_rho >= 0 && p.ad_rho < 1) || !(p.ad_eps > 0)) { *err = "params.ad_rho in [0,1), ad_eps > 0"; return DOCK_E_INPUT; }
-    if (p.max_generations < 0) { *err = "params.max_generations: must be >= 0"; return DOCK_E_INPUT; }
-    if (p.gens_per_graph < 1 || p.gens_per_graph > 4096) { *err = "params.gens_per_graph: 1..4096"; return DOCK_E_INPUT; }
-    return DOCK_OK;
 }
 
 // n_ls = ceil(ls_rate * pop - 1e-4) clamped to [0, pop] (DESIGN.md §3 reading 16a).
@@ -142,6 +101,107 @@ struct DevBuf {
 
 }  // namespace
 
+namespace dk {
+
+bool prob_ok(float p) { return std::isfinite(p) && p >= 0.f && p <= 1.f; }
+
+int validate_params(const dock_params &p, std::string *err) {
+    if (!prob_ok(p.p_tour) || !prob_ok(p.p_cross) || !prob_ok(p.p_mut)) { *err = "params: probabilities must be in [0,1]"; return DOCK_E_INPUT; }
+    if (!std::isfinite(p.mut_trans) || !std::isfinite(p.mut_angle) || p.mut_trans < 0 || p.mut_angle < 0) { *err = "params.mut_*: must be finite, >= 0"; return DOCK_E_INPUT; }
+    if (p.ls_method != DOCK_LS_ADADELTA && p.ls_method != DOCK_LS_SOLIS_WETS) { *err = "params.ls_method: 0 or 1"; return DOCK_E_INPUT; }
+    if (!prob_ok(p.ls_rate)) { *err = "params.ls_rate: must be in [0,1]"; return DOCK_E_INPUT; }
+    if (p.ls_max_iters < 0) { *err = "params.ls_max_iters: must be >= 0"; return DOCK_E_INPUT; }
+    if (!(p.sw_rho > 0) || !(p.sw_rho_min > 0) || !(p.sw_expand > 0) || !(p.sw_contract > 0) || p.sw_cons_succ < 1 || p.sw_cons_fail < 1) { *err = "params.sw_*: must be positive"; return DOCK_E_INPUT; }
+    if (!(p.ad_rho >= 0 && p.ad_rho < 1) || !(p.ad_eps > 0)) { *err = "params.ad_rho in [0,1), ad_eps > 0"; return DOCK_E_INPUT; }
+    if (p.max_generations < 0) { *err = "params.max_generations: must be >= 0"; return DOCK_E_INPUT; }
+    if (p.gens_per_graph < 1 || p.gens_per_graph > 4096) { *err = "params.gens_per_graph: 1..4096"; return DOCK_E_INPUT; }
+    return DOCK_OK;
+}
+
+Receptor::~Receptor() {
+    if (d_maps) { cudaSetDevice(device); cudaFree(d_maps); }
+}
+
+int receptor_upload(const dock_grids *grids, const std::vector<float4> &packed, int device,
+                    std::shared_ptr<Receptor> *out, std::string *err) {
+    auto r = std::make_shared<Receptor>();
+    r->device = device;
+    r->bytes = packed.size() * sizeof(float4);
+    if (cudaSetDevice(device) != cudaSuccess || cudaMalloc(&r->d_maps, r->bytes) != cudaSuccess ||
+        cudaMemcpy(r->d_maps, packed.data(), r->bytes, cudaMemcpyHostToDevice) != cudaSuccess) {
+        cudaGetLastError();
+        *err = "receptor upload to device " + std::to_string(device) + " failed";
+        return DOCK_E_INTERNAL;
+    }
+    GridDev &g = r->grid;
+    g.maps = r->d_maps;
+    g.nx = grids->nx; g.ny = grids->ny; g.nz = grids->nz; g.n_types = grids->n_types;
+    g.ox = grids->origin[0]; g.oy = grids->origin[1]; g.oz = grids->origin[2];
+    g.s = grids->spacing; g.inv_s = 1.0f / grids->spacing;
+    g.hx = g.ox + (float)(g.nx - 1) * g.s; g.hy = g.oy + (float)(g.ny - 1) * g.s; g.hz = g.oz + (float)(g.nz - 1) * g.s;
+    *out = std::move(r);
+    return DOCK_OK;
+}
+
+int ctx_create(std::shared_ptr<Receptor> rec, const dock_params &p, dock_ctx **out, std::string *err) {
+    *out = nullptr;
+    auto *c = new dock_ctx();
+    c->params = p;
+    c->device = rec->device;
+    c->grid = rec->grid;
+    c->rec = std::move(rec);
+    auto bail = [&](const std::string &m) { *err = m; dock_free(c); return (int)DOCK_E_INTERNAL; };
+    if (cudaSetDevice(c->device) != cudaSuccess) return bail("cudaSetDevice failed");
+    if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess) return bail("cudaStreamCreate failed");
+    if (setup_kernel_attributes() != cudaSuccess) return bail("cudaFuncSetAttribute failed (is this an sm_100 device?)");
+    if (cudaMalloc(&c->d_dfs2orig, sizeof(int) * kMaxAtoms) != cudaSuccess) return bail("device allocation failed");
+    if (p.l2_persist) {
+        // NS: "Grid maps live in HBM with L2-persistence windows".
+        cudaDeviceProp prop;
+        if (cudaGetDeviceProperties(&prop, c->device) == cudaSuccess && prop.persistingL2CacheMaxSize > 0 &&
+            prop.accessPolicyMaxWindowSize > 0) {
+            const size_t win = std::min(c->rec->bytes, (size_t)prop.accessPolicyMaxWindowSize);
+            const size_t lim = std::min(win, (size_t)prop.persistingL2CacheMaxSize);
+            cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, lim);
+            cudaStreamAttrValue attr{};
+            attr.accessPolicyWindow.base_ptr = c->rec->d_maps;
+            attr.accessPolicyWindow.num_bytes = win;
+            attr.accessPolicyWindow.hitRatio = (float)std::min(1.0, (double)lim / (double)win);
+            attr.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+            attr.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+            cudaStreamSetAttribute(c->stream, cudaStreamAttributeAccessPolicyWindow, &attr);
+        }
+        cudaGetLastError();   // the window is an optimisation: never fatal
+    }
+    *out = c;
+    return DOCK_OK;
+}
+
+int ctx_reserve(dock_ctx *c, size_t blob_bytes, int runs, int pop) {
+    CK(cudaSetDevice(c->device));
+    if (blob_bytes > c->blob_cap) {
+        if (c->d_blob) { CK(cudaStreamSynchronize(c->stream)); cudaFree(c->d_blob); }
+        c->d_blob = nullptr; c->blob_cap = 0;
+        CK(cudaMalloc(&c->d_blob, blob_bytes));
+        c->blob_cap = blob_bytes;
+    }
+    if (runs > 0 && pop > 0) return ensure_buffers(c, runs, pop);
+    return DOCK_OK;
+}
+
+int ctx_attach_ligand(dock_ctx *c, Prepared &&p) {
+    c->prep = std::move(p);
+    if (int rc = ctx_reserve(c, c->prep.blob.size(), 0, 0)) return rc;
+    CK(cudaMemcpyAsync(c->d_blob, c->prep.blob.data(), c->prep.blob.size(), cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemcpyAsync(c->d_dfs2orig, c->prep.dfs2orig.data(), sizeof(int) * c->prep.N, cudaMemcpyHostToDevice, c->stream));
+    CK(cudaStreamSynchronize(c->stream));   // host vectors may be reused by the caller
+    c->lig = c->prep.layout;
+    c->lig.blob = c->d_blob;
+    return DOCK_OK;
+}
+
+}  // namespace dk
+
 extern "C" {
 
 int dock_params_default(dock_params *p) {
@@ -177,61 +237,23 @@ int dock_init(const dock_grids *grids, const dock_type_param *type_params, const
     dock_params p;
     if (params) p = *params; else dock_params_default(&p);
     std::string err;
-    if (validate_params(p, &err) != DOCK_OK) { g_init_error = err; return DOCK_E_INPUT; }
+    if (dk::validate_params(p, &err) != DOCK_OK) { g_init_error = err; return DOCK_E_INPUT; }
     std::vector<float4> packed;
     if (dk::pack_grid(grids, &packed, &err) != DOCK_OK) { g_init_error = err; return DOCK_E_INPUT; }
-    auto *c = new dock_ctx();
-    c->params = p;
-    if (dk::prepare_ligand(ligand, type_params, grids->n_types, &c->prep, &err) != DOCK_OK) {
-        g_init_error = err; delete c; return DOCK_E_INPUT;
-    }
+    dk::Prepared prep;
+    if (dk::prepare_ligand(ligand, type_params, grids->n_types, &prep, &err) != DOCK_OK) { g_init_error = err; return DOCK_E_INPUT; }
     int ndev = 0;
     if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev < 1) {
         cudaGetLastError();
-        g_init_error = "no CUDA device (this library has no CPU fallback)"; delete c; return DOCK_E_INTERNAL;
+        g_init_error = "no CUDA device (this library has no CPU fallback)";
+        return DOCK_E_INTERNAL;
     }
-    if (p.device < 0 || p.device >= ndev) { g_init_error = "params.device: no such CUDA device"; delete c; return DOCK_E_INPUT; }
-    c->device = p.device;
-    auto bail = [&](int rc) { g_init_error = c->err; dock_free(c); return rc; };
-    if (cudaSetDevice(c->device) != cudaSuccess) { c->err = "cudaSetDevice failed"; return bail(DOCK_E_INTERNAL); }
-    if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess) { c->err = "cudaStreamCreate failed"; return bail(DOCK_E_INTERNAL); }
-    if (dk::setup_kernel_attributes() != cudaSuccess) { c->err = "cudaFuncSetAttribute failed (is this an sm_100 device?)"; return bail(DOCK_E_INTERNAL); }
-    c->maps_bytes = packed.size() * sizeof(float4);
-    if (cudaMalloc(&c->d_maps, c->maps_bytes) != cudaSuccess ||
-        cudaMemcpy(c->d_maps, packed.data(), c->maps_bytes, cudaMemcpyHostToDevice) != cudaSuccess ||
-        cudaMalloc(&c->d_blob, c->prep.blob.size()) != cudaSuccess ||
-        cudaMemcpy(c->d_blob, c->prep.blob.data(), c->prep.blob.size(), cudaMemcpyHostToDevice) != cudaSuccess ||
-        cudaMalloc(&c->d_dfs2orig, sizeof(int) * c->prep.N) != cudaSuccess ||
-        cudaMemcpy(c->d_dfs2orig, c->prep.dfs2orig.data(), sizeof(int) * c->prep.N, cudaMemcpyHostToDevice) != cudaSuccess) {
-        c->err = "device allocation/upload failed";
-        return bail(DOCK_E_INTERNAL);
-    }
-    c->lig = c->prep.layout;
-    c->lig.blob = c->d_blob;
-    dk::GridDev &g = c->grid;
-    g.maps = c->d_maps;
-    g.nx = grids->nx; g.ny = grids->ny; g.nz = grids->nz; g.n_types = grids->n_types;
-    g.ox = grids->origin[0]; g.oy = grids->origin[1]; g.oz = grids->origin[2];
-    g.s = grids->spacing; g.inv_s = 1.0f / grids->spacing;
-    g.hx = g.ox + (float)(g.nx - 1) * g.s; g.hy = g.oy + (float)(g.ny - 1) * g.s; g.hz = g.oz + (float)(g.nz - 1) * g.s;
-    if (p.l2_persist) {
-        // NS: "Grid maps live in HBM with L2-persistence windows".
-        cudaDeviceProp prop;
-        if (cudaGetDeviceProperties(&prop, c->device) == cudaSuccess && prop.persistingL2CacheMaxSize > 0 &&
-            prop.accessPolicyMaxWindowSize > 0) {
-            const size_t win = std::min(c->maps_bytes, (size_t)prop.accessPolicyMaxWindowSize);
-            const size_t lim = std::min(win, (size_t)prop.persistingL2CacheMaxSize);
-            cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, lim);
-            cudaStreamAttrValue attr{};
-            attr.accessPolicyWindow.base_ptr = c->d_maps;
-            attr.accessPolicyWindow.num_bytes = win;
-            attr.accessPolicyWindow.hitRatio = (float)std::min(1.0, (double)lim / (double)win);
-            attr.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
-            attr.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
-            cudaStreamSetAttribute(c->stream, cudaStreamAttributeAccessPolicyWindow, &attr);
-        }
-        cudaGetLastError();   // the window is an optimisation: never fatal
-    }
+    if (p.device < 0 || p.device >= ndev) { g_init_error = "params.device: no such CUDA device"; return DOCK_E_INPUT; }
+    std::shared_ptr<dk::Receptor> rec;
+    if (int rc = dk::receptor_upload(grids, packed, p.device, &rec, &err)) { g_init_error = err; return rc; }
+    dock_ctx *c = nullptr;
+    if (int rc = dk::ctx_create(rec, p, &c, &err)) { g_init_error = err; return rc; }
+    if (int rc = dk::ctx_attach_ligand(c, std::move(prep))) { g_init_error = c->err; dock_free(c); return rc; }
     *out = c;
     return DOCK_OK;
 }
@@ -240,13 +262,13 @@ void dock_free(dock_ctx *c) {
     if (!c) return;
     cudaSetDevice(c->device);
     if (c->stream) cudaStreamSynchronize(c->stream);
-    cudaFree(c->d_maps); cudaFree(c->d_blob); cudaFree(c->d_dfs2orig);
+    cudaFree(c->d_blob); cudaFree(c->d_dfs2orig);
     cudaFree(c->d_genes); cudaFree(c->d_E); cudaFree(c->d_state); cudaFree(c->d_perm); cudaFree(c->d_ls_evals);
     if (c->h_state) cudaFreeHost(c->h_state);
     for (cudaEvent_t e : c->events) cudaEventDestroy(e);
     if (c->stream) cudaStreamDestroy(c->stream);
     cudaGetLastError();
-    delete c;
+    delete c;   // drops this context's reference to the receptor upload
 }
 
 const char *dock_last_error(const dock_ctx *c) { return c ? c->err.c_str() : g_init_error.c_str(); }
@@ -257,7 +279,7 @@ int dock_n_pairs(const dock_ctx *c) { return c ? c->prep.P : -1; }
 int64_t dock_launch_count(const dock_ctx *c) { return c ? c->launches : -1; }
 
 int64_t dock_upload_bytes(const dock_ctx *c) {
-    return c ? (int64_t)(c->maps_bytes + c->prep.blob.size() + sizeof(int) * c->prep.N) : -1;
+    return c ? (int64_t)(c->rec->bytes + c->prep.blob.size() + sizeof(int) * c->prep.N) : -1;
 }
 
 int dock_kernel_stats(const dock_ctx *c, double *ms, int64_t *launches) {

@@ -1,0 +1,76 @@
+// engine.h — host-side engine objects shared by the single-ligand ABI (dock_abi.cpp)
+// and the multi-ligand / multi-GPU scheduler (screen.cpp).
+//
+//   Receptor  one upload of the packed grid maps per device ("every GPU
+//             holds its own copy of the receptor grid"); shared by every context on it.
+//   dock_ctx  one (device, stream, ligand block, population buffers) engine.  A screen
+//             worker keeps one dock_ctx per in-flight slot and swaps ligands into it.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "../../include/dock.h"
+#include "kernels.cuh"
+#include "prep.h"
+
+namespace dk {
+
+struct Receptor {
+    int device = 0;
+    float4 *d_maps = nullptr;
+    size_t bytes = 0;
+    GridDev grid{};
+    Receptor() = default;
+    Receptor(const Receptor &) = delete;
+    Receptor &operator=(const Receptor &) = delete;
+    ~Receptor();
+};
+
+// Upload packed maps (pack_grid output) to `device`.  DOCK_OK / DOCK_E_INTERNAL.
+int receptor_upload(const dock_grids *g, const std::vector<float4> &packed, int device,
+                    std::shared_ptr<Receptor> *out, std::string *err);
+
+}  // namespace dk
+
+struct dock_ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    std::shared_ptr<dk::Receptor> rec;
+    dk::Prepared prep;
+    dk::LigDev lig{};
+    dk::GridDev grid{};
+    dock_params params{};
+    uint8_t *d_blob = nullptr;
+    size_t blob_cap = 0;
+    int *d_dfs2orig = nullptr;
+    int cap_runs = 0, cap_pop = 0;
+    float *d_genes = nullptr, *d_E = nullptr;
+    dk::RunState *d_state = nullptr;
+    int *d_perm = nullptr, *d_ls_evals = nullptr;
+    dk::RunState *h_state = nullptr;
+    int h_state_cap = 0;
+    std::string err;
+    long long launches = 0;
+    double prof_ms[3] = {0, 0, 0};
+    long long prof_n[3] = {0, 0, 0};
+    std::vector<cudaEvent_t> events;   // profiling: 3 per captured generation + 2 for init
+};
+
+namespace dk {
+
+// New context on rec->device with its own non-blocking stream and the grid's L2
+// persistence window (NS).  No ligand attached yet.
+int ctx_create(std::shared_ptr<Receptor> rec, const dock_params &p, dock_ctx **out, std::string *err);
+
+// Move a prepared ligand into the context and upload its constant block on the context's
+// stream.  Device buffers only grow (reserve_blob pre-sizes them so a screen never frees
+// device memory, which would synchronise the whole device, while other slots run).
+int ctx_attach_ligand(dock_ctx *c, Prepared &&p);
+int ctx_reserve(dock_ctx *c, size_t blob_bytes, int runs, int pop);
+
+int validate_params(const dock_params &p, std::string *err);
+
+}  // namespace dk
