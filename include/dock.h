@@ -86,6 +86,10 @@ typedef struct {
     int32_t l2_persist;          /* 1: pin the grid in L2 with an access-policy window */
     int32_t gens_per_graph;      /* generations per CUDA-graph launch (>= 1) */
     int32_t profile;             /* 1: CUDA events around every GA and LS launch (dock_kernel_stats) */
+    int32_t sw_depth;            /* Solis-Wets speculation depth: 0 = auto (deepest whose launch fits one
+                                    wave), 1 = both trial points of one iteration at once, 2 or 3 =
+                                    the 3-way outcome tree of 2 / 3 iterations (3^D - 1 lane groups
+                                    per individual).  Results are identical for every depth (D9). */
 } dock_params;
 
 /* Fills the defaults: p_tour .60, p_cross .80, p_mut .02, 2.0 Å / 0.523 rad, ADADELTA,

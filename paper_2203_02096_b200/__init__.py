@@ -14,7 +14,8 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libdock.so")
+# DOCK_LIB selects an experimental in-tree build variant (scripts/variants.py); default: the product library.
+LIB_PATH = os.environ.get("DOCK_LIB") or os.path.join(_HERE, "libdock.so")
 
 DOCK_OK, DOCK_E_INPUT, DOCK_E_INTERNAL = 0, 1, 2
 LS_ADADELTA, LS_SOLIS_WETS = 0, 1
@@ -49,7 +50,20 @@ class Params(C.Structure):
                 ("sw_rho_min", C.c_float), ("sw_expand", C.c_float), ("sw_contract", C.c_float),
                 ("sw_cons_succ", C.c_int32), ("sw_cons_fail", C.c_int32), ("ad_rho", C.c_float),
                 ("ad_eps", C.c_float), ("max_generations", C.c_int32), ("device", C.c_int32),
-                ("l2_persist", C.c_int32), ("gens_per_graph", C.c_int32), ("profile", C.c_int32)]
+                ("l2_persist", C.c_int32), ("gens_per_graph", C.c_int32), ("profile", C.c_int32), ("sw_depth", C.c_int32)]
+
+
+class ScreenOpts(C.Structure):
+    _fields_ = [("n_devices", C.c_int32), ("devices", C.POINTER(C.c_int32)), ("slots_per_device", C.c_int32),
+                ("prep_threads", C.c_int32)]
+
+
+class ScreenStats(C.Structure):
+    _fields_ = [("prep_ms", C.c_double), ("dock_ms", C.c_double), ("total_evals", C.c_int64),
+                ("n_failed", C.c_int32), ("launches", C.c_int64)]
+
+
+MAX_GENES = 38
 
 
 def _load():
@@ -81,6 +95,9 @@ def _load():
         "dock_launch_count": (i64, [v]),
         "dock_kernel_stats": (i32, [v, P(C.c_double), P(i64)]),
         "dock_upload_bytes": (i64, [v]),
+        "dock_screen": (i32, [P(Grids), P(TypeParam), P(Ligand), i32, P(u32), P(Params), P(ScreenOpts), i32, i32,
+                              i64, u64, P(f), P(i32), P(f), P(i64), P(i32), P(i32), P(ScreenStats)]),
+        "dock_screen_last_error": (C.c_char_p, []),
         "dock_topology": (i32, [P(Ligand), P(TypeParam), i32, P(i32), P(i32), P(C.c_uint8), P(i32), P(i32), i32]),
     }
     for name, (res, args) in sig.items():
@@ -95,7 +112,7 @@ EXPORTED = ("dock_params_default", "dock_builtin_type_param", "dock_init", "dock
             "dock_n_atoms", "dock_n_torsions", "dock_n_genes", "dock_n_pairs", "dock_run", "dock_run_ex",
             "dock_run_device", "dock_eval", "dock_eval_device", "dock_get_pairs", "dock_get_torsions",
             "dock_philox", "dock_stream_words", "dock_ga_step", "dock_ls_step", "dock_launch_count",
-            "dock_topology", "dock_kernel_stats", "dock_upload_bytes")
+            "dock_topology", "dock_kernel_stats", "dock_upload_bytes", "dock_screen", "dock_screen_last_error")
 
 
 def topology(types, charges, xyz, bonds, rotatable, type_params, roles):
@@ -162,6 +179,80 @@ def philox(ctr, key):
 def stream_words(seed, ligand_id, purpose, slot, gen, run, m0, n):
     out = np.zeros(n, np.uint32)
     _check(lib.dock_stream_words(seed, ligand_id, purpose, slot, gen, run, m0, n, _ptr(out, C.c_uint32)))
+    return out
+
+
+def _grids_struct(maps, n, spacing, origin, n_types):
+    g = Grids()
+    g.nx, g.ny, g.nz = (int(v) for v in n)
+    g.spacing = float(spacing)
+    for d in range(3):
+        g.origin[d] = float(origin[d])
+    g.n_types = int(n_types)
+    g.maps = _ptr(maps, C.c_float)
+    return g
+
+
+def _type_array(type_params, roles):
+    tp = np.asarray(type_params, dtype=np.float32).reshape(-1, 4)
+    roles = np.asarray(roles, dtype=np.int32).reshape(-1)
+    tarr = (TypeParam * tp.shape[0])()
+    for t in range(tp.shape[0]):
+        tarr[t] = TypeParam(*(float(x) for x in tp[t]), int(roles[t]))
+    return tarr, tp.shape[0]
+
+
+def screen(grid, ligands, pop, runs, max_evals, seed, ligand_ids=None, devices=None, slots_per_device=0,
+           prep_threads=0, params: Params | None = None, **overrides):
+    """dock_screen (include/dock.h): dock every ligand against one receptor on the given
+    CUDA devices.  grid: gen.synth-like object (maps/n/spacing/origin/type_params());
+    ligands: objects with types/charges/xyz/bonds/rotatable.  Returns a dict of per-ligand
+    arrays (best_E, best_run, best_genes [n, 38] zero padded, evals, status, device) and
+    the screen stats."""
+    maps = np.ascontiguousarray(grid.maps, dtype=np.float32).reshape(-1)
+    tp, roles = grid.type_params()
+    tarr, nt = _type_array(tp, roles)
+    g = _grids_struct(maps, grid.n, grid.spacing, grid.origin, nt)
+    n = len(ligands)
+    keep = []
+    larr = (Ligand * max(n, 1))()
+    for i, lig in enumerate(ligands):
+        t = np.ascontiguousarray(lig.types, dtype=np.int32)
+        q = np.ascontiguousarray(lig.charges, dtype=np.float32)
+        x = np.ascontiguousarray(lig.xyz, dtype=np.float32).reshape(-1)
+        b = np.ascontiguousarray(lig.bonds, dtype=np.int32).reshape(-1)
+        r = np.ascontiguousarray(lig.rotatable, dtype=np.uint8)
+        keep.append((t, q, x, b, r))
+        L = larr[i]
+        L.n_atoms = t.shape[0]; L.type = _ptr(t, C.c_int32); L.charge = _ptr(q, C.c_float)
+        L.xyz = _ptr(x, C.c_float); L.n_bonds = b.shape[0] // 2
+        L.bonds = _ptr(b, C.c_int32) if L.n_bonds else None
+        L.rotatable = _ptr(r, C.c_uint8) if L.n_bonds else None
+    ids = None if ligand_ids is None else np.ascontiguousarray(ligand_ids, dtype=np.uint32)
+    if params is None:
+        params = params_default(**overrides)
+    else:
+        for k, val in overrides.items():
+            setattr(params, k, val)
+    o = ScreenOpts()
+    dv = None
+    if devices is not None:
+        dv = np.ascontiguousarray(devices, dtype=np.int32)
+        o.n_devices = dv.shape[0]; o.devices = _ptr(dv, C.c_int32)
+    o.slots_per_device = int(slots_per_device); o.prep_threads = int(prep_threads)
+    out = dict(best_E=np.zeros(n, np.float32), best_run=np.zeros(n, np.int32),
+               best_genes=np.zeros((n, MAX_GENES), np.float32), evals=np.zeros(n, np.int64),
+               status=np.zeros(n, np.int32), device=np.zeros(n, np.int32))
+    st = ScreenStats()
+    rc = lib.dock_screen(C.byref(g), tarr, larr, n, _ptr(ids, C.c_uint32), C.byref(params), C.byref(o), pop, runs,
+                         max_evals, seed, _ptr(out["best_E"], C.c_float), _ptr(out["best_run"], C.c_int32),
+                         _ptr(out["best_genes"], C.c_float), _ptr(out["evals"], C.c_int64),
+                         _ptr(out["status"], C.c_int32), _ptr(out["device"], C.c_int32), C.byref(st))
+    if rc != DOCK_OK:
+        msg = lib.dock_screen_last_error()
+        raise DockError(rc, msg.decode() if msg else "")
+    out["stats"] = dict(prep_ms=st.prep_ms, dock_ms=st.dock_ms, total_evals=st.total_evals, n_failed=st.n_failed,
+                        launches=st.launches)
     return out
 
 

@@ -24,16 +24,18 @@ def _stale() -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not _stale():
+def build(force: bool = False, verbose: bool = False, out: str | None = None, defines=()) -> str:
+    """Compile libdock.so (or, for experiments, a variant with extra -D defines at `out`)."""
+    lib = out or LIB
+    if not force and out is None and not _stale():
         return LIB
-    obj_dir = os.path.join(ROOT, "build", "obj")
+    obj_dir = os.path.join(ROOT, "build", "obj" if out is None else "obj_" + os.path.basename(out))
     os.makedirs(obj_dir, exist_ok=True)
     procs, objs = [], []
     for src in SOURCES:
         obj = os.path.join(obj_dir, src + ".o")
         objs.append(obj)
-        cmd = [NVCC, *FLAGS, "-c", os.path.join(CSRC, src), "-o", obj]
+        cmd = [NVCC, *FLAGS, *[f"-D{d}" for d in defines], "-c", os.path.join(CSRC, src), "-o", obj]
         if src.endswith(".cu") and verbose:
             cmd += ["-Xptxas", "-v"]
         procs.append((cmd, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT)))
@@ -44,10 +46,11 @@ def build(force: bool = False, verbose: bool = False) -> str:
             raise RuntimeError("nvcc failed: " + " ".join(cmd))
         if verbose:
             sys.stderr.write(out.decode(errors="replace"))
-    tmp = LIB + f".{os.getpid()}.tmp"
+    tmp = lib + f".{os.getpid()}.tmp"
+    os.makedirs(os.path.dirname(lib), exist_ok=True)
     subprocess.check_call([NVCC, *FLAGS, "-shared", "-o", tmp, *objs])
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, lib)
+    return lib
 
 
 if __name__ == "__main__":

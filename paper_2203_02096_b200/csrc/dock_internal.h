@@ -58,6 +58,7 @@ struct SearchDev {
     int ls_method, ls_iters, n_ls;
     float sw_rho, sw_rho_min, sw_expand, sw_contract;
     int sw_cons_succ, sw_cons_fail;
+    int sw_depth;                 // 0 auto, 1..3 (dock_params.sw_depth)
     float ad_rho, ad_eps;
     int max_generations;
     long long max_evals;

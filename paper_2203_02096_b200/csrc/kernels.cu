@@ -317,8 +317,11 @@ __device__ __forceinline__ LsTarget ls_target(const SearchDev &sp, const PopDev 
 // ---------------------------------------------------------------------------
 // k_ls_adadelta: max_iters x (energy + gradient, ADADELTA step), best tracking (D10).
 // ---------------------------------------------------------------------------
+#ifndef DK_ADA_MINB
+#define DK_ADA_MINB 1   // min resident CTAs/SM for the ADADELTA kernel (register cap 65536/(256*MINB))
+#endif
 template <int W, int MAXC>
-__global__ void __launch_bounds__(256) k_ls_adadelta(const LigDev L, const GridDev g, const ScratchLayout SL,
+__global__ void __launch_bounds__(256, (MAXC <= 4 ? DK_ADA_MINB : 1)) k_ls_adadelta(const LigDev L, const GridDev g, const ScratchLayout SL,
                                                      const SearchDev sp, const PopDev pop, const LsArgs a) {
     extern __shared__ uint4 smem_u4[];
     uint8_t *sm = reinterpret_cast<uint8_t *>(smem_u4);
@@ -373,6 +376,32 @@ __global__ void __launch_bounds__(256) k_ls_adadelta(const LigDev L, const GridD
 }
 
 // ---------------------------------------------------------------------------
+// Solis-Wets arithmetic (D9), written with explicit round-to-nearest intrinsics so every
+// kernel that replays it (k_ls_sw, the speculative k_ls_sw_tree, its resolution step)
+// produces bit-identical genes: no FMA contraction can differ between call sites.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ float sw_deviate(const uint2 key, uint32_t slot, uint32_t gen, uint32_t run, int G, int it,
+                                            int j, float rho) {
+    const uint32_t m = 2u * (uint32_t)G * (uint32_t)it + 2u * (uint32_t)j;   // m even: m, m+1 share a block
+    const uint4 blk = stream_block(key, kSW, slot, gen, run, m >> 2);
+    const uint32_t w1 = lane_of(blk, m & 3), w2 = lane_of(blk, (m + 1) & 3);
+    return __fmul_rn(rho, __fadd_rn(u01(w1) - 0.5f, u01(w2) - 0.5f));     // triangular on (-rho, rho), exact
+}
+__device__ __forceinline__ float sw_c1(float x, float b, float d) { return __fadd_rn(__fadd_rn(x, b), d); }
+__device__ __forceinline__ float sw_c2(float x, float b, float d) { return __fsub_rn(__fsub_rn(x, b), d); }
+// outcome o: 0 = x+b+d accepted, 1 = x-b-d accepted, 2 = both rejected
+__device__ __forceinline__ void sw_gene_step(int o, float d, float &x, float &b) {
+    if (o == 0) { x = sw_c1(x, b, d); b = __fmaf_rn(0.2f, b, __fmul_rn(0.4f, d)); }
+    else if (o == 1) { x = sw_c2(x, b, d); b = __fsub_rn(b, __fmul_rn(0.4f, d)); }
+    else { b = __fmul_rn(0.5f, b); }
+}
+__device__ __forceinline__ void sw_scalar_step(int o, const SearchDev &sp, float &rho, int &succ, int &fail) {
+    if (o < 2) { ++succ; fail = 0; } else { ++fail; succ = 0; }
+    if (succ >= sp.sw_cons_succ) { rho *= sp.sw_expand; succ = 0; }
+    if (fail >= sp.sw_cons_fail) { rho *= sp.sw_contract; fail = 0; }
+}
+
+// ---------------------------------------------------------------------------
 // k_ls_sw: Solis-Wets (D9; P:64 citing Solis & Wets 1981).  One warp per individual.
 // W <= 16: the two half-warps score x+b+d and x-b-d concurrently.
 // ---------------------------------------------------------------------------
@@ -413,12 +442,9 @@ __global__ void __launch_bounds__(256) k_ls_sw(const LigDev L, const GridDev g, 
         for (int s = 0; s < NSET; ++s) {
             const int j = lane + 32 * s;
             if (j < G) {
-                const uint32_t m = 2u * (uint32_t)G * (uint32_t)it + 2u * (uint32_t)j;   // m even: m, m+1 share a block
-                const uint4 blk = stream_block(key, kSW, t.slot, t.gen, t.run_g, m >> 2);
-                const uint32_t w1 = lane_of(blk, m & 3), w2 = lane_of(blk, (m + 1) & 3);
-                d[s] = rho * ((u01(w1) - 0.5f) + (u01(w2) - 0.5f));   // exact: triangular on (-rho, rho)
-                c1[s] = x[s] + b[s] + d[s];
-                c2[s] = x[s] - b[s] - d[s];
+                d[s] = sw_deviate(key, t.slot, t.gen, t.run_g, G, it, j, rho);
+                c1[s] = sw_c1(x[s], b[s], d[s]);
+                c2[s] = sw_c2(x[s], b[s], d[s]);
                 S0.genes[j] = c1[s];
                 if (NG == 2) S1.genes[j] = c2[s];
             }
@@ -435,8 +461,9 @@ __global__ void __launch_bounds__(256) k_ls_sw(const LigDev L, const GridDev g, 
         ++ne;
         if (E1 < Ex) {
 #pragma unroll
-            for (int s = 0; s < NSET; ++s) { x[s] = c1[s]; b[s] = 0.2f * b[s] + 0.4f * d[s]; }
-            Ex = E1; ++succ; fail = 0;
+            for (int s = 0; s < NSET; ++s) sw_gene_step(0, d[s], x[s], b[s]);
+            Ex = E1;
+            sw_scalar_step(0, sp, rho, succ, fail);
         } else {
             if (NG == 1) {
                 __syncwarp();
@@ -451,16 +478,15 @@ __global__ void __launch_bounds__(256) k_ls_sw(const LigDev L, const GridDev g, 
             ++ne;
             if (E2 < Ex) {
 #pragma unroll
-                for (int s = 0; s < NSET; ++s) { x[s] = c2[s]; b[s] = b[s] - 0.4f * d[s]; }
-                Ex = E2; ++succ; fail = 0;
+                for (int s = 0; s < NSET; ++s) sw_gene_step(1, d[s], x[s], b[s]);
+                Ex = E2;
+                sw_scalar_step(1, sp, rho, succ, fail);
             } else {
 #pragma unroll
-                for (int s = 0; s < NSET; ++s) b[s] = 0.5f * b[s];
-                ++fail; succ = 0;
+                for (int s = 0; s < NSET; ++s) sw_gene_step(2, d[s], x[s], b[s]);
+                sw_scalar_step(2, sp, rho, succ, fail);
             }
         }
-        if (succ >= sp.sw_cons_succ) { rho *= sp.sw_expand; succ = 0; }
-        if (fail >= sp.sw_cons_fail) { rho *= sp.sw_contract; fail = 0; }
         __syncwarp();
     }
 #pragma unroll
@@ -469,6 +495,132 @@ __global__ void __launch_bounds__(256) k_ls_sw(const LigDev L, const GridDev g, 
         if (j < G) t.row[j] = x[s];
     }
     if (lane == 0) { *t.E = Ex; *t.evals = ne; }
+}
+
+// ---------------------------------------------------------------------------
+// k_ls_sw_tree: speculative Solis-Wets for under-filled launches (1stp: 9 LS individuals
+// x 20 runs = 180 chains on 148 SMs).  Each SW iteration has three outcomes (x+b+d
+// accepted, x-b-d accepted, both rejected, D9), and the next iteration's deviates are
+// known in advance (counter-based Philox, D2).  So one CTA of 3^D - 1 lane groups
+// evaluates every trial point of the next D iterations at once: level l holds 3^l parent
+// states x 2 candidates.  Afterwards the actual path is resolved sequentially from the
+// energies, with exactly D9's decisions and evaluation count.  Every group replays its
+// path with the same sw_* arithmetic as the resolution, so the result is bit-identical
+// to k_ls_sw; only the latency changes (D iterations per evaluation round trip).
+// ---------------------------------------------------------------------------
+__host__ __device__ constexpr int ipow3(int d) { return d == 0 ? 1 : 3 * ipow3(d - 1); }
+template <int W, int D>
+constexpr int tree_threads() { return ((ipow3(D) - 1) * W + 31) / 32 * 32; }
+
+template <int W, int MAXC, int D>
+__global__ void __launch_bounds__(tree_threads<W, D>(), (W == 16 && D == 3) ? 2 : 1) k_ls_sw_tree(const LigDev L, const GridDev g,
+                                                                     const ScratchLayout SL, const SearchDev sp,
+                                                                     const PopDev pop, const LsArgs a) {
+    constexpr int NGR = ipow3(D) - 1;
+    extern __shared__ uint4 smem_u4[];
+    uint8_t *sm = reinterpret_cast<uint8_t *>(smem_u4);
+    const int G = L.G;
+    const LsTarget t = ls_target(sp, pop, a, blockIdx.x, G);
+    if (!t.act) return;                                      // uniform: one individual per CTA
+    const int staged = staged_bytes(L, false);
+    const LigSm Ls = stage_ligand(L, sm, staged);
+    float *sx = reinterpret_cast<float *>(sm + staged + NGR * SL.bytes);
+    float *sb = sx + kMaxGenes;
+    float *sE = sb + kMaxGenes;
+    const int grp = threadIdx.x / W, sub = threadIdx.x % W;
+    const bool in_grp = grp < NGR;
+    const Scratch S = scratch_at(sm + staged + (in_grp ? grp : 0) * SL.bytes, SL);
+    const unsigned gmask = group_mask<W>();
+    const uint2 key = make_uint2(sp.key0, sp.key1);
+    for (int j = threadIdx.x; j < G; j += blockDim.x) { sx[j] = t.row[j]; sb[j] = 0.0f; }
+    // this group's node: level lvl, parent state sigma (base-3 outcome digits), candidate
+    int lvl = 0;
+    while (lvl + 1 < D && grp >= ipow3(lvl + 1) - 1) ++lvl;
+    const int sigma = (grp - (ipow3(lvl) - 1)) >> 1, cand = (grp - (ipow3(lvl) - 1)) & 1;
+    int digit[D];
+    {
+        int v = sigma;
+#pragma unroll
+        for (int k = D - 1; k >= 0; --k) {
+            digit[k] = 0;
+            if (k < lvl) { digit[k] = v % 3; v /= 3; }
+        }
+    }
+    __syncthreads();
+    float Ex = *t.E, rho = sp.sw_rho;
+    int succ = 0, fail = 0, ne = 0, it = 0;
+    while (it < a.iters && !(rho < sp.sw_rho_min)) {
+        // ---- 1. every live node's trial genotype, then its energy ----
+        if (in_grp) {
+            float rl[D];
+            float r = rho;
+            int su = succ, fa = fail;
+            bool live = true;
+#pragma unroll
+            for (int k = 0; k < D; ++k) {
+                rl[k] = r;
+                if (k < lvl) {
+                    if (r < sp.sw_rho_min) live = false;
+                    sw_scalar_step(digit[k], sp, r, su, fa);
+                }
+            }
+            if (r < sp.sw_rho_min || it + lvl >= a.iters) live = false;
+            if (live) {
+                for (int j = sub; j < G; j += W) {
+                    float x = sx[j], b = sb[j];
+#pragma unroll
+                    for (int k = 0; k < D; ++k)
+                        if (k < lvl)
+                            sw_gene_step(digit[k], sw_deviate(key, t.slot, t.gen, t.run_g, G, it + k, j, rl[k]), x, b);
+                    const float d = sw_deviate(key, t.slot, t.gen, t.run_g, G, it + lvl, j, r);
+                    S.genes[j] = cand ? sw_c2(x, b, d) : sw_c1(x, b, d);
+                }
+            }
+            __syncwarp(gmask);
+            const float e = live ? eval_group<W, MAXC, false>(Ls, g, S, sub, gmask) : INFINITY;
+            if (sub == 0) sE[grp] = e;
+        }
+        __syncthreads();
+        // ---- 2. resolve the actual path (every thread, identical scalar logic) ----
+        int path[D], rho_steps = 0, it0 = it;
+        float rl[D];
+        int sg = 0;
+#pragma unroll
+        for (int k = 0; k < D; ++k) {
+            path[k] = 2; rl[k] = 0.0f;
+        }
+#pragma unroll
+        for (int k = 0; k < D; ++k) {
+            if (it >= a.iters || rho < sp.sw_rho_min) break;
+            rl[k] = rho;
+            const int id = ipow3(k) - 1 + 2 * sg;
+            int o;
+            ++ne;
+            if (sE[id] < Ex) { o = 0; Ex = sE[id]; }
+            else {
+                ++ne;
+                if (sE[id + 1] < Ex) { o = 1; Ex = sE[id + 1]; }
+                else o = 2;
+            }
+            sw_scalar_step(o, sp, rho, succ, fail);
+            path[k] = o;
+            sg = 3 * sg + o;
+            ++it;
+            ++rho_steps;
+        }
+        // ---- 3. advance x and b along the resolved path ----
+        for (int j = threadIdx.x; j < G; j += blockDim.x) {
+            float x = sx[j], b = sb[j];
+#pragma unroll
+            for (int k = 0; k < D; ++k)
+                if (k < rho_steps)
+                    sw_gene_step(path[k], sw_deviate(key, t.slot, t.gen, t.run_g, G, it0 + k, j, rl[k]), x, b);
+            sx[j] = x; sb[j] = b;
+        }
+        __syncthreads();
+    }
+    for (int j = threadIdx.x; j < G; j += blockDim.x) t.row[j] = sx[j];
+    if (threadIdx.x == 0) { *t.E = Ex; *t.evals = ne; }
 }
 
 // ---------------------------------------------------------------------------
@@ -562,7 +714,9 @@ cudaError_t setup_kernel_attributes() {
     if (e == cudaSuccess) e = allow_smem(k_init<W, MAXC>);                           \
     if (e == cudaSuccess) e = allow_smem(k_ga<W, MAXC>);                             \
     if (e == cudaSuccess) e = allow_smem(k_ls_adadelta<W, MAXC>);                    \
-    if (e == cudaSuccess) e = allow_smem(k_ls_sw<W, MAXC>);
+    if (e == cudaSuccess) e = allow_smem(k_ls_sw<W, MAXC>);                         \
+    if (e == cudaSuccess) e = allow_smem(k_ls_sw_tree<W, MAXC, 2>);                  \
+    if (e == cudaSuccess) e = allow_smem(k_ls_sw_tree<W, MAXC, 3>);
     DK_ATTR(16, 1) DK_ATTR(32, 1) DK_ATTR(32, 2) DK_ATTR(32, 3) DK_ATTR(32, 4) DK_ATTR(32, 8)
 #undef DK_ATTR
     return e;
@@ -615,9 +769,39 @@ cudaError_t launch_ls(const LigDev &L, const GridDev &g, const SearchDev &sp, co
     if (n_total <= 0) return cudaSuccess;
     const GroupCfg cfg = pick_group(L.N);
     if (sp.ls_method == 1) {
-        // Solis-Wets: one warp per individual; few individuals -> one warp per CTA so
-        // they spread over all SMs.
         const ScratchLayout SL = scratch_layout(L.N, L.T, L.G, false, 0);
+        // Speculation depth: the deepest tree whose CTAs are all co-resident (one wave);
+        // a full launch gains nothing from speculation and uses the plain kernel.
+        int depth = sp.sw_depth;
+        if (depth == 0) {
+            depth = 1;
+            int dev = 0, nsm = 148;
+            cudaGetDevice(&dev);
+            cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+            for (int D = 3; D >= 2 && depth == 1; --D) {
+                const int ngr = D == 3 ? 26 : 8;
+                const size_t sm_b = (size_t)L.blob_bytes + (size_t)ngr * SL.bytes + 4 * (2 * kMaxGenes + ngr);
+                int per_sm = 0;
+                DK_DISPATCH(cfg, {
+                    if (D == 3) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_ls_sw_tree<W, MAXC, 3>, tree_threads<W, 3>(), sm_b);
+                    else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_ls_sw_tree<W, MAXC, 2>, tree_threads<W, 2>(), sm_b);
+                });
+                cudaGetLastError();
+                if (sm_b <= (size_t)kSmemMax && per_sm > 0 && (long long)n_total <= (long long)per_sm * nsm) depth = D;
+            }
+        }
+        if (depth >= 2) {
+            const int ngr = depth == 3 ? 26 : 8;
+            const size_t smem = (size_t)L.blob_bytes + (size_t)ngr * SL.bytes + 4 * (2 * kMaxGenes + ngr);
+            if (smem > (size_t)kSmemMax) return cudaErrorInvalidConfiguration;
+            DK_DISPATCH(cfg, {
+                if (depth == 3) k_ls_sw_tree<W, MAXC, 3><<<n_total, tree_threads<W, 3>(), smem, s>>>(L, g, SL, sp, pop, a);
+                else k_ls_sw_tree<W, MAXC, 2><<<n_total, tree_threads<W, 2>(), smem, s>>>(L, g, SL, sp, pop, a);
+            });
+            return cudaGetLastError();
+        }
+        // depth 1: one warp per individual; few individuals -> one warp per CTA so they
+        // spread over all SMs.
         const int ng = cfg.W <= 16 ? 2 : 1;
         const int warps = n_total >= 148 * 8 ? 8 : 1;
         const size_t smem = (size_t)L.blob_bytes + (size_t)warps * ng * SL.bytes;

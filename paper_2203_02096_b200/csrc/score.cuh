@@ -72,6 +72,14 @@ __device__ __forceinline__ float ex2_approx(float x) {
     return y;
 }
 
+// 1/x on the SFU without the IEEE-denormal fix-up __fdividef(1, x) carries (ρ² ≥ 1e-4
+// after the D5 clamp, so the operand is always a normal number).
+__device__ __forceinline__ float rcp_approx(float x) {
+    float y;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
 // sin/cos of an unwrapped angle: two-constant Cody-Waite reduction to [-pi, pi], then the
 // SFU (__sincosf, |err| < 4e-7 there).  Genes are never wrapped (D3), so the reduction
 // matters; beyond |x| = 1e5 the accurate library path is used.
@@ -89,7 +97,7 @@ __device__ __forceinline__ void fast_sincos(float x, float &s, float &c) {
 // D5 pair energy from precomputed pair constants (energy-only path).
 __device__ __forceinline__ float pair_e_pre(float rho2, float4 pp, bool hb) {
     rho2 = fmaxf(rho2, 1e-4f);                           // 0.01 Å clamp
-    const float inv = __fdividef(1.0f, rho2);
+    const float inv = rcp_approx(rho2);
     const float x2 = pp.x * inv, x4 = x2 * x2, x6 = x4 * x2, x12 = x6 * x6;
     const float vdw = hb ? fmaf(5.0f, x12, -6.0f * (x6 * x4)) : fmaf(-2.0f, x6, x12);   // 12-10 / 12-6
     return fmaf(pp.y, vdw, fmaf(pp.w, inv, pp.z * ex2_approx(rho2 * kExpScale)));
@@ -99,7 +107,7 @@ __device__ __forceinline__ float pair_e_pre(float rho2, float4 pp, bool hb) {
 __device__ __forceinline__ float pair_eg(float rho2, float4 pi, float qi, float4 pj, float qj, bool hb, float &dE) {
     const bool clamped = rho2 < 1e-4f;
     rho2 = fmaxf(rho2, 1e-4f);
-    const float inv = __fdividef(1.0f, rho2);
+    const float inv = rcp_approx(rho2);
     const float req = pi.x + pj.x;                       // (R_i + R_j)/2
     const float eps = pi.y * pj.y;                       // sqrt(eps_i eps_j)
     const float SV = fmaf(pi.z, pj.w, pj.z * pi.w);      // S_i V_j + S_j V_i

@@ -303,3 +303,85 @@ def test_full_size_sampled_outputs(dock, name, runs, budget):
 
 
 CONFIGS_LS = {"1stp": (1, 0.06), "7cpa": (0, 1.0), "3ce3": (0, 1.0)}
+
+
+# ---------------------------------------------------------------------------
+# dock_screen (multi-ligand scheduler): every ligand's result equals a
+# standalone dock_run_ex with ligand_id = its index, whatever the slot count and order;
+# an invalid ligand is rejected with DOCK_E_INPUT and does not stop the screen.
+# ---------------------------------------------------------------------------
+def test_screen_matches_single_ligand_runs(dock):
+    from gen import hts_ligands
+    from gen.synth import TYPE_NAMES, make_grid
+    ligs = hts_ligands(7, seed=9)
+    grid = make_grid(24, 0.5, list(TYPE_NAMES), seed=77)
+    kw = dict(ls_method=0, ls_rate=0.25, ls_max_iters=20)
+    pop, runs, budget, seed = 24, 3, 3000, 1234
+    import copy
+    bad = hts_ligands(1, seed=10)[0]
+    ring = copy.deepcopy(bad)
+    ring.bonds = np.vstack([bad.bonds, [[0, len(bad.types) - 1]]]).astype(np.int32)
+    ring.rotatable = np.concatenate([np.ones(len(bad.bonds), np.uint8), [0]]).astype(np.uint8)
+    allligs = ligs[:3] + [ring] + ligs[3:]
+    out_a = dock.screen(grid, allligs, pop, runs, budget, seed, devices=[0], slots_per_device=3, **kw)
+    out_b = dock.screen(grid, allligs, pop, runs, budget, seed, devices=[0], slots_per_device=1, **kw)
+    assert out_a["status"][3] == dock.DOCK_E_INPUT and np.isnan(out_a["best_E"][3])
+    assert out_a["stats"]["n_failed"] == 1
+    for k in ("best_E", "best_run", "best_genes", "evals", "status"):
+        np.testing.assert_array_equal(out_a[k], out_b[k], err_msg=k)
+    for i, lig in enumerate(allligs):
+        if i == 3:
+            continue
+        d = dock.Docker.from_inputs(grid, lig, **kw)
+        r = d.run(pop, runs, budget, seed, ligand_id=i, xyz=False)
+        bE = r["best_E"]
+        br = int(np.argmin(np.where(np.isnan(bE), np.inf, bE)))
+        assert out_a["status"][i] == 0
+        assert out_a["best_E"][i] == bE[br] and out_a["best_run"][i] == br
+        np.testing.assert_array_equal(out_a["best_genes"][i, : d.G], r["best_genes"][br])
+        assert np.all(out_a["best_genes"][i, d.G:] == 0)
+        assert out_a["evals"][i] == r["evals"].sum()
+        d.close()
+
+
+# ---------------------------------------------------------------------------
+# Speculative Solis-Wets (k_ls_sw_tree, depth 2 and 3): bit-identical to the plain
+# kernel (depth 1) for the LS hook and for whole runs, and equal to the oracle's D9.
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("name", ["tiny", "1stp", "3ce3"])
+def test_sw_speculation_depths_bit_identical(dock, name):
+    cfg, lig, grid = config_inputs(name)
+    P = oracle.Problem(grid, lig)
+    n = 40
+    outs = {}
+    for depth in (1, 2, 3):
+        d = dock.Docker.from_inputs(grid, lig, ls_method=1, sw_depth=depth)
+        X = random_genotypes(grid, d.T, n, seed=43, frac_out=0.0, shrink=0.2)
+        E0 = np.array([P.energy(x, grad=False)["E"] for x in X], np.float32)
+        slots = np.arange(n, dtype=np.int32) * 5 + 1
+        outs[depth] = d.ls_step(1, X, E0, 37, seed=11, run=3, gen=2, slots=slots)
+        d.close()
+    for depth in (2, 3):
+        for a, b in zip(outs[1], outs[depth]):
+            np.testing.assert_array_equal(a, b)
+    g, E, ev = outs[3]
+    pp = oracle.params(ls_max_iters=37)
+    ok = 0
+    for i in range(n):
+        x, Eo, evo = oracle.solis_wets(P, pp, 11, 0, 3, 2, int(slots[i]), X[i], float(E0[i]))
+        assert E[i] <= E0[i]
+        ok += int(ev[i] == evo and abs(E[i] - Eo) <= e_tol(Eo))
+    assert ok >= 0.9 * n, ok
+
+
+def test_sw_speculation_full_run_identical(dock):
+    cfg, lig, grid = config_inputs("1stp")
+    res = []
+    for depth in (1, 2, 3, 0):
+        d = dock.Docker.from_inputs(grid, lig, ls_method=1, ls_rate=cfg.ls_rate, ls_max_iters=cfg.ls_iters,
+                                    sw_depth=depth)
+        res.append(d.run(cfg.pop, 4, 60_000, 42, xyz=False))
+        d.close()
+    for r in res[1:]:
+        for k in ("best_E", "best_genes", "evals", "generations"):
+            np.testing.assert_array_equal(res[0][k], r[k], err_msg=k)
