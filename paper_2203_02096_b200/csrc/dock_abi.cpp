@@ -71,7 +71,9 @@ int ensure_buffers(dock_ctx *c, int runs, int pop) {
     cudaFree(c->d_genes); cudaFree(c->d_E); cudaFree(c->d_state); cudaFree(c->d_perm); cudaFree(c->d_ls_evals);
     c->d_genes = nullptr; c->d_E = nullptr; c->d_state = nullptr; c->d_perm = nullptr; c->d_ls_evals = nullptr;
     c->cap_runs = c->cap_pop = 0;
-    const size_t G = (size_t)c->prep.G;
+    // rows are strided by the ligand's G, but sized for the largest G so a context can be
+    // reused for any ligand (dock_screen slots)
+    const size_t G = (size_t)dk::kMaxGenes;
     CK(cudaMalloc(&c->d_genes, 2 * (size_t)R * P * G * sizeof(float)));
     CK(cudaMalloc(&c->d_E, 2 * (size_t)R * P * sizeof(float)));
     CK(cudaMalloc(&c->d_state, (size_t)R * sizeof(dk::RunState)));

@@ -31,6 +31,7 @@ ScratchLayout scratch_layout(int N, int T, int G, bool grad, int extra) {
     int o = 0;
     s.off_r = o; o += a16(16 * N);
     s.off_W = o; o += a16(48 * (T > 0 ? T : 1));
+    s.off_tp = o; o += a16(4 * (T > 0 ? T : 1));
     s.off_ts = o; if (grad) o += a16(32 * N);
     s.off_genes = o; o += a16(4 * G);
     s.off_grad = o; if (grad) o += a16(4 * G);
@@ -77,6 +78,7 @@ __device__ __forceinline__ Scratch scratch_at(uint8_t *base, const ScratchLayout
     Scratch s;
     s.r = reinterpret_cast<float4 *>(base + SL.off_r);
     s.W = reinterpret_cast<float4 *>(base + SL.off_W);
+    s.tp = reinterpret_cast<int *>(base + SL.off_tp);
     s.ts = reinterpret_cast<float4 *>(base + SL.off_ts);
     s.genes = reinterpret_cast<float *>(base + SL.off_genes);
     s.grad = reinterpret_cast<float *>(base + SL.off_grad);
@@ -318,7 +320,7 @@ __device__ __forceinline__ LsTarget ls_target(const SearchDev &sp, const PopDev 
 // k_ls_adadelta: max_iters x (energy + gradient, ADADELTA step), best tracking (D10).
 // ---------------------------------------------------------------------------
 #ifndef DK_ADA_MINB
-#define DK_ADA_MINB 1   // min resident CTAs/SM for the ADADELTA kernel (register cap 65536/(256*MINB))
+#define DK_ADA_MINB 2   // min resident CTAs/SM for the ADADELTA kernel (register cap 65536/(256*MINB))
 #endif
 template <int W, int MAXC>
 __global__ void __launch_bounds__(256, (MAXC <= 4 ? DK_ADA_MINB : 1)) k_ls_adadelta(const LigDev L, const GridDev g, const ScratchLayout SL,
@@ -380,12 +382,19 @@ __global__ void __launch_bounds__(256, (MAXC <= 4 ? DK_ADA_MINB : 1)) k_ls_adade
 // kernel that replays it (k_ls_sw, the speculative k_ls_sw_tree, its resolution step)
 // produces bit-identical genes: no FMA contraction can differ between call sites.
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ float sw_deviate(const uint2 key, uint32_t slot, uint32_t gen, uint32_t run, int G, int it,
-                                            int j, float rho) {
+// (u1 - 1/2) + (u2 - 1/2) of gene j, iteration it: state independent (counter-based, D2)
+__device__ __forceinline__ float sw_tri(const uint2 key, uint32_t slot, uint32_t gen, uint32_t run, int G, int it,
+                                        int j) {
     const uint32_t m = 2u * (uint32_t)G * (uint32_t)it + 2u * (uint32_t)j;   // m even: m, m+1 share a block
     const uint4 blk = stream_block(key, kSW, slot, gen, run, m >> 2);
     const uint32_t w1 = lane_of(blk, m & 3), w2 = lane_of(blk, (m + 1) & 3);
-    return __fmul_rn(rho, __fadd_rn(u01(w1) - 0.5f, u01(w2) - 0.5f));     // triangular on (-rho, rho), exact
+    return __fadd_rn(u01(w1) - 0.5f, u01(w2) - 0.5f);
+}
+// d = rho * tri: the centred triangular deviate on (-rho, rho) (exact in FP32)
+__device__ __forceinline__ float sw_dev(float rho, float tri) { return __fmul_rn(rho, tri); }
+__device__ __forceinline__ float sw_deviate(const uint2 key, uint32_t slot, uint32_t gen, uint32_t run, int G, int it,
+                                            int j, float rho) {
+    return sw_dev(rho, sw_tri(key, slot, gen, run, G, it, j));
 }
 __device__ __forceinline__ float sw_c1(float x, float b, float d) { return __fadd_rn(__fadd_rn(x, b), d); }
 __device__ __forceinline__ float sw_c2(float x, float b, float d) { return __fsub_rn(__fsub_rn(x, b), d); }
@@ -527,6 +536,7 @@ __global__ void __launch_bounds__(tree_threads<W, D>(), (W == 16 && D == 3) ? 2 
     float *sx = reinterpret_cast<float *>(sm + staged + NGR * SL.bytes);
     float *sb = sx + kMaxGenes;
     float *sE = sb + kMaxGenes;
+    float *stri = sE + NGR;                                  // [D][G] deviate shapes of this round
     const int grp = threadIdx.x / W, sub = threadIdx.x % W;
     const bool in_grp = grp < NGR;
     const Scratch S = scratch_at(sm + staged + (in_grp ? grp : 0) * SL.bytes, SL);
@@ -550,6 +560,12 @@ __global__ void __launch_bounds__(tree_threads<W, D>(), (W == 16 && D == 3) ? 2 
     float Ex = *t.E, rho = sp.sw_rho;
     int succ = 0, fail = 0, ne = 0, it = 0;
     while (it < a.iters && !(rho < sp.sw_rho_min)) {
+        // ---- 0. the round's deviate shapes, one Philox block per (iteration, gene) ----
+        for (int q = threadIdx.x; q < D * G; q += blockDim.x) {
+            const int k = q / G, j = q - k * G;
+            stri[q] = sw_tri(key, t.slot, t.gen, t.run_g, G, it + k, j);
+        }
+        __syncthreads();
         // ---- 1. every live node's trial genotype, then its energy ----
         if (in_grp) {
             float rl[D];
@@ -570,9 +586,8 @@ __global__ void __launch_bounds__(tree_threads<W, D>(), (W == 16 && D == 3) ? 2 
                     float x = sx[j], b = sb[j];
 #pragma unroll
                     for (int k = 0; k < D; ++k)
-                        if (k < lvl)
-                            sw_gene_step(digit[k], sw_deviate(key, t.slot, t.gen, t.run_g, G, it + k, j, rl[k]), x, b);
-                    const float d = sw_deviate(key, t.slot, t.gen, t.run_g, G, it + lvl, j, r);
+                        if (k < lvl) sw_gene_step(digit[k], sw_dev(rl[k], stri[k * G + j]), x, b);
+                    const float d = sw_dev(r, stri[lvl * G + j]);
                     S.genes[j] = cand ? sw_c2(x, b, d) : sw_c1(x, b, d);
                 }
             }
@@ -613,8 +628,7 @@ __global__ void __launch_bounds__(tree_threads<W, D>(), (W == 16 && D == 3) ? 2 
             float x = sx[j], b = sb[j];
 #pragma unroll
             for (int k = 0; k < D; ++k)
-                if (k < rho_steps)
-                    sw_gene_step(path[k], sw_deviate(key, t.slot, t.gen, t.run_g, G, it0 + k, j, rl[k]), x, b);
+                if (k < rho_steps) sw_gene_step(path[k], sw_dev(rl[k], stri[k * G + j]), x, b);
             sx[j] = x; sb[j] = b;
         }
         __syncthreads();
@@ -778,9 +792,12 @@ cudaError_t launch_ls(const LigDev &L, const GridDev &g, const SearchDev &sp, co
             int dev = 0, nsm = 148;
             cudaGetDevice(&dev);
             cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-            for (int D = 3; D >= 2 && depth == 1; --D) {
+            // Measured on B200 (profiles/r01, 1stp): depth 2 = 1.45x, depth 3 = 1.19x over depth 1 --
+            // 26 groups/CTA contend for issue and spill at the 2-CTA/SM register cap -- so
+            // auto stops at depth 2; depth 3 stays available explicitly.
+            for (int D = 2; D >= 2 && depth == 1; --D) {
                 const int ngr = D == 3 ? 26 : 8;
-                const size_t sm_b = (size_t)L.blob_bytes + (size_t)ngr * SL.bytes + 4 * (2 * kMaxGenes + ngr);
+                const size_t sm_b = (size_t)L.blob_bytes + (size_t)ngr * SL.bytes + 4 * (2 * kMaxGenes + ngr + D * kMaxGenes);
                 int per_sm = 0;
                 DK_DISPATCH(cfg, {
                     if (D == 3) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_ls_sw_tree<W, MAXC, 3>, tree_threads<W, 3>(), sm_b);
@@ -792,7 +809,7 @@ cudaError_t launch_ls(const LigDev &L, const GridDev &g, const SearchDev &sp, co
         }
         if (depth >= 2) {
             const int ngr = depth == 3 ? 26 : 8;
-            const size_t smem = (size_t)L.blob_bytes + (size_t)ngr * SL.bytes + 4 * (2 * kMaxGenes + ngr);
+            const size_t smem = (size_t)L.blob_bytes + (size_t)ngr * SL.bytes + 4 * (2 * kMaxGenes + ngr + depth * kMaxGenes);
             if (smem > (size_t)kSmemMax) return cudaErrorInvalidConfiguration;
             DK_DISPATCH(cfg, {
                 if (depth == 3) k_ls_sw_tree<W, MAXC, 3><<<n_total, tree_threads<W, 3>(), smem, s>>>(L, g, SL, sp, pop, a);

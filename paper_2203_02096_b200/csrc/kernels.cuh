@@ -9,7 +9,7 @@ namespace dk {
 
 // Scratch layout of one lane group (bytes, 16-aligned offsets).
 struct ScratchLayout {
-    int off_r, off_W, off_ts, off_genes, off_grad, off_extra, bytes;
+    int off_r, off_W, off_tp, off_ts, off_genes, off_grad, off_extra, bytes;
 };
 
 // Local-search launch arguments.  use_state = 1: engine mode (per-run state decides the

@@ -37,6 +37,7 @@ struct LigSm {
 struct Scratch {
     float4 *r;                    // [N]  pose (x,y,z) and charge
     float4 *W;                    // [3T] torsion composite transforms (rows R|t)
+    int *tp;                      // [T]  pointer-jumping ancestor of each torsion
     float4 *ts;                   // [2N] per-atom (r-t) x g and g (gradient only)
     float *genes;                 // [G]  genotype being evaluated
     float *grad;                  // [G]  genotype gradient (gradient only)
@@ -75,9 +76,13 @@ __device__ __forceinline__ float ex2_approx(float x) {
 // 1/x on the SFU without the IEEE-denormal fix-up __fdividef(1, x) carries (ρ² ≥ 1e-4
 // after the D5 clamp, so the operand is always a normal number).
 __device__ __forceinline__ float rcp_approx(float x) {
+#ifdef DK_RCP_FDIV
+    return __fdividef(1.0f, x);   // A/B variant: the IEEE-denormal-safe form
+#else
     float y;
     asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
     return y;
+#endif
 }
 
 // sin/cos of an unwrapped angle: two-constant Cody-Waite reduction to [-pi, pi], then the
@@ -289,52 +294,73 @@ __device__ float eval_group(const LigSm &L, const GridDev &grid, const Scratch &
     const float R20 = 2.f * (qx * qz - qw * qy), R21 = 2.f * (qy * qz + qw * qx), R22 = 1.f - 2.f * (qx * qx + qy * qy);
     const float tx = x[0], ty = x[1], tz = x[2];
 
-    // ---- a3: per-torsion local transform Rot(u_k, tau_k) about A_k (all torsions in
-    // parallel, lane-owned), then composites W_k = W_parent o local_k level by level ----
-    constexpr int KT = (kMaxTors + W - 1) / W;
-    float lr[KT][12];
-#pragma unroll
-    for (int tt = 0; tt < KT; ++tt) {
-        const int k = sub + W * tt;
-        if (k < L.T) {
+    // ---- a3: torsion composites W_k = Root o L_a1 o ... o L_k (parents first; L_k =
+    // Rot(u_k, tau_k) about A_k).  Lane k builds L_k; the chains are then collapsed by
+    // pointer jumping (A_k <- A_anc(k) o A_k, anc <- anc(anc)) in ceil(log2(depth))
+    // rounds instead of one round per tree level; finally W_k = Root o A_k.  One torsion
+    // per lane: T <= N - 1 <= W (N <= 16 for W = 16; T <= 32 = W otherwise). ----
+    {
+        const int k = sub;
+        const bool own = k < L.T;
+        float m[12];
+        int anc = -1;
+        if (own) {
             float st, ct;
             fast_sincos(x[6 + k], st, ct);
             const float4 u = L.tU[k], A = L.tA[k];
             const float oc = 1.0f - ct;
-            float *m = lr[tt];
             m[0] = fmaf(oc * u.x, u.x, ct);     m[1] = fmaf(oc * u.x, u.y, -st * u.z); m[2] = fmaf(oc * u.x, u.z, st * u.y);
             m[3] = fmaf(oc * u.y, u.x, st * u.z); m[4] = fmaf(oc * u.y, u.y, ct);    m[5] = fmaf(oc * u.y, u.z, -st * u.x);
             m[6] = fmaf(oc * u.z, u.x, -st * u.y); m[7] = fmaf(oc * u.z, u.y, st * u.x); m[8] = fmaf(oc * u.z, u.z, ct);
             m[9] = A.x - fmaf(m[0], A.x, fmaf(m[1], A.y, m[2] * A.z));
             m[10] = A.y - fmaf(m[3], A.x, fmaf(m[4], A.y, m[5] * A.z));
             m[11] = A.z - fmaf(m[6], A.x, fmaf(m[7], A.y, m[8] * A.z));
+            anc = L.tmeta[k].x;
         }
+        // (P o M) for affine P = rows p0..p2 (R|t) and M = m: new rows in place
+#define DK_COMPOSE(p0, p1, p2)                                                                    \
+    {                                                                                             \
+        float o_[12];                                                                             \
+        o_[0] = fmaf(p0.x, m[0], fmaf(p0.y, m[3], p0.z * m[6]));                                 \
+        o_[1] = fmaf(p0.x, m[1], fmaf(p0.y, m[4], p0.z * m[7]));                                 \
+        o_[2] = fmaf(p0.x, m[2], fmaf(p0.y, m[5], p0.z * m[8]));                                 \
+        o_[9] = fmaf(p0.x, m[9], fmaf(p0.y, m[10], fmaf(p0.z, m[11], p0.w)));                    \
+        o_[3] = fmaf(p1.x, m[0], fmaf(p1.y, m[3], p1.z * m[6]));                                 \
+        o_[4] = fmaf(p1.x, m[1], fmaf(p1.y, m[4], p1.z * m[7]));                                 \
+        o_[5] = fmaf(p1.x, m[2], fmaf(p1.y, m[5], p1.z * m[8]));                                 \
+        o_[10] = fmaf(p1.x, m[9], fmaf(p1.y, m[10], fmaf(p1.z, m[11], p1.w)));                   \
+        o_[6] = fmaf(p2.x, m[0], fmaf(p2.y, m[3], p2.z * m[6]));                                 \
+        o_[7] = fmaf(p2.x, m[1], fmaf(p2.y, m[4], p2.z * m[7]));                                 \
+        o_[8] = fmaf(p2.x, m[2], fmaf(p2.y, m[5], p2.z * m[8]));                                 \
+        o_[11] = fmaf(p2.x, m[9], fmaf(p2.y, m[10], fmaf(p2.z, m[11], p2.w)));                   \
+        _Pragma("unroll") for (int i_ = 0; i_ < 12; ++i_) m[i_] = o_[i_];                        \
     }
-    for (int l = 0; l < L.n_levels; ++l) {
-        const int k0 = L.lvl[l], k1 = L.lvl[l + 1];
-#pragma unroll
-        for (int tt = 0; tt < KT; ++tt) {
-            const int k = sub + W * tt;
-            if (k >= k0 && k < k1) {
-                const float *m = lr[tt];
-                const int par = L.tmeta[k].x;
-                float4 p0, p1, p2;
-                if (par < 0) {
-                    p0 = make_float4(R00, R01, R02, tx);
-                    p1 = make_float4(R10, R11, R12, ty);
-                    p2 = make_float4(R20, R21, R22, tz);
-                } else {
-                    p0 = S.W[3 * par]; p1 = S.W[3 * par + 1]; p2 = S.W[3 * par + 2];
-                }
-#define DK_ROW(P)                                                                                   \
-    make_float4(fmaf(P.x, m[0], fmaf(P.y, m[3], P.z * m[6])), fmaf(P.x, m[1], fmaf(P.y, m[4], P.z * m[7])), \
-                fmaf(P.x, m[2], fmaf(P.y, m[5], P.z * m[8])), fmaf(P.x, m[9], fmaf(P.y, m[10], fmaf(P.z, m[11], P.w))))
-                S.W[3 * k] = DK_ROW(p0);
-                S.W[3 * k + 1] = DK_ROW(p1);
-                S.W[3 * k + 2] = DK_ROW(p2);
-#undef DK_ROW
+        for (int span = 1; span < L.n_levels; span *= 2) {
+            if (own) {
+                S.W[3 * k] = make_float4(m[0], m[1], m[2], m[9]);
+                S.W[3 * k + 1] = make_float4(m[3], m[4], m[5], m[10]);
+                S.W[3 * k + 2] = make_float4(m[6], m[7], m[8], m[11]);
+                S.tp[k] = anc;
             }
+            __syncwarp(mask);
+            int nanc = anc;
+            if (own && anc >= 0) {
+                const float4 p0 = S.W[3 * anc], p1 = S.W[3 * anc + 1], p2 = S.W[3 * anc + 2];
+                nanc = S.tp[anc];
+                DK_COMPOSE(p0, p1, p2)
+            }
+            __syncwarp(mask);
+            anc = nanc;
         }
+        if (own) {
+            const float4 p0 = make_float4(R00, R01, R02, tx), p1 = make_float4(R10, R11, R12, ty),
+                         p2 = make_float4(R20, R21, R22, tz);
+            DK_COMPOSE(p0, p1, p2)
+            S.W[3 * k] = make_float4(m[0], m[1], m[2], m[9]);
+            S.W[3 * k + 1] = make_float4(m[3], m[4], m[5], m[10]);
+            S.W[3 * k + 2] = make_float4(m[6], m[7], m[8], m[11]);
+        }
+#undef DK_COMPOSE
         __syncwarp(mask);
     }
 

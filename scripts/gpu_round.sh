@@ -3,7 +3,7 @@
 # Usage (via gpurun): bash scripts/gpu_round.sh <tag> [configs...]
 set -u
 TAG=${1:-r01}; shift || true
-CFGS=${@:-"1stp 3ce3 7cpa"}
+CFGS=${@:-"1stp 3ce3 7cpa hts"}
 OUT=gpurun_out/$TAG
 mkdir -p $OUT
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,temperature.gpu --format=csv > $OUT/gpu.txt 2>&1
@@ -14,7 +14,7 @@ for C in $CFGS; do
   timeout 900 python bench.py --config $C > $OUT/bench_$C.json 2> $OUT/bench_$C.err; echo "bench $C rc=$?"; tail -c 600 $OUT/bench_$C.json
 done
 if [ "${PROFILE:-1}" = "1" ]; then
-  bash scripts/gpu_profile.sh 1stp k_ls_sw $TAG
+  bash scripts/gpu_profile.sh 1stp k_ls_sw_tree $TAG
   bash scripts/gpu_profile.sh 7cpa k_ls_adadelta $TAG
   ls -la gpurun_out/
 fi
