@@ -385,3 +385,54 @@ def test_sw_speculation_full_run_identical(dock):
     for r in res[1:]:
         for k in ("best_E", "best_genes", "evals", "generations"):
             np.testing.assert_array_equal(res[0][k], r[k], err_msg=k)
+
+
+# ---------------------------------------------------------------------------
+# Deep torsion trees: every internal bond of a zig-zag chain rotatable (depth T), so the
+# pointer-jumping composites run ceil(log2(T)) rounds; W = 16 and W = 32 lane groups.
+# ---------------------------------------------------------------------------
+def _chain_ligand(n, seed):
+    from gen.synth import Ligand, TYPE_NAMES
+    rng = np.random.default_rng(seed)
+    xyz = np.zeros((n, 3), np.float64)
+    for i in range(n):
+        xyz[i] = (1.25 * i, 0.44 * (i % 2), 0.1 * np.sin(i))
+    xyz -= xyz.mean(0)
+    names = ["C"] * n
+    names[0], names[-1] = "OA", "N"
+    q = rng.normal(0, 0.15, n)
+    q -= q.mean()
+    bonds = np.array([[i, i + 1] for i in range(n - 1)], np.int32)
+    rot = np.zeros(n - 1, np.uint8)
+    rot[1:-1] = 1
+    tn = list(TYPE_NAMES)
+    return Ligand(type_names=tn, types=np.array([tn.index(a) for a in names], np.int32),
+                  charges=q.astype(np.float32), xyz=xyz.astype(np.float32), bonds=bonds, rotatable=rot,
+                  atom_names=names)
+
+
+@pytest.mark.parametrize("n_atoms", [12, 16, 20, 34])
+def test_deep_torsion_chain_parity(dock, n_atoms):
+    from gen.synth import TYPE_NAMES, make_grid
+    lig = _chain_ligand(n_atoms, seed=n_atoms)
+    grid = make_grid(40, 0.5, list(TYPE_NAMES), seed=3)
+    d = dock.Docker.from_inputs(grid, lig)
+    P = oracle.Problem(grid, lig)
+    assert d.T == n_atoms - 3
+    X = random_genotypes(grid, d.T, 200, seed=7, frac_out=0.0, shrink=0.1)
+    X[:, 6:] *= 0.05                 # near-extended chains: few self-clashes
+    E, Gd, xyz = d.eval(X, grad=True, xyz=True)
+    bad = []
+    for i in range(X.shape[0]):
+        ref = P.energy(X[i].astype(np.float64))
+        if np.abs(xyz[i] - ref["xyz"]).max() > 1e-4:
+            bad.append(("x", i))
+            continue
+        fm, cm = P.margins(ref["xyz"])
+        tol, gtol = pose_tols(P, ref)
+        if abs(E[i] - ref["E"]) > tol:
+            bad.append(("E", i))
+        if fm >= 1e-4 and cm >= 1e-4 and np.abs(Gd[i] - ref["grad"]).max() > gtol:
+            bad.append(("g", i))
+    assert not bad, bad[:10]
+    d.close()
