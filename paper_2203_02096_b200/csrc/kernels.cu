@@ -29,7 +29,9 @@ static inline __host__ __device__ int a16(int x) { return (x + 15) & ~15; }
 ScratchLayout scratch_layout(int N, int T, int G, bool grad, int extra) {
     ScratchLayout s;
     int o = 0;
-    s.off_r = o; o += a16(16 * N);
+    // gradient kernels keep the pose in the duplicated chunk layout [NC][2W] (intra_tiles)
+    const int Wg = N <= 16 ? 16 : 32;
+    s.off_r = o; o += a16(grad ? 16 * 2 * Wg * ((N + Wg - 1) / Wg) : 16 * N);
     s.off_W = o; o += a16(48 * (T > 0 ? T : 1));
     s.off_tp = o; o += a16(4 * (T > 0 ? T : 1));
     s.off_ts = o; if (grad) o += a16(32 * N);
@@ -71,6 +73,9 @@ __device__ __forceinline__ LigSm stage_ligand(const LigDev &L, uint8_t *sm, int 
     v.pairs = reinterpret_cast<const uint32_t *>(sm + L.off_pairs);
     v.pprm = reinterpret_cast<const float4 *>(sm + L.off_pprm);
     v.mask = reinterpret_cast<const uint32_t *>(sm + L.off_mask);
+    v.pdup = reinterpret_cast<const int *>(sm + L.off_pdup);
+    v.tab = sm + L.off_tab;
+    v.NC = L.NC; v.NT1 = L.NT1;
     return v;
 }
 
@@ -115,7 +120,7 @@ __global__ void __launch_bounds__(256) k_eval(const LigDev L, const GridDev g, c
         for (int j = sub; j < G; j += W) grad[(size_t)gi * G + j] = S.grad[j];
     if (xyz) {
         for (int a = sub; a < L.N; a += W) {
-            const float4 r = S.r[a];
+            const float4 r = S.r[GRAD ? ridx<W>(a) : a];
             float *o = xyz + ((size_t)gi * L.N + dfs2orig[a]) * 3;
             o[0] = r.x; o[1] = r.y; o[2] = r.z;
         }

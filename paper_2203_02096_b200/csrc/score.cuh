@@ -31,7 +31,14 @@ struct LigSm {
     const uint32_t *pairs;        // i | j<<8 | hb<<16
     const float4 *pprm;           // per pair: r_eq^2, eps_ij, S_iV_j+S_jV_i, 332.06363/4 q_i q_j
     const uint32_t *mask;         // [N][NW] pair-membership bit rows
+    const int *pdup;              // [NC][2W] partner type byte offsets (duplicated chunks)
+    const uint8_t *tab;           // [NT1][NT1] 32-byte type-pair records
+    int NC, NT1;
 };
+
+// Gradient-path pose index: chunk c = a / W lives at [c][2W], its copy at [c][2W] + W.
+template <int W>
+__device__ __forceinline__ int ridx(int a) { return a + (a & ~(W - 1)); }
 
 // Per-group scratch in shared memory.
 struct Scratch {
@@ -128,6 +135,23 @@ __device__ __forceinline__ float pair_eg(float rho2, float4 pi, float qi, float4
     return Evdw + Eel + Eds;
 }
 
+// D5 pair energy and dE/d(rho^2) from a type-pair record (gradient path):
+// E_vdw = A x^12 - B6 x^6 - B10 x^10, x^2 = r_eq^2 / rho^2; rho^2 dE_vdw/drho^2 =
+// -6 A x^12 + 3 B6 x^6 + 5 B10 x^10; E_el = qq / rho^2; E_ds = SV exp(-rho^2 / 2 sigma^2).
+__device__ __forceinline__ float pair_eg_tab(float rho2, float4 tb, float sv, float qq, float &dE) {
+    const bool clamped = rho2 < 1e-4f;
+    rho2 = fmaxf(rho2, 1e-4f);                           // 0.01 Å clamp; zero force inside
+    const float inv = rcp_approx(rho2);
+    const float x2 = tb.x * inv, x4 = x2 * x2, x6 = x4 * x2, x12 = x6 * x6, x10 = x6 * x4;
+    const float tA = tb.y * x12, tB = tb.z * x6, tC = tb.w * x10;
+    const float Eel = qq * inv;
+    const float Eds = sv * ex2_approx(rho2 * kExpScale);
+    const float dvr = fmaf(-6.0f, tA, fmaf(3.0f, tB, 5.0f * tC));
+    const float d = fmaf(dvr - Eel, inv, -Eds * kInvTwoSigma2);
+    dE = clamped ? 0.0f : d;
+    return (tA - tB - tC) + Eel + Eds;
+}
+
 // D4 intermolecular energy of one atom and its gradient.
 __device__ __forceinline__ float inter_atom(const GridDev &g, int type, float q, float rx, float ry,
                                             float rz, float &gx, float &gy, float &gz) {
@@ -173,13 +197,15 @@ __device__ __forceinline__ float inter_atom(const GridDev &g, int type, float q,
 // One D5 pair inside the gradient tiles: energy into e, force into the own-atom
 // accumulator (+dE d) and the partner accumulator (-dE d); the factor 2 of
 // dE/dr_i = 2 dE/drho2 (r_i - r_j) is applied once per atom at the end.
-__device__ __forceinline__ void tile_pair(bool on, float rxi, float ryi, float rzi, float4 pi, float qi, int rolei,
-                                          float4 rj, float4 pj, int rolej, float &e, float &gxi, float &gyi,
-                                          float &gzi, float &fx, float &fy, float &fz) {
+__device__ __forceinline__ void tile_pair(bool on, float rxi, float ryi, float rzi, float qi, const uint8_t *trow,
+                                          float4 rj, int tj_off, float &e, float &gxi, float &gyi, float &gzi,
+                                          float &fx, float &fy, float &fz) {
     const float dx = rxi - rj.x, dy = ryi - rj.y, dz = rzi - rj.z;
     const float rho2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
+    const float4 tb = *reinterpret_cast<const float4 *>(trow + tj_off);
+    const float sv = *reinterpret_cast<const float *>(trow + tj_off + 16);
     float dE;
-    const float E = pair_eg(rho2, pi, qi, pj, rj.w, (rolei | rolej) == 3, dE);
+    const float E = pair_eg_tab(rho2, tb, sv, qi * rj.w, dE);
     dE = on ? dE : 0.0f;
     e += on ? E : 0.0f;
     gxi = fmaf(dE, dx, gxi); gyi = fmaf(dE, dy, gyi); gzi = fmaf(dE, dz, gzi);
@@ -191,9 +217,15 @@ __device__ __forceinline__ void tile_pair(bool on, float rxi, float ryi, float r
 //    J*W+((l+s) mod W); the partner's force accumulator travels with the partner (one
 //    lane shift per step) and returns to its owner after the tile.  Diagonal tiles use
 //    s = 1..W/2 (s = W/2 only for l < W/2), so each unordered pair appears once.
+//    Pose and partner types are stored chunk-duplicated ([c][2W]), so the partner of
+//    step s is entry l + s of the chunk row -- a fixed offset from a per-tile base, no
+//    wrap-around or clamping arithmetic -- and the pair-membership bits are pre-rotated
+//    per lane, so bit s is the step-s partner.
 //  * a short tail chunk (t atoms) is paired by broadcast: all lanes meet tail atom j at
 //    once and j's force is a butterfly sum.
-// Pair membership comes from bit rows (D1 pair list); fixed order -> deterministic.
+//  * pair constants come from the per-type-pair table (r_eq^2, A, B6, B10, SV), the
+//    charges from the pose records (own charge pre-scaled by 332.06363/4).
+// Fixed order -> deterministic.
 template <int W, int MAXC>
 __device__ __forceinline__ void intra_tiles(const LigSm &L, const Scratch &S, int sub, unsigned mask,
                                             const float (&rx)[MAXC], const float (&ry)[MAXC], const float (&rz)[MAXC],
@@ -201,19 +233,17 @@ __device__ __forceinline__ void intra_tiles(const LigSm &L, const Scratch &S, in
     const int N = L.N;
     const int Bf = N / W, t = N - Bf * W;
     // cost model (issue slots): rotation of the tail as a padded chunk vs broadcast
-    const bool tail_rot = t > 0 && (W / 2 + Bf * W) * 53 < t * ((Bf + 1) * 50 + 3 * 5);
+    const bool tail_rot = t > 0 && (W / 2 + Bf * W) * 40 < t * ((Bf + 1) * 40 + 3 * 5);
     const int Bt = Bf + (tail_rot ? 1 : 0);
-    float4 pa[MAXC];
+    const uint8_t *trow[MAXC];
     float qa[MAXC];
-    int ra[MAXC];
     float hx[MAXC], hy[MAXC], hz[MAXC];   // pair-force sums (x 2 at the end)
 #pragma unroll
     for (int c = 0; c < MAXC; ++c) {
         const int a = sub + W * c;
         const bool ok = a < N;
-        pa[c] = ok ? L.par[a] : make_float4(0.f, 0.f, 0.f, 0.f);
-        qa[c] = ok ? S.r[a].w : 0.0f;
-        ra[c] = ok ? (L.meta[a] >> 8) & 3 : 0;
+        trow[c] = L.tab + (size_t)(ok ? (L.meta[a] & 0xff) : (L.NT1 - 1)) * L.NT1 * 32;
+        qa[c] = ok ? kElec4 * S.r[ridx<W>(a)].w : 0.0f;
         hx[c] = hy[c] = hz[c] = 0.0f;
     }
 #pragma unroll
@@ -224,18 +254,23 @@ __device__ __forceinline__ void intra_tiles(const LigSm &L, const Scratch &S, in
             if (J >= Bt) break;
             const int aI = I * W + sub;
             const int jb = J * W;
-            const uint32_t mw = aI < N ? (L.mask[aI * L.NW + (jb >> 5)] >> (jb & 31)) : 0u;
+            uint32_t mw = aI < N ? (L.mask[aI * L.NW + (jb >> 5)] >> (jb & 31)) : 0u;
+            uint32_t rot;
+            if constexpr (W == 32) {
+                rot = __funnelshift_r(mw, mw, sub);             // bit s = partner (sub + s) mod 32
+            } else {
+                mw &= 0xffffu;
+                rot = ((mw | (mw << 16)) >> sub) & 0xffffu;
+            }
+            if (I == J && sub >= W / 2) rot &= ~(1u << (W / 2));   // each diagonal pair once
+            const float4 *rrow = S.r + J * 2 * W + sub;         // partner of step s: rrow[s]
+            const int *prow = L.pdup + J * 2 * W + sub;
             const int s0 = (I == J) ? 1 : 0, s1 = (I == J) ? W / 2 : W - 1;
             float fx = 0.f, fy = 0.f, fz = 0.f;
+#pragma unroll 4
             for (int s = s0; s <= s1; ++s) {
-                const int jj = (sub + s) & (W - 1);
-                const int j = min(jb + jj, N - 1);
-                bool on = (mw >> jj) & 1u;
-                if (I == J && s == W / 2 && sub >= W / 2) on = false;
-                const float4 rj = S.r[j], pj = L.par[j];
-                const int rolej = (L.meta[j] >> 8) & 3;
-                tile_pair(on, rx[I], ry[I], rz[I], pa[I], qa[I], ra[I], rj, pj, rolej, e, hx[I], hy[I], hz[I], fx,
-                          fy, fz);
+                tile_pair((rot >> s) & 1u, rx[I], ry[I], rz[I], qa[I], trow[I], rrow[s], prow[s], e, hx[I], hy[I],
+                          hz[I], fx, fy, fz);
                 if (s < s1) {
                     const int src = (sub + 1) & (W - 1);
                     fx = __shfl_sync(mask, fx, src, W);
@@ -253,8 +288,8 @@ __device__ __forceinline__ void intra_tiles(const LigSm &L, const Scratch &S, in
     if (t > 0 && !tail_rot) {
         for (int k = 0; k < t; ++k) {
             const int j = Bf * W + k;                       // uniform: shared-memory broadcast
-            const float4 rj = S.r[j], pj = L.par[j];
-            const int rolej = (L.meta[j] >> 8) & 3;
+            const float4 rj = S.r[ridx<W>(j)];
+            const int tj_off = L.pdup[ridx<W>(j)];
             const uint32_t *mrow = L.mask + (size_t)j * L.NW;
             float fx = 0.f, fy = 0.f, fz = 0.f;
 #pragma unroll
@@ -262,8 +297,7 @@ __device__ __forceinline__ void intra_tiles(const LigSm &L, const Scratch &S, in
                 if (I > Bf) break;
                 const int a = I * W + sub;
                 const bool on = (I < Bf || sub < k) && ((mrow[a >> 5] >> (a & 31)) & 1u);
-                tile_pair(on, rx[I], ry[I], rz[I], pa[I], qa[I], ra[I], rj, pj, rolej, e, hx[I], hy[I], hz[I], fx,
-                          fy, fz);
+                tile_pair(on, rx[I], ry[I], rz[I], qa[I], trow[I], rj, tj_off, e, hx[I], hy[I], hz[I], fx, fy, fz);
             }
             fx = gsum<W>(fx, mask); fy = gsum<W>(fy, mask); fz = gsum<W>(fz, mask);
 #pragma unroll
@@ -385,8 +419,18 @@ __device__ float eval_group(const LigSm &L, const GridDev &grid, const Scratch &
                 ry[c] = fmaf(w1.x, p.x, fmaf(w1.y, p.y, fmaf(w1.z, p.z, w1.w)));
                 rz[c] = fmaf(w2.x, p.x, fmaf(w2.y, p.y, fmaf(w2.z, p.z, w2.w)));
             }
-            S.r[a] = make_float4(rx[c], ry[c], rz[c], p.w);
+            if constexpr (GRAD) {
+                const float4 rv = make_float4(rx[c], ry[c], rz[c], p.w);
+                S.r[ridx<W>(a)] = rv;
+                S.r[ridx<W>(a) + W] = rv;
+            } else {
+                S.r[a] = make_float4(rx[c], ry[c], rz[c], p.w);
+            }
             e_part += inter_atom(grid, meta & 0xff, p.w, rx[c], ry[c], rz[c], gx[c], gy[c], gz[c]);
+        } else if (GRAD && c < L.NC) {
+            // padded chunk entries: finite zeros (null type, zero charge) for the tiles
+            S.r[ridx<W>(a)] = make_float4(0.f, 0.f, 0.f, 0.f);
+            S.r[ridx<W>(a) + W] = make_float4(0.f, 0.f, 0.f, 0.f);
         }
     }
     __syncwarp(mask);
@@ -434,7 +478,7 @@ __device__ float eval_group(const LigSm &L, const GridDev &grid, const Scratch &
                 cx += c4.x; cy += c4.y; cz += c4.z;
                 hx += g4.x; hy += g4.y; hz += g4.z;
             }
-            const float4 ra = S.r[tm.y], rb = S.r[tm.z];
+            const float4 ra = S.r[ridx<W>(tm.y)], rb = S.r[ridx<W>(tm.z)];
             const float dax = ra.x - tx, day = ra.y - ty, daz = ra.z - tz;
             const float sx = cx - (day * hz - daz * hy), sy = cy - (daz * hx - dax * hz), sz = cz - (dax * hy - day * hx);
             const float wx = rb.x - ra.x, wy = rb.y - ra.y, wz = rb.z - ra.z;
