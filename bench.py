@@ -475,12 +475,73 @@ def run_hts(args, cfg, grid):
         dist.destroy_process_group()
 
 
+# ---------------------------------------------------------------------------
+# --micro: the two isolated parts of an evaluation for roofline evidence
+# ---------------------------------------------------------------------------
+def run_micro(args, cfg, lig, grid):
+    import numpy as np
+    import torch
+    import paper_2203_02096_b200 as dock
+    from gen import random_genotypes
+
+    dev = torch.device("cuda", 0)
+    d = dock.Docker.from_inputs(grid, lig, ls_method=0)
+    n = cfg.runs * cfg.pop
+    X = torch.from_numpy(random_genotypes(grid, d.T, n, seed=5, frac_out=0.0, shrink=0.2)).to(dev)
+    out = torch.empty(n, dtype=torch.float32, device=dev)
+    st = torch.cuda.Stream(device=dev)
+    iters = args.micro_iters
+    res = {}
+    for part, name in ((0, "inter"), (1, "intra")):
+        with torch.cuda.stream(st):
+            for _ in range(2):
+                d.bench_part(part, X, out, iters, stream=st.cuda_stream)
+            e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(st)
+            for _ in range(args.steps):
+                d.bench_part(part, X, out, iters, stream=st.cuda_stream)
+            e1.record(st)
+        torch.cuda.synchronize()
+        res[name] = e0.elapsed_time(e1) / args.steps / 1e3
+    # L2 streaming-read reference: a 48 MiB resident buffer summed repeatedly (torch)
+    buf = torch.ones(12 * 1024 * 1024, dtype=torch.float32, device=dev)
+    for _ in range(3):
+        buf.sum()
+    e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(50):
+        buf.sum()
+    e1.record()
+    torch.cuda.synchronize()
+    l2_gbs = 50 * buf.numel() * 4 / (e0.elapsed_time(e1) / 1e3) / 1e9
+    peaks = measured_peaks()
+    sm_mhz = float(peaks.get("sm_max_mhz", 1965.0))
+    lookups = n * iters * d.N
+    t_in = res["inter"]
+    pair_steps = n * iters * d.P
+    t_pr = res["intra"]
+    fl = pair_steps * F_PAIR_EG / t_pr / 1e12
+    line = {"metric": "microbench", "config": {"workload": workload_desc(cfg), "genotypes": n, "iters": iters},
+            "inter": {"kernel": "k_bench_part<kInter> (pose + trilinear E+G)", "ms": 1e3 * t_in,
+                      "atom_lookups_per_s": lookups / t_in,
+                      "algorithmic_GBps_96B": 96 * lookups / t_in / 1e9,
+                      "moved_GBps_128B": 128 * lookups / t_in / 1e9,
+                      "hbm_peak_GBps": peaks.get("hbm_gbs"), "l2_stream_read_ref_GBps": l2_gbs},
+            "intra": {"kernel": "k_bench_part<kIntra> (pose + pair tiles E+forces)", "ms": 1e3 * t_pr,
+                      "pairs_per_s": pair_steps / t_pr, "tflops_model": fl,
+                      "fp32_peak_tflops": fp32_peak_tflops(sm_mhz), "frac": fl / fp32_peak_tflops(sm_mhz)}}
+    print(json.dumps(line), flush=True)
+    d.close()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="1stp", choices=["tiny", "1stp", "3ce3", "7cpa", "hts"])
+    ap.add_argument("--micro", action="store_true", help="isolated inter/intra microbenchmarks (roofline evidence)")
+    ap.add_argument("--micro-iters", type=int, default=20)
     ap.add_argument("--sw-depth", type=int, default=0, help="Solis-Wets speculation depth (0 = auto)")
     ap.add_argument("--n-ligs", type=int, default=256, help="hts: ligands per step (sample of configs[4])")
     ap.add_argument("--slots", type=int, default=4, help="hts: ligands in flight per GPU")
@@ -489,7 +550,9 @@ def main():
     args = ap.parse_args()
     from gen import config_inputs
     cfg, lig, grid = config_inputs(args.config)
-    if args.config == "hts":
+    if args.micro:
+        run_micro(args, cfg, lig, grid)
+    elif args.config == "hts":
         run_hts(args, cfg, grid)
     elif args.impl == "reference":
         run_reference(args, cfg, lig, grid)

@@ -145,6 +145,14 @@ int dock_eval(dock_ctx *ctx, int32_t n, const float *genotypes, float *energy, f
 int dock_eval_device(dock_ctx *ctx, int32_t n, const float *d_genotypes, float *d_energy,
                      float *d_grad, float *d_xyz, void *stream);   /* stream NULL = legacy default */
 
+/* Microbenchmark of one part of the evaluation, for roofline evidence:
+   part 0 = pose + intermolecular grid interpolation with gradient (a3+a4), part 1 = pose
+   + intramolecular pair tiles with forces (a3+a5).  n device genotypes, each evaluated
+   `iters` times (translation nudged by 1e-3 Å per iteration); d_out[n] receives a
+   checksum.  Enqueued on `stream` (NULL = legacy default); not a parity hook. */
+int dock_bench_part(dock_ctx *ctx, int32_t part, int32_t n, int32_t iters, const float *d_genotypes,
+                    float *d_out, void *stream);
+
 /* D1 on the host, without a device (runs the same preprocessing as dock_init):
    *n_tors, axis [T*2] (a on the root side), moved [T*n_atoms], *n_pairs, pairs [P*2]
    (lexicographic, caller indices).  pair_cap = capacity of `pairs` in pairs; returns

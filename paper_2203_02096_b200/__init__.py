@@ -86,6 +86,7 @@ def _load():
         "dock_run_device": (i32, [v, i32, i32, i32, u32, i64, u64, v, v, v, v, v]),
         "dock_eval": (i32, [v, i32, P(f), P(f), P(f), P(f)]),
         "dock_eval_device": (i32, [v, i32, v, v, v, v, v]),
+        "dock_bench_part": (i32, [v, i32, i32, i32, v, v, v]),
         "dock_get_pairs": (i32, [v, P(i32)]),
         "dock_get_torsions": (i32, [v, P(i32), P(C.c_uint8)]),
         "dock_philox": (i32, [i32, P(u32), P(u32), P(u32)]),
@@ -112,7 +113,8 @@ EXPORTED = ("dock_params_default", "dock_builtin_type_param", "dock_init", "dock
             "dock_n_atoms", "dock_n_torsions", "dock_n_genes", "dock_n_pairs", "dock_run", "dock_run_ex",
             "dock_run_device", "dock_eval", "dock_eval_device", "dock_get_pairs", "dock_get_torsions",
             "dock_philox", "dock_stream_words", "dock_ga_step", "dock_ls_step", "dock_launch_count",
-            "dock_topology", "dock_kernel_stats", "dock_upload_bytes", "dock_screen", "dock_screen_last_error")
+            "dock_topology", "dock_kernel_stats", "dock_upload_bytes", "dock_screen", "dock_screen_last_error",
+            "dock_bench_part")
 
 
 def topology(types, charges, xyz, bonds, rotatable, type_params, roles):
@@ -367,6 +369,12 @@ class Docker:
         self._chk(lib.dock_eval_device(self._ctx, n, genotypes.data_ptr(), energy.data_ptr(),
                                        grad.data_ptr() if grad is not None else None,
                                        xyz.data_ptr() if xyz is not None else None, stream or None))
+
+    def bench_part(self, part, genotypes, out, iters, stream=0):
+        """Microbenchmark (dock_bench_part): part 0 = pose + grid interpolation, 1 = pose +
+        pair tiles; torch CUDA tensors genotypes [n, G] and out [n]."""
+        self._chk(lib.dock_bench_part(self._ctx, part, genotypes.shape[0], iters, genotypes.data_ptr(),
+                                      out.data_ptr(), stream or None))
 
     # ---- D8-D11 ----
     def run(self, pop, runs, max_evals, seed, run_base=0, ligand_id=0, xyz=True):

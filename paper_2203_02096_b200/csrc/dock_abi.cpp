@@ -8,7 +8,11 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <climits>
+#include <mutex>
+#include <cstdio>
+#include <cstdlib>
 #include <cmath>
 #include <cstring>
 #include <string>
@@ -19,6 +23,22 @@
 namespace {
 
 thread_local std::string g_init_error;
+
+// DOCK_TRACE=1: wall time of host-side phases to stderr (diagnostics of the e2e path).
+struct Trace {
+    const char *name;
+    std::chrono::steady_clock::time_point t0;
+    static bool on() {
+        static const bool v = std::getenv("DOCK_TRACE") != nullptr;
+        return v;
+    }
+    explicit Trace(const char *n) : name(n), t0(std::chrono::steady_clock::now()) {}
+    ~Trace() {
+        if (on())
+            std::fprintf(stderr, "[dock] %s %.3f ms\n", name,
+                         std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
+    }
+};
 
 #define CK(call)                                                                          \
     do {                                                                                  \
@@ -68,23 +88,22 @@ dk::PopDev pop_of(const dock_ctx *c) {
 int ensure_buffers(dock_ctx *c, int runs, int pop) {
     if (runs <= c->cap_runs && pop <= c->cap_pop) return DOCK_OK;
     const int R = std::max(runs, c->cap_runs), P = std::max(pop, c->cap_pop);
-    cudaFree(c->d_genes); cudaFree(c->d_E); cudaFree(c->d_state); cudaFree(c->d_perm); cudaFree(c->d_ls_evals);
+    CK(cudaStreamSynchronize(c->stream));
+    dk::dfree(c->d_genes, c->stream); dk::dfree(c->d_E, c->stream); dk::dfree(c->d_state, c->stream);
+    dk::dfree(c->d_perm, c->stream); dk::dfree(c->d_ls_evals, c->stream);
     c->d_genes = nullptr; c->d_E = nullptr; c->d_state = nullptr; c->d_perm = nullptr; c->d_ls_evals = nullptr;
     c->cap_runs = c->cap_pop = 0;
     // rows are strided by the ligand's G, but sized for the largest G so a context can be
     // reused for any ligand (dock_screen slots)
     const size_t G = (size_t)dk::kMaxGenes;
-    CK(cudaMalloc(&c->d_genes, 2 * (size_t)R * P * G * sizeof(float)));
-    CK(cudaMalloc(&c->d_E, 2 * (size_t)R * P * sizeof(float)));
-    CK(cudaMalloc(&c->d_state, (size_t)R * sizeof(dk::RunState)));
-    CK(cudaMalloc(&c->d_perm, (size_t)R * P * sizeof(int)));
-    CK(cudaMalloc(&c->d_ls_evals, (size_t)R * P * sizeof(int)));
-    if (R > c->h_state_cap) {
-        if (c->h_state) cudaFreeHost(c->h_state);
-        c->h_state = nullptr;
-        CK(cudaMallocHost(&c->h_state, (size_t)R * sizeof(dk::RunState)));
-        c->h_state_cap = R;
-    }
+    cudaStream_t s = c->stream;
+    CK(dk::dmalloc((void **)&c->d_genes, 2 * (size_t)R * P * G * sizeof(float), s));
+    CK(dk::dmalloc((void **)&c->d_E, 2 * (size_t)R * P * sizeof(float), s));
+    CK(dk::dmalloc((void **)&c->d_state, (size_t)R * sizeof(dk::RunState), s));
+    CK(dk::dmalloc((void **)&c->d_perm, (size_t)R * P * sizeof(int), s));
+    CK(dk::dmalloc((void **)&c->d_ls_evals, (size_t)R * P * sizeof(int), s));
+    CK(cudaStreamSynchronize(s));   // usable from any stream (dock_run_device's) from here on
+    c->h_state.resize(R);
     c->cap_runs = R; c->cap_pop = P;
     return DOCK_OK;
 }
@@ -97,9 +116,14 @@ int check_run_args(dock_ctx *c, int pop, int runs, int run_base, int64_t max_eva
     return DOCK_OK;
 }
 
+// Scratch buffer of a hook call: pool-allocated on the call's stream, freed on it (the
+// hooks synchronise that stream before returning).
 struct DevBuf {
     void *p = nullptr;
-    ~DevBuf() { if (p) cudaFree(p); }
+    cudaStream_t s = nullptr;
+    explicit DevBuf(cudaStream_t st) : s(st) {}
+    cudaError_t alloc(size_t bytes) { return dk::dmalloc(&p, bytes, s); }
+    ~DevBuf() { dk::dfree(p, s); }
 };
 
 }  // namespace
@@ -122,8 +146,24 @@ int validate_params(const dock_params &p, std::string *err) {
     return DOCK_OK;
 }
 
+void pool_setup(int device) {
+    static std::mutex mu;
+    static std::vector<int> done;
+    std::lock_guard<std::mutex> lk(mu);
+    if (std::find(done.begin(), done.end(), device) != done.end()) return;
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+        uint64_t keep = UINT64_MAX;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+    cudaGetLastError();
+    done.push_back(device);
+}
+
 Receptor::~Receptor() {
-    if (d_maps) { cudaSetDevice(device); cudaFree(d_maps); }
+    cudaSetDevice(device);
+    dfree(d_maps, stream);
+    if (stream) cudaStreamDestroy(stream);
 }
 
 int receptor_upload(const dock_grids *grids, const std::vector<float4> &packed, int device,
@@ -131,8 +171,11 @@ int receptor_upload(const dock_grids *grids, const std::vector<float4> &packed, 
     auto r = std::make_shared<Receptor>();
     r->device = device;
     r->bytes = packed.size() * sizeof(float4);
-    if (cudaSetDevice(device) != cudaSuccess || cudaMalloc(&r->d_maps, r->bytes) != cudaSuccess ||
-        cudaMemcpy(r->d_maps, packed.data(), r->bytes, cudaMemcpyHostToDevice) != cudaSuccess) {
+    if (cudaSetDevice(device) != cudaSuccess ||
+        (pool_setup(device), cudaStreamCreateWithFlags(&r->stream, cudaStreamNonBlocking)) != cudaSuccess ||
+        dmalloc((void **)&r->d_maps, r->bytes, r->stream) != cudaSuccess ||
+        cudaMemcpyAsync(r->d_maps, packed.data(), r->bytes, cudaMemcpyHostToDevice, r->stream) != cudaSuccess ||
+        cudaStreamSynchronize(r->stream) != cudaSuccess) {
         cudaGetLastError();
         *err = "receptor upload to device " + std::to_string(device) + " failed";
         return DOCK_E_INTERNAL;
@@ -158,7 +201,9 @@ int ctx_create(std::shared_ptr<Receptor> rec, const dock_params &p, dock_ctx **o
     if (cudaSetDevice(c->device) != cudaSuccess) return bail("cudaSetDevice failed");
     if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess) return bail("cudaStreamCreate failed");
     if (setup_kernel_attributes() != cudaSuccess) return bail("cudaFuncSetAttribute failed (is this an sm_100 device?)");
-    if (cudaMalloc(&c->d_dfs2orig, sizeof(int) * kMaxAtoms) != cudaSuccess) return bail("device allocation failed");
+    if (dmalloc((void **)&c->d_dfs2orig, sizeof(int) * kMaxAtoms, c->stream) != cudaSuccess ||
+        cudaStreamSynchronize(c->stream) != cudaSuccess)
+        return bail("device allocation failed");
     if (p.l2_persist) {
         // NS: "Grid maps live in HBM with L2-persistence windows".
         cudaDeviceProp prop;
@@ -184,9 +229,10 @@ int ctx_create(std::shared_ptr<Receptor> rec, const dock_params &p, dock_ctx **o
 int ctx_reserve(dock_ctx *c, size_t blob_bytes, int runs, int pop) {
     CK(cudaSetDevice(c->device));
     if (blob_bytes > c->blob_cap) {
-        if (c->d_blob) { CK(cudaStreamSynchronize(c->stream)); cudaFree(c->d_blob); }
+        if (c->d_blob) { CK(cudaStreamSynchronize(c->stream)); dfree(c->d_blob, c->stream); }
         c->d_blob = nullptr; c->blob_cap = 0;
-        CK(cudaMalloc(&c->d_blob, blob_bytes));
+        CK(dmalloc((void **)&c->d_blob, blob_bytes, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
         c->blob_cap = blob_bytes;
     }
     if (runs > 0 && pop > 0) return ensure_buffers(c, runs, pop);
@@ -243,9 +289,15 @@ int dock_init(const dock_grids *grids, const dock_type_param *type_params, const
     std::string err;
     if (dk::validate_params(p, &err) != DOCK_OK) { g_init_error = err; return DOCK_E_INPUT; }
     std::vector<float4> packed;
-    if (dk::pack_grid(grids, &packed, &err) != DOCK_OK) { g_init_error = err; return DOCK_E_INPUT; }
+    {
+        Trace tr("init.pack_grid");
+        if (dk::pack_grid(grids, &packed, &err) != DOCK_OK) { g_init_error = err; return DOCK_E_INPUT; }
+    }
     dk::Prepared prep;
-    if (dk::prepare_ligand(ligand, type_params, grids->n_types, &prep, &err) != DOCK_OK) { g_init_error = err; return DOCK_E_INPUT; }
+    {
+        Trace tr("init.prepare_ligand");
+        if (dk::prepare_ligand(ligand, type_params, grids->n_types, &prep, &err) != DOCK_OK) { g_init_error = err; return DOCK_E_INPUT; }
+    }
     int ndev = 0;
     if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev < 1) {
         cudaGetLastError();
@@ -254,9 +306,16 @@ int dock_init(const dock_grids *grids, const dock_type_param *type_params, const
     }
     if (p.device < 0 || p.device >= ndev) { g_init_error = "params.device: no such CUDA device"; return DOCK_E_INPUT; }
     std::shared_ptr<dk::Receptor> rec;
-    if (int rc = dk::receptor_upload(grids, packed, p.device, &rec, &err)) { g_init_error = err; return rc; }
+    {
+        Trace tr("init.receptor_upload");
+        if (int rc = dk::receptor_upload(grids, packed, p.device, &rec, &err)) { g_init_error = err; return rc; }
+    }
     dock_ctx *c = nullptr;
-    if (int rc = dk::ctx_create(rec, p, &c, &err)) { g_init_error = err; return rc; }
+    {
+        Trace tr("init.ctx_create");
+        if (int rc = dk::ctx_create(rec, p, &c, &err)) { g_init_error = err; return rc; }
+    }
+    Trace tr("init.attach_ligand");
     if (int rc = dk::ctx_attach_ligand(c, std::move(prep))) { g_init_error = c->err; dock_free(c); return rc; }
     *out = c;
     return DOCK_OK;
@@ -264,14 +323,26 @@ int dock_init(const dock_grids *grids, const dock_type_param *type_params, const
 
 void dock_free(dock_ctx *c) {
     if (!c) return;
+    Trace tr("free.total");
     cudaSetDevice(c->device);
-    if (c->stream) cudaStreamSynchronize(c->stream);
-    cudaFree(c->d_blob); cudaFree(c->d_dfs2orig);
-    cudaFree(c->d_genes); cudaFree(c->d_E); cudaFree(c->d_state); cudaFree(c->d_perm); cudaFree(c->d_ls_evals);
-    if (c->h_state) cudaFreeHost(c->h_state);
-    for (cudaEvent_t e : c->events) cudaEventDestroy(e);
-    if (c->stream) cudaStreamDestroy(c->stream);
+    {
+        Trace t1("free.sync");
+        if (c->stream) cudaStreamSynchronize(c->stream);
+    }
+    {
+        Trace t2("free.device_buffers");
+        cudaStream_t s = c->stream;
+        dk::dfree(c->d_blob, s); dk::dfree(c->d_dfs2orig, s);
+        dk::dfree(c->d_genes, s); dk::dfree(c->d_E, s); dk::dfree(c->d_state, s); dk::dfree(c->d_perm, s);
+        dk::dfree(c->d_ls_evals, s);
+    }
+    {
+        Trace t3("free.events_and_stream");
+        for (cudaEvent_t e : c->events) cudaEventDestroy(e);
+        if (c->stream) cudaStreamDestroy(c->stream);
+    }
     cudaGetLastError();
+    Trace t4("free.receptor_release");
     delete c;   // drops this context's reference to the receptor upload
 }
 
@@ -327,6 +398,7 @@ int dock_run_device(dock_ctx *c, int32_t pop, int32_t runs, int32_t run_base, ui
     // capture K generations once; the kernels read the generation from device state
     cudaGraph_t graph = nullptr;
     cudaGraphExec_t exec = nullptr;
+    auto t_cap = std::chrono::steady_clock::now();
     CK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
     cudaError_t ce = cudaSuccess;
     for (int k = 0; k < K && ce == cudaSuccess; ++k) {
@@ -348,12 +420,15 @@ int dock_run_device(dock_ctx *c, int32_t pop, int32_t runs, int32_t run_base, ui
         c->err = "cudaGraphInstantiate failed";
         return DOCK_E_INTERNAL;
     }
+    if (Trace::on())
+        std::fprintf(stderr, "[dock] run.graph_capture+instantiate %.3f ms\n",
+                     std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_cap).count());
     const int per_graph = K * (do_ls ? 3 : 2);
     const long long max_batches = (long long)c->params.max_generations / K + 2;
     int rc = DOCK_OK;
     for (long long b = 0; b < max_batches; ++b) {
         cudaError_t e = cudaGraphLaunch(exec, s);
-        if (e == cudaSuccess) e = cudaMemcpyAsync(c->h_state, c->d_state, sizeof(dk::RunState) * runs, cudaMemcpyDeviceToHost, s);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(c->h_state.data(), c->d_state, sizeof(dk::RunState) * runs, cudaMemcpyDeviceToHost, s);
         if (e == cudaSuccess) e = cudaStreamSynchronize(s);
         if (e != cudaSuccess) { c->err = std::string("generation batch: ") + cudaGetErrorString(e); rc = DOCK_E_INTERNAL; break; }
         c->launches += per_graph;
@@ -392,17 +467,17 @@ int dock_run_ex(dock_ctx *c, int32_t pop, int32_t runs, int32_t run_base, uint32
     if (!best_energy || !best_genotype) return input_error(c, "best_energy/best_genotype: NULL");
     CK(cudaSetDevice(c->device));
     const int G = c->prep.G, N = c->prep.N;
-    DevBuf bE, bG, bEv, bGen, bX, bE2;
-    CK(cudaMalloc(&bE.p, sizeof(float) * runs));
-    CK(cudaMalloc(&bG.p, sizeof(float) * runs * G));
-    CK(cudaMalloc(&bEv.p, sizeof(int64_t) * runs));
-    CK(cudaMalloc(&bGen.p, sizeof(int32_t) * runs));
+    DevBuf bE(c->stream), bG(c->stream), bEv(c->stream), bGen(c->stream), bX(c->stream), bE2(c->stream);
+    CK(bE.alloc(sizeof(float) * runs));
+    CK(bG.alloc(sizeof(float) * runs * G));
+    CK(bEv.alloc(sizeof(int64_t) * runs));
+    CK(bGen.alloc(sizeof(int32_t) * runs));
     int rc = dock_run_device(c, pop, runs, run_base, ligand_id, max_evals, seed, (float *)bE.p, (float *)bG.p,
                              (int64_t *)bEv.p, (int32_t *)bGen.p, c->stream);
     if (rc != DOCK_OK) return rc;
     if (best_xyz) {
-        CK(cudaMalloc(&bX.p, sizeof(float) * runs * N * 3));
-        CK(cudaMalloc(&bE2.p, sizeof(float) * runs));
+        CK(bX.alloc(sizeof(float) * runs * N * 3));
+        CK(bE2.alloc(sizeof(float) * runs));
         CK(dk::launch_eval(c->lig, c->grid, runs, (const float *)bG.p, (float *)bE2.p, nullptr, (float *)bX.p,
                            c->d_dfs2orig, c->stream));
         c->launches += 1;
@@ -433,6 +508,17 @@ int dock_eval_device(dock_ctx *c, int32_t n, const float *d_genotypes, float *d_
     return DOCK_OK;
 }
 
+int dock_bench_part(dock_ctx *c, int32_t part, int32_t n, int32_t iters, const float *d_genotypes, float *d_out,
+                    void *stream) {
+    if (!c) return DOCK_E_INPUT;
+    if (part < 0 || part > 1 || n < 0 || iters < 1) return input_error(c, "part in {0,1}, n >= 0, iters >= 1");
+    if (n > 0 && (!d_genotypes || !d_out)) return input_error(c, "d_genotypes/d_out: NULL");
+    CK(cudaSetDevice(c->device));
+    CK(dk::launch_bench_part(c->lig, c->grid, part, n, iters, d_genotypes, d_out, (cudaStream_t)stream));
+    c->launches += 1;
+    return DOCK_OK;
+}
+
 int dock_eval(dock_ctx *c, int32_t n, const float *genotypes, float *energy, float *grad, float *xyz) {
     if (!c) return DOCK_E_INPUT;
     if (n < 0) return input_error(c, "n: must be >= 0");
@@ -442,11 +528,11 @@ int dock_eval(dock_ctx *c, int32_t n, const float *genotypes, float *energy, flo
         if (!std::isfinite(genotypes[i])) return input_error(c, "genotypes[" + std::to_string(i) + "]: non-finite");
     CK(cudaSetDevice(c->device));
     const int G = c->prep.G, N = c->prep.N;
-    DevBuf dg, dE, dgr, dx;
-    CK(cudaMalloc(&dg.p, sizeof(float) * n * G));
-    CK(cudaMalloc(&dE.p, sizeof(float) * n));
-    if (grad) CK(cudaMalloc(&dgr.p, sizeof(float) * n * G));
-    if (xyz) CK(cudaMalloc(&dx.p, sizeof(float) * n * N * 3));
+    DevBuf dg(c->stream), dE(c->stream), dgr(c->stream), dx(c->stream);
+    CK(dg.alloc(sizeof(float) * n * G));
+    CK(dE.alloc(sizeof(float) * n));
+    if (grad) CK(dgr.alloc(sizeof(float) * n * G));
+    if (xyz) CK(dx.alloc(sizeof(float) * n * N * 3));
     CK(cudaMemcpyAsync(dg.p, genotypes, sizeof(float) * n * G, cudaMemcpyHostToDevice, c->stream));
     CK(dk::launch_eval(c->lig, c->grid, n, (const float *)dg.p, (float *)dE.p, (float *)dgr.p, (float *)dx.p,
                        c->d_dfs2orig, c->stream));
@@ -495,10 +581,10 @@ int dock_philox(int32_t n, const uint32_t *ctr4, const uint32_t *key2, uint32_t 
     if (n == 0) return DOCK_OK;
     dock_ctx tmp;
     dock_ctx *c = &tmp;
-    DevBuf dc, dk_, dout;
-    CK(cudaMalloc(&dc.p, 16 * (size_t)n));
-    CK(cudaMalloc(&dk_.p, 8 * (size_t)n));
-    CK(cudaMalloc(&dout.p, 16 * (size_t)n));
+    DevBuf dc(c->stream), dk_(c->stream), dout(c->stream);
+    CK(dc.alloc(16 * (size_t)n));
+    CK(dk_.alloc(8 * (size_t)n));
+    CK(dout.alloc(16 * (size_t)n));
     CK(cudaMemcpy(dc.p, ctr4, 16 * (size_t)n, cudaMemcpyHostToDevice));
     CK(cudaMemcpy(dk_.p, key2, 8 * (size_t)n, cudaMemcpyHostToDevice));
     CK(dk::launch_philox(n, (const uint32_t *)dc.p, (const uint32_t *)dk_.p, (uint32_t *)dout.p, nullptr));
@@ -513,8 +599,8 @@ int dock_stream_words(uint64_t seed, uint32_t ligand_id, uint32_t purpose, uint3
     dock_ctx tmp;
     dock_ctx *c = &tmp;
     const uint64_t k = seed + (uint64_t)ligand_id * 0x9E3779B97F4A7C15ull;
-    DevBuf d;
-    CK(cudaMalloc(&d.p, 4 * (size_t)n));
+    DevBuf d(c->stream);
+    CK(d.alloc(4 * (size_t)n));
     CK(dk::launch_stream_words((uint32_t)k, (uint32_t)(k >> 32), purpose, slot, gen, run, m0, n, (uint32_t *)d.p, nullptr));
     CK(cudaMemcpy(out, d.p, 4 * (size_t)n, cudaMemcpyDeviceToHost));
     return DOCK_OK;
@@ -535,8 +621,8 @@ int dock_ga_step(dock_ctx *c, uint64_t seed, uint32_t ligand_id, int32_t run, in
     const dk::PopDev pd = pop_of(c);
     const int cur = (gen - 1) & 1, nxt = gen & 1;
     dk::RunState st{0, gen - 1, 0};
-    DevBuf ddbg;
-    CK(cudaMalloc(&ddbg.p, sizeof(int) * 8 * pop));
+    DevBuf ddbg(c->stream);
+    CK(ddbg.alloc(sizeof(int) * 8 * pop));
     CK(cudaMemcpyAsync(c->d_genes + (size_t)cur * 1 * pop * G, old_genes, sizeof(float) * pop * G, cudaMemcpyHostToDevice, c->stream));
     CK(cudaMemcpyAsync(c->d_E + (size_t)cur * pop, old_E, sizeof(float) * pop, cudaMemcpyHostToDevice, c->stream));
     CK(cudaMemcpyAsync(c->d_state, &st, sizeof(st), cudaMemcpyHostToDevice, c->stream));
@@ -561,11 +647,11 @@ int dock_ls_step(dock_ctx *c, int32_t method, int32_t n, int32_t iters, uint64_t
     const int G = c->prep.G;
     dk::SearchDev sp = make_search(c, 2, 1, run, ligand_id, LLONG_MAX, seed);
     sp.ls_method = method;
-    DevBuf dg, dE, dev, dsl;
-    CK(cudaMalloc(&dg.p, sizeof(float) * n * G));
-    CK(cudaMalloc(&dE.p, sizeof(float) * n));
-    CK(cudaMalloc(&dev.p, sizeof(int) * n));
-    CK(cudaMalloc(&dsl.p, sizeof(int) * n));
+    DevBuf dg(c->stream), dE(c->stream), dev(c->stream), dsl(c->stream);
+    CK(dg.alloc(sizeof(float) * n * G));
+    CK(dE.alloc(sizeof(float) * n));
+    CK(dev.alloc(sizeof(int) * n));
+    CK(dsl.alloc(sizeof(int) * n));
     CK(cudaMemcpyAsync(dg.p, genes, sizeof(float) * n * G, cudaMemcpyHostToDevice, c->stream));
     CK(cudaMemcpyAsync(dE.p, energy, sizeof(float) * n, cudaMemcpyHostToDevice, c->stream));
     CK(cudaMemcpyAsync(dsl.p, slots, sizeof(int) * n, cudaMemcpyHostToDevice, c->stream));

@@ -38,14 +38,12 @@ struct LigDev {
     int NW;           // words per mask row = ceil(N / 32)
     // gradient-path pair tiles (score.cuh intra_tiles): lane groups of Wg lanes, atom
     // chunks of Wg, each chunk stored twice in a row ([c][2*Wg]) so a rotating partner
-    // index never wraps; padded entries use the all-zero "null" type nt.
+    // index never wraps; padded entries are all-zero params.
     int Wg;           // lanes per group of the gradient kernels (16 if N <= 16, else 32)
     int NC;           // chunks = ceil(N / Wg)
-    int NT1;          // type-pair table side = n_types + 1 (last = null type)
-    int off_pdup;     // int[NC][2*Wg]  partner byte offset into a table row = type * 32
-    int off_tab;      // float4[NT1][NT1][2]  {r_eq^2, A, B6, B10}, {S_iV_j + S_jV_i, 0, 0, 0}:
-                      //   E_vdw = A x^12 - B6 x^6 - B10 x^10 (A = eps, B6 = 2 eps, B10 = 0, or
-                      //   A = 5 eps, B6 = 0, B10 = 6 eps for a donor-acceptor pair; D5)
+    int off_ppar;     // float4[NC][2*Wg] partner params {R/2, sqrt(eps), S, V}, duplicated chunks;
+                      //   R/2 negated for acceptors and sqrt(eps) negated for donors (role
+                      //   in the sign bits; magnitudes via free |.| operand modifiers)
     const uint8_t *blob;          // device pointer
 };
 

@@ -18,8 +18,19 @@
 
 namespace dk {
 
+// Stream-ordered device memory (cudaMallocAsync / cudaFreeAsync from the device's default
+// pool, release threshold raised so freed blocks stay cached in the process).  A plain
+// cudaFree synchronises the device and was measured at 100-400 ms per context teardown
+// on B200 (profiles/r01f, DOCK_TRACE); pool frees are asynchronous and cheap.
+void pool_setup(int device);
+inline cudaError_t dmalloc(void **p, size_t bytes, cudaStream_t s) { return cudaMallocAsync(p, bytes ? bytes : 16, s); }
+inline void dfree(void *p, cudaStream_t s) {
+    if (p) cudaFreeAsync(p, s);
+}
+
 struct Receptor {
     int device = 0;
+    cudaStream_t stream = nullptr;   // owns the upload and the final free
     float4 *d_maps = nullptr;
     size_t bytes = 0;
     GridDev grid{};
@@ -50,8 +61,7 @@ struct dock_ctx {
     float *d_genes = nullptr, *d_E = nullptr;
     dk::RunState *d_state = nullptr;
     int *d_perm = nullptr, *d_ls_evals = nullptr;
-    dk::RunState *h_state = nullptr;
-    int h_state_cap = 0;
+    std::vector<dk::RunState> h_state;   // termination poll target (pageable: read right after a sync)
     std::string err;
     long long launches = 0;
     double prof_ms[3] = {0, 0, 0};

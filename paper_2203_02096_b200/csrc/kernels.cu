@@ -73,9 +73,8 @@ __device__ __forceinline__ LigSm stage_ligand(const LigDev &L, uint8_t *sm, int 
     v.pairs = reinterpret_cast<const uint32_t *>(sm + L.off_pairs);
     v.pprm = reinterpret_cast<const float4 *>(sm + L.off_pprm);
     v.mask = reinterpret_cast<const uint32_t *>(sm + L.off_mask);
-    v.pdup = reinterpret_cast<const int *>(sm + L.off_pdup);
-    v.tab = sm + L.off_tab;
-    v.NC = L.NC; v.NT1 = L.NT1;
+    v.ppar = reinterpret_cast<const float4 *>(sm + L.off_ppar);
+    v.NC = L.NC;
     return v;
 }
 
@@ -541,7 +540,7 @@ __global__ void __launch_bounds__(tree_threads<W, D>(), (W == 16 && D == 3) ? 2 
     float *sx = reinterpret_cast<float *>(sm + staged + NGR * SL.bytes);
     float *sb = sx + kMaxGenes;
     float *sE = sb + kMaxGenes;
-    float *stri = sE + NGR;                                  // [D][G] deviate shapes of this round
+    float *stri0 = sE + NGR;                                 // [2][D][G] deviate shapes, double-buffered by round
     const int grp = threadIdx.x / W, sub = threadIdx.x % W;
     const bool in_grp = grp < NGR;
     const Scratch S = scratch_at(sm + staged + (in_grp ? grp : 0) * SL.bytes, SL);
@@ -561,16 +560,16 @@ __global__ void __launch_bounds__(tree_threads<W, D>(), (W == 16 && D == 3) ? 2 
             if (k < lvl) { digit[k] = v % 3; v /= 3; }
         }
     }
+    // deviate shapes of the first round (one Philox block per (iteration, gene))
+    for (int q = threadIdx.x; q < D * G; q += blockDim.x) {
+        const int k = q / G, j = q - k * G;
+        stri0[q] = sw_tri(key, t.slot, t.gen, t.run_g, G, k, j);
+    }
     __syncthreads();
     float Ex = *t.E, rho = sp.sw_rho;
-    int succ = 0, fail = 0, ne = 0, it = 0;
+    int succ = 0, fail = 0, ne = 0, it = 0, cur = 0;
     while (it < a.iters && !(rho < sp.sw_rho_min)) {
-        // ---- 0. the round's deviate shapes, one Philox block per (iteration, gene) ----
-        for (int q = threadIdx.x; q < D * G; q += blockDim.x) {
-            const int k = q / G, j = q - k * G;
-            stri[q] = sw_tri(key, t.slot, t.gen, t.run_g, G, it + k, j);
-        }
-        __syncthreads();
+        const float *stri = stri0 + cur * D * kMaxGenes;
         // ---- 1. every live node's trial genotype, then its energy ----
         if (in_grp) {
             float rl[D];
@@ -628,14 +627,24 @@ __global__ void __launch_bounds__(tree_threads<W, D>(), (W == 16 && D == 3) ? 2 
             ++it;
             ++rho_steps;
         }
-        // ---- 3. advance x and b along the resolved path ----
-        for (int j = threadIdx.x; j < G; j += blockDim.x) {
-            float x = sx[j], b = sb[j];
+        // ---- 3. advance x and b along the resolved path (warp 0), and meanwhile the next
+        // round's deviate shapes (iterations it..it+D-1; the other warps) ----
+        if (threadIdx.x < 32) {
+            for (int j = threadIdx.x; j < G; j += 32) {
+                float x = sx[j], b = sb[j];
 #pragma unroll
-            for (int k = 0; k < D; ++k)
-                if (k < rho_steps) sw_gene_step(path[k], sw_dev(rl[k], stri[k * G + j]), x, b);
-            sx[j] = x; sb[j] = b;
+                for (int k = 0; k < D; ++k)
+                    if (k < rho_steps) sw_gene_step(path[k], sw_dev(rl[k], stri[k * G + j]), x, b);
+                sx[j] = x; sb[j] = b;
+            }
+        } else {
+            float *nxt = stri0 + (cur ^ 1) * D * kMaxGenes;
+            for (int q = threadIdx.x - 32; q < D * G; q += blockDim.x - 32) {
+                const int k = q / G, j = q - k * G;
+                nxt[q] = sw_tri(key, t.slot, t.gen, t.run_g, G, it + k, j);
+            }
         }
+        cur ^= 1;
         __syncthreads();
     }
     for (int j = threadIdx.x; j < G; j += blockDim.x) t.row[j] = sx[j];
@@ -691,6 +700,37 @@ __global__ void __launch_bounds__(256) k_best(const int G, const SearchDev sp, c
     }
 }
 
+// ---------------------------------------------------------------------------
+// k_bench_part: microbenchmark of one part of the evaluation: PARTS =
+// kInter -> pose + grid interpolation (a3+a4, energy + gradient), PARTS = kIntra -> pose
+// + pair tiles (a3+a5, energy + forces).  Each group evaluates its genotype `iters`
+// times, nudging the translation by 1e-3 Å per iteration (ADADELTA-like locality).
+// ---------------------------------------------------------------------------
+template <int W, int MAXC, int PARTS>
+__global__ void __launch_bounds__(256, (MAXC <= 4 ? DK_ADA_MINB : 1)) k_bench_part(const LigDev L, const GridDev g,
+                                                                                  const ScratchLayout SL, int n, int iters,
+                                                                                  const float *__restrict__ genes, float *E) {
+    extern __shared__ uint4 smem_u4[];
+    uint8_t *sm = reinterpret_cast<uint8_t *>(smem_u4);
+    const int gl = threadIdx.x / W, sub = threadIdx.x % W;
+    const int gi = blockIdx.x * (blockDim.x / W) + gl;
+    const bool act = gi < n;
+    if (!__syncthreads_or(act)) return;
+    const LigSm Ls = stage_ligand(L, sm, staged_bytes(L, true));
+    if (!act) return;
+    const Scratch S = scratch_at(sm + staged_bytes(L, true) + gl * SL.bytes, SL);
+    const unsigned mask = group_mask<W>();
+    for (int j = sub; j < L.G; j += W) S.genes[j] = genes[(size_t)gi * L.G + j];
+    __syncwarp(mask);
+    float acc = 0.0f;
+    for (int it = 0; it < iters; ++it) {
+        acc += eval_group<W, MAXC, true, PARTS>(Ls, g, S, sub, mask);
+        if (sub == 0) S.genes[0] += 1e-3f;
+        __syncwarp(mask);
+    }
+    if (sub == 0) E[gi] = acc;
+}
+
 __global__ void k_philox(int n, const uint4 *ctr, const uint2 *key, uint4 *out) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i < n) out[i] = philox4x32_10(ctr[i], key[i]);
@@ -735,7 +775,9 @@ cudaError_t setup_kernel_attributes() {
     if (e == cudaSuccess) e = allow_smem(k_ls_adadelta<W, MAXC>);                    \
     if (e == cudaSuccess) e = allow_smem(k_ls_sw<W, MAXC>);                         \
     if (e == cudaSuccess) e = allow_smem(k_ls_sw_tree<W, MAXC, 2>);                  \
-    if (e == cudaSuccess) e = allow_smem(k_ls_sw_tree<W, MAXC, 3>);
+    if (e == cudaSuccess) e = allow_smem(k_ls_sw_tree<W, MAXC, 3>);                  \
+    if (e == cudaSuccess) e = allow_smem(k_bench_part<W, MAXC, kInter>);             \
+    if (e == cudaSuccess) e = allow_smem(k_bench_part<W, MAXC, kIntra>);
     DK_ATTR(16, 1) DK_ATTR(32, 1) DK_ATTR(32, 2) DK_ATTR(32, 3) DK_ATTR(32, 4) DK_ATTR(32, 8)
 #undef DK_ATTR
     return e;
@@ -802,7 +844,7 @@ cudaError_t launch_ls(const LigDev &L, const GridDev &g, const SearchDev &sp, co
             // auto stops at depth 2; depth 3 stays available explicitly.
             for (int D = 2; D >= 2 && depth == 1; --D) {
                 const int ngr = D == 3 ? 26 : 8;
-                const size_t sm_b = (size_t)L.blob_bytes + (size_t)ngr * SL.bytes + 4 * (2 * kMaxGenes + ngr + D * kMaxGenes);
+                const size_t sm_b = (size_t)L.blob_bytes + (size_t)ngr * SL.bytes + 4 * (2 * kMaxGenes + ngr + 2 * D * kMaxGenes);
                 int per_sm = 0;
                 DK_DISPATCH(cfg, {
                     if (D == 3) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_ls_sw_tree<W, MAXC, 3>, tree_threads<W, 3>(), sm_b);
@@ -814,7 +856,7 @@ cudaError_t launch_ls(const LigDev &L, const GridDev &g, const SearchDev &sp, co
         }
         if (depth >= 2) {
             const int ngr = depth == 3 ? 26 : 8;
-            const size_t smem = (size_t)L.blob_bytes + (size_t)ngr * SL.bytes + 4 * (2 * kMaxGenes + ngr + depth * kMaxGenes);
+            const size_t smem = (size_t)L.blob_bytes + (size_t)ngr * SL.bytes + 4 * (2 * kMaxGenes + ngr + 2 * depth * kMaxGenes);
             if (smem > (size_t)kSmemMax) return cudaErrorInvalidConfiguration;
             DK_DISPATCH(cfg, {
                 if (depth == 3) k_ls_sw_tree<W, MAXC, 3><<<n_total, tree_threads<W, 3>(), smem, s>>>(L, g, SL, sp, pop, a);
@@ -838,6 +880,22 @@ cudaError_t launch_ls(const LigDev &L, const GridDev &g, const SearchDev &sp, co
         const int blocks = ceil_div(n_total, groups);
         DK_DISPATCH(cfg, { k_ls_adadelta<W, MAXC><<<blocks, kThreads, smem, s>>>(L, g, SL, sp, pop, a); });
     }
+    return cudaGetLastError();
+}
+
+cudaError_t launch_bench_part(const LigDev &L, const GridDev &g, int part, int n, int iters, const float *genes,
+                              float *E, cudaStream_t s) {
+    if (n <= 0) return cudaSuccess;
+    const GroupCfg cfg = pick_group(L.N);
+    const ScratchLayout SL = scratch_layout(L.N, L.T, L.G, true, 0);
+    const int groups = kThreads / cfg.W;
+    const size_t smem = (size_t)staged_bytes(L, true) + (size_t)groups * SL.bytes;
+    if (smem > (size_t)kSmemMax) return cudaErrorInvalidConfiguration;
+    const int blocks = ceil_div(n, groups);
+    DK_DISPATCH(cfg, {
+        if (part == 0) k_bench_part<W, MAXC, kInter><<<blocks, kThreads, smem, s>>>(L, g, SL, n, iters, genes, E);
+        else k_bench_part<W, MAXC, kIntra><<<blocks, kThreads, smem, s>>>(L, g, SL, n, iters, genes, E);
+    });
     return cudaGetLastError();
 }
 

@@ -42,6 +42,8 @@ cudaError_t launch_ga(const LigDev &L, const GridDev &g, const SearchDev &sp, co
                       int *dbg, cudaStream_t s);
 cudaError_t launch_ls(const LigDev &L, const GridDev &g, const SearchDev &sp, const PopDev &pop,
                       const LsArgs &a, int n_total, cudaStream_t s);
+cudaError_t launch_bench_part(const LigDev &L, const GridDev &g, int part, int n, int iters, const float *genes,
+                              float *E, cudaStream_t s);
 cudaError_t launch_gen_end(const SearchDev &sp, const PopDev &pop, cudaStream_t s);
 cudaError_t launch_best(const LigDev &L, const SearchDev &sp, const PopDev &pop, float *bestE,
                         float *bestG, long long *evals, int *gens, cudaStream_t s);

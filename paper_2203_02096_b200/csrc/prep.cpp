@@ -218,9 +218,7 @@ int prepare_ligand(const dock_ligand *l, const dock_type_param *tp, int n_types,
     L.off_mask = off; off += a16(4 * N * L.NW);
     L.Wg = N <= 16 ? 16 : 32;
     L.NC = (N + L.Wg - 1) / L.Wg;
-    L.NT1 = n_types + 1;
-    L.off_pdup = off; off += a16(4 * L.NC * 2 * L.Wg);
-    L.off_tab = off; off += 32 * L.NT1 * L.NT1;
+    L.off_ppar = off; off += 16 * L.NC * 2 * L.Wg;
     L.grad_bytes = off;              // the gradient kernels stage only up to here
     L.off_pairs = off; off += a16(4 * P);
     L.off_pprm = off; off += 16 * P;
@@ -267,28 +265,20 @@ int prepare_ligand(const dock_ligand *l, const dock_type_param *tp, int n_types,
         tU[k] = make_float4((float)(u[0] / n), (float)(u[1] / n), (float)(u[2] / n), 0.f);
         tm[k] = make_int4(parent[k], pos[a], pos[b], lo[k] | (hi[k] << 16));
     }
-    // gradient-path tiles: duplicated partner type offsets and the type-pair table (D5)
+    // gradient-path tiles: chunk-duplicated partner params, H-bond role in the signs
+    // (R/2 < 0: acceptor, sqrt(eps) < 0: donor; D5)
     {
-        int *pd = reinterpret_cast<int *>(bl + L.off_pdup);
+        float4 *pp = reinterpret_cast<float4 *>(bl + L.off_ppar);
         for (int c = 0; c < L.NC; ++c)
             for (int q = 0; q < 2 * L.Wg; ++q) {
                 const int p = c * L.Wg + (q % L.Wg);
-                pd[c * 2 * L.Wg + q] = 32 * (p < N ? l->type[order[p]] : n_types);
-            }
-        float4 *tb = reinterpret_cast<float4 *>(bl + L.off_tab);
-        for (int ti = 0; ti < L.NT1; ++ti)
-            for (int tj = 0; tj < L.NT1; ++tj) {
-                float4 *r = tb + 2 * (ti * L.NT1 + tj);
-                r[0] = make_float4(0.f, 0.f, 0.f, 0.f);
-                r[1] = make_float4(0.f, 0.f, 0.f, 0.f);
-                if (ti == n_types || tj == n_types) continue;
-                const dock_type_param &a = tp[ti], &b = tp[tj];
-                const double req = 0.5 * ((double)a.R + (double)b.R);
-                const double eps = std::sqrt((double)a.eps * (double)b.eps);
-                const bool hb = (a.role == 1 && b.role == 2) || (a.role == 2 && b.role == 1);
-                r[0] = make_float4((float)(req * req), (float)((hb ? 5.0 : 1.0) * eps), (float)(hb ? 0.0 : 2.0 * eps),
-                                   (float)(hb ? 6.0 * eps : 0.0));
-                r[1] = make_float4((float)((double)a.S * b.V + (double)b.S * a.V), 0.f, 0.f, 0.f);
+                float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+                if (p < N) {
+                    const dock_type_param &t = tp[l->type[order[p]]];
+                    const float h = 0.5f * t.R, e = (float)std::sqrt((double)t.eps);
+                    v = make_float4(t.role == 2 ? -h : h, t.role == 1 ? -e : e, t.S, t.V);
+                }
+                pp[c * 2 * L.Wg + q] = v;
             }
     }
     auto hb_of = [&](int i, int j) {

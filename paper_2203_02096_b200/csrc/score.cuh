@@ -31,9 +31,8 @@ struct LigSm {
     const uint32_t *pairs;        // i | j<<8 | hb<<16
     const float4 *pprm;           // per pair: r_eq^2, eps_ij, S_iV_j+S_jV_i, 332.06363/4 q_i q_j
     const uint32_t *mask;         // [N][NW] pair-membership bit rows
-    const int *pdup;              // [NC][2W] partner type byte offsets (duplicated chunks)
-    const uint8_t *tab;           // [NT1][NT1] 32-byte type-pair records
-    int NC, NT1;
+    const float4 *ppar;           // [NC][2W] signed partner params (duplicated chunks)
+    int NC;
 };
 
 // Gradient-path pose index: chunk c = a / W lives at [c][2W], its copy at [c][2W] + W.
@@ -135,21 +134,30 @@ __device__ __forceinline__ float pair_eg(float rho2, float4 pi, float qi, float4
     return Evdw + Eel + Eds;
 }
 
-// D5 pair energy and dE/d(rho^2) from a type-pair record (gradient path):
-// E_vdw = A x^12 - B6 x^6 - B10 x^10, x^2 = r_eq^2 / rho^2; rho^2 dE_vdw/drho^2 =
-// -6 A x^12 + 3 B6 x^6 + 5 B10 x^10; E_el = qq / rho^2; E_ds = SV exp(-rho^2 / 2 sigma^2).
-__device__ __forceinline__ float pair_eg_tab(float rho2, float4 tb, float sv, float qq, float &dE) {
+// D5 vdW/H-bond part from (x^2, A, B): E = A x^12 - |B| x^n, n = 6 (B >= +0) or 10 (B
+// negative); returns E and rho^2 dE/drho^2 = -6 A x^12 + (n/2) |B| x^n.
+__device__ __forceinline__ float vdw_ab(float x2, float A, float B, float &dvr) {
+    const float x4 = x2 * x2, x6 = x4 * x2, x12 = x6 * x6;
+    const bool ten = __float_as_int(B) < 0;
+    const float xn = ten ? x6 * x4 : x6;
+    const float tA = A * x12, tB = fabsf(B) * xn;
+    dvr = fmaf(-6.0f, tA, (ten ? 5.0f : 3.0f) * tB);
+    return tA - tB;
+}
+
+// D5 pair energy and dE/d(rho^2) on the gradient path, given the vdW coefficients:
+// E_el = qq / rho^2; E_ds = SV exp(-rho^2 / 2 sigma^2); zero force inside the clamp.
+__device__ __forceinline__ float pair_eg_ab(float rho2, float req2, float A, float B, float sv, float qq, float &dE) {
     const bool clamped = rho2 < 1e-4f;
-    rho2 = fmaxf(rho2, 1e-4f);                           // 0.01 Å clamp; zero force inside
+    rho2 = fmaxf(rho2, 1e-4f);                           // 0.01 Å clamp
     const float inv = rcp_approx(rho2);
-    const float x2 = tb.x * inv, x4 = x2 * x2, x6 = x4 * x2, x12 = x6 * x6, x10 = x6 * x4;
-    const float tA = tb.y * x12, tB = tb.z * x6, tC = tb.w * x10;
+    float dvr;
+    const float Evdw = vdw_ab(req2 * inv, A, B, dvr);
     const float Eel = qq * inv;
     const float Eds = sv * ex2_approx(rho2 * kExpScale);
-    const float dvr = fmaf(-6.0f, tA, fmaf(3.0f, tB, 5.0f * tC));
     const float d = fmaf(dvr - Eel, inv, -Eds * kInvTwoSigma2);
     dE = clamped ? 0.0f : d;
-    return (tA - tB - tC) + Eel + Eds;
+    return Evdw + Eel + Eds;
 }
 
 // D4 intermolecular energy of one atom and its gradient.
@@ -194,18 +202,31 @@ __device__ __forceinline__ float inter_atom(const GridDev &g, int type, float q,
     return kOut * (1.0f + d);
 }
 
+// Own-atom pair data of a lane (gradient tiles).
+// (A per-type-pair table lookup was measured slower: random 16-byte shared-memory reads
+// bank-conflict across lanes, profiles/r01f; these per-atom partner reads are consecutive.)
+struct OwnPair {
+    float q;                      // 332.06363/4 * q_i
+    float R, e, S, V;             // |R_i|/2, |sqrt eps_i|, S_i, V_i
+    bool hbc, don;                // H-bond capable, donor (else acceptor)
+};
+
 // One D5 pair inside the gradient tiles: energy into e, force into the own-atom
 // accumulator (+dE d) and the partner accumulator (-dE d); the factor 2 of
 // dE/dr_i = 2 dE/drho2 (r_i - r_j) is applied once per atom at the end.
-__device__ __forceinline__ void tile_pair(bool on, float rxi, float ryi, float rzi, float qi, const uint8_t *trow,
-                                          float4 rj, int tj_off, float &e, float &gxi, float &gyi, float &gzi,
-                                          float &fx, float &fy, float &fz) {
+// Partner data: pose record rj (x, y, z, q) and signed params pj (role in the signs).
+__device__ __forceinline__ void tile_pair(bool on, float rxi, float ryi, float rzi, const OwnPair &o, float4 rj,
+                                          float4 pj, float &e, float &gxi, float &gyi, float &gzi, float &fx,
+                                          float &fy, float &fz) {
     const float dx = rxi - rj.x, dy = ryi - rj.y, dz = rzi - rj.z;
     const float rho2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
-    const float4 tb = *reinterpret_cast<const float4 *>(trow + tj_off);
-    const float sv = *reinterpret_cast<const float *>(trow + tj_off + 16);
-    float dE;
-    const float E = pair_eg_tab(rho2, tb, sv, qi * rj.w, dE);
+    float dE, E;
+    const float req = o.R + fabsf(pj.x);                 // (R_i + R_j) / 2
+    const float eps = o.e * fabsf(pj.y);                 // sqrt(eps_i eps_j)
+    const bool hb = o.hbc && __float_as_int(o.don ? pj.x : pj.y) < 0;   // donor-acceptor (role in sign bits)
+    const float A = hb ? 5.0f * eps : eps;
+    const float B = hb ? -6.0f * eps : 2.0f * eps;
+    E = pair_eg_ab(rho2, req * req, A, B, fmaf(o.S, pj.w, pj.z * o.V), o.q * rj.w, dE);
     dE = on ? dE : 0.0f;
     e += on ? E : 0.0f;
     gxi = fmaf(dE, dx, gxi); gyi = fmaf(dE, dy, gyi); gzi = fmaf(dE, dz, gzi);
@@ -223,8 +244,8 @@ __device__ __forceinline__ void tile_pair(bool on, float rxi, float ryi, float r
 //    per lane, so bit s is the step-s partner.
 //  * a short tail chunk (t atoms) is paired by broadcast: all lanes meet tail atom j at
 //    once and j's force is a butterfly sum.
-//  * pair constants come from the per-type-pair table (r_eq^2, A, B6, B10, SV), the
-//    charges from the pose records (own charge pre-scaled by 332.06363/4).
+//  * partner params are stored chunk-duplicated too, with the H-bond role in their sign
+//    bits; the charges come from the pose records (own charge pre-scaled by 332.06363/4).
 // Fixed order -> deterministic.
 template <int W, int MAXC>
 __device__ __forceinline__ void intra_tiles(const LigSm &L, const Scratch &S, int sub, unsigned mask,
@@ -235,15 +256,17 @@ __device__ __forceinline__ void intra_tiles(const LigSm &L, const Scratch &S, in
     // cost model (issue slots): rotation of the tail as a padded chunk vs broadcast
     const bool tail_rot = t > 0 && (W / 2 + Bf * W) * 40 < t * ((Bf + 1) * 40 + 3 * 5);
     const int Bt = Bf + (tail_rot ? 1 : 0);
-    const uint8_t *trow[MAXC];
-    float qa[MAXC];
+    OwnPair own[MAXC];
     float hx[MAXC], hy[MAXC], hz[MAXC];   // pair-force sums (x 2 at the end)
 #pragma unroll
     for (int c = 0; c < MAXC; ++c) {
         const int a = sub + W * c;
         const bool ok = a < N;
-        trow[c] = L.tab + (size_t)(ok ? (L.meta[a] & 0xff) : (L.NT1 - 1)) * L.NT1 * 32;
-        qa[c] = ok ? kElec4 * S.r[ridx<W>(a)].w : 0.0f;
+        own[c].q = ok ? kElec4 * S.r[ridx<W>(a)].w : 0.0f;
+        const float4 pp = L.ppar[ridx<W>(a)];
+        own[c].R = fabsf(pp.x); own[c].e = fabsf(pp.y); own[c].S = pp.z; own[c].V = pp.w;
+        own[c].hbc = __float_as_int(pp.x) < 0 || __float_as_int(pp.y) < 0;   // sign bits: -0.0 counts
+        own[c].don = __float_as_int(pp.y) < 0;
         hx[c] = hy[c] = hz[c] = 0.0f;
     }
 #pragma unroll
@@ -264,13 +287,13 @@ __device__ __forceinline__ void intra_tiles(const LigSm &L, const Scratch &S, in
             }
             if (I == J && sub >= W / 2) rot &= ~(1u << (W / 2));   // each diagonal pair once
             const float4 *rrow = S.r + J * 2 * W + sub;         // partner of step s: rrow[s]
-            const int *prow = L.pdup + J * 2 * W + sub;
+            const float4 *qrow = L.ppar + J * 2 * W + sub;
             const int s0 = (I == J) ? 1 : 0, s1 = (I == J) ? W / 2 : W - 1;
             float fx = 0.f, fy = 0.f, fz = 0.f;
 #pragma unroll 4
             for (int s = s0; s <= s1; ++s) {
-                tile_pair((rot >> s) & 1u, rx[I], ry[I], rz[I], qa[I], trow[I], rrow[s], prow[s], e, hx[I], hy[I],
-                          hz[I], fx, fy, fz);
+                tile_pair((rot >> s) & 1u, rx[I], ry[I], rz[I], own[I], rrow[s], qrow[s], e, hx[I], hy[I], hz[I], fx,
+                          fy, fz);
                 if (s < s1) {
                     const int src = (sub + 1) & (W - 1);
                     fx = __shfl_sync(mask, fx, src, W);
@@ -289,7 +312,7 @@ __device__ __forceinline__ void intra_tiles(const LigSm &L, const Scratch &S, in
         for (int k = 0; k < t; ++k) {
             const int j = Bf * W + k;                       // uniform: shared-memory broadcast
             const float4 rj = S.r[ridx<W>(j)];
-            const int tj_off = L.pdup[ridx<W>(j)];
+            const float4 pj = L.ppar[ridx<W>(j)];
             const uint32_t *mrow = L.mask + (size_t)j * L.NW;
             float fx = 0.f, fy = 0.f, fz = 0.f;
 #pragma unroll
@@ -297,7 +320,7 @@ __device__ __forceinline__ void intra_tiles(const LigSm &L, const Scratch &S, in
                 if (I > Bf) break;
                 const int a = I * W + sub;
                 const bool on = (I < Bf || sub < k) && ((mrow[a >> 5] >> (a & 31)) & 1u);
-                tile_pair(on, rx[I], ry[I], rz[I], qa[I], trow[I], rj, tj_off, e, hx[I], hy[I], hz[I], fx, fy, fz);
+                tile_pair(on, rx[I], ry[I], rz[I], own[I], rj, pj, e, hx[I], hy[I], hz[I], fx, fy, fz);
             }
             fx = gsum<W>(fx, mask); fy = gsum<W>(fy, mask); fz = gsum<W>(fz, mask);
 #pragma unroll
@@ -313,7 +336,12 @@ __device__ __forceinline__ void intra_tiles(const LigSm &L, const Scratch &S, in
 
 // Energy (and genotype gradient into S.grad) of the genotype in S.genes.
 // Every lane of the group returns the same total energy.
-template <int W, int MAXC, bool GRAD>
+// PARTS (microbenchmarks only, SURVEY.md §8(d) "isolating the two kernels for ncu"):
+// bit 0 = intermolecular grid term (a4), bit 1 = intramolecular pairs (a5); the
+// production kernels use both.
+constexpr int kInter = 1, kIntra = 2, kAll = 3;
+
+template <int W, int MAXC, bool GRAD, int PARTS = kAll>
 __device__ float eval_group(const LigSm &L, const GridDev &grid, const Scratch &S, int sub, unsigned mask) {
     const float *x = S.genes;
     // ---- a3: orientation quaternion q = (cos a/2, sin(a/2) n) -> R(q) (D3) ----
@@ -426,7 +454,8 @@ __device__ float eval_group(const LigSm &L, const GridDev &grid, const Scratch &
             } else {
                 S.r[a] = make_float4(rx[c], ry[c], rz[c], p.w);
             }
-            e_part += inter_atom(grid, meta & 0xff, p.w, rx[c], ry[c], rz[c], gx[c], gy[c], gz[c]);
+            if constexpr ((PARTS & kInter) != 0)
+                e_part += inter_atom(grid, meta & 0xff, p.w, rx[c], ry[c], rz[c], gx[c], gy[c], gz[c]);
         } else if (GRAD && c < L.NC) {
             // padded chunk entries: finite zeros (null type, zero charge) for the tiles
             S.r[ridx<W>(a)] = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -436,7 +465,15 @@ __device__ float eval_group(const LigSm &L, const GridDev &grid, const Scratch &
     __syncwarp(mask);
 
     // ---- a5: intramolecular pairs ----
-    if constexpr (!GRAD) {
+    if constexpr ((PARTS & kIntra) == 0) {
+        if constexpr (GRAD) {
+#pragma unroll
+            for (int c = 0; c < MAXC; ++c) {   // keep the per-atom gradients live
+                e_part += gx[c] + gy[c] + gz[c];
+            }
+        }
+        return gsum<W>(e_part, mask);
+    } else if constexpr (!GRAD) {
 #pragma unroll 4
         for (int q = sub; q < L.P; q += W) {
             const uint32_t w = L.pairs[q];
@@ -448,6 +485,12 @@ __device__ float eval_group(const LigSm &L, const GridDev &grid, const Scratch &
         return gsum<W>(e_part, mask);
     } else {
         intra_tiles<W, MAXC>(L, S, sub, mask, rx, ry, rz, gx, gy, gz, e_part);
+        if constexpr (PARTS == kIntra) {
+            const float E = gsum<W>(e_part, mask);
+#pragma unroll
+            for (int c = 0; c < MAXC; ++c) e_part += gx[c] + gy[c] + gz[c];
+            return E + 0.0f * gsum<W>(e_part, mask);
+        }
         const float E = gsum<W>(e_part, mask);
 
         // ---- a6: back-projection to genotype space (D7) ----

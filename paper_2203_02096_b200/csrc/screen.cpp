@@ -14,7 +14,7 @@
 //   4. one worker thread per slot pulls the next ligand from a shared atomic cursor
 //      (dynamic LPT: the longest remaining ligand goes to the first free slot);
 //   5. per ligand: dock_run_device on the slot's stream, 4 B + 4 B + G*4 B per run back
-//      to pinned host memory, best over runs on the host (lowest run on ties).
+//      to host memory, best over runs on the host (lowest run on ties).
 // A ligand's result depends only on (inputs, seed, ligand_id): the Philox key is
 // seed + ligand_id * 0x9E3779B97F4A7C15 (D2), never the slot or the device.
 #include <cuda_runtime.h>
@@ -39,12 +39,11 @@ thread_local std::string g_screen_error;
 struct SlotBufs {
     float *d_bE = nullptr, *d_bG = nullptr;
     int64_t *d_ev = nullptr;
-    float *h_bE = nullptr, *h_bG = nullptr;
-    int64_t *h_ev = nullptr;
-    void release() {
-        cudaFree(d_bE); cudaFree(d_bG); cudaFree(d_ev);
-        cudaFreeHost(h_bE); cudaFreeHost(h_bG); cudaFreeHost(h_ev);
-        d_bE = d_bG = h_bE = h_bG = nullptr; d_ev = h_ev = nullptr;
+    std::vector<float> h_bE, h_bG;
+    std::vector<int64_t> h_ev;
+    void release(cudaStream_t s) {
+        dk::dfree(d_bE, s); dk::dfree(d_bG, s); dk::dfree(d_ev, s);
+        d_bE = d_bG = nullptr; d_ev = nullptr;
     }
 };
 
@@ -133,7 +132,7 @@ extern "C" int dock_screen(const dock_grids *grids, const dock_type_param *type_
     auto cleanup = [&] {
         for (auto &s : slot_v) {
             if (s.ctx) { cudaSetDevice(s.device); cudaStreamSynchronize(s.ctx->stream); }
-            s.b.release();
+            if (s.ctx) s.b.release(s.ctx->stream);
             dock_free(s.ctx);
         }
         slot_v.clear();
@@ -149,13 +148,13 @@ extern "C" int dock_screen(const dock_grids *grids, const dock_type_param *type_
             if ((rc = dk::ctx_create(rec, p, &s.ctx, &err)) != DOCK_OK) { g_screen_error = err; cleanup(); return rc; }
             slot_v.push_back(s);
             Slot &sl = slot_v.back();
+            sl.b.h_bE.resize(runs); sl.b.h_bG.resize((size_t)runs * DOCK_MAX_GENES); sl.b.h_ev.resize(runs);
+            const cudaStream_t st = sl.ctx->stream;
             if ((rc = dk::ctx_reserve(sl.ctx, max_blob, runs, pop)) != DOCK_OK ||
-                cudaMalloc(&sl.b.d_bE, sizeof(float) * runs) != cudaSuccess ||
-                cudaMalloc(&sl.b.d_bG, sizeof(float) * runs * DOCK_MAX_GENES) != cudaSuccess ||
-                cudaMalloc(&sl.b.d_ev, sizeof(int64_t) * runs) != cudaSuccess ||
-                cudaMallocHost(&sl.b.h_bE, sizeof(float) * runs) != cudaSuccess ||
-                cudaMallocHost(&sl.b.h_bG, sizeof(float) * runs * DOCK_MAX_GENES) != cudaSuccess ||
-                cudaMallocHost(&sl.b.h_ev, sizeof(int64_t) * runs) != cudaSuccess) {
+                dk::dmalloc((void **)&sl.b.d_bE, sizeof(float) * runs, st) != cudaSuccess ||
+                dk::dmalloc((void **)&sl.b.d_bG, sizeof(float) * runs * DOCK_MAX_GENES, st) != cudaSuccess ||
+                dk::dmalloc((void **)&sl.b.d_ev, sizeof(int64_t) * runs, st) != cudaSuccess ||
+                cudaStreamSynchronize(st) != cudaSuccess) {
                 g_screen_error = "slot setup on device " + std::to_string(d) + ": " +
                                  (sl.ctx->err.empty() ? "allocation failed" : sl.ctx->err);
                 cudaGetLastError();
@@ -184,9 +183,9 @@ extern "C" int dock_screen(const dock_grids *grids, const dock_type_param *type_
                 r = dock_run_device(c, pop, runs, 0, lid, max_evals, seed, s.b.d_bE, s.b.d_bG, s.b.d_ev, nullptr,
                                     c->stream);
             if (r == DOCK_OK) {
-                cudaError_t e = cudaMemcpyAsync(s.b.h_bE, s.b.d_bE, sizeof(float) * runs, cudaMemcpyDeviceToHost, c->stream);
-                if (e == cudaSuccess) e = cudaMemcpyAsync(s.b.h_bG, s.b.d_bG, sizeof(float) * runs * G, cudaMemcpyDeviceToHost, c->stream);
-                if (e == cudaSuccess) e = cudaMemcpyAsync(s.b.h_ev, s.b.d_ev, sizeof(int64_t) * runs, cudaMemcpyDeviceToHost, c->stream);
+                cudaError_t e = cudaMemcpyAsync(s.b.h_bE.data(), s.b.d_bE, sizeof(float) * runs, cudaMemcpyDeviceToHost, c->stream);
+                if (e == cudaSuccess) e = cudaMemcpyAsync(s.b.h_bG.data(), s.b.d_bG, sizeof(float) * runs * G, cudaMemcpyDeviceToHost, c->stream);
+                if (e == cudaSuccess) e = cudaMemcpyAsync(s.b.h_ev.data(), s.b.d_ev, sizeof(int64_t) * runs, cudaMemcpyDeviceToHost, c->stream);
                 if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
                 if (e != cudaSuccess) { c->err = std::string("result copy: ") + cudaGetErrorString(e); r = DOCK_E_INTERNAL; }
             }
@@ -208,7 +207,8 @@ extern "C" int dock_screen(const dock_grids *grids, const dock_type_param *type_
             }
             best_energy[i] = s.b.h_bE[br];
             if (best_run) best_run[i] = br;
-            std::copy(s.b.h_bG + (size_t)br * G, s.b.h_bG + (size_t)(br + 1) * G, best_genotype + (size_t)i * DOCK_MAX_GENES);
+            std::copy(s.b.h_bG.begin() + (size_t)br * G, s.b.h_bG.begin() + (size_t)(br + 1) * G,
+                      best_genotype + (size_t)i * DOCK_MAX_GENES);
             if (evals_used) evals_used[i] = ev;
             if (device_of) device_of[i] = s.device;
             total_evals.fetch_add(ev);
