@@ -199,19 +199,37 @@ int ctx_create(std::shared_ptr<Receptor> rec, const dock_params &p, dock_ctx **o
     c->rec = std::move(rec);
     auto bail = [&](const std::string &m) { *err = m; dock_free(c); return (int)DOCK_E_INTERNAL; };
     if (cudaSetDevice(c->device) != cudaSuccess) return bail("cudaSetDevice failed");
-    if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess) return bail("cudaStreamCreate failed");
-    if (setup_kernel_attributes() != cudaSuccess) return bail("cudaFuncSetAttribute failed (is this an sm_100 device?)");
+    {
+        Trace tr("ctx.stream_create");
+        if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess) return bail("cudaStreamCreate failed");
+    }
+    {
+        // kernel attributes are per device and process: set them once
+        Trace tr("ctx.kernel_attributes");
+        static std::mutex mu;
+        static std::vector<int> done;
+        std::lock_guard<std::mutex> lk(mu);
+        if (std::find(done.begin(), done.end(), c->device) == done.end()) {
+            if (setup_kernel_attributes() != cudaSuccess) return bail("cudaFuncSetAttribute failed (is this an sm_100 device?)");
+            done.push_back(c->device);
+        }
+    }
+    Trace tr_rest("ctx.alloc_and_l2_window");
     if (dmalloc((void **)&c->d_dfs2orig, sizeof(int) * kMaxAtoms, c->stream) != cudaSuccess ||
         cudaStreamSynchronize(c->stream) != cudaSuccess)
         return bail("device allocation failed");
     if (p.l2_persist) {
         // NS: "Grid maps live in HBM with L2-persistence windows".
-        cudaDeviceProp prop;
-        if (cudaGetDeviceProperties(&prop, c->device) == cudaSuccess && prop.persistingL2CacheMaxSize > 0 &&
-            prop.accessPolicyMaxWindowSize > 0) {
-            const size_t win = std::min(c->rec->bytes, (size_t)prop.accessPolicyMaxWindowSize);
-            const size_t lim = std::min(win, (size_t)prop.persistingL2CacheMaxSize);
-            cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, lim);
+        // single attribute queries: cudaGetDeviceProperties is slow (all properties)
+        int max_persist = 0, max_window = 0;
+        cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, c->device);
+        cudaDeviceGetAttribute(&max_window, cudaDevAttrMaxAccessPolicyWindowSize, c->device);
+        if (max_persist > 0 && max_window > 0) {
+            const size_t win = std::min(c->rec->bytes, (size_t)max_window);
+            const size_t lim = std::min(win, (size_t)max_persist);
+            size_t cur = 0;
+            cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize);
+            if (cur < lim) cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, lim);   // only ever grows
             cudaStreamAttrValue attr{};
             attr.accessPolicyWindow.base_ptr = c->rec->d_maps;
             attr.accessPolicyWindow.num_bytes = win;

@@ -337,19 +337,22 @@ __global__ void __launch_bounds__(256, (MAXC <= 4 ? DK_ADA_MINB : 1)) k_ls_adade
     const LsTarget t = ls_target(sp, pop, a, gi, G);
     if (!__syncthreads_or(t.act)) return;
     const LigSm Ls = stage_ligand(L, sm, staged_bytes(L, true));
-    if (!t.act) return;
+    // Both lane groups of a warp stay converged (an inactive group shadows its partner on a
+    // dummy genotype and writes nothing), so the group shuffles take a constant full-warp
+    // mask: no divergence checks around every SHFL (measured: MATCH.ANY + BRA.DIV paths).
+    if (!__any_sync(0xffffffffu, t.act)) return;
     const Scratch S = scratch_at(sm + staged_bytes(L, true) + gl * SL.bytes, SL);
-    const unsigned mask = group_mask<W>();
+    constexpr unsigned mask = 0xffffffffu;
     constexpr int NSET = (kMaxGenes + W - 1) / W;
     float x[NSET], sg[NSET], sd[NSET], bx[NSET];
 #pragma unroll
     for (int s = 0; s < NSET; ++s) {
         const int j = sub + W * s;
-        x[s] = j < G ? t.row[j] : 0.0f;
+        x[s] = (j < G && t.act) ? t.row[j] : 0.0f;
         bx[s] = x[s]; sg[s] = 0.0f; sd[s] = 0.0f;
         if (j < G) S.genes[j] = x[s];
     }
-    float Ebest = *t.E;
+    float Ebest = t.act ? *t.E : 0.0f;
     const float rho = sp.ad_rho, eps = sp.ad_eps;
     __syncwarp(mask);
     for (int it = 0; it < a.iters; ++it) {
@@ -373,6 +376,7 @@ __global__ void __launch_bounds__(256, (MAXC <= 4 ? DK_ADA_MINB : 1)) k_ls_adade
         }
         __syncwarp(mask);
     }
+    if (!t.act) return;
 #pragma unroll
     for (int s = 0; s < NSET; ++s) {
         const int j = sub + W * s;
@@ -436,7 +440,7 @@ __global__ void __launch_bounds__(256) k_ls_sw(const LigDev L, const GridDev g, 
     const Scratch S0 = scratch_at(wbase, SL);
     const Scratch S1 = scratch_at(wbase + (NG - 1) * SL.bytes, SL);
     const Scratch Sg = grp == 0 ? S0 : S1;
-    const unsigned gmask = group_mask<W>();
+    constexpr unsigned gmask = 0xffffffffu;   // a warp = one individual: both groups always converged
     const uint2 key = make_uint2(sp.key0, sp.key1);
     constexpr int NSET = (kMaxGenes + 31) / 32;
     float x[NSET], b[NSET], d[NSET], c1[NSET], c2[NSET];
@@ -544,9 +548,12 @@ __global__ void __launch_bounds__(tree_threads<W, D>(), (W == 16 && D == 3) ? 2 
     const int grp = threadIdx.x / W, sub = threadIdx.x % W;
     const bool in_grp = grp < NGR;
     const Scratch S = scratch_at(sm + staged + (in_grp ? grp : 0) * SL.bytes, SL);
-    const unsigned gmask = group_mask<W>();
+    // every group evaluates every round (a moot node on stale genes, result unused), so
+    // the warps stay converged and the group shuffles take a constant full-warp mask
+    constexpr unsigned gmask = 0xffffffffu;
     const uint2 key = make_uint2(sp.key0, sp.key1);
     for (int j = threadIdx.x; j < G; j += blockDim.x) { sx[j] = t.row[j]; sb[j] = 0.0f; }
+    for (int j = sub; j < G; j += W) S.genes[j] = 0.0f;      // finite genes for a moot first round
     // this group's node: level lvl, parent state sigma (base-3 outcome digits), candidate
     int lvl = 0;
     while (lvl + 1 < D && grp >= ipow3(lvl + 1) - 1) ++lvl;
@@ -596,8 +603,8 @@ __global__ void __launch_bounds__(tree_threads<W, D>(), (W == 16 && D == 3) ? 2 
                 }
             }
             __syncwarp(gmask);
-            const float e = live ? eval_group<W, MAXC, false>(Ls, g, S, sub, gmask) : INFINITY;
-            if (sub == 0) sE[grp] = e;
+            const float e = eval_group<W, MAXC, false>(Ls, g, S, sub, gmask);
+            if (sub == 0) sE[grp] = live ? e : INFINITY;
         }
         __syncthreads();
         // ---- 2. resolve the actual path (every thread, identical scalar logic) ----
