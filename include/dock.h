@@ -85,7 +85,8 @@ typedef struct {
     int32_t device;              /* CUDA device ordinal */
     int32_t l2_persist;          /* 1: pin the grid in L2 with an access-policy window */
     int32_t gens_per_graph;      /* generations per CUDA-graph launch (>= 1) */
-    int32_t profile;             /* 1: CUDA events around every GA and LS launch (dock_kernel_stats) */
+    int32_t profile;             /* 1: CUDA events around every LS launch, 2: also every GA launch
+                                    (dock_kernel_stats); 0: none */
     int32_t sw_depth;            /* Solis-Wets speculation depth: 0 = auto (deepest whose launch fits one
                                     wave), 1 = both trial points of one iteration at once, 2 or 3 =
                                     the 3-way outcome tree of 2 / 3 iterations (3^D - 1 lane groups
@@ -231,9 +232,10 @@ const char *dock_screen_last_error(void);
 /* Kernel-launch counter of this context (for the benchmark's gpu_launches claim). */
 int64_t dock_launch_count(const dock_ctx *ctx);
 
-/* With params.profile = 1: device time (ms, CUDA events on the launching stream) and
+/* With params.profile >= 1: device time (ms, CUDA events on the launching stream) and
    launch counts accumulated over the last dock_run* call, per kernel class
-   0 = k_ga (offspring), 1 = k_ls_* (local search), 2 = k_init.  Arrays of 3. */
+   0 = k_ga (offspring; profile >= 2 only), 1 = k_ls_* (local search), 2 = k_init.
+   Arrays of 3. */
 int dock_kernel_stats(const dock_ctx *ctx, double *ms, int64_t *launches);
 
 /* Bytes dock_init copied host -> device (packed grid + ligand block + atom map). */

@@ -420,7 +420,9 @@ int dock_run_device(dock_ctx *c, int32_t pop, int32_t runs, int32_t run_base, ui
     CK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
     cudaError_t ce = cudaSuccess;
     for (int k = 0; k < K && ce == cudaSuccess; ++k) {
-        if (prof) ce = cudaEventRecordWithFlags(ev[3 * k], s, cudaEventRecordExternal);
+        // profile 1: events around the LS node only (2 graph nodes per generation);
+        // profile 2: also around the GA node
+        if (prof && c->params.profile >= 2) ce = cudaEventRecordWithFlags(ev[3 * k], s, cudaEventRecordExternal);
         if (ce == cudaSuccess) ce = dk::launch_ga(c->lig, c->grid, sp, pd, nullptr, s);
         if (ce == cudaSuccess && prof) ce = cudaEventRecordWithFlags(ev[3 * k + 1], s, cudaEventRecordExternal);
         if (ce == cudaSuccess && do_ls) ce = dk::launch_ls(c->lig, c->grid, sp, pd, la, runs * sp.n_ls, s);
@@ -455,7 +457,7 @@ int dock_run_device(dock_ctx *c, int32_t pop, int32_t runs, int32_t run_base, ui
             cudaError_t pe = cudaSuccess;
             if (b == 0 && (pe = cudaEventElapsedTime(&t, ev[3 * K], ev[3 * K + 1])) == cudaSuccess) { c->prof_ms[2] += t; c->prof_n[2] += 1; }
             for (int k = 0; k < K && pe == cudaSuccess; ++k) {
-                if ((pe = cudaEventElapsedTime(&t, ev[3 * k], ev[3 * k + 1])) == cudaSuccess) { c->prof_ms[0] += t; c->prof_n[0] += 1; }
+                if (c->params.profile >= 2 && (pe = cudaEventElapsedTime(&t, ev[3 * k], ev[3 * k + 1])) == cudaSuccess) { c->prof_ms[0] += t; c->prof_n[0] += 1; }
                 if (pe == cudaSuccess && do_ls && (pe = cudaEventElapsedTime(&t, ev[3 * k + 1], ev[3 * k + 2])) == cudaSuccess) { c->prof_ms[1] += t; c->prof_n[1] += 1; }
             }
             if (pe != cudaSuccess) {
