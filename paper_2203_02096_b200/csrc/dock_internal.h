@@ -41,6 +41,7 @@ struct LigDev {
     // index never wraps; padded entries are all-zero params.
     int Wg;           // lanes per group of the gradient kernels (16 if N <= 16, else 32)
     int NC;           // chunks = ceil(N / Wg)
+    int energy_tiles; // 1: energy-only kernels also use the pair tiles (pair list too large to stage)
     int off_ppar;     // float4[NC][2*Wg] partner params {R/2, sqrt(eps), S, V}, duplicated chunks;
                       //   R/2 negated for acceptors and sqrt(eps) negated for donors (role
                       //   in the sign bits; magnitudes via free |.| operand modifiers)

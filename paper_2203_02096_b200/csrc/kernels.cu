@@ -26,12 +26,14 @@ namespace dk {
 
 static inline __host__ __device__ int a16(int x) { return (x + 15) & ~15; }
 
-ScratchLayout scratch_layout(int N, int T, int G, bool grad, int extra) {
+ScratchLayout scratch_layout(const LigDev &L, bool grad, int extra) {
     ScratchLayout s;
+    const int N = L.N, T = L.T, G = L.G;
     int o = 0;
-    // gradient kernels keep the pose in the duplicated chunk layout [NC][2W] (intra_tiles)
-    const int Wg = N <= 16 ? 16 : 32;
-    s.off_r = o; o += a16(grad ? 16 * 2 * Wg * ((N + Wg - 1) / Wg) : 16 * N);
+    // the pair tiles (gradient kernels, and energy kernels of ligands too large for the
+    // pair list, L.energy_tiles) keep the pose in the duplicated chunk layout [NC][2W]
+    const bool dup = grad || L.energy_tiles;
+    s.off_r = o; o += a16(dup ? 16 * 2 * L.Wg * L.NC : 16 * N);
     s.off_W = o; o += a16(48 * (T > 0 ? T : 1));
     s.off_tp = o; o += a16(4 * (T > 0 ? T : 1));
     s.off_ts = o; if (grad) o += a16(32 * N);
@@ -53,7 +55,7 @@ GroupCfg pick_group(int N) {
 // Bytes of the ligand block a kernel stages: gradient kernels skip the pair list and the
 // pair constants of the energy-only path.
 static inline __host__ __device__ int staged_bytes(const LigDev &L, bool grad) {
-    return grad ? L.grad_bytes : L.blob_bytes;
+    return (grad || L.energy_tiles) ? L.grad_bytes : L.blob_bytes;
 }
 
 __device__ __forceinline__ LigSm stage_ligand(const LigDev &L, uint8_t *sm, int bytes) {
@@ -75,6 +77,7 @@ __device__ __forceinline__ LigSm stage_ligand(const LigDev &L, uint8_t *sm, int 
     v.mask = reinterpret_cast<const uint32_t *>(sm + L.off_mask);
     v.ppar = reinterpret_cast<const float4 *>(sm + L.off_ppar);
     v.NC = L.NC;
+    v.energy_tiles = L.energy_tiles;
     return v;
 }
 
@@ -119,7 +122,7 @@ __global__ void __launch_bounds__(256) k_eval(const LigDev L, const GridDev g, c
         for (int j = sub; j < G; j += W) grad[(size_t)gi * G + j] = S.grad[j];
     if (xyz) {
         for (int a = sub; a < L.N; a += W) {
-            const float4 r = S.r[GRAD ? ridx<W>(a) : a];
+            const float4 r = S.r[(GRAD || L.energy_tiles) ? ridx<W>(a) : a];
             float *o = xyz + ((size_t)gi * L.N + dfs2orig[a]) * 3;
             o[0] = r.x; o[1] = r.y; o[2] = r.z;
         }
@@ -797,7 +800,7 @@ cudaError_t launch_eval(const LigDev &L, const GridDev &g, int n, const float *g
     if (n <= 0) return cudaSuccess;
     const GroupCfg cfg = pick_group(L.N);
     const bool want_grad = grad != nullptr;
-    const ScratchLayout SL = scratch_layout(L.N, L.T, L.G, want_grad, 0);
+    const ScratchLayout SL = scratch_layout(L, want_grad, 0);
     const int groups = kThreads / cfg.W;
     const size_t smem = (size_t)staged_bytes(L, want_grad) + (size_t)groups * SL.bytes;
     if (smem > (size_t)kSmemMax) return cudaErrorInvalidConfiguration;
@@ -811,9 +814,9 @@ cudaError_t launch_eval(const LigDev &L, const GridDev &g, int n, const float *g
 
 cudaError_t launch_init(const LigDev &L, const GridDev &g, const SearchDev &sp, const PopDev &pop, cudaStream_t s) {
     const GroupCfg cfg = pick_group(L.N);
-    const ScratchLayout SL = scratch_layout(L.N, L.T, L.G, false, 0);
+    const ScratchLayout SL = scratch_layout(L, false, 0);
     const int groups = kThreads / cfg.W;
-    const size_t smem = (size_t)L.blob_bytes + (size_t)groups * SL.bytes;
+    const size_t smem = (size_t)staged_bytes(L, false) + (size_t)groups * SL.bytes;
     if (smem > (size_t)kSmemMax) return cudaErrorInvalidConfiguration;
     const int blocks = ceil_div((long long)sp.runs * sp.pop, groups);
     DK_DISPATCH(cfg, { k_init<W, MAXC><<<blocks, kThreads, smem, s>>>(L, g, SL, sp, pop); });
@@ -823,9 +826,9 @@ cudaError_t launch_init(const LigDev &L, const GridDev &g, const SearchDev &sp, 
 cudaError_t launch_ga(const LigDev &L, const GridDev &g, const SearchDev &sp, const PopDev &pop, int *dbg,
                       cudaStream_t s) {
     const GroupCfg cfg = pick_group(L.N);
-    const ScratchLayout SL = scratch_layout(L.N, L.T, L.G, false, 4 * sp.pop);
+    const ScratchLayout SL = scratch_layout(L, false, 4 * sp.pop);
     const int groups = kThreads / cfg.W;
-    const size_t smem = (size_t)L.blob_bytes + (size_t)groups * SL.bytes;
+    const size_t smem = (size_t)staged_bytes(L, false) + (size_t)groups * SL.bytes;
     if (smem > (size_t)kSmemMax) return cudaErrorInvalidConfiguration;
     const int blocks = ceil_div((long long)sp.runs * sp.pop, groups);
     DK_DISPATCH(cfg, { k_ga<W, MAXC><<<blocks, kThreads, smem, s>>>(L, g, SL, sp, pop, dbg); });
@@ -837,7 +840,7 @@ cudaError_t launch_ls(const LigDev &L, const GridDev &g, const SearchDev &sp, co
     if (n_total <= 0) return cudaSuccess;
     const GroupCfg cfg = pick_group(L.N);
     if (sp.ls_method == 1) {
-        const ScratchLayout SL = scratch_layout(L.N, L.T, L.G, false, 0);
+        const ScratchLayout SL = scratch_layout(L, false, 0);
         // Speculation depth: the deepest tree whose CTAs are all co-resident (one wave);
         // a full launch gains nothing from speculation and uses the plain kernel.
         int depth = sp.sw_depth;
@@ -851,7 +854,7 @@ cudaError_t launch_ls(const LigDev &L, const GridDev &g, const SearchDev &sp, co
             // auto stops at depth 2; depth 3 stays available explicitly.
             for (int D = 2; D >= 2 && depth == 1; --D) {
                 const int ngr = D == 3 ? 26 : 8;
-                const size_t sm_b = (size_t)L.blob_bytes + (size_t)ngr * SL.bytes + 4 * (2 * kMaxGenes + ngr + 2 * D * kMaxGenes);
+                const size_t sm_b = (size_t)staged_bytes(L, false) + (size_t)ngr * SL.bytes + 4 * (2 * kMaxGenes + ngr + 2 * D * kMaxGenes);
                 int per_sm = 0;
                 DK_DISPATCH(cfg, {
                     if (D == 3) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_ls_sw_tree<W, MAXC, 3>, tree_threads<W, 3>(), sm_b);
@@ -863,7 +866,7 @@ cudaError_t launch_ls(const LigDev &L, const GridDev &g, const SearchDev &sp, co
         }
         if (depth >= 2) {
             const int ngr = depth == 3 ? 26 : 8;
-            const size_t smem = (size_t)L.blob_bytes + (size_t)ngr * SL.bytes + 4 * (2 * kMaxGenes + ngr + 2 * depth * kMaxGenes);
+            const size_t smem = (size_t)staged_bytes(L, false) + (size_t)ngr * SL.bytes + 4 * (2 * kMaxGenes + ngr + 2 * depth * kMaxGenes);
             if (smem > (size_t)kSmemMax) return cudaErrorInvalidConfiguration;
             DK_DISPATCH(cfg, {
                 if (depth == 3) k_ls_sw_tree<W, MAXC, 3><<<n_total, tree_threads<W, 3>(), smem, s>>>(L, g, SL, sp, pop, a);
@@ -875,12 +878,12 @@ cudaError_t launch_ls(const LigDev &L, const GridDev &g, const SearchDev &sp, co
         // spread over all SMs.
         const int ng = cfg.W <= 16 ? 2 : 1;
         const int warps = n_total >= 148 * 8 ? 8 : 1;
-        const size_t smem = (size_t)L.blob_bytes + (size_t)warps * ng * SL.bytes;
+        const size_t smem = (size_t)staged_bytes(L, false) + (size_t)warps * ng * SL.bytes;
         if (smem > (size_t)kSmemMax) return cudaErrorInvalidConfiguration;
         const int blocks = ceil_div(n_total, warps);
         DK_DISPATCH(cfg, { k_ls_sw<W, MAXC><<<blocks, warps * 32, smem, s>>>(L, g, SL, sp, pop, a); });
     } else {
-        const ScratchLayout SL = scratch_layout(L.N, L.T, L.G, true, 0);
+        const ScratchLayout SL = scratch_layout(L, true, 0);
         const int groups = kThreads / cfg.W;
         const size_t smem = (size_t)staged_bytes(L, true) + (size_t)groups * SL.bytes;
         if (smem > (size_t)kSmemMax) return cudaErrorInvalidConfiguration;
@@ -894,7 +897,7 @@ cudaError_t launch_bench_part(const LigDev &L, const GridDev &g, int part, int n
                               float *E, cudaStream_t s) {
     if (n <= 0) return cudaSuccess;
     const GroupCfg cfg = pick_group(L.N);
-    const ScratchLayout SL = scratch_layout(L.N, L.T, L.G, true, 0);
+    const ScratchLayout SL = scratch_layout(L, true, 0);
     const int groups = kThreads / cfg.W;
     const size_t smem = (size_t)staged_bytes(L, true) + (size_t)groups * SL.bytes;
     if (smem > (size_t)kSmemMax) return cudaErrorInvalidConfiguration;

@@ -30,7 +30,7 @@ struct GroupCfg {
     int MAXC;   // atom chunks per lane (1, 2, 4, 8)
 };
 GroupCfg pick_group(int N);
-ScratchLayout scratch_layout(int N, int T, int G, bool grad, int extra_bytes);
+ScratchLayout scratch_layout(const LigDev &L, bool grad, int extra_bytes);
 
 cudaError_t setup_kernel_attributes();
 

@@ -220,8 +220,13 @@ int prepare_ligand(const dock_ligand *l, const dock_type_param *tp, int n_types,
     L.NC = (N + L.Wg - 1) / L.Wg;
     L.off_ppar = off; off += 16 * L.NC * 2 * L.Wg;
     L.grad_bytes = off;              // the gradient kernels stage only up to here
-    L.off_pairs = off; off += a16(4 * P);
-    L.off_pprm = off; off += 16 * P;
+    // Energy-only kernels stage the pair list + per-pair constants (20 B per pair) when it
+    // fits comfortably in shared memory; beyond that (P > ~4,900, e.g. N >= ~110) they use
+    // the pair tiles like the gradient kernels, and the list is not stored at all.
+    L.energy_tiles = (20 * P > 96 * 1024) ? 1 : 0;
+    const int Ps = L.energy_tiles ? 0 : P;
+    L.off_pairs = off; off += a16(4 * Ps);
+    L.off_pprm = off; off += 16 * Ps;
     L.blob_bytes = a16(off);
     o.blob.assign(L.blob_bytes, 0);
     uint8_t *bl = o.blob.data();
@@ -292,6 +297,9 @@ int prepare_ligand(const dock_ligand *l, const dock_type_param *tp, int n_types,
         const int i = pairs[2 * q], j = pairs[2 * q + 1];
         int di = pos[i], dj = pos[j];
         if (di > dj) std::swap(di, dj);
+        bmask[di * L.NW + (dj >> 5)] |= 1u << (dj & 31);
+        bmask[dj * L.NW + (di >> 5)] |= 1u << (di & 31);
+        if (L.energy_tiles) continue;
         const int hb = hb_of(i, j) ? 1 : 0;
         bpairs[q] = (uint32_t)di | ((uint32_t)dj << 8) | ((uint32_t)hb << 16);
         // D5 pair constants for the energy-only path
@@ -300,8 +308,6 @@ int prepare_ligand(const dock_ligand *l, const dock_type_param *tp, int n_types,
         pprm[q] = make_float4((float)(req * req), (float)std::sqrt((double)ti.eps * (double)tj.eps),
                               (float)((double)ti.S * tj.V + (double)tj.S * ti.V),
                               (float)(332.06363 / 4.0 * (double)l->charge[i] * (double)l->charge[j]));
-        bmask[di * L.NW + (dj >> 5)] |= 1u << (dj & 31);
-        bmask[dj * L.NW + (di >> 5)] |= 1u << (di & 31);
     }
     return DOCK_OK;
 }

@@ -33,6 +33,7 @@ struct LigSm {
     const uint32_t *mask;         // [N][NW] pair-membership bit rows
     const float4 *ppar;           // [NC][2W] signed partner params (duplicated chunks)
     int NC;
+    int energy_tiles;             // energy-only evaluation through the pair tiles (no pair list)
 };
 
 // Gradient-path pose index: chunk c = a / W lives at [c][2W], its copy at [c][2W] + W.
@@ -447,7 +448,7 @@ __device__ float eval_group(const LigSm &L, const GridDev &grid, const Scratch &
                 ry[c] = fmaf(w1.x, p.x, fmaf(w1.y, p.y, fmaf(w1.z, p.z, w1.w)));
                 rz[c] = fmaf(w2.x, p.x, fmaf(w2.y, p.y, fmaf(w2.z, p.z, w2.w)));
             }
-            if constexpr (GRAD) {
+            if (GRAD || L.energy_tiles) {
                 const float4 rv = make_float4(rx[c], ry[c], rz[c], p.w);
                 S.r[ridx<W>(a)] = rv;
                 S.r[ridx<W>(a) + W] = rv;
@@ -456,7 +457,7 @@ __device__ float eval_group(const LigSm &L, const GridDev &grid, const Scratch &
             }
             if constexpr ((PARTS & kInter) != 0)
                 e_part += inter_atom(grid, meta & 0xff, p.w, rx[c], ry[c], rz[c], gx[c], gy[c], gz[c]);
-        } else if (GRAD && c < L.NC) {
+        } else if ((GRAD || L.energy_tiles) && c < L.NC) {
             // padded chunk entries: finite zeros (null type, zero charge) for the tiles
             S.r[ridx<W>(a)] = make_float4(0.f, 0.f, 0.f, 0.f);
             S.r[ridx<W>(a) + W] = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -474,6 +475,10 @@ __device__ float eval_group(const LigSm &L, const GridDev &grid, const Scratch &
         }
         return gsum<W>(e_part, mask);
     } else if constexpr (!GRAD) {
+        if (L.energy_tiles) {           // large ligand: pair list not staged, use the tiles
+            intra_tiles<W, MAXC>(L, S, sub, mask, rx, ry, rz, gx, gy, gz, e_part);
+            return gsum<W>(e_part, mask);
+        }
 #pragma unroll 4
         for (int q = sub; q < L.P; q += W) {
             const uint32_t w = L.pairs[q];

@@ -436,3 +436,53 @@ def test_deep_torsion_chain_parity(dock, n_atoms):
             bad.append(("g", i))
     assert not bad, bad[:10]
     d.close()
+
+
+# ---------------------------------------------------------------------------
+# Large ligands (beyond the paper's 108-atom PL input, P > 4,900 pairs): the energy-only
+# kernels switch to the pair tiles (the pair list would not fit in shared memory).
+# ---------------------------------------------------------------------------
+@pytest.fixture(scope="module")
+def large_case():
+    from gen import make_ligand
+    from gen.synth import TYPE_NAMES, make_grid
+    lig = make_ligand(160, 30, 7, type_names=list(TYPE_NAMES))
+    grid = make_grid(48, 0.6, list(TYPE_NAMES), seed=11)
+    return lig, grid
+
+
+def test_large_ligand_energy_tiles_parity(dock, large_case):
+    lig, grid = large_case
+    d = dock.Docker.from_inputs(grid, lig)
+    P = oracle.Problem(grid, lig)
+    assert d.N == 160 and d.P > 5000
+    X = random_genotypes(grid, d.T, 60, seed=3, frac_out=0.0, shrink=0.05)
+    X[:, 6:] *= 0.1
+    E, Gd, xyz = d.eval(X, grad=True, xyz=True)
+    E0, _, _ = d.eval(X, grad=False)            # energy-only kernel: pair-tile path
+    bad = []
+    for i in range(X.shape[0]):
+        ref = P.energy(X[i].astype(np.float64))
+        tol, gtol = pose_tols(P, ref)
+        fm, cm = P.margins(ref["xyz"])
+        if np.abs(xyz[i] - ref["xyz"]).max() > 1e-4:
+            bad.append(("x", i))
+        if abs(E[i] - ref["E"]) > tol or abs(E0[i] - ref["E"]) > tol:
+            bad.append(("E", i, float(E[i]), float(E0[i]), ref["E"]))
+        if fm >= 1e-4 and cm >= 1e-4 and np.abs(Gd[i] - ref["grad"]).max() > gtol:
+            bad.append(("g", i))
+    assert not bad, bad[:5]
+    d.close()
+
+
+@pytest.mark.parametrize("method", [0, 1])
+def test_large_ligand_run(dock, large_case, method):
+    lig, grid = large_case
+    d = dock.Docker.from_inputs(grid, lig, ls_method=method, ls_rate=0.1, ls_max_iters=20)
+    r = d.run(40, 2, 4000, 42, xyz=True)
+    P = oracle.Problem(grid, lig)
+    assert np.all(r["evals"] >= 4000)
+    for k in range(2):
+        ref = P.energy(r["best_genes"][k].astype(np.float64), grad=False)["E"]
+        assert abs(ref - r["best_E"][k]) <= max(1e-3, 1e-4 * abs(ref)) * 10, (ref, r["best_E"][k])
+    d.close()
