@@ -32,8 +32,9 @@ struct LigDev {
     int off_tA;       // float4[T]  torsion axis origin A = p[a_k]
     int off_tU;       // float4[T]  unit axis u = (p[b_k] - p[a_k]) / |.|
     int off_tmeta;    // int4[T]    parent torsion (-1 root), a (dfs), b (dfs), lo | hi << 16
-    int off_pairs;    // uint32[P]  i | j << 8 | hb << 16   (dfs indices, i < j)
-    int off_pprm;     // float4[P]  r_eq^2, eps_ij, S_iV_j + S_jV_i, 332.06363/4 q_i q_j
+    int off_pairs;    // uint32[P]  16 i | 16 j << 16: pose-record byte offsets (dfs indices, i < j)
+    int off_pprm;     // float4[P]  r_eq^2, +-eps_ij (negative: H-bond pair), S_iV_j + S_jV_i,
+                      //            332.06363/4 q_i q_j
     int off_mask;     // uint32[N][NW] pair-membership bit rows (dfs indices)
     int NW;           // words per mask row = ceil(N / 32)
     // gradient-path pair tiles (score.cuh intra_tiles): lane groups of Wg lanes, atom

@@ -194,20 +194,30 @@ __global__ void __launch_bounds__(256) k_ga(const LigDev L, const GridDev g, con
     if (gi < sp.runs * P) { st = pop.state[r]; act = run_active(st, sp); }
     if (!__syncthreads_or(act)) return;            // finished runs cost one state read
     const LigSm Ls = stage_ligand(L, sm, staged_bytes(L, false));
-    if (!act) return;
+    // Both lane groups of a warp stay converged through the evaluation (the elite slot and
+    // inactive groups evaluate a dummy genotype and write nothing), so its shuffles take a
+    // constant full-warp mask.
+    if (!__any_sync(0xffffffffu, act)) return;
     const int k = gi % P;
-    const uint32_t gen = (uint32_t)st.gen + 1u;
-    const int cur = st.gen & 1, nxt = gen & 1;
-    const float *oldG = pop.genes + ((size_t)cur * sp.runs + r) * P * G;
-    const float *oldE = pop.E + ((size_t)cur * sp.runs + r) * P;
-    float *newG = pop.genes + ((size_t)nxt * sp.runs + r) * P * G;
-    float *newE = pop.E + ((size_t)nxt * sp.runs + r) * P;
     const Scratch S = scratch_at(sm + staged_bytes(L, false) + gl * SL.bytes, SL);
     const unsigned mask = group_mask<W>();
     const uint2 key = make_uint2(sp.key0, sp.key1);
-    const uint32_t run_g = (uint32_t)(sp.run_base + r);
+    const uint32_t gen = act ? (uint32_t)st.gen + 1u : 1u;
+    const int cur = act ? (st.gen & 1) : 0, nxt = gen & 1;
+    const int rr = act ? r : 0;
+    const float *oldG = pop.genes + ((size_t)cur * sp.runs + rr) * P * G;
+    const float *oldE = pop.E + ((size_t)cur * sp.runs + rr) * P;
+    float *newG = pop.genes + ((size_t)nxt * sp.runs + rr) * P * G;
+    float *newE = pop.E + ((size_t)nxt * sp.runs + rr) * P;
+    const uint32_t run_g = (uint32_t)(sp.run_base + rr);
+    bool child = false;                 // this group scores a real offspring
+    int A = 0, B = 0, c1 = 0, c2 = 0;
+    bool cross = false;
+    unsigned long long mbits = 0ull;
 
-    if (k == 0) {
+    if (!act) {
+        for (int j = sub; j < G; j += W) S.genes[j] = 0.0f;
+    } else if (k == 0) {
         // elitism: argmin, NaN = +inf, ties -> lowest index; copied without re-evaluation
         float bv = INFINITY;
         int bi = 0x7fffffff;
@@ -221,7 +231,11 @@ __global__ void __launch_bounds__(256) k_ga(const LigDev L, const GridDev g, con
             const int oi = __shfl_xor_sync(mask, bi, m, W);
             if (ov < bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; }
         }
-        for (int j = sub; j < G; j += W) newG[j] = oldG[(size_t)bi * G + j];
+        for (int j = sub; j < G; j += W) {
+            const float v = oldG[(size_t)bi * G + j];
+            newG[j] = v;
+            S.genes[j] = v;                 // shadow evaluation only
+        }
         if (sub == 0) newE[0] = oldE[bi];
         // local-search sample: partial Fisher-Yates over the new population (D8.3)
         int *perm = reinterpret_cast<int *>(sm + staged_bytes(L, false) + gl * SL.bytes + SL.off_extra);
@@ -241,39 +255,39 @@ __global__ void __launch_bounds__(256) k_ga(const LigDev L, const GridDev g, con
             int *d = dbg + (size_t)gi * 8;
             d[0] = bi; d[1] = bi; d[2] = 0; d[3] = 0; d[4] = 0; d[5] = 0; d[6] = 0; d[7] = bi;
         }
-        return;
-    }
-    // slot k >= 1: words 0..8 from the first three Philox blocks
-    const uint4 b0 = stream_block(key, kGA, (uint32_t)k, gen, run_g, 0u);
-    const uint4 b1 = stream_block(key, kGA, (uint32_t)k, gen, run_g, 1u);
-    const uint4 b2 = stream_block(key, kGA, (uint32_t)k, gen, run_g, 2u);
-    const int A = tournament(oldE, P, b0.x, b0.y, b0.z, sp.p_tour);
-    const int B = tournament(oldE, P, b0.w, b1.x, b1.y, sp.p_tour);
-    const bool cross = u01(b1.z) < sp.p_cross;
-    int c1 = 0, c2 = 0;
-    if (cross) {
-        c1 = (int)below(b1.w, (uint32_t)(G + 1));
-        c2 = (int)below(b2.x, (uint32_t)(G + 1));
-        if (c2 < c1) { const int t = c1; c1 = c2; c2 = t; }
-    }
-    unsigned long long mbits = 0ull;
-    for (int j = sub; j < G; j += W) {
-        const uint32_t m = 9u + 2u * (uint32_t)j;                 // mutation coin; delta = m + 1
-        const uint4 bc = stream_block(key, kGA, (uint32_t)k, gen, run_g, m >> 2);
-        const uint32_t wc = lane_of(bc, m & 3);
-        const uint32_t md = m + 1u;
-        const uint32_t wd = ((md >> 2) == (m >> 2)) ? lane_of(bc, md & 3)
-                                                    : lane_of(stream_block(key, kGA, (uint32_t)k, gen, run_g, md >> 2), md & 3);
-        float v = (cross && c1 <= j && j < c2) ? oldG[(size_t)B * G + j] : oldG[(size_t)A * G + j];
-        if (u01(wc) < sp.p_mut) {
-            const float mag = j < 3 ? sp.mut_trans : sp.mut_angle;
-            v += (2.0f * u01(wd) - 1.0f) * mag;
-            mbits |= 1ull << j;
+    } else {
+        // slot k >= 1: words 0..8 from the first three Philox blocks
+        child = true;
+        const uint4 b0 = stream_block(key, kGA, (uint32_t)k, gen, run_g, 0u);
+        const uint4 b1 = stream_block(key, kGA, (uint32_t)k, gen, run_g, 1u);
+        const uint4 b2 = stream_block(key, kGA, (uint32_t)k, gen, run_g, 2u);
+        A = tournament(oldE, P, b0.x, b0.y, b0.z, sp.p_tour);
+        B = tournament(oldE, P, b0.w, b1.x, b1.y, sp.p_tour);
+        cross = u01(b1.z) < sp.p_cross;
+        if (cross) {
+            c1 = (int)below(b1.w, (uint32_t)(G + 1));
+            c2 = (int)below(b2.x, (uint32_t)(G + 1));
+            if (c2 < c1) { const int t = c1; c1 = c2; c2 = t; }
         }
-        S.genes[j] = v;
+        for (int j = sub; j < G; j += W) {
+            const uint32_t m = 9u + 2u * (uint32_t)j;                 // mutation coin; delta = m + 1
+            const uint4 bc = stream_block(key, kGA, (uint32_t)k, gen, run_g, m >> 2);
+            const uint32_t wc = lane_of(bc, m & 3);
+            const uint32_t md = m + 1u;
+            const uint32_t wd = ((md >> 2) == (m >> 2)) ? lane_of(bc, md & 3)
+                                                        : lane_of(stream_block(key, kGA, (uint32_t)k, gen, run_g, md >> 2), md & 3);
+            float v = (cross && c1 <= j && j < c2) ? oldG[(size_t)B * G + j] : oldG[(size_t)A * G + j];
+            if (u01(wc) < sp.p_mut) {
+                const float mag = j < 3 ? sp.mut_trans : sp.mut_angle;
+                v += (2.0f * u01(wd) - 1.0f) * mag;
+                mbits |= 1ull << j;
+            }
+            S.genes[j] = v;
+        }
     }
-    __syncwarp(mask);
-    const float e = eval_group<W, MAXC, false>(Ls, g, S, sub, mask);
+    __syncwarp();
+    const float e = eval_group<W, MAXC, false>(Ls, g, S, sub, 0xffffffffu);
+    if (!child) return;
     for (int j = sub; j < G; j += W) newG[(size_t)k * G + j] = S.genes[j];
     if (sub == 0) newE[k] = e;
     if (dbg) {

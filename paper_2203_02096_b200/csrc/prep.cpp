@@ -301,11 +301,14 @@ int prepare_ligand(const dock_ligand *l, const dock_type_param *tp, int n_types,
         bmask[dj * L.NW + (di >> 5)] |= 1u << (di & 31);
         if (L.energy_tiles) continue;
         const int hb = hb_of(i, j) ? 1 : 0;
-        bpairs[q] = (uint32_t)di | ((uint32_t)dj << 8) | ((uint32_t)hb << 16);
+        // byte offsets of the two pose records (16 B each) in the pair list; the H-bond flag
+        // is the sign bit of eps_ij in the pair constants
+        bpairs[q] = (uint32_t)(16 * di) | ((uint32_t)(16 * dj) << 16);
         // D5 pair constants for the energy-only path
         const dock_type_param &ti = tp[l->type[i]], &tj = tp[l->type[j]];
         const double req = 0.5 * ((double)ti.R + (double)tj.R);
-        pprm[q] = make_float4((float)(req * req), (float)std::sqrt((double)ti.eps * (double)tj.eps),
+        const float eps_ij = (float)std::sqrt((double)ti.eps * (double)tj.eps);
+        pprm[q] = make_float4((float)(req * req), hb ? -eps_ij : eps_ij,
                               (float)((double)ti.S * tj.V + (double)tj.S * ti.V),
                               (float)(332.06363 / 4.0 * (double)l->charge[i] * (double)l->charge[j]));
     }

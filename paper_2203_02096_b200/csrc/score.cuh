@@ -107,12 +107,13 @@ __device__ __forceinline__ void fast_sincos(float x, float &s, float &c) {
 }
 
 // D5 pair energy from precomputed pair constants (energy-only path).
-__device__ __forceinline__ float pair_e_pre(float rho2, float4 pp, bool hb) {
+__device__ __forceinline__ float pair_e_pre(float rho2, float4 pp) {
+    const bool hb = __float_as_int(pp.y) < 0;            // H-bond pair: eps_ij stored negated
     rho2 = fmaxf(rho2, 1e-4f);                           // 0.01 Å clamp
     const float inv = rcp_approx(rho2);
     const float x2 = pp.x * inv, x4 = x2 * x2, x6 = x4 * x2, x12 = x6 * x6;
     const float vdw = hb ? fmaf(5.0f, x12, -6.0f * (x6 * x4)) : fmaf(-2.0f, x6, x12);   // 12-10 / 12-6
-    return fmaf(pp.y, vdw, fmaf(pp.w, inv, pp.z * ex2_approx(rho2 * kExpScale)));
+    return fmaf(fabsf(pp.y), vdw, fmaf(pp.w, inv, pp.z * ex2_approx(rho2 * kExpScale)));
 }
 
 // D5 pair energy and dE/d(rho^2) from per-atom parameters (gradient path).
@@ -357,11 +358,12 @@ __device__ float eval_group(const LigSm &L, const GridDev &grid, const Scratch &
     const float R20 = 2.f * (qx * qz - qw * qy), R21 = 2.f * (qy * qz + qw * qx), R22 = 1.f - 2.f * (qx * qx + qy * qy);
     const float tx = x[0], ty = x[1], tz = x[2];
 
-    // ---- a3: torsion composites W_k = Root o L_a1 o ... o L_k (parents first; L_k =
+    // ---- a3: torsion composites A_k = L_a1 o ... o L_k (parents first; L_k =
     // Rot(u_k, tau_k) about A_k).  Lane k builds L_k; the chains are then collapsed by
     // pointer jumping (A_k <- A_anc(k) o A_k, anc <- anc(anc)) in ceil(log2(depth))
-    // rounds instead of one round per tree level; finally W_k = Root o A_k.  One torsion
-    // per lane: T <= N - 1 <= W (N <= 16 for W = 16; T <= 32 = W otherwise). ----
+    // rounds instead of one round per tree level.  Each atom then applies its deepest
+    // A_k and the root transform r = t + R(q) y.  One torsion per lane:
+    // T <= N - 1 <= W (N <= 16 for W = 16; T <= 32 = W otherwise). ----
     {
         const int k = sub;
         const bool own = k < L.T;
@@ -415,10 +417,7 @@ __device__ float eval_group(const LigSm &L, const GridDev &grid, const Scratch &
             __syncwarp(mask);
             anc = nanc;
         }
-        if (own) {
-            const float4 p0 = make_float4(R00, R01, R02, tx), p1 = make_float4(R10, R11, R12, ty),
-                         p2 = make_float4(R20, R21, R22, tz);
-            DK_COMPOSE(p0, p1, p2)
+        if (own) {   // A_k (torsion space); the root transform is applied per atom below
             S.W[3 * k] = make_float4(m[0], m[1], m[2], m[9]);
             S.W[3 * k + 1] = make_float4(m[3], m[4], m[5], m[10]);
             S.W[3 * k + 2] = make_float4(m[6], m[7], m[8], m[11]);
@@ -438,16 +437,16 @@ __device__ float eval_group(const LigSm &L, const GridDev &grid, const Scratch &
             const int meta = L.meta[a];
             const int deep = (meta >> 16) - 1;
             const float4 p = L.p[a];
-            if (deep < 0) {
-                rx[c] = fmaf(R00, p.x, fmaf(R01, p.y, fmaf(R02, p.z, tx)));
-                ry[c] = fmaf(R10, p.x, fmaf(R11, p.y, fmaf(R12, p.z, ty)));
-                rz[c] = fmaf(R20, p.x, fmaf(R21, p.y, fmaf(R22, p.z, tz)));
-            } else {
+            float yx = p.x, yy = p.y, yz = p.z;            // y = A_deep p (torsions, D3)
+            if (deep >= 0) {
                 const float4 w0 = S.W[3 * deep], w1 = S.W[3 * deep + 1], w2 = S.W[3 * deep + 2];
-                rx[c] = fmaf(w0.x, p.x, fmaf(w0.y, p.y, fmaf(w0.z, p.z, w0.w)));
-                ry[c] = fmaf(w1.x, p.x, fmaf(w1.y, p.y, fmaf(w1.z, p.z, w1.w)));
-                rz[c] = fmaf(w2.x, p.x, fmaf(w2.y, p.y, fmaf(w2.z, p.z, w2.w)));
+                yx = fmaf(w0.x, p.x, fmaf(w0.y, p.y, fmaf(w0.z, p.z, w0.w)));
+                yy = fmaf(w1.x, p.x, fmaf(w1.y, p.y, fmaf(w1.z, p.z, w1.w)));
+                yz = fmaf(w2.x, p.x, fmaf(w2.y, p.y, fmaf(w2.z, p.z, w2.w)));
             }
+            rx[c] = fmaf(R00, yx, fmaf(R01, yy, fmaf(R02, yz, tx)));   // r = t + R(q) y
+            ry[c] = fmaf(R10, yx, fmaf(R11, yy, fmaf(R12, yz, ty)));
+            rz[c] = fmaf(R20, yx, fmaf(R21, yy, fmaf(R22, yz, tz)));
             if (GRAD || L.energy_tiles) {
                 const float4 rv = make_float4(rx[c], ry[c], rz[c], p.w);
                 S.r[ridx<W>(a)] = rv;
@@ -483,9 +482,11 @@ __device__ float eval_group(const LigSm &L, const GridDev &grid, const Scratch &
         for (int q = sub; q < L.P; q += W) {
             const uint32_t w = L.pairs[q];
             const float4 pp = L.pprm[q];
-            const float4 ri = S.r[w & 0xff], rj = S.r[(w >> 8) & 0xff];
+            const uint8_t *rb = reinterpret_cast<const uint8_t *>(S.r);
+            const float4 ri = *reinterpret_cast<const float4 *>(rb + (w & 0xffffu));
+            const float4 rj = *reinterpret_cast<const float4 *>(rb + (w >> 16));
             const float dx = ri.x - rj.x, dy = ri.y - rj.y, dz = ri.z - rj.z;
-            e_part += pair_e_pre(fmaf(dx, dx, fmaf(dy, dy, dz * dz)), pp, (w >> 16) & 1u);
+            e_part += pair_e_pre(fmaf(dx, dx, fmaf(dy, dy, dz * dz)), pp);
         }
         return gsum<W>(e_part, mask);
     } else {

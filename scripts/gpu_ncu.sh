@@ -2,7 +2,7 @@
 # ncu captures summarised on the box (raw counters + SASS source view as CSV); the
 # .ncu-rep files are deleted to stay under gpurun's 64 MiB copy-back limit.
 set -u
-OUT=gpurun_out/r01j; mkdir -p $OUT
+OUT=gpurun_out/${1:-ncu}; mkdir -p $OUT
 python -c "import __graft_entry__ as g; g.build()" > $OUT/build.log 2>&1 || { echo BUILD FAILED; tail -30 $OUT/build.log; exit 1; }
 cap() {  # tag kernel-regex skip cmd...
   local tag=$1 re=$2 skip=$3; shift 3
