@@ -128,6 +128,42 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
+def dist_setup(local, world):
+    """One process per GPU, NCCL.  Returns (device, collective device).  BENCH_DIST_TEST=1 is
+    a test-only mode: gloo over CPU tensors and GPU local % device_count, so the multi-rank
+    path (sharding, barriers, max-over-ranks, gathers) runs on a 1-GPU box."""
+    import torch
+    import torch.distributed as dist
+    test = os.environ.get("BENCH_DIST_TEST") == "1"
+    idx = local % max(1, torch.cuda.device_count()) if test else local
+    torch.cuda.set_device(idx)
+    dev = torch.device("cuda", idx)
+    if world > 1:
+        if test:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
+    return dev, (torch.device("cpu") if test else dev)
+
+
+def all_gather_cat(t, cdev):
+    """Concatenate `t` from every rank (rank order) on the collective device."""
+    import torch
+    import torch.distributed as dist
+    x = t.to(cdev)
+    parts = [torch.empty_like(x) for _ in range(dist.get_world_size())]
+    dist.all_gather(parts, x)
+    return torch.cat(parts)
+
+
+def reduce_scalar(v, dtype, op, cdev):
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([v], dtype=dtype, device=cdev)
+    dist.all_reduce(t, op=op)
+    return t.item()
+
+
 def env_rank():
     return int(os.environ.get("RANK", 0)), int(os.environ.get("LOCAL_RANK", 0)), int(os.environ.get("WORLD_SIZE", 1))
 
@@ -199,12 +235,10 @@ def run_ours(args, cfg, lig, grid):
     import paper_2203_02096_b200 as dock
 
     rank, local, world = env_rank()
-    torch.cuda.set_device(local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    dev = torch.device("cuda", local)
+    dev, cdev = dist_setup(local, world)
+    gpu = dev.index
     d = dock.Docker.from_inputs(grid, lig, ls_method=cfg.ls_method, ls_rate=cfg.ls_rate,
-                                ls_max_iters=cfg.ls_iters, profile=1, device=local, sw_depth=args.sw_depth)
+                                ls_max_iters=cfg.ls_iters, profile=1, device=gpu, sw_depth=args.sw_depth)
     runs = cfg.runs
     run_base = rank * runs
     stream = torch.cuda.Stream(device=dev)
@@ -212,8 +246,7 @@ def run_ours(args, cfg, lig, grid):
     bG = torch.empty(runs, d.G, dtype=torch.float32, device=dev)
     ev = torch.empty(runs, dtype=torch.int64, device=dev)
     gens = torch.empty(runs, dtype=torch.int32, device=dev)
-    gather_E = torch.empty(world * runs, dtype=torch.float32, device=dev)
-    gather_G = torch.empty(world * runs, d.G, dtype=torch.float32, device=dev)
+    gathered = {}
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
     moved_total = int(np.asarray(d.torsions()[1]).sum())
     f_e = flops_per_eval(d.N, d.T, d.P, moved_total, grad=False)
@@ -224,13 +257,13 @@ def run_ours(args, cfg, lig, grid):
             d.run_device(cfg.pop, runs, cfg.max_evals, seed, bE, bG, ev, gens, run_base=run_base,
                          stream=stream.cuda_stream)
             if world > 1:   # NS: NCCL only for the final gather of best poses
-                dist.all_gather_into_tensor(gather_E, bE)
-                dist.all_gather_into_tensor(gather_G, bG)
+                gathered["E"] = all_gather_cat(bE, cdev)
+                gathered["G"] = all_gather_cat(bG, cdev)
 
     for w in range(args.warmup):
         step(42)
     torch.cuda.synchronize()
-    clocks = ClockSampler(local)
+    clocks = ClockSampler(gpu)
     clocks.start()
     times, evals, ls_ms, ls_n = [], 0, 0.0, 0
     launches0 = d.launches
@@ -256,12 +289,8 @@ def run_ours(args, cfg, lig, grid):
     t_max = t_local
     tot_evals = evals
     if world > 1:
-        tt = torch.tensor([t_local], dtype=torch.float64, device=dev)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        t_max = float(tt.item())
-        te = torch.tensor([evals], dtype=torch.int64, device=dev)
-        dist.all_reduce(te)
-        tot_evals = int(te.item())
+        t_max = float(reduce_scalar(t_local, torch.float64, dist.ReduceOp.MAX, cdev))
+        tot_evals = int(reduce_scalar(evals, torch.int64, dist.ReduceOp.SUM, cdev))
     value = tot_evals / (t_max / 1e3)
     ms_per_step = t_max / args.steps
 
@@ -303,7 +332,7 @@ def run_ours(args, cfg, lig, grid):
         t0 = time.perf_counter()
         dd = dock.Docker(grid.maps, grid.n, grid.spacing, grid.origin, tp, roles, lig.types, lig.charges,
                          lig.xyz, lig.bonds, lig.rotatable, ls_method=cfg.ls_method, ls_rate=cfg.ls_rate,
-                         ls_max_iters=cfg.ls_iters, device=local)
+                         ls_max_iters=cfg.ls_iters, device=gpu)
         r = dd.run(cfg.pop, runs, cfg.max_evals, 42, run_base=run_base, xyz=True)
         h2d = dd.upload_bytes
         dd.close()
@@ -313,12 +342,8 @@ def run_ours(args, cfg, lig, grid):
         d2h = r["best_E"].nbytes + r["best_genes"].nbytes + r["best_xyz"].nbytes + r["evals"].nbytes + \
             r["generations"].nbytes + 16 * runs * int(np.ceil(r["generations"].max() / 16 + 1))
     if world > 1:
-        tt = torch.tensor([e2e_t], dtype=torch.float64, device=dev)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        e2e_t = float(tt.item())
-        te = torch.tensor([e2e_evals], dtype=torch.int64, device=dev)
-        dist.all_reduce(te)
-        e2e_evals = int(te.item())
+        e2e_t = float(reduce_scalar(e2e_t, torch.float64, dist.ReduceOp.MAX, cdev))
+        e2e_evals = int(reduce_scalar(e2e_evals, torch.int64, dist.ReduceOp.SUM, cdev))
     e2e_value = e2e_evals / e2e_t
 
     line = None
@@ -383,9 +408,8 @@ def run_hts(args, cfg, grid):
         if rank != 0:
             return
     else:
-        torch.cuda.set_device(local)
-        if world > 1:
-            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        dev, cdev = dist_setup(local, world)
+        local = dev.index
     ligs = hts_ligands(args.n_ligs)
     per_lig_evals = cfg.runs * cfg.max_evals
     sample_desc = (f"configs[4] sample: {args.n_ligs} of the 10k synthetic ligands (N ~ U{{10..70}}, "
@@ -443,13 +467,9 @@ def run_hts(args, cfg, grid):
     t_max = t_local
     tot_evals = evals
     if world > 1:
-        tt = torch.tensor([t_local], dtype=torch.float64, device=dev)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        t_max = float(tt.item())
-        te = torch.tensor([evals], dtype=torch.int64, device=dev)
-        dist.all_reduce(te)
-        tot_evals = int(te.item())
-        res = sched.gather_records(mine, out, len(ligs), device=dev)   # NCCL: final gather only
+        t_max = float(reduce_scalar(t_local, torch.float64, dist.ReduceOp.MAX, cdev))
+        tot_evals = int(reduce_scalar(evals, torch.int64, dist.ReduceOp.SUM, cdev))
+        res = sched.gather_records(mine, out, len(ligs), device=cdev)   # NCCL: final gather only
     else:
         res = out
     lph = 3600.0 * len(ligs) * args.steps / t_max
