@@ -571,7 +571,9 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="1stp", choices=["tiny", "1stp", "3ce3", "7cpa", "hts"])
+    ap.add_argument("--config", default="1stp", choices=["tiny", "1stp", "3ce3", "7cpa", "hts", "ps", "pm", "pl"])
+    ap.add_argument("--runs", type=int, default=0, help="override runs per GPU (NEXT-1 sweeps)")
+    ap.add_argument("--max-evals", type=int, default=0, help="override evals per run (NEXT-1 sweeps)")
     ap.add_argument("--micro", action="store_true", help="isolated inter/intra microbenchmarks (roofline evidence)")
     ap.add_argument("--micro-iters", type=int, default=20)
     ap.add_argument("--sw-depth", type=int, default=0, help="Solis-Wets speculation depth (0 = auto)")
@@ -582,6 +584,10 @@ def main():
     args = ap.parse_args()
     from gen import config_inputs
     cfg, lig, grid = config_inputs(args.config)
+    if args.runs > 0:
+        cfg.runs = args.runs
+    if args.max_evals > 0:
+        cfg.max_evals = args.max_evals
     if args.micro:
         run_micro(args, cfg, lig, grid)
     elif args.config == "hts":

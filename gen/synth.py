@@ -68,6 +68,14 @@ CONFIGS = {
                    "configs[2]: 3ce3-shaped, 40 atoms, 8 torsions, 64^3 grid, pop 150, 50 runs, ADADELTA"),
     "7cpa": Config("7cpa", 70, 15, 80, 0.375, 10, 256, 100, 2_500_000, 0, 1.0, 300, 4, 104,
                    "configs[3]: 7cpa-shaped, 70 atoms, 15 torsions, 80^3 grid, pop 256, 100 runs, ADADELTA"),
+    # NEXT-1: the paper's own input shapes (PAPER.md:66 [§II-A]: "21, 43,
+    # and 108 atoms, and 2, 15, and 31 rotatable bonds"), with the paper's Solis-Wets LS.
+    "ps": Config("ps", 21, 2, 64, 0.375, 8, 150, 10, 2_500_000, 1, 0.06, 300, 6, 106,
+                 "NEXT-1 PS: paper's small input shape, 21 atoms, 2 torsions, Solis-Wets"),
+    "pm": Config("pm", 43, 15, 64, 0.375, 8, 150, 10, 2_500_000, 1, 0.06, 300, 7, 107,
+                 "NEXT-1 PM: paper's medium input shape, 43 atoms, 15 torsions, Solis-Wets"),
+    "pl": Config("pl", 108, 31, 80, 0.375, 10, 150, 10, 2_500_000, 1, 0.06, 300, 8, 108,
+                 "NEXT-1 PL: paper's large input shape, 108 atoms, 31 torsions, Solis-Wets"),
     # configs[4]: 10k ligands N~U{10..70} vs one 64^3 receptor; see hts_ligands().
     "hts": Config("hts", 0, 0, 64, 0.375, 10, 150, 10, 250_000, 0, 1.0, 300, 5, 105,
                   "configs[4]: 10k synthetic ligands of mixed sizes vs one receptor grid"),

@@ -103,7 +103,7 @@ def test_stream_words_bit_exact(dock, purpose, slot, gen, run):
 # ---------------------------------------------------------------------------
 # a3-a6 / D3-D7: pose, energy, gradient
 # ---------------------------------------------------------------------------
-@pytest.mark.parametrize("name,n", [("tiny", 3000), ("1stp", 1500), ("3ce3", 600), ("7cpa", 300)])
+@pytest.mark.parametrize("name,n", [("tiny", 3000), ("1stp", 1500), ("3ce3", 600), ("7cpa", 300), ("pm", 400), ("pl", 120)])
 def test_energy_gradient_pose_parity(dock, name, n):
     cfg, lig, grid, d, P = setup(dock, name)
     # pairs/torsions of the device context equal the oracle's (bit-exact)
