@@ -863,9 +863,11 @@ cudaError_t launch_ls(const LigDev &L, const GridDev &g, const SearchDev &sp, co
             int dev = 0, nsm = 148;
             cudaGetDevice(&dev);
             cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-            // Measured on B200 (profiles/r01, 1stp): depth 2 = 1.45x, depth 3 = 1.19x over depth 1 --
-            // 26 groups/CTA contend for issue and spill at the 2-CTA/SM register cap -- so
-            // auto stops at depth 2; depth 3 stays available explicitly.
+            // Measured on B200 (profiles/r01n, NEXT-1 sweep): depth 2 wins whenever its CTAs
+            // fit one wave (1stp 1.7x, PS/PM/PL with 10 runs 2.0x / 2.4x / 3.6x) and, for
+            // large ligands (P >= 2000, PL), up to ~4 waves (1.43x at 900 chains); small
+            // ligands at 900 chains prefer depth 1 (0.91x / 0.96x).  Depth 3 (26 groups)
+            // never won (issue contention, spills at the 2-CTA/SM register cap).
             for (int D = 2; D >= 2 && depth == 1; --D) {
                 const int ngr = D == 3 ? 26 : 8;
                 const size_t sm_b = (size_t)staged_bytes(L, false) + (size_t)ngr * SL.bytes + 4 * (2 * kMaxGenes + ngr + 2 * D * kMaxGenes);
@@ -875,7 +877,8 @@ cudaError_t launch_ls(const LigDev &L, const GridDev &g, const SearchDev &sp, co
                     else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_ls_sw_tree<W, MAXC, 2>, tree_threads<W, 2>(), sm_b);
                 });
                 cudaGetLastError();
-                if (sm_b <= (size_t)kSmemMax && per_sm > 0 && (long long)n_total <= (long long)per_sm * nsm) depth = D;
+                const long long waves = L.P >= 2000 ? 4 : 1;
+                if (sm_b <= (size_t)kSmemMax && per_sm > 0 && (long long)n_total <= waves * per_sm * nsm) depth = D;
             }
         }
         if (depth >= 2) {

@@ -136,6 +136,9 @@ __device__ __forceinline__ float pair_eg(float rho2, float4 pi, float qi, float4
     return Evdw + Eel + Eds;
 }
 
+// S_i V_j + S_j V_i from own and partner params {R/2, sqrt eps, S, V}
+__device__ __forceinline__ float o_sv(float4 pi, float4 pj) { return fmaf(pi.z, pj.w, pj.z * pi.w); }
+
 // D5 vdW/H-bond part from (x^2, A, B): E = A x^12 - |B| x^n, n = 6 (B >= +0) or 10 (B
 // negative); returns E and rho^2 dE/drho^2 = -6 A x^12 + (n/2) |B| x^n.
 __device__ __forceinline__ float vdw_ab(float x2, float A, float B, float &dvr) {
@@ -336,6 +339,59 @@ __device__ __forceinline__ void intra_tiles(const LigSm &L, const Scratch &S, in
     }
 }
 
+// Energy-only pair tiles (large ligands whose pair list is not staged, L.energy_tiles):
+// the same rotation and membership bits as intra_tiles, but no forces, so no partner
+// accumulators and no shuffles.  The tail chunk is rotated too (no reductions to save).
+template <int W, int MAXC>
+__device__ __forceinline__ float intra_tiles_energy(const LigSm &L, const Scratch &S, int sub,
+                                                    const float (&rx)[MAXC], const float (&ry)[MAXC],
+                                                    const float (&rz)[MAXC]) {
+    const int N = L.N;
+    const int Bt = L.NC;
+    float e = 0.0f;
+#pragma unroll
+    for (int I = 0; I < MAXC; ++I) {
+        if (I >= Bt) break;
+        const int aI = I * W + sub;
+        const bool okI = aI < N;
+        const float4 po = L.ppar[ridx<W>(aI)];
+        const float qi = okI ? kElec4 * S.r[ridx<W>(aI)].w : 0.0f;
+        const float Ri = fabsf(po.x), ei = fabsf(po.y);
+        const bool hbc = __float_as_int(po.x) < 0 || __float_as_int(po.y) < 0, don = __float_as_int(po.y) < 0;
+#pragma unroll
+        for (int J = I; J < MAXC; ++J) {
+            if (J >= Bt) break;
+            const int jb = J * W;
+            uint32_t mw = okI ? (L.mask[aI * L.NW + (jb >> 5)] >> (jb & 31)) : 0u;
+            uint32_t rot;
+            if constexpr (W == 32) {
+                rot = __funnelshift_r(mw, mw, sub);
+            } else {
+                mw &= 0xffffu;
+                rot = ((mw | (mw << 16)) >> sub) & 0xffffu;
+            }
+            if (I == J && sub >= W / 2) rot &= ~(1u << (W / 2));
+            const float4 *rrow = S.r + J * 2 * W + sub;
+            const float4 *qrow = L.ppar + J * 2 * W + sub;
+            const int s0 = (I == J) ? 1 : 0, s1 = (I == J) ? W / 2 : W - 1;
+#pragma unroll 4
+            for (int st = s0; st <= s1; ++st) {
+                const float4 rj = rrow[st], pj = qrow[st];
+                const float dx = rx[I] - rj.x, dy = ry[I] - rj.y, dz = rz[I] - rj.z;
+                const float rho2 = fmaxf(fmaf(dx, dx, fmaf(dy, dy, dz * dz)), 1e-4f);
+                const float inv = rcp_approx(rho2);
+                const float req = Ri + fabsf(pj.x), eps = ei * fabsf(pj.y);
+                const bool hb = hbc && __float_as_int(don ? pj.x : pj.y) < 0;
+                float dvr;
+                const float Ev = vdw_ab(req * req * inv, hb ? 5.0f * eps : eps, hb ? -6.0f * eps : 2.0f * eps, dvr);
+                const float E = Ev + fmaf(qi * rj.w, inv, o_sv(po, pj) * ex2_approx(rho2 * kExpScale));
+                e += ((rot >> st) & 1u) ? E : 0.0f;
+            }
+        }
+    }
+    return e;
+}
+
 // Energy (and genotype gradient into S.grad) of the genotype in S.genes.
 // Every lane of the group returns the same total energy.
 // PARTS (microbenchmarks only, SURVEY.md §8(d) "isolating the two kernels for ncu"):
@@ -475,7 +531,7 @@ __device__ float eval_group(const LigSm &L, const GridDev &grid, const Scratch &
         return gsum<W>(e_part, mask);
     } else if constexpr (!GRAD) {
         if (L.energy_tiles) {           // large ligand: pair list not staged, use the tiles
-            intra_tiles<W, MAXC>(L, S, sub, mask, rx, ry, rz, gx, gy, gz, e_part);
+            e_part += intra_tiles_energy<W, MAXC>(L, S, sub, rx, ry, rz);
             return gsum<W>(e_part, mask);
         }
 #pragma unroll 4
