@@ -102,6 +102,8 @@ def _load():
         "dock_topology": (i32, [P(Ligand), P(TypeParam), i32, P(i32), P(i32), P(C.c_uint8), P(i32), P(i32), i32]),
     }
     for name, (res, args) in sig.items():
+        if os.environ.get("DOCK_LIB") and not hasattr(L, name):
+            continue                # experimental older build (A/B timing): symbol absent
         fn = getattr(L, name)
         fn.restype = res
         fn.argtypes = args

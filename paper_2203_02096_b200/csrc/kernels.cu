@@ -855,6 +855,13 @@ cudaError_t launch_ls(const LigDev &L, const GridDev &g, const SearchDev &sp, co
     const GroupCfg cfg = pick_group(L.N);
     if (sp.ls_method == 1) {
         const ScratchLayout SL = scratch_layout(L, false, 0);
+#ifndef DK_TREE_W32
+#define DK_TREE_W32 0
+#endif
+        // latency-bound tree: optionally give small ligands (W = 16) a full warp per node so
+        // each lane has half the pairs of the energy sum
+        GroupCfg tcfg = cfg;
+        if (DK_TREE_W32 && cfg.W == 16) { tcfg.W = 32; tcfg.MAXC = 1; }
         // Speculation depth: the deepest tree whose CTAs are all co-resident (one wave);
         // a full launch gains nothing from speculation and uses the plain kernel.
         int depth = sp.sw_depth;
@@ -872,7 +879,7 @@ cudaError_t launch_ls(const LigDev &L, const GridDev &g, const SearchDev &sp, co
                 const int ngr = D == 3 ? 26 : 8;
                 const size_t sm_b = (size_t)staged_bytes(L, false) + (size_t)ngr * SL.bytes + 4 * (2 * kMaxGenes + ngr + 2 * D * kMaxGenes);
                 int per_sm = 0;
-                DK_DISPATCH(cfg, {
+                DK_DISPATCH(tcfg, {
                     if (D == 3) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_ls_sw_tree<W, MAXC, 3>, tree_threads<W, 3>(), sm_b);
                     else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_ls_sw_tree<W, MAXC, 2>, tree_threads<W, 2>(), sm_b);
                 });
@@ -885,7 +892,7 @@ cudaError_t launch_ls(const LigDev &L, const GridDev &g, const SearchDev &sp, co
             const int ngr = depth == 3 ? 26 : 8;
             const size_t smem = (size_t)staged_bytes(L, false) + (size_t)ngr * SL.bytes + 4 * (2 * kMaxGenes + ngr + 2 * depth * kMaxGenes);
             if (smem > (size_t)kSmemMax) return cudaErrorInvalidConfiguration;
-            DK_DISPATCH(cfg, {
+            DK_DISPATCH(tcfg, {
                 if (depth == 3) k_ls_sw_tree<W, MAXC, 3><<<n_total, tree_threads<W, 3>(), smem, s>>>(L, g, SL, sp, pop, a);
                 else k_ls_sw_tree<W, MAXC, 2><<<n_total, tree_threads<W, 2>(), smem, s>>>(L, g, SL, sp, pop, a);
             });
