@@ -103,7 +103,7 @@ int ensure_buffers(dock_ctx *c, int runs, int pop) {
     CK(dk::dmalloc((void **)&c->d_perm, (size_t)R * P * sizeof(int), s));
     CK(dk::dmalloc((void **)&c->d_ls_evals, (size_t)R * P * sizeof(int), s));
     CK(cudaStreamSynchronize(s));   // usable from any stream (dock_run_device's) from here on
-    c->h_state.resize(R);
+    if (!c->h_state.reserve(R)) { c->err = "pinned host allocation failed"; return DOCK_E_INTERNAL; }
     c->cap_runs = R; c->cap_pop = P;
     return DOCK_OK;
 }
@@ -144,6 +144,38 @@ int validate_params(const dock_params &p, std::string *err) {
     if (p.gens_per_graph < 1 || p.gens_per_graph > 4096) { *err = "params.gens_per_graph: 1..4096"; return DOCK_E_INPUT; }
     if (p.sw_depth < 0 || p.sw_depth > 3) { *err = "params.sw_depth: 0..3"; return DOCK_E_INPUT; }
     return DOCK_OK;
+}
+
+namespace {
+std::mutex g_pinned_mu;
+std::vector<std::pair<size_t, void *>> g_pinned_free;   // (size class, block)
+size_t pinned_class(size_t b) {
+    size_t c = 256;
+    while (c < b) c <<= 1;
+    return c;
+}
+}  // namespace
+
+void *pinned_get(size_t bytes) {
+    const size_t cls = pinned_class(bytes);
+    {
+        std::lock_guard<std::mutex> lk(g_pinned_mu);
+        for (size_t i = 0; i < g_pinned_free.size(); ++i)
+            if (g_pinned_free[i].first == cls) {
+                void *p = g_pinned_free[i].second;
+                g_pinned_free.erase(g_pinned_free.begin() + i);
+                return p;
+            }
+    }
+    void *p = nullptr;
+    if (cudaMallocHost(&p, cls) != cudaSuccess) { cudaGetLastError(); return nullptr; }
+    return p;
+}
+
+void pinned_put(void *p, size_t bytes) {
+    if (!p) return;
+    std::lock_guard<std::mutex> lk(g_pinned_mu);
+    g_pinned_free.push_back({pinned_class(bytes), p});
 }
 
 void pool_setup(int device) {
@@ -395,7 +427,14 @@ int dock_run_device(dock_ctx *c, int32_t pop, int32_t runs, int32_t run_base, ui
     cudaStream_t s = stream ? (cudaStream_t)stream : c->stream;
     const dk::SearchDev sp = make_search(c, pop, runs, run_base, ligand_id, max_evals, seed);
     const dk::PopDev pd = pop_of(c);
-    const int K = c->params.gens_per_graph;
+    int K = c->params.gens_per_graph;
+    if (sp.ls_method == DOCK_LS_ADADELTA || sp.n_ls == 0 || sp.ls_iters == 0) {
+        // evaluations per generation are fixed (D10: exactly ls_iters per LS), so a short
+        // job needs fewer captured generations than gens_per_graph (no trailing no-ops)
+        const long long per_gen = (long long)(pop - 1) + (long long)sp.n_ls * sp.ls_iters;
+        const long long need = per_gen > 0 ? (max_evals - pop + per_gen - 1) / per_gen : 1;
+        K = (int)std::max(1LL, std::min<long long>(K, std::min<long long>(need, c->params.max_generations)));
+    }
     const bool prof = c->params.profile != 0;
     for (int i = 0; i < 3; ++i) { c->prof_ms[i] = 0; c->prof_n[i] = 0; }
     if (prof && (int)c->events.size() < 3 * K + 2) {

@@ -28,6 +28,32 @@ inline void dfree(void *p, cudaStream_t s) {
     if (p) cudaFreeAsync(p, s);
 }
 
+// Pinned host blocks for the small per-batch device->host reads (termination poll, screen
+// results), cached for the life of the process: cudaFreeHost is slow, and pageable
+// copies from several worker threads serialise through the driver's staging buffer
+// (measured: dock_screen with 4 slots lost 25 % with pageable polls, profiles/r01o).
+void *pinned_get(size_t bytes);
+void pinned_put(void *p, size_t bytes);
+template <typename T>
+struct PinnedBuf {
+    T *p = nullptr;
+    size_t n = 0;
+    PinnedBuf() = default;
+    PinnedBuf(const PinnedBuf &) = delete;
+    PinnedBuf &operator=(const PinnedBuf &) = delete;
+    PinnedBuf(PinnedBuf &&o) noexcept : p(o.p), n(o.n) { o.p = nullptr; o.n = 0; }
+    ~PinnedBuf() { if (p) pinned_put(p, n * sizeof(T)); }
+    bool reserve(size_t count) {
+        if (count <= n) return true;
+        if (p) pinned_put(p, n * sizeof(T));
+        p = static_cast<T *>(pinned_get(count * sizeof(T)));
+        n = p ? count : 0;
+        return p != nullptr;
+    }
+    T &operator[](size_t i) { return p[i]; }
+    T *data() { return p; }
+};
+
 struct Receptor {
     int device = 0;
     cudaStream_t stream = nullptr;   // owns the upload and the final free
@@ -61,7 +87,7 @@ struct dock_ctx {
     float *d_genes = nullptr, *d_E = nullptr;
     dk::RunState *d_state = nullptr;
     int *d_perm = nullptr, *d_ls_evals = nullptr;
-    std::vector<dk::RunState> h_state;   // termination poll target (pageable: read right after a sync)
+    dk::PinnedBuf<dk::RunState> h_state;   // termination poll target
     std::string err;
     long long launches = 0;
     double prof_ms[3] = {0, 0, 0};

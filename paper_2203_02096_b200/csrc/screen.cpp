@@ -39,8 +39,8 @@ thread_local std::string g_screen_error;
 struct SlotBufs {
     float *d_bE = nullptr, *d_bG = nullptr;
     int64_t *d_ev = nullptr;
-    std::vector<float> h_bE, h_bG;
-    std::vector<int64_t> h_ev;
+    dk::PinnedBuf<float> h_bE, h_bG;
+    dk::PinnedBuf<int64_t> h_ev;
     void release(cudaStream_t s) {
         dk::dfree(d_bE, s); dk::dfree(d_bG, s); dk::dfree(d_ev, s);
         d_bE = d_bG = nullptr; d_ev = nullptr;
@@ -127,6 +127,7 @@ extern "C" int dock_screen(const dock_grids *grids, const dock_type_param *type_
     // ---- 3. receptors and slot contexts ----
     struct Slot { dock_ctx *ctx = nullptr; SlotBufs b; int device = 0; };
     std::vector<Slot> slot_v;
+    slot_v.reserve(devs.size() * (size_t)slots);
     int rc = DOCK_OK;
     std::vector<std::shared_ptr<dk::Receptor>> recs;
     auto cleanup = [&] {
@@ -146,9 +147,13 @@ extern "C" int dock_screen(const dock_grids *grids, const dock_type_param *type_
             Slot s;
             s.device = d;
             if ((rc = dk::ctx_create(rec, p, &s.ctx, &err)) != DOCK_OK) { g_screen_error = err; cleanup(); return rc; }
-            slot_v.push_back(s);
+            slot_v.push_back(std::move(s));
             Slot &sl = slot_v.back();
-            sl.b.h_bE.resize(runs); sl.b.h_bG.resize((size_t)runs * DOCK_MAX_GENES); sl.b.h_ev.resize(runs);
+            if (!sl.b.h_bE.reserve(runs) || !sl.b.h_bG.reserve((size_t)runs * DOCK_MAX_GENES) || !sl.b.h_ev.reserve(runs)) {
+                g_screen_error = "pinned host allocation failed";
+                cleanup();
+                return DOCK_E_INTERNAL;
+            }
             const cudaStream_t st = sl.ctx->stream;
             if ((rc = dk::ctx_reserve(sl.ctx, max_blob, runs, pop)) != DOCK_OK ||
                 dk::dmalloc((void **)&sl.b.d_bE, sizeof(float) * runs, st) != cudaSuccess ||
@@ -207,7 +212,7 @@ extern "C" int dock_screen(const dock_grids *grids, const dock_type_param *type_
             }
             best_energy[i] = s.b.h_bE[br];
             if (best_run) best_run[i] = br;
-            std::copy(s.b.h_bG.begin() + (size_t)br * G, s.b.h_bG.begin() + (size_t)(br + 1) * G,
+            std::copy(s.b.h_bG.data() + (size_t)br * G, s.b.h_bG.data() + (size_t)(br + 1) * G,
                       best_genotype + (size_t)i * DOCK_MAX_GENES);
             if (evals_used) evals_used[i] = ev;
             if (device_of) device_of[i] = s.device;
