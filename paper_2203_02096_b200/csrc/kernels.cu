@@ -855,13 +855,9 @@ cudaError_t launch_ls(const LigDev &L, const GridDev &g, const SearchDev &sp, co
     const GroupCfg cfg = pick_group(L.N);
     if (sp.ls_method == 1) {
         const ScratchLayout SL = scratch_layout(L, false, 0);
-#ifndef DK_TREE_W32
-#define DK_TREE_W32 0
-#endif
-        // latency-bound tree: optionally give small ligands (W = 16) a full warp per node so
-        // each lane has half the pairs of the energy sum
-        GroupCfg tcfg = cfg;
-        if (DK_TREE_W32 && cfg.W == 16) { tcfg.W = 32; tcfg.MAXC = 1; }
+        // (A full warp per node for W = 16 ligands -- half the pairs per lane -- was measured
+        // 0.63x on 1stp: twice the warps per round, same critical path.)
+        const GroupCfg tcfg = cfg;
         // Speculation depth: the deepest tree whose CTAs are all co-resident (one wave);
         // a full launch gains nothing from speculation and uses the plain kernel.
         int depth = sp.sw_depth;

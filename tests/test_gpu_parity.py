@@ -487,3 +487,39 @@ def test_large_ligand_run(dock, large_case, method):
         tol, _ = pose_tols(P, ref)
         assert abs(ref["E"] - r["best_E"][k]) <= tol, (ref["E"], r["best_E"][k])
     d.close()
+
+
+# ---------------------------------------------------------------------------
+# Maximum sizes: N = 256 atoms (the ABI limit), T = 32 torsions (the limit): MAXC = 8
+# chunks, energy-only kernels on the pair tiles (P ~ 30k pairs).
+# ---------------------------------------------------------------------------
+def test_max_size_ligand_parity_and_run(dock):
+    from gen.synth import TYPE_NAMES, make_grid
+    n = 256
+    lig = _chain_ligand(n, seed=5)
+    # a helix-like chain (compact enough for the grid), 32 rotatable bonds spread along it
+    k = np.arange(n)
+    lig.xyz = np.stack([4.0 * np.cos(k * 0.7), 4.0 * np.sin(k * 0.7), 0.35 * k], 1).astype(np.float32)
+    lig.xyz -= lig.xyz.mean(0)
+    rot = np.zeros(n - 1, np.uint8)
+    rot[np.linspace(2, n - 4, 32).astype(int)] = 1
+    lig.rotatable = rot
+    grid = make_grid(40, 2.5, list(TYPE_NAMES), seed=9)
+    d = dock.Docker.from_inputs(grid, lig, ls_method=1, ls_rate=0.2, ls_max_iters=5)
+    P = oracle.Problem(grid, lig)
+    assert d.N == 256 and d.T == 32 and d.P > 25000
+    X = random_genotypes(grid, d.T, 24, seed=4, frac_out=0.0, shrink=0.02)
+    X[:, 6:] *= 0.05
+    E, Gd, xyz = d.eval(X, grad=True, xyz=True)
+    E0, _, _ = d.eval(X, grad=False)
+    for i in range(X.shape[0]):
+        ref = P.energy(X[i].astype(np.float64))
+        tol, gtol = pose_tols(P, ref)
+        assert np.abs(xyz[i] - ref["xyz"]).max() <= 1e-4 * max(1.0, np.abs(ref["xyz"]).max() / 30)
+        assert abs(E[i] - ref["E"]) <= tol and abs(E0[i] - ref["E"]) <= tol, (i, E[i], E0[i], ref["E"])
+        fm, cm = P.margins(ref["xyz"])
+        if fm >= 1e-4 and cm >= 1e-4:
+            assert np.abs(Gd[i] - ref["grad"]).max() <= gtol, i
+    r = d.run(8, 1, 200, 42, xyz=False)
+    assert r["evals"][0] >= 200 and np.isfinite(r["best_E"][0])
+    d.close()
