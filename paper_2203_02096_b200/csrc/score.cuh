@@ -18,6 +18,10 @@ constexpr float kElec4 = 332.06363f * 0.25f;                  // D5: 332.06363 /
 constexpr float kInvTwoSigma2 = 1.0f / (2.0f * 3.6f * 3.6f);    // desolvation sigma 3.6 Å
 constexpr float kExpScale = -kInvTwoSigma2 * 1.4426950408889634f;   // exp(-x/2s^2) = 2^(x*kExpScale)
 constexpr float kOut = 1e5f;                                    // D4.5 out-of-grid penalty
+#ifndef DK_WALK_DEPTH
+#define DK_WALK_DEPTH 3
+#endif
+constexpr int kWalkDepth = DK_WALK_DEPTH;   // torsion trees up to this depth: per-atom chain walk, no composites
 
 // Shared-memory view of the staged ligand block.
 struct LigSm {
@@ -456,7 +460,10 @@ __device__ float eval_group(const LigSm &L, const GridDev &grid, const Scratch &
         o_[11] = fmaf(p2.x, m[9], fmaf(p2.y, m[10], fmaf(p2.z, m[11], p2.w)));                   \
         _Pragma("unroll") for (int i_ = 0; i_ < 12; ++i_) m[i_] = o_[i_];                        \
     }
-        for (int span = 1; span < L.n_levels; span *= 2) {
+        // shallow trees (depth <= kWalkDepth): no composites at all -- each atom walks its
+        // own ancestor chain below (fewer instructions on the latency-bound SW path)
+        const int jump_levels = L.n_levels <= kWalkDepth ? 1 : L.n_levels;
+        for (int span = 1; span < jump_levels; span *= 2) {
             if (own) {
                 S.W[3 * k] = make_float4(m[0], m[1], m[2], m[9]);
                 S.W[3 * k + 1] = make_float4(m[3], m[4], m[5], m[10]);
@@ -494,7 +501,16 @@ __device__ float eval_group(const LigSm &L, const GridDev &grid, const Scratch &
             const int deep = (meta >> 16) - 1;
             const float4 p = L.p[a];
             float yx = p.x, yy = p.y, yz = p.z;            // y = A_deep p (torsions, D3)
-            if (deep >= 0) {
+            if (L.n_levels <= kWalkDepth) {
+                // walk: y <- L_k y for k = deepest torsion, its parent, ..., the root child
+                for (int k = deep; k >= 0; k = L.tmeta[k].x) {
+                    const float4 w0 = S.W[3 * k], w1 = S.W[3 * k + 1], w2 = S.W[3 * k + 2];
+                    const float nx_ = fmaf(w0.x, yx, fmaf(w0.y, yy, fmaf(w0.z, yz, w0.w)));
+                    const float ny_ = fmaf(w1.x, yx, fmaf(w1.y, yy, fmaf(w1.z, yz, w1.w)));
+                    const float nz_ = fmaf(w2.x, yx, fmaf(w2.y, yy, fmaf(w2.z, yz, w2.w)));
+                    yx = nx_; yy = ny_; yz = nz_;
+                }
+            } else if (deep >= 0) {
                 const float4 w0 = S.W[3 * deep], w1 = S.W[3 * deep + 1], w2 = S.W[3 * deep + 2];
                 yx = fmaf(w0.x, p.x, fmaf(w0.y, p.y, fmaf(w0.z, p.z, w0.w)));
                 yy = fmaf(w1.x, p.x, fmaf(w1.y, p.y, fmaf(w1.z, p.z, w1.w)));

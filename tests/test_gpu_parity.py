@@ -509,7 +509,9 @@ def test_max_size_ligand_parity_and_run(dock):
     P = oracle.Problem(grid, lig)
     assert d.N == 256 and d.T == 32 and d.P > 25000
     X = random_genotypes(grid, d.T, 24, seed=4, frac_out=0.0, shrink=0.02)
-    X[:, 6:] *= 0.05
+    # small torsions only: an 89 Å helix bent by 32 large torsions leaves the box, and the
+    # 1e5 kcal/mol/Å out-of-grid slope turns FP32 pose rounding into > 1e-4 relative energy
+    X[:, 6:] = 0.02 * np.sin(np.arange(X.shape[0] * d.T).reshape(X.shape[0], d.T))
     E, Gd, xyz = d.eval(X, grad=True, xyz=True)
     E0, _, _ = d.eval(X, grad=False)
     for i in range(X.shape[0]):
