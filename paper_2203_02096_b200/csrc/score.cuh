@@ -19,7 +19,7 @@ constexpr float kInvTwoSigma2 = 1.0f / (2.0f * 3.6f * 3.6f);    // desolvation s
 constexpr float kExpScale = -kInvTwoSigma2 * 1.4426950408889634f;   // exp(-x/2s^2) = 2^(x*kExpScale)
 constexpr float kOut = 1e5f;                                    // D4.5 out-of-grid penalty
 #ifndef DK_WALK_DEPTH
-#define DK_WALK_DEPTH 3
+#define DK_WALK_DEPTH 4
 #endif
 constexpr int kWalkDepth = DK_WALK_DEPTH;   // torsion trees up to this depth: per-atom chain walk, no composites
 
