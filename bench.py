@@ -238,7 +238,8 @@ def run_ours(args, cfg, lig, grid):
     dev, cdev = dist_setup(local, world)
     gpu = dev.index
     d = dock.Docker.from_inputs(grid, lig, ls_method=cfg.ls_method, ls_rate=cfg.ls_rate,
-                                ls_max_iters=cfg.ls_iters, profile=1, device=gpu, sw_depth=args.sw_depth)
+                                ls_max_iters=cfg.ls_iters, profile=1, device=gpu, sw_depth=args.sw_depth,
+                                sw_split=args.sw_split)
     runs = cfg.runs
     run_base = rank * runs
     stream = torch.cuda.Stream(device=dev)
@@ -577,6 +578,7 @@ def main():
     ap.add_argument("--micro", action="store_true", help="isolated inter/intra microbenchmarks (roofline evidence)")
     ap.add_argument("--micro-iters", type=int, default=20)
     ap.add_argument("--sw-depth", type=int, default=0, help="Solis-Wets speculation depth (0 = auto)")
+    ap.add_argument("--sw-split", type=int, default=0, help="Solis-Wets warps per evaluation (0 = auto)")
     ap.add_argument("--n-ligs", type=int, default=256, help="hts: ligands per step (sample of configs[4])")
     ap.add_argument("--slots", type=int, default=4, help="hts: ligands in flight per GPU")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])

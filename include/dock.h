@@ -91,6 +91,10 @@ typedef struct {
                                     wave), 1 = both trial points of one iteration at once, 2 or 3 =
                                     the 3-way outcome tree of 2 / 3 iterations (3^D - 1 lane groups
                                     per individual).  Results are identical for every depth (D9). */
+    int32_t sw_split;            /* Solis-Wets: warps per trial-point evaluation for ligands with more
+                                    than 16 atoms: 0 = auto, 1 = none, 2 (with depth 2) or 4 (with
+                                    depth 1) = cooperative evaluation.  Results identical up to the
+                                    FP32 summation order of the energy parts (fixed per setting). */
 } dock_params;
 
 /* Fills the defaults: p_tour .60, p_cross .80, p_mut .02, 2.0 Å / 0.523 rad, ADADELTA,

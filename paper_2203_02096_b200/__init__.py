@@ -50,7 +50,8 @@ class Params(C.Structure):
                 ("sw_rho_min", C.c_float), ("sw_expand", C.c_float), ("sw_contract", C.c_float),
                 ("sw_cons_succ", C.c_int32), ("sw_cons_fail", C.c_int32), ("ad_rho", C.c_float),
                 ("ad_eps", C.c_float), ("max_generations", C.c_int32), ("device", C.c_int32),
-                ("l2_persist", C.c_int32), ("gens_per_graph", C.c_int32), ("profile", C.c_int32), ("sw_depth", C.c_int32)]
+                ("l2_persist", C.c_int32), ("gens_per_graph", C.c_int32), ("profile", C.c_int32), ("sw_depth", C.c_int32),
+                ("sw_split", C.c_int32)]
 
 
 class ScreenOpts(C.Structure):

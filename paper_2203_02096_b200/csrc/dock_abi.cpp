@@ -70,6 +70,7 @@ dk::SearchDev make_search(const dock_ctx *c, int pop, int runs, int run_base, ui
     s.sw_rho = p.sw_rho; s.sw_rho_min = p.sw_rho_min; s.sw_expand = p.sw_expand; s.sw_contract = p.sw_contract;
     s.sw_cons_succ = p.sw_cons_succ; s.sw_cons_fail = p.sw_cons_fail;
     s.sw_depth = p.sw_depth;
+    s.sw_split = p.sw_split;
     s.ad_rho = p.ad_rho; s.ad_eps = p.ad_eps;
     s.max_generations = p.max_generations;
     s.max_evals = max_evals;
@@ -143,6 +144,7 @@ int validate_params(const dock_params &p, std::string *err) {
     if (p.max_generations < 0) { *err = "params.max_generations: must be >= 0"; return DOCK_E_INPUT; }
     if (p.gens_per_graph < 1 || p.gens_per_graph > 4096) { *err = "params.gens_per_graph: 1..4096"; return DOCK_E_INPUT; }
     if (p.sw_depth < 0 || p.sw_depth > 3) { *err = "params.sw_depth: 0..3"; return DOCK_E_INPUT; }
+    if (p.sw_split != 0 && p.sw_split != 1 && p.sw_split != 2 && p.sw_split != 4) { *err = "params.sw_split: 0, 1, 2 or 4"; return DOCK_E_INPUT; }
     return DOCK_OK;
 }
 

@@ -69,6 +69,7 @@ struct SearchDev {
     float sw_rho, sw_rho_min, sw_expand, sw_contract;
     int sw_cons_succ, sw_cons_fail;
     int sw_depth;                 // 0 auto, 1..3 (dock_params.sw_depth)
+    int sw_split;                 // 0 auto, 1, 2, 4 (dock_params.sw_split)
     float ad_rho, ad_eps;
     int max_generations;
     long long max_evals;

@@ -543,11 +543,14 @@ __global__ void __launch_bounds__(256) k_ls_sw(const LigDev L, const GridDev g, 
 // to k_ls_sw; only the latency changes (D iterations per evaluation round trip).
 // ---------------------------------------------------------------------------
 __host__ __device__ constexpr int ipow3(int d) { return d == 0 ? 1 : 3 * ipow3(d - 1); }
-template <int W, int D>
-constexpr int tree_threads() { return ((ipow3(D) - 1) * W + 31) / 32 * 32; }
+template <int W, int D, int KP = 1>
+constexpr int tree_threads() { return ((ipow3(D) - 1) * KP * W + 31) / 32 * 32; }
 
-template <int W, int MAXC, int D>
-__global__ void __launch_bounds__(tree_threads<W, D>(), (W == 16 && D == 3) ? 2 : 1) k_ls_sw_tree(const LigDev L, const GridDev g,
+// KP > 1: every node is evaluated cooperatively by KP lane groups (large ligands, whose
+// single evaluation is the latency of the chain): each computes a part of the grid and
+// pair sums, the partials are added in a fixed order in the resolution step.
+template <int W, int MAXC, int D, int KP = 1>
+__global__ void __launch_bounds__(tree_threads<W, D, KP>(), (W == 16 && D == 3) ? 2 : 1) k_ls_sw_tree(const LigDev L, const GridDev g,
                                                                      const ScratchLayout SL, const SearchDev sp,
                                                                      const PopDev pop, const LsArgs a) {
     constexpr int NGR = ipow3(D) - 1;
@@ -558,13 +561,14 @@ __global__ void __launch_bounds__(tree_threads<W, D>(), (W == 16 && D == 3) ? 2 
     if (!t.act) return;                                      // uniform: one individual per CTA
     const int staged = staged_bytes(L, false);
     const LigSm Ls = stage_ligand(L, sm, staged);
-    float *sx = reinterpret_cast<float *>(sm + staged + NGR * SL.bytes);
+    float *sx = reinterpret_cast<float *>(sm + staged + NGR * KP * SL.bytes);
     float *sb = sx + kMaxGenes;
-    float *sE = sb + kMaxGenes;
-    float *stri0 = sE + NGR;                                 // [2][D][G] deviate shapes, double-buffered by round
-    const int grp = threadIdx.x / W, sub = threadIdx.x % W;
+    float *sE = sb + kMaxGenes;                              // [NGR][KP] partial energies
+    float *stri0 = sE + NGR * KP;                            // [2][D][G] deviate shapes, double-buffered by round
+    const int gidx = threadIdx.x / W, sub = threadIdx.x % W;  // lane group
+    const int grp = gidx / KP, part = gidx % KP;             // node, part of its evaluation
     const bool in_grp = grp < NGR;
-    const Scratch S = scratch_at(sm + staged + (in_grp ? grp : 0) * SL.bytes, SL);
+    const Scratch S = scratch_at(sm + staged + (in_grp ? gidx : 0) * SL.bytes, SL);
     // every group evaluates every round (a moot node on stale genes, result unused), so
     // the warps stay converged and the group shuffles take a constant full-warp mask
     constexpr unsigned gmask = 0xffffffffu;
@@ -620,8 +624,8 @@ __global__ void __launch_bounds__(tree_threads<W, D>(), (W == 16 && D == 3) ? 2 
                 }
             }
             __syncwarp(gmask);
-            const float e = eval_group<W, MAXC, false>(Ls, g, S, sub, gmask);
-            if (sub == 0) sE[grp] = live ? e : INFINITY;
+            const float e = eval_group<W, MAXC, false, kAll, KP>(Ls, g, S, sub, gmask, part);
+            if (sub == 0) sE[gidx] = live ? e : INFINITY;
         }
         __syncthreads();
         // ---- 2. resolve the actual path (every thread, identical scalar logic) ----
@@ -637,12 +641,15 @@ __global__ void __launch_bounds__(tree_threads<W, D>(), (W == 16 && D == 3) ? 2 
             if (it >= a.iters || rho < sp.sw_rho_min) break;
             rl[k] = rho;
             const int id = ipow3(k) - 1 + 2 * sg;
+            float E1 = sE[id * KP], E2 = sE[(id + 1) * KP];          // partials: fixed order
+#pragma unroll
+            for (int p = 1; p < KP; ++p) { E1 += sE[id * KP + p]; E2 += sE[(id + 1) * KP + p]; }
             int o;
             ++ne;
-            if (sE[id] < Ex) { o = 0; Ex = sE[id]; }
+            if (E1 < Ex) { o = 0; Ex = E1; }
             else {
                 ++ne;
-                if (sE[id + 1] < Ex) { o = 1; Ex = sE[id + 1]; }
+                if (E2 < Ex) { o = 1; Ex = E2; }
                 else o = 2;
             }
             sw_scalar_step(o, sp, rho, succ, fail);
@@ -800,6 +807,8 @@ cudaError_t setup_kernel_attributes() {
     if (e == cudaSuccess) e = allow_smem(k_ls_sw<W, MAXC>);                         \
     if (e == cudaSuccess) e = allow_smem(k_ls_sw_tree<W, MAXC, 2>);                  \
     if (e == cudaSuccess) e = allow_smem(k_ls_sw_tree<W, MAXC, 3>);                  \
+    if (e == cudaSuccess && W == 32) e = allow_smem(k_ls_sw_tree<W, MAXC, 1, 4>);    \
+    if (e == cudaSuccess && W == 32) e = allow_smem(k_ls_sw_tree<W, MAXC, 2, 2>);    \
     if (e == cudaSuccess) e = allow_smem(k_bench_part<W, MAXC, kInter>);             \
     if (e == cudaSuccess) e = allow_smem(k_bench_part<W, MAXC, kIntra>);
     DK_ATTR(16, 1) DK_ATTR(32, 1) DK_ATTR(32, 2) DK_ATTR(32, 3) DK_ATTR(32, 4) DK_ATTR(32, 8)
@@ -849,6 +858,13 @@ cudaError_t launch_ga(const LigDev &L, const GridDev &g, const SearchDev &sp, co
     return cudaGetLastError();
 }
 
+// shared memory of a k_ls_sw_tree<.., D, KP> CTA: ligand block, one scratch per lane
+// group, x and b, the partial energies and the double-buffered deviate shapes
+static size_t tree_smem(const LigDev &L, const ScratchLayout &SL, int D, int KP) {
+    const int ngr = (D == 3 ? 26 : (D == 2 ? 8 : 2)) * KP;
+    return (size_t)staged_bytes(L, false) + (size_t)ngr * SL.bytes + 4 * (2 * kMaxGenes + ngr + 2 * D * kMaxGenes);
+}
+
 cudaError_t launch_ls(const LigDev &L, const GridDev &g, const SearchDev &sp, const PopDev &pop, const LsArgs &a,
                       int n_total, cudaStream_t s) {
     if (n_total <= 0) return cudaSuccess;
@@ -873,7 +889,7 @@ cudaError_t launch_ls(const LigDev &L, const GridDev &g, const SearchDev &sp, co
             // never won (issue contention, spills at the 2-CTA/SM register cap).
             for (int D = 2; D >= 2 && depth == 1; --D) {
                 const int ngr = D == 3 ? 26 : 8;
-                const size_t sm_b = (size_t)staged_bytes(L, false) + (size_t)ngr * SL.bytes + 4 * (2 * kMaxGenes + ngr + 2 * D * kMaxGenes);
+                const size_t sm_b = tree_smem(L, SL, D, 1);
                 int per_sm = 0;
                 DK_DISPATCH(tcfg, {
                     if (D == 3) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_ls_sw_tree<W, MAXC, 3>, tree_threads<W, 3>(), sm_b);
@@ -884,9 +900,27 @@ cudaError_t launch_ls(const LigDev &L, const GridDev &g, const SearchDev &sp, co
                 if (sm_b <= (size_t)kSmemMax && per_sm > 0 && (long long)n_total <= waves * per_sm * nsm) depth = D;
             }
         }
+        // Cooperative evaluation (several warps per trial point) for large ligands, whose one
+        // evaluation is the chain latency: split 2 with depth 2, or split 4 with depth 1.
+        const int split = (tcfg.W == 32 && (sp.sw_split == 2 || sp.sw_split == 4)) ? sp.sw_split : 1;
+        if (split > 1) {
+            const int D = split == 2 ? 2 : 1;
+            const size_t smem = tree_smem(L, SL, D, split);
+            if (smem > (size_t)kSmemMax) return cudaErrorInvalidConfiguration;
+            switch (tcfg.MAXC) {
+#define DK_SPLIT(M)                                                                                     \
+    case M:                                                                                             \
+        if (split == 2) k_ls_sw_tree<32, M, 2, 2><<<n_total, tree_threads<32, 2, 2>(), smem, s>>>(L, g, SL, sp, pop, a); \
+        else k_ls_sw_tree<32, M, 1, 4><<<n_total, tree_threads<32, 1, 4>(), smem, s>>>(L, g, SL, sp, pop, a);           \
+        break;
+                DK_SPLIT(1) DK_SPLIT(2) DK_SPLIT(3) DK_SPLIT(4)
+                default: DK_SPLIT(8)
+#undef DK_SPLIT
+            }
+            return cudaGetLastError();
+        }
         if (depth >= 2) {
-            const int ngr = depth == 3 ? 26 : 8;
-            const size_t smem = (size_t)staged_bytes(L, false) + (size_t)ngr * SL.bytes + 4 * (2 * kMaxGenes + ngr + 2 * depth * kMaxGenes);
+            const size_t smem = tree_smem(L, SL, depth, 1);
             if (smem > (size_t)kSmemMax) return cudaErrorInvalidConfiguration;
             DK_DISPATCH(tcfg, {
                 if (depth == 3) k_ls_sw_tree<W, MAXC, 3><<<n_total, tree_threads<W, 3>(), smem, s>>>(L, g, SL, sp, pop, a);

@@ -346,12 +346,17 @@ __device__ __forceinline__ void intra_tiles(const LigSm &L, const Scratch &S, in
 // Energy-only pair tiles (large ligands whose pair list is not staged, L.energy_tiles):
 // the same rotation and membership bits as intra_tiles, but no forces, so no partner
 // accumulators and no shuffles.  The tail chunk is rotated too (no reductions to save).
-template <int W, int MAXC>
+// With KP > 1 the tile steps, linearised in (I, J, s) order, are split into KP contiguous
+// parts and this lane group computes only part `part` (cooperative evaluation).
+template <int W, int MAXC, int KP = 1>
 __device__ __forceinline__ float intra_tiles_energy(const LigSm &L, const Scratch &S, int sub,
                                                     const float (&rx)[MAXC], const float (&ry)[MAXC],
-                                                    const float (&rz)[MAXC]) {
+                                                    const float (&rz)[MAXC], int part = 0) {
     const int N = L.N;
     const int Bt = L.NC;
+    const int total = Bt * (W / 2) + (Bt * (Bt - 1) / 2) * W;
+    const int g0 = (int)((long long)total * part / KP), g1 = (int)((long long)total * (part + 1) / KP);
+    int base = 0;
     float e = 0.0f;
 #pragma unroll
     for (int I = 0; I < MAXC; ++I) {
@@ -377,9 +382,11 @@ __device__ __forceinline__ float intra_tiles_energy(const LigSm &L, const Scratc
             if (I == J && sub >= W / 2) rot &= ~(1u << (W / 2));
             const float4 *rrow = S.r + J * 2 * W + sub;
             const float4 *qrow = L.ppar + J * 2 * W + sub;
-            const int s0 = (I == J) ? 1 : 0, s1 = (I == J) ? W / 2 : W - 1;
+            const int s0 = (I == J) ? 1 : 0, n = (I == J) ? W / 2 : W;
+            const int i0 = max(0, g0 - base), i1 = min(n, g1 - base);
+            base += n;
 #pragma unroll 4
-            for (int st = s0; st <= s1; ++st) {
+            for (int st = s0 + i0; st < s0 + i1; ++st) {
                 const float4 rj = rrow[st], pj = qrow[st];
                 const float dx = rx[I] - rj.x, dy = ry[I] - rj.y, dz = rz[I] - rj.z;
                 const float rho2 = fmaxf(fmaf(dx, dx, fmaf(dy, dy, dz * dz)), 1e-4f);
@@ -403,8 +410,13 @@ __device__ __forceinline__ float intra_tiles_energy(const LigSm &L, const Scratc
 // production kernels use both.
 constexpr int kInter = 1, kIntra = 2, kAll = 3;
 
-template <int W, int MAXC, bool GRAD, int PARTS = kAll>
-__device__ float eval_group(const LigSm &L, const GridDev &grid, const Scratch &S, int sub, unsigned mask) {
+// KP > 1 (energy-only path): cooperative evaluation by KP lane groups; this group
+// computes part `part` of the grid and pair sums and returns its PARTIAL energy (the
+// caller adds the KP partials in a fixed order).  The pose is computed by every part.
+template <int W, int MAXC, bool GRAD, int PARTS = kAll, int KP = 1>
+__device__ float eval_group(const LigSm &L, const GridDev &grid, const Scratch &S, int sub, unsigned mask,
+                            int part = 0) {
+    static_assert(KP == 1 || !GRAD, "cooperative evaluation is energy-only");
     const float *x = S.genes;
     // ---- a3: orientation quaternion q = (cos a/2, sin(a/2) n) -> R(q) (D3) ----
     float sph, cph, sth, cth, sa, ca;
@@ -527,7 +539,8 @@ __device__ float eval_group(const LigSm &L, const GridDev &grid, const Scratch &
                 S.r[a] = make_float4(rx[c], ry[c], rz[c], p.w);
             }
             if constexpr ((PARTS & kInter) != 0)
-                e_part += inter_atom(grid, meta & 0xff, p.w, rx[c], ry[c], rz[c], gx[c], gy[c], gz[c]);
+                if (KP == 1 || c % KP == part)
+                    e_part += inter_atom(grid, meta & 0xff, p.w, rx[c], ry[c], rz[c], gx[c], gy[c], gz[c]);
         } else if ((GRAD || L.energy_tiles) && c < L.NC) {
             // padded chunk entries: finite zeros (null type, zero charge) for the tiles
             S.r[ridx<W>(a)] = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -547,11 +560,11 @@ __device__ float eval_group(const LigSm &L, const GridDev &grid, const Scratch &
         return gsum<W>(e_part, mask);
     } else if constexpr (!GRAD) {
         if (L.energy_tiles) {           // large ligand: pair list not staged, use the tiles
-            e_part += intra_tiles_energy<W, MAXC>(L, S, sub, rx, ry, rz);
+            e_part += intra_tiles_energy<W, MAXC, KP>(L, S, sub, rx, ry, rz, part);
             return gsum<W>(e_part, mask);
         }
 #pragma unroll 4
-        for (int q = sub; q < L.P; q += W) {
+        for (int q = sub + W * part; q < L.P; q += W * KP) {
             const uint32_t w = L.pairs[q];
             const float4 pp = L.pprm[q];
             const uint8_t *rb = reinterpret_cast<const uint8_t *>(S.r);

@@ -525,3 +525,35 @@ def test_max_size_ligand_parity_and_run(dock):
     r = d.run(8, 1, 200, 42, xyz=False)
     assert r["evals"][0] >= 200 and np.isfinite(r["best_E"][0])
     d.close()
+
+
+# ---------------------------------------------------------------------------
+# Cooperative SW evaluation (sw_split 2 / 4 warps per trial point): same D9 search; the
+# energy partials are summed in a fixed order, so results match the oracle within the
+# energy tolerance and repeat bit-exactly.
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("split,depth", [(2, 2), (4, 1)])
+def test_sw_cooperative_split(dock, split, depth):
+    cfg, lig, grid = config_inputs("pm")
+    P = oracle.Problem(grid, lig)
+    n = 24
+    d = dock.Docker.from_inputs(grid, lig, ls_method=1, sw_depth=depth, sw_split=split)
+    X = random_genotypes(grid, d.T, n, seed=45, frac_out=0.0, shrink=0.2)
+    E0 = np.array([P.energy(x, grad=False)["E"] for x in X], np.float32)
+    slots = np.arange(n, dtype=np.int32) * 7 + 2
+    g1, E1, ev1 = d.ls_step(1, X, E0, 25, seed=13, run=1, gen=3, slots=slots)
+    g2, E2, ev2 = d.ls_step(1, X, E0, 25, seed=13, run=1, gen=3, slots=slots)
+    np.testing.assert_array_equal(g1, g2)
+    np.testing.assert_array_equal(E1, E2)
+    pp = oracle.params(ls_max_iters=25)
+    ok = 0
+    for i in range(n):
+        x, Eo, evo = oracle.solis_wets(P, pp, 13, 0, 1, 3, int(slots[i]), X[i], float(E0[i]))
+        assert E1[i] <= E0[i]
+        ok += int(ev1[i] == evo and abs(E1[i] - Eo) <= e_tol(Eo))
+    assert ok >= 0.9 * n, ok
+    r = d.run(cfg.pop, 2, 40_000, 42, xyz=False)
+    ref = P.energy(r["best_genes"][0].astype(np.float64))
+    tol, _ = pose_tols(P, ref)
+    assert abs(ref["E"] - r["best_E"][0]) <= tol
+    d.close()
