@@ -490,7 +490,23 @@ __global__ void __launch_bounds__(256) k_ls_sw(const LigDev L, const GridDev g, 
             E1 = __shfl_sync(0xffffffffu, e, 0);
             E2 = __shfl_sync(0xffffffffu, e, W);
         } else {
-            E1 = eval_group<W, MAXC, false>(Ls, g, S0, sub, gmask);
+            // x+b+d, then x-b-d only if the first failed: one evaluation call site (the
+            // kernel's instruction footprint matters at one warp per SM)
+            E1 = INFINITY;
+            for (int trial = 0; trial < 2; ++trial) {
+                if (trial == 1) {
+                    if (E1 < Ex) break;
+                    __syncwarp();
+#pragma unroll
+                    for (int s = 0; s < NSET; ++s) {
+                        const int j = lane + 32 * s;
+                        if (j < G) S0.genes[j] = c2[s];
+                    }
+                    __syncwarp();
+                }
+                const float e = eval_group<W, MAXC, false>(Ls, g, S0, sub, gmask);
+                if (trial == 0) E1 = e; else E2 = e;
+            }
         }
         ++ne;
         if (E1 < Ex) {
@@ -499,16 +515,6 @@ __global__ void __launch_bounds__(256) k_ls_sw(const LigDev L, const GridDev g, 
             Ex = E1;
             sw_scalar_step(0, sp, rho, succ, fail);
         } else {
-            if (NG == 1) {
-                __syncwarp();
-#pragma unroll
-                for (int s = 0; s < NSET; ++s) {
-                    const int j = lane + 32 * s;
-                    if (j < G) S0.genes[j] = c2[s];
-                }
-                __syncwarp();
-                E2 = eval_group<W, MAXC, false>(Ls, g, S0, sub, gmask);
-            }
             ++ne;
             if (E2 < Ex) {
 #pragma unroll
@@ -796,6 +802,16 @@ static cudaError_t allow_smem(K kernel) {
     return cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemMax);
 }
 
+// cooperative SW trees exist for 32-lane groups only
+template <int W, int MAXC>
+static cudaError_t allow_split() {
+    if constexpr (W == 32) {
+        cudaError_t e = allow_smem(k_ls_sw_tree<W, MAXC, 1, 4>);
+        return e == cudaSuccess ? allow_smem(k_ls_sw_tree<W, MAXC, 2, 2>) : e;
+    }
+    return cudaSuccess;
+}
+
 cudaError_t setup_kernel_attributes() {
     cudaError_t e = cudaSuccess;
 #define DK_ATTR(W, MAXC)                                                             \
@@ -807,8 +823,7 @@ cudaError_t setup_kernel_attributes() {
     if (e == cudaSuccess) e = allow_smem(k_ls_sw<W, MAXC>);                         \
     if (e == cudaSuccess) e = allow_smem(k_ls_sw_tree<W, MAXC, 2>);                  \
     if (e == cudaSuccess) e = allow_smem(k_ls_sw_tree<W, MAXC, 3>);                  \
-    if (e == cudaSuccess && W == 32) e = allow_smem(k_ls_sw_tree<W, MAXC, 1, 4>);    \
-    if (e == cudaSuccess && W == 32) e = allow_smem(k_ls_sw_tree<W, MAXC, 2, 2>);    \
+    if (e == cudaSuccess) e = allow_split<W, MAXC>();                                 \
     if (e == cudaSuccess) e = allow_smem(k_bench_part<W, MAXC, kInter>);             \
     if (e == cudaSuccess) e = allow_smem(k_bench_part<W, MAXC, kIntra>);
     DK_ATTR(16, 1) DK_ATTR(32, 1) DK_ATTR(32, 2) DK_ATTR(32, 3) DK_ATTR(32, 4) DK_ATTR(32, 8)
@@ -902,7 +917,11 @@ cudaError_t launch_ls(const LigDev &L, const GridDev &g, const SearchDev &sp, co
         }
         // Cooperative evaluation (several warps per trial point) for large ligands, whose one
         // evaluation is the chain latency: split 2 with depth 2, or split 4 with depth 1.
-        const int split = (tcfg.W == 32 && (sp.sw_split == 2 || sp.sw_split == 4)) ? sp.sw_split : 1;
+        // Measured (profiles/next1): PL (P = 5,358) 4 warps x depth 1 beats depth 2 by 1.27x
+        // (10 runs) and 1.24x (100 runs); PM (P ~ 700) is best without splitting.
+        int split = sp.sw_split;
+        if (split == 0) split = (L.P >= 2000 && sp.sw_depth == 0) ? 4 : 1;
+        if (tcfg.W != 32 || (split != 2 && split != 4)) split = 1;
         if (split > 1) {
             const int D = split == 2 ? 2 : 1;
             const size_t smem = tree_smem(L, SL, D, split);

@@ -224,6 +224,7 @@ int prepare_ligand(const dock_ligand *l, const dock_type_param *tp, int n_types,
     // fits comfortably in shared memory; beyond that (P > ~4,900, e.g. N >= ~110) they use
     // the pair tiles like the gradient kernels, and the list is not stored at all.
     L.energy_tiles = (20 * P > 96 * 1024) ? 1 : 0;
+    if (L.energy_tiles && N <= 96) return fail("internal: energy tiles need N > 96");   // see score.cuh
     const int Ps = L.energy_tiles ? 0 : P;
     L.off_pairs = off; off += a16(4 * Ps);
     L.off_pprm = off; off += 16 * Ps;

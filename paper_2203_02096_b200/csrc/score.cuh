@@ -559,9 +559,15 @@ __device__ float eval_group(const LigSm &L, const GridDev &grid, const Scratch &
         }
         return gsum<W>(e_part, mask);
     } else if constexpr (!GRAD) {
-        if (L.energy_tiles) {           // large ligand: pair list not staged, use the tiles
-            e_part += intra_tiles_energy<W, MAXC, KP>(L, S, sub, rx, ry, rz, part);
-            return gsum<W>(e_part, mask);
+        // large ligand (pair list not staged): the tiles.  Only MAXC >= 4 (N > 96) can need
+        // them -- N <= 96 gives P <= 4,560 pairs, 91 KB of list, under the 96 KB limit -- so
+        // smaller instantiations do not carry this code (instruction-cache footprint of
+        // the latency-bound SW kernels: measured 0.8x on PM when it was always compiled in).
+        if constexpr (MAXC >= 4) {
+            if (L.energy_tiles) {
+                e_part += intra_tiles_energy<W, MAXC, KP>(L, S, sub, rx, ry, rz, part);
+                return gsum<W>(e_part, mask);
+            }
         }
 #pragma unroll 4
         for (int q = sub + W * part; q < L.P; q += W * KP) {
