@@ -43,6 +43,17 @@ struct LigDev {
     int Wg;           // lanes per group of the gradient kernels (16 if N <= 16, else 32)
     int NC;           // chunks = ceil(N / Wg)
     int energy_tiles; // 1: energy-only kernels also use the pair tiles (pair list too large to stage)
+    int tail_rot;     // 1: the partial last chunk is rotated as a padded chunk, 0: broadcast
+    // Gradient-path pair-slot tables (slot_mode = 1, small and mid-size ligands): every
+    // (tile, step, lane) of intra_tiles and every (tail atom, chunk, lane) of the broadcast
+    // tail gets its D5 pair constants precomputed in double on the host --
+    // {r_eq^2, A, B (sign = 12-10 H-bond form), S_iV_j + S_jV_i} and 332.06363/4 q_i q_j,
+    // all zero for a non-pair -- so the pair loop neither combines per-atom parameters nor
+    // tests membership bits.  Consecutive lanes read consecutive 16-byte slots.
+    int slot_mode;
+    int off_slot4;    // float4[n_slots]
+    int off_slotq;    // float[n_slots]
+    int n_slots;
     int off_ppar;     // float4[NC][2*Wg] partner params {R/2, sqrt(eps), S, V}, duplicated chunks;
                       //   R/2 negated for acceptors and sqrt(eps) negated for donors (role
                       //   in the sign bits; magnitudes via free |.| operand modifiers)

@@ -77,6 +77,10 @@ __device__ __forceinline__ LigSm stage_ligand(const LigDev &L, uint8_t *sm, int 
     v.mask = reinterpret_cast<const uint32_t *>(sm + L.off_mask);
     v.ppar = reinterpret_cast<const float4 *>(sm + L.off_ppar);
     v.NC = L.NC;
+    v.tail_rot = L.tail_rot;
+    v.slot_mode = L.slot_mode;
+    v.slot4 = reinterpret_cast<const float4 *>(sm + L.off_slot4);
+    v.slotq = reinterpret_cast<const float *>(sm + L.off_slotq);
     v.energy_tiles = L.energy_tiles;
     return v;
 }

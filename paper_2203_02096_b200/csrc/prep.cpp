@@ -219,6 +219,16 @@ int prepare_ligand(const dock_ligand *l, const dock_type_param *tp, int n_types,
     L.Wg = N <= 16 ? 16 : 32;
     L.NC = (N + L.Wg - 1) / L.Wg;
     L.off_ppar = off; off += 16 * L.NC * 2 * L.Wg;
+    // tile schedule of the gradient path (must match score.cuh intra_tiles)
+    const int Wg = L.Wg, Bf = N / Wg, tail = N - Bf * Wg;
+    L.tail_rot = (tail > 0 && (Wg / 2 + Bf * Wg) * 40 < tail * ((Bf + 1) * 40 + 3 * 5)) ? 1 : 0;
+    const int Bt = Bf + L.tail_rot;
+    const int tile_steps = Bt * (Wg / 2) + (Bt * (Bt - 1) / 2) * Wg;
+    const int bcast_slots = (tail > 0 && !L.tail_rot) ? tail * (Bf + 1) * Wg : 0;
+    L.n_slots = tile_steps * Wg + bcast_slots;
+    L.slot_mode = (20 * L.n_slots <= 64 * 1024) ? 1 : 0;      // beyond: per-atom params + bits
+    L.off_slot4 = off; off += L.slot_mode ? 16 * L.n_slots : 0;
+    L.off_slotq = off; off += L.slot_mode ? a16(4 * L.n_slots) : 0;
     L.grad_bytes = off;              // the gradient kernels stage only up to here
     // Energy-only kernels stage the pair list + per-pair constants (20 B per pair) when it
     // fits comfortably in shared memory; beyond that (P > ~4,900, e.g. N >= ~110) they use
@@ -291,6 +301,46 @@ int prepare_ligand(const dock_ligand *l, const dock_type_param *tp, int n_types,
         const int ri = role_of(i), rj = role_of(j);
         return (ri == 1 && rj == 2) || (ri == 2 && rj == 1);
     };
+    if (L.slot_mode) {
+        // pair-slot tables in the exact order intra_tiles visits them (DFS positions)
+        std::vector<uint8_t> is_pair((size_t)N * N, 0);
+        for (size_t q = 0; q + 1 < pairs.size(); q += 2) {
+            const int di = pos[pairs[q]], dj = pos[pairs[q + 1]];
+            is_pair[(size_t)di * N + dj] = is_pair[(size_t)dj * N + di] = 1;
+        }
+        float4 *s4 = reinterpret_cast<float4 *>(bl + L.off_slot4);
+        float *sq = reinterpret_cast<float *>(bl + L.off_slotq);
+        auto fill = [&](int slot, int da, int db, bool on) {
+            s4[slot] = make_float4(0.f, 0.f, 0.f, 0.f);
+            sq[slot] = 0.f;
+            if (!on || da >= N || db >= N || !is_pair[(size_t)da * N + db]) return;
+            const int ia = order[da], ib = order[db];
+            const dock_type_param &ta = tp[l->type[ia]], &tb = tp[l->type[ib]];
+            const double req = 0.5 * ((double)ta.R + (double)tb.R);
+            const double eps = std::sqrt((double)ta.eps * (double)tb.eps);
+            const bool hb = hb_of(ia, ib);
+            s4[slot] = make_float4((float)(req * req), (float)((hb ? 5.0 : 1.0) * eps),
+                                   hb ? -(float)(6.0 * eps) : (float)(2.0 * eps),
+                                   (float)((double)ta.S * tb.V + (double)tb.S * ta.V));
+            sq[slot] = (float)(332.06363 / 4.0 * (double)l->charge[ia] * (double)l->charge[ib]);
+        };
+        int slot = 0;
+        for (int I = 0; I < Bt; ++I)
+            for (int J = I; J < Bt; ++J) {
+                const int s0 = (I == J) ? 1 : 0, s1 = (I == J) ? Wg / 2 : Wg - 1;
+                for (int st = s0; st <= s1; ++st)
+                    for (int ln = 0; ln < Wg; ++ln, ++slot) {
+                        const bool once = !(I == J && st == Wg / 2 && ln >= Wg / 2);
+                        fill(slot, I * Wg + ln, J * Wg + ((ln + st) & (Wg - 1)), once);
+                    }
+            }
+        if (tail > 0 && !L.tail_rot)
+            for (int k = 0; k < tail; ++k)
+                for (int I = 0; I <= Bf; ++I)
+                    for (int ln = 0; ln < Wg; ++ln, ++slot)
+                        fill(slot, I * Wg + ln, Bf * Wg + k, I < Bf || ln < k);
+        if (slot != L.n_slots) return fail("internal: pair-slot count mismatch");
+    }
     uint32_t *bpairs = reinterpret_cast<uint32_t *>(bl + L.off_pairs);
     float4 *pprm = reinterpret_cast<float4 *>(bl + L.off_pprm);
     uint32_t *bmask = reinterpret_cast<uint32_t *>(bl + L.off_mask);

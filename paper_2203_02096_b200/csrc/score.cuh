@@ -36,7 +36,9 @@ struct LigSm {
     const float4 *pprm;           // per pair: r_eq^2, eps_ij, S_iV_j+S_jV_i, 332.06363/4 q_i q_j
     const uint32_t *mask;         // [N][NW] pair-membership bit rows
     const float4 *ppar;           // [NC][2W] signed partner params (duplicated chunks)
-    int NC;
+    const float4 *slot4;          // pair-slot constants {r_eq^2, A, B, SV} (slot_mode)
+    const float *slotq;           // pair-slot 332.06363/4 q_i q_j (slot_mode)
+    int NC, tail_rot, slot_mode;
     int energy_tiles;             // energy-only evaluation through the pair tiles (no pair list)
 };
 
@@ -262,8 +264,8 @@ __device__ __forceinline__ void intra_tiles(const LigSm &L, const Scratch &S, in
                                             float (&gx)[MAXC], float (&gy)[MAXC], float (&gz)[MAXC], float &e) {
     const int N = L.N;
     const int Bf = N / W, t = N - Bf * W;
-    // cost model (issue slots): rotation of the tail as a padded chunk vs broadcast
-    const bool tail_rot = t > 0 && (W / 2 + Bf * W) * 40 < t * ((Bf + 1) * 40 + 3 * 5);
+    // tail as a padded rotated chunk vs broadcast: decided on the host (prep.cpp cost model)
+    const bool tail_rot = L.tail_rot != 0;
     const int Bt = Bf + (tail_rot ? 1 : 0);
     OwnPair own[MAXC];
     float hx[MAXC], hy[MAXC], hz[MAXC];   // pair-force sums (x 2 at the end)
@@ -330,6 +332,88 @@ __device__ __forceinline__ void intra_tiles(const LigSm &L, const Scratch &S, in
                 const int a = I * W + sub;
                 const bool on = (I < Bf || sub < k) && ((mrow[a >> 5] >> (a & 31)) & 1u);
                 tile_pair(on, rx[I], ry[I], rz[I], own[I], rj, pj, e, hx[I], hy[I], hz[I], fx, fy, fz);
+            }
+            fx = gsum<W>(fx, mask); fy = gsum<W>(fy, mask); fz = gsum<W>(fz, mask);
+#pragma unroll
+            for (int c = 0; c < MAXC; ++c)
+                if (c == Bf && sub == k) { hx[c] += fx; hy[c] += fy; hz[c] += fz; }
+        }
+    }
+#pragma unroll
+    for (int c = 0; c < MAXC; ++c) {
+        gx[c] = fmaf(2.0f, hx[c], gx[c]); gy[c] = fmaf(2.0f, hy[c], gy[c]); gz[c] = fmaf(2.0f, hz[c], gz[c]);
+    }
+}
+
+// One pair inside the slot-table tiles: constants c = {r_eq^2, A, B, SV} and qq from the
+// slot (all zero for a non-pair, so no membership test), force as in tile_pair.
+__device__ __forceinline__ void slot_pair(float rxi, float ryi, float rzi, float4 rj, float4 c, float qq, float &e,
+                                          float &gxi, float &gyi, float &gzi, float &fx, float &fy, float &fz) {
+    const float dx = rxi - rj.x, dy = ryi - rj.y, dz = rzi - rj.z;
+    const float rho2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
+    float dE;
+    e += pair_eg_ab(rho2, c.x, c.y, c.z, c.w, qq, dE);
+    gxi = fmaf(dE, dx, gxi); gyi = fmaf(dE, dy, gyi); gzi = fmaf(dE, dz, gzi);
+    fx = fmaf(-dE, dx, fx); fy = fmaf(-dE, dy, fy); fz = fmaf(-dE, dz, fz);
+}
+
+// intra_tiles with precomputed pair-slot constants (L.slot_mode, prep.cpp): the same
+// rotation / broadcast schedule and force bookkeeping, one 16-byte + one 4-byte
+// conflict-free shared-memory read per slot instead of partner params and pair bits.
+template <int W, int MAXC>
+__device__ __forceinline__ void intra_tiles_slots(const LigSm &L, const Scratch &S, int sub, unsigned mask,
+                                                  const float (&rx)[MAXC], const float (&ry)[MAXC],
+                                                  const float (&rz)[MAXC], float (&gx)[MAXC], float (&gy)[MAXC],
+                                                  float (&gz)[MAXC], float &e) {
+    const int N = L.N;
+    const int Bf = N / W, t = N - Bf * W;
+    const bool tail_rot = L.tail_rot != 0;
+    const int Bt = Bf + (tail_rot ? 1 : 0);
+    float hx[MAXC], hy[MAXC], hz[MAXC];
+#pragma unroll
+    for (int c = 0; c < MAXC; ++c) hx[c] = hy[c] = hz[c] = 0.0f;
+    int slot0 = 0;                        // first slot of the current tile
+#pragma unroll
+    for (int I = 0; I < MAXC; ++I) {
+        if (I >= Bt) break;
+#pragma unroll
+        for (int J = I; J < MAXC; ++J) {
+            if (J >= Bt) break;
+            const float4 *rrow = S.r + J * 2 * W + sub;         // partner of step s: rrow[s]
+            const int s0 = (I == J) ? 1 : 0, s1 = (I == J) ? W / 2 : W - 1;
+            const float4 *crow = L.slot4 + slot0 + sub - s0 * W;   // constants of step s: crow[s * W]
+            const float *qrow = L.slotq + slot0 + sub - s0 * W;
+            slot0 += (s1 - s0 + 1) * W;
+            float fx = 0.f, fy = 0.f, fz = 0.f;
+#pragma unroll 4
+            for (int s = s0; s <= s1; ++s) {
+                slot_pair(rx[I], ry[I], rz[I], rrow[s], crow[s * W], qrow[s * W], e, hx[I], hy[I], hz[I], fx, fy,
+                          fz);
+                if (s < s1) {
+                    const int src = (sub + 1) & (W - 1);
+                    fx = __shfl_sync(mask, fx, src, W);
+                    fy = __shfl_sync(mask, fy, src, W);
+                    fz = __shfl_sync(mask, fz, src, W);
+                }
+            }
+            const int back = (sub - s1) & (W - 1);
+            fx = __shfl_sync(mask, fx, back, W);
+            fy = __shfl_sync(mask, fy, back, W);
+            fz = __shfl_sync(mask, fz, back, W);
+            hx[J] += fx; hy[J] += fy; hz[J] += fz;
+        }
+    }
+    if (t > 0 && !tail_rot) {
+        for (int k = 0; k < t; ++k) {
+            const int j = Bf * W + k;                       // uniform: shared-memory broadcast
+            const float4 rj = S.r[ridx<W>(j)];
+            const int sk = slot0 + k * (Bf + 1) * W + sub;
+            float fx = 0.f, fy = 0.f, fz = 0.f;
+#pragma unroll
+            for (int I = 0; I < MAXC; ++I) {
+                if (I > Bf) break;
+                slot_pair(rx[I], ry[I], rz[I], rj, L.slot4[sk + I * W], L.slotq[sk + I * W], e, hx[I], hy[I], hz[I],
+                          fx, fy, fz);
             }
             fx = gsum<W>(fx, mask); fy = gsum<W>(fy, mask); fz = gsum<W>(fz, mask);
 #pragma unroll
@@ -581,7 +665,8 @@ __device__ float eval_group(const LigSm &L, const GridDev &grid, const Scratch &
         }
         return gsum<W>(e_part, mask);
     } else {
-        intra_tiles<W, MAXC>(L, S, sub, mask, rx, ry, rz, gx, gy, gz, e_part);
+        if (L.slot_mode) intra_tiles_slots<W, MAXC>(L, S, sub, mask, rx, ry, rz, gx, gy, gz, e_part);
+        else intra_tiles<W, MAXC>(L, S, sub, mask, rx, ry, rz, gx, gy, gz, e_part);
         if constexpr (PARTS == kIntra) {
             const float E = gsum<W>(e_part, mask);
 #pragma unroll
