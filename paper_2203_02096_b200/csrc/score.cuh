@@ -693,22 +693,39 @@ __device__ float eval_group(const LigSm &L, const GridDev &grid, const Scratch &
         sgx = gsum<W>(sgx, mask); sgy = gsum<W>(sgy, mask); sgz = gsum<W>(sgz, mask);
         Gx = gsum<W>(Gx, mask); Gy = gsum<W>(Gy, mask); Gz = gsum<W>(Gz, mask);
         __syncwarp(mask);
-        // torsions: dE/dtau_k = w_k . sum_{a in moved(k)} (r_a - r_{a_k}) x g_a
-        for (int k = sub; k < L.T; k += W) {
-            const int4 tm = L.tmeta[k];
-            const int lo = tm.w & 0xffff, hi = tm.w >> 16;
+        // torsions: dE/dtau_k = w_k . sum_{a in moved(k)} (r_a - r_{a_k}) x g_a.  The moved
+        // set is one DFS range [lo, hi); LPT = largest power of two <= W / T lanes share a
+        // torsion (strided over the range, then a butterfly inside the segment), so idle
+        // lanes shorten the longest range walk (T <= W always holds, see a3).
+        {
+            const int T = L.T;
+            const int lpt = T * 16 <= W ? 16 : (T * 8 <= W ? 8 : (T * 4 <= W ? 4 : (T * 2 <= W ? 2 : 1)));
+            const int k = sub / lpt, sl = sub - k * lpt;
+            const bool own = k < T;
             float cx = 0.f, cy = 0.f, cz = 0.f, hx = 0.f, hy = 0.f, hz = 0.f;
-            for (int a = lo; a < hi; ++a) {
-                const float4 c4 = S.ts[2 * a], g4 = S.ts[2 * a + 1];
-                cx += c4.x; cy += c4.y; cz += c4.z;
-                hx += g4.x; hy += g4.y; hz += g4.z;
+            int4 tm = make_int4(0, 0, 0, 0);
+            if (own) {
+                tm = L.tmeta[k];
+                const int lo = tm.w & 0xffff, hi = tm.w >> 16;
+                for (int a = lo + sl; a < hi; a += lpt) {
+                    const float4 c4 = S.ts[2 * a], g4 = S.ts[2 * a + 1];
+                    cx += c4.x; cy += c4.y; cz += c4.z;
+                    hx += g4.x; hy += g4.y; hz += g4.z;
+                }
             }
-            const float4 ra = S.r[ridx<W>(tm.y)], rb = S.r[ridx<W>(tm.z)];
-            const float dax = ra.x - tx, day = ra.y - ty, daz = ra.z - tz;
-            const float sx = cx - (day * hz - daz * hy), sy = cy - (daz * hx - dax * hz), sz = cz - (dax * hy - day * hx);
-            const float wx = rb.x - ra.x, wy = rb.y - ra.y, wz = rb.z - ra.z;
-            const float inw = rsqrtf(wx * wx + wy * wy + wz * wz);
-            S.grad[6 + k] = (wx * sx + wy * sy + wz * sz) * inw;
+            for (int m = lpt >> 1; m >= 1; m >>= 1) {     // fixed-order segment butterfly
+                cx += __shfl_xor_sync(mask, cx, m, W); cy += __shfl_xor_sync(mask, cy, m, W);
+                cz += __shfl_xor_sync(mask, cz, m, W); hx += __shfl_xor_sync(mask, hx, m, W);
+                hy += __shfl_xor_sync(mask, hy, m, W); hz += __shfl_xor_sync(mask, hz, m, W);
+            }
+            if (own && sl == 0) {
+                const float4 ra = S.r[ridx<W>(tm.y)], rb = S.r[ridx<W>(tm.z)];
+                const float dax = ra.x - tx, day = ra.y - ty, daz = ra.z - tz;
+                const float sx = cx - (day * hz - daz * hy), sy = cy - (daz * hx - dax * hz), sz = cz - (dax * hy - day * hx);
+                const float wx = rb.x - ra.x, wy = rb.y - ra.y, wz = rb.z - ra.z;
+                const float inw = rsqrtf(wx * wx + wy * wy + wz * wz);
+                S.grad[6 + k] = (wx * sx + wy * sy + wz * sz) * inw;
+            }
         }
         // translation and orientation: omega = adot n + sin(a) ndot + (1 - cos a) n x ndot
         if (sub < 6) {
