@@ -1,6 +1,13 @@
 #!/bin/bash
 set -u
-OUT=gpurun_out/ab9; mkdir -p $OUT
-bash scripts/gpu_tests.sh ab9t
-timeout 600 python bench.py --config hts --n-ligs 256 --steps 2 --warmup 2 --no-cpu > $OUT/hts.json 2>$OUT/hts.err
-python -c "import json;d=json.loads(open('$OUT/hts.json').read().strip().splitlines()[-1]);print('hts', '%.4g'%d['value'], '%.1f ms'%d['ms_per_step'], d['score_evals_per_s'])"
+OUT=gpurun_out/ab10; mkdir -p $OUT
+bash scripts/gpu_tests.sh ab10t
+cap() {  # tag kernel-regex skip cmd...
+  local tag=$1 re=$2 skip=$3; shift 3
+  timeout 600 ncu --set full --clock-control none --import-source on -k regex:$re -s $skip -c 1 -o /tmp/$tag "$@" > $OUT/ncu_$tag.log 2>&1
+  python scripts/ncu_summary.py full /tmp/$tag.ncu-rep > $OUT/full_$tag.txt 2>&1
+  ncu -i /tmp/$tag.ncu-rep --page source --csv --print-source sass > $OUT/sass_$tag.csv 2>/dev/null; gzip -f $OUT/sass_$tag.csv
+  rm -f /tmp/$tag.ncu-rep
+  echo "captured $tag: $(grep -m1 kernel $OUT/full_$tag.txt)"
+}
+cap ls_7cpa k_ls_adadelta 5 python bench.py --config 7cpa --steps 1 --warmup 0 --no-cpu
