@@ -28,6 +28,37 @@ def build_oracle(force: bool = False) -> str:
     return _SO
 
 
+class CScoring(C.Structure):
+    _fields_ = [
+        ("w_vdw", C.c_double), ("w_hb", C.c_double), ("w_el", C.c_double), ("w_ds", C.c_double),
+        ("w_tors", C.c_double), ("qasp", C.c_double), ("smooth", C.c_double),
+        ("cut_vdw", C.c_double), ("cut_el", C.c_double), ("diel", C.c_int),
+        ("diel_A", C.c_double), ("diel_eps0", C.c_double), ("diel_lambda", C.c_double),
+        ("diel_k", C.c_double), ("sigma", C.c_double),
+    ]
+
+
+# NEXT-2: AutoDock 4.1's calibrated free-energy coefficients, charge-dependent
+# solvation parameter, smoothing window, cutoffs and Mehler-Solmajer dielectric constants.
+AD41 = dict(w_vdw=0.1662, w_hb=0.1209, w_el=0.1406, w_ds=0.1322, w_tors=0.2983, qasp=0.01097,
+            smooth=0.5, cut_vdw=8.0, cut_el=20.48, diel=1, diel_A=-8.5525, diel_eps0=78.4,
+            diel_lambda=0.003627, diel_k=7.7839, sigma=3.6)
+# The same variant with every AD4 change switched off: must reduce to D5.
+D5_AS_AD4 = dict(w_vdw=1.0, w_hb=1.0, w_el=1.0, w_ds=1.0, w_tors=0.0, qasp=0.0, smooth=0.0,
+                 cut_vdw=0.0, cut_el=0.0, diel=0, diel_A=0.0, diel_eps0=0.0, diel_lambda=0.0,
+                 diel_k=0.0, sigma=3.6)
+
+
+def scoring(**kw):
+    """CScoring from AD41 with overrides.  Real values are rounded to float32 (the ABI's
+    type), so both sides start from the same numbers."""
+    v = dict(AD41); v.update(kw)
+    c = CScoring()
+    for k, val in v.items():
+        setattr(c, k, int(val) if k == "diel" else float(np.float32(val)))
+    return c
+
+
 class CProblem(C.Structure):
     _fields_ = [
         ("nx", C.c_int), ("ny", C.c_int), ("nz", C.c_int),
@@ -41,6 +72,7 @@ class CProblem(C.Structure):
         ("T", C.c_int), ("tor_a", C.POINTER(C.c_int)), ("tor_b", C.POINTER(C.c_int)),
         ("moved", C.POINTER(C.c_ubyte)),
         ("P", C.c_int), ("pairs", C.POINTER(C.c_int)),
+        ("sf", C.POINTER(CScoring)),
     ]
 
 
@@ -78,6 +110,10 @@ def lib():
         L.or_inter.argtypes = [P(CProblem), P(d), P(d)]; L.or_inter.restype = d
         L.or_pair_energy.argtypes = [P(CProblem), i, i, d, P(d)]; L.or_pair_energy.restype = d
         L.or_intra.argtypes = [P(CProblem), P(d), P(d)]; L.or_intra.restype = d
+        L.or_pair_energy_ad4.argtypes = [P(CProblem), i, i, d, P(d)]; L.or_pair_energy_ad4.restype = d
+        L.or_dielectric.argtypes = [P(CScoring), d, P(d)]; L.or_dielectric.restype = d
+        L.or_kink_margin.argtypes = [P(CProblem), P(d)]; L.or_kink_margin.restype = d
+        L.or_binding_dG.argtypes = [P(CProblem), d]; L.or_binding_dG.restype = d
         L.or_energy.argtypes = [P(CProblem), P(d), P(d), P(d), P(d)]; L.or_energy.restype = d
         L.or_margins.argtypes = [P(CProblem), P(d), P(d), P(d)]
         L.or_elite.argtypes = [i, P(d)]; L.or_elite.restype = i
@@ -155,7 +191,7 @@ class Problem:
     """Holds numpy buffers alive and the CProblem view over them."""
 
     def __init__(self, grid, lig=None, *, types=None, charges=None, xyz=None, bonds=None,
-                 rotatable=None, topo=None, type_params=None):
+                 rotatable=None, topo=None, type_params=None, sf=None):
         if lig is not None:
             types, charges, xyz, bonds, rotatable = lig.types, lig.charges, lig.xyz, lig.bonds, lig.rotatable
         self.grid = grid
@@ -197,6 +233,9 @@ class Problem:
         c.T = self.T; c.tor_a = _p(self.tor_a, C.c_int); c.tor_b = _p(self.tor_b, C.c_int)
         c.moved = _p(self.moved, C.c_ubyte)
         c.P = self.P; c.pairs = _p(self.pairs, C.c_int)
+        # sf: None (D5), a CScoring, or a dict of overrides of AD41 (NEXT-2 variant)
+        self.sf = scoring(**sf) if isinstance(sf, dict) else sf
+        c.sf = C.pointer(self.sf) if self.sf is not None else None
         self.c = c
 
     def ref(self):
@@ -237,6 +276,14 @@ class Problem:
                             _p(xyz, C.c_double), _p(terms, C.c_double))
         return dict(E=e, grad=gg if grad else None, xyz=xyz.reshape(self.N, 3), inter=terms[0], intra=terms[1])
 
+    # NEXT-2
+    def kink_margin(self, xyz):
+        x = _f64(xyz).reshape(-1)
+        return float(lib().or_kink_margin(self.ref(), _p(x, C.c_double)))
+
+    def binding_dG(self, e_inter):
+        return float(lib().or_binding_dG(self.ref(), float(e_inter)))
+
     def margins(self, xyz):
         x = _f64(xyz).reshape(-1); fm = C.c_double(0); cm = C.c_double(0)
         lib().or_margins(self.ref(), _p(x, C.c_double), C.byref(fm), C.byref(cm))
@@ -263,6 +310,13 @@ def params(**kw):
         else:
             setattr(p, k, int(val))
     return p
+
+
+def dielectric(sf, r):
+    """(eps(r), d eps / dr) of a CScoring (NEXT-2)."""
+    de = C.c_double(0)
+    e = lib().or_dielectric(C.byref(sf), float(r), C.byref(de))
+    return e, de.value
 
 
 def elite(E):

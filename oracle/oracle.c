@@ -330,6 +330,7 @@ double or_inter(const or_problem *P, const double *xyz, double *grad) {
 #define DESOLV_SIGMA 3.6
 
 double or_pair_energy(const or_problem *P, int i, int j, double rho2_in, double *dE_drho2) {
+    if (P->sf) return or_pair_energy_ad4(P, i, j, rho2_in, dE_drho2);   /* NEXT-2 variant */
     int ti = P->type[i], tj = P->type[j];
     double req = 0.5 * (P->tR[ti] + P->tR[tj]);                        /* r_eq = (R_i + R_j)/2 */
     double eps = sqrt(P->teps[ti] * P->teps[tj]);                      /* eps_ij = sqrt(eps_i eps_j) */
@@ -353,6 +354,94 @@ double or_pair_energy(const or_problem *P, int i, int j, double rho2_in, double 
     double dds = -Eds / (2.0 * DESOLV_SIGMA * DESOLV_SIGMA);
     if (dE_drho2) *dE_drho2 = clamped ? 0.0 : (dvdw + del + dds);
     return Evdw + Eel + Eds;
+}
+
+/* ========================================================================
+ * NEXT-2 — D5-AD4: the AutoDock4.1-calibrated pair energy (SURVEY.md §8(f) rank 2,
+ * SPEC S:219-223, 232).  Same pair list, clamp and role rule as D5; per
+ * pair, with r = |r_i - r_j| (r >= 0.01 Å after the D5 clamp):
+ *   vdW / H-bond: the D5 12-6 / 12-10 form times w_vdw / w_hb, evaluated at the smoothed
+ *     distance r_s (AD4 smoothing: the potential is replaced by its minimum over
+ *     [r - smooth/2, r + smooth/2]; the D5 forms have one minimum, at r_eq, so
+ *     r_s = r + smooth/2 below r_eq - smooth/2, r - smooth/2 above r_eq + smooth/2, and
+ *     r_eq in between), and only for r < cut_vdw;
+ *   electrostatic: w_el 332.06363 q_i q_j / (r eps(r)), eps(r) the Mehler-Solmajer
+ *     sigmoid A + B / (1 + k exp(-lambda B r)), B = eps0 - A (diel = 1), or 4r (diel = 0);
+ *   desolvation: w_ds (S'_i V_j + S'_j V_i) exp(-r^2 / (2 sigma^2)), S'_i = S_i + qasp |q_i|;
+ *   electrostatic and desolvation only for r < cut_el.
+ * Derivatives are taken piece by piece (zero on the smoothing plateau and beyond a
+ * cutoff) and returned as dE/d(rho^2) = (dE/dr) / (2r), zero under the clamp as in D5.
+ * ======================================================================== */
+double or_dielectric(const or_scoring *s, double r, double *deps_dr) {
+    if (s->diel == 0) {                                                 /* eps(r) = 4r */
+        if (deps_dr) *deps_dr = 4.0;
+        return 4.0 * r;
+    }
+    double B = s->diel_eps0 - s->diel_A;
+    double e = exp(-s->diel_lambda * B * r);
+    double den = 1.0 + s->diel_k * e;
+    if (deps_dr) *deps_dr = B * s->diel_k * s->diel_lambda * B * e / (den * den);
+    return s->diel_A + B / den;
+}
+
+double or_pair_energy_ad4(const or_problem *P, int i, int j, double rho2_in, double *dE_drho2) {
+    const or_scoring *s = P->sf;
+    int ti = P->type[i], tj = P->type[j];
+    double req = 0.5 * (P->tR[ti] + P->tR[tj]);
+    double eps = sqrt(P->teps[ti] * P->teps[tj]);
+    int hb = (P->trole[ti] == 1 && P->trole[tj] == 2) || (P->trole[ti] == 2 && P->trole[tj] == 1);
+    int clamped = rho2_in < 1e-4;
+    double r = sqrt(clamped ? 1e-4 : rho2_in);
+    /* vdW / H-bond at the smoothed distance */
+    double h = 0.5 * s->smooth, rs, drs;
+    if (r < req - h) { rs = r + h; drs = 1.0; }
+    else if (r > req + h) { rs = r - h; drs = 1.0; }
+    else { rs = req; drs = 0.0; }
+    double x = req / rs;
+    double x6 = pow(x, 6), x10 = pow(x, 10), x12 = pow(x, 12);
+    double Ev, dEv_drs;
+    if (hb) {
+        Ev = s->w_hb * eps * (5.0 * x12 - 6.0 * x10);
+        dEv_drs = s->w_hb * eps * (-60.0 * x12 + 60.0 * x10) / rs;
+    } else {
+        Ev = s->w_vdw * eps * (x12 - 2.0 * x6);
+        dEv_drs = s->w_vdw * eps * (-12.0 * x12 + 12.0 * x6) / rs;
+    }
+    double dEv = dEv_drs * drs;
+    if (s->cut_vdw > 0.0 && r >= s->cut_vdw) { Ev = 0.0; dEv = 0.0; }
+    /* electrostatics */
+    double de_dr, epsr = or_dielectric(s, r, &de_dr);
+    double Eel = s->w_el * ELEC_K * P->q[i] * P->q[j] / (r * epsr);
+    double dEel = -Eel * (1.0 / r + de_dr / epsr);                     /* d/dr [1/(r eps)] */
+    /* desolvation with charge-dependent solvation parameters */
+    double Si = P->tS[ti] + s->qasp * fabs(P->q[i]), Sj = P->tS[tj] + s->qasp * fabs(P->q[j]);
+    double SV = Si * P->tV[tj] + Sj * P->tV[ti];
+    double Eds = s->w_ds * SV * exp(-r * r / (2.0 * s->sigma * s->sigma));
+    double dEds = -Eds * r / (s->sigma * s->sigma);
+    if (s->cut_el > 0.0 && r >= s->cut_el) { Eel = Eds = dEel = dEds = 0.0; }
+    if (dE_drho2) *dE_drho2 = clamped ? 0.0 : (dEv + dEel + dEds) / (2.0 * r);
+    return Ev + Eel + Eds;
+}
+
+double or_kink_margin(const or_problem *P, const double *xyz) {
+    if (!P->sf) return 1e300;
+    const or_scoring *s = P->sf;
+    double m = 1e300;
+    for (int p = 0; p < P->P; ++p) {
+        int i = P->pairs[2 * p], j = P->pairs[2 * p + 1];
+        double r2 = 0.0;
+        for (int d = 0; d < 3; ++d) { double v = xyz[3 * i + d] - xyz[3 * j + d]; r2 += v * v; }
+        double r = sqrt(r2);
+        double req = 0.5 * (P->tR[P->type[i]] + P->tR[P->type[j]]);
+        double k[4] = {req - 0.5 * s->smooth, req + 0.5 * s->smooth, s->cut_vdw, s->cut_el};
+        for (int t = 0; t < 4; ++t)
+            if (fabs(r - k[t]) < m) m = fabs(r - k[t]);
+    }
+    return m;
+}
+
+double or_binding_dG(const or_problem *P, double e_inter) {
+    return e_inter + (P->sf ? P->sf->w_tors * P->T : 0.0);             /* AD4 unbound = bound model */
 }
 
 double or_intra(const or_problem *P, const double *xyz, double *grad) {

@@ -34,6 +34,21 @@ extern "C" {
 #define OR_MAX_TORS 32
 #define OR_MAX_GENES (6 + OR_MAX_TORS)
 
+/* NEXT-2 (DESIGN.md §11 reading D5-AD4): the AutoDock4.1-
+   calibrated form of the intramolecular pair energy.  SPEC S:219-223, 232 name what D5
+   leaves out (sigmoidal dielectric, free-energy weights, smoothing, cutoffs, torsional
+   entropy); the values are AutoDock 4.1's, passed in by the caller. */
+typedef struct {
+    double w_vdw, w_hb, w_el, w_ds, w_tors;  /* free-energy coefficients */
+    double qasp;               /* charge-dependent solvation: S_i -> S_i + qasp |q_i| */
+    double smooth;             /* vdW / H-bond smoothing window width (Å) */
+    double cut_vdw;            /* vdW / H-bond terms only for r < cut_vdw (Å); <= 0: no cutoff */
+    double cut_el;             /* electrostatic + desolvation only for r < cut_el; <= 0: none */
+    int diel;                  /* 0: eps(r) = 4 r (D5); 1: Mehler-Solmajer sigmoid */
+    double diel_A, diel_eps0, diel_lambda, diel_k;   /* eps(r) = A + B/(1 + k e^{-lambda B r}), B = eps0 - A */
+    double sigma;              /* desolvation Gaussian width (Å) */
+} or_scoring;
+
 /* A docking problem: receptor grid + per-type parameters + preprocessed ligand. */
 typedef struct {
     int nx, ny, nz;            /* grid nodes per axis */
@@ -52,6 +67,7 @@ typedef struct {
     const unsigned char *moved;/* [T*N] 1 if atom moves with torsion k */
     int P;                     /* intramolecular pairs */
     const int *pairs;          /* [P*2] */
+    const or_scoring *sf;      /* NULL: D5; else the D5-AD4 variant (NEXT-2) */
 } or_problem;
 
 typedef struct {
@@ -87,6 +103,15 @@ double or_inter(const or_problem *P, const double *xyz, double *grad /*[N*3] nul
 /* ---- D5: intramolecular ---- */
 double or_pair_energy(const or_problem *P, int i, int j, double rho2_in, double *dE_drho2);
 double or_intra(const or_problem *P, const double *xyz, double *grad /*[N*3] nullable*/);
+/* ---- NEXT-2: the AD4 pair energy, dielectric, kink margin and binding estimate ---- */
+double or_pair_energy_ad4(const or_problem *P, int i, int j, double rho2_in, double *dE_drho2);
+double or_dielectric(const or_scoring *s, double r, double *deps_dr /* nullable */);
+/* smallest |r - k| over pairs and kinks k of the AD4 pair energy (r_eq +- smooth/2,
+   cut_vdw, cut_el): where FP32 and double may sit on different sides (gradient jumps,
+   or energy jumps at a cutoff).  1e300 for D5 problems. */
+double or_kink_margin(const or_problem *P, const double *xyz);
+/* AD4 binding estimate of a pose (unbound = bound model): E_inter + w_tors * T. */
+double or_binding_dG(const or_problem *P, double e_inter);
 /* ---- D6 + D7: total energy and genotype gradient ---- */
 double or_energy(const or_problem *P, const double *genes, double *ggrad /*[G] nullable*/,
                  double *xyz /*[N*3] nullable*/, double *terms /*[2] inter,intra nullable*/);
