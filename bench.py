@@ -41,14 +41,19 @@ F_PAIR_EG = 55         # D5 energy + dE/drho2 + force on both atoms (unique pair
 F_ATOM_BACK = 18       # (r - t) x g, sums
 F_TORSION_BACK = 20    # per-torsion projection (plus 6 per moved atom)
 F_GENE_ADADELTA = 12
+# NEXT-2 D5-AD4 pair: + r, smoothing, the sigmoidal dielectric and two cutoffs
+F_PAIR_E_AD4 = 52
+F_PAIR_EG_AD4 = 84
+
+SCORING = 0            # --scoring: 0 = D5, 1 = D5-AD4 (dock_params.scoring)
 
 
 def flops_per_eval(N, T, P, moved_total, grad):
     f = F_ORIENT + T * F_TORSION + N * (F_ATOM_POSE + F_ATOM_INTER)
     if grad:
-        f += P * F_PAIR_EG + N * F_ATOM_BACK + T * F_TORSION_BACK + 6 * moved_total + (6 + T) * F_GENE_ADADELTA
+        f += P * (F_PAIR_EG_AD4 if SCORING else F_PAIR_EG) + N * F_ATOM_BACK + T * F_TORSION_BACK + 6 * moved_total + (6 + T) * F_GENE_ADADELTA
     else:
-        f += P * F_PAIR_E
+        f += P * (F_PAIR_E_AD4 if SCORING else F_PAIR_E)
     return f
 
 
@@ -172,7 +177,7 @@ def workload_desc(cfg):
     ls = "Solis-Wets" if cfg.ls_method == 1 else "ADADELTA"
     return (f"{cfg.name}-shaped ({cfg.note.split(':')[0]}): {cfg.n_atoms} atoms, {cfg.n_tors} torsions, "
             f"{cfg.grid_n}^3 grid, pop {cfg.pop}, {cfg.runs} runs/GPU, {cfg.max_evals} evals/run, {ls} "
-            f"ls_rate {cfg.ls_rate}, {cfg.ls_iters} iters")
+            f"ls_rate {cfg.ls_rate}, {cfg.ls_iters} iters" + (", AD4.1-calibrated scoring (NEXT-2)" if SCORING else ""))
 
 
 # ---------------------------------------------------------------------------
@@ -180,7 +185,7 @@ def workload_desc(cfg):
 # ---------------------------------------------------------------------------
 def oracle_sample(cfg, lig, grid, budget, threads, seed=42):
     import oracle
-    P = oracle.Problem(grid, lig)
+    P = oracle.Problem(grid, lig, sf={} if SCORING else None)
     pp = oracle.params(ls_method=cfg.ls_method, ls_rate=cfg.ls_rate, ls_max_iters=cfg.ls_iters)
     out = [None] * threads
 
@@ -238,7 +243,7 @@ def run_ours(args, cfg, lig, grid):
     dev, cdev = dist_setup(local, world)
     gpu = dev.index
     d = dock.Docker.from_inputs(grid, lig, ls_method=cfg.ls_method, ls_rate=cfg.ls_rate,
-                                ls_max_iters=cfg.ls_iters, profile=1, device=gpu, sw_depth=args.sw_depth,
+                                ls_max_iters=cfg.ls_iters, profile=1, device=gpu, sw_depth=args.sw_depth, scoring=SCORING,
                                 sw_split=args.sw_split)
     runs = cfg.runs
     run_base = rank * runs
@@ -333,7 +338,7 @@ def run_ours(args, cfg, lig, grid):
         t0 = time.perf_counter()
         dd = dock.Docker(grid.maps, grid.n, grid.spacing, grid.origin, tp, roles, lig.types, lig.charges,
                          lig.xyz, lig.bonds, lig.rotatable, ls_method=cfg.ls_method, ls_rate=cfg.ls_rate,
-                         ls_max_iters=cfg.ls_iters, device=gpu)
+                         ls_max_iters=cfg.ls_iters, device=gpu, scoring=SCORING)
         r = dd.run(cfg.pop, runs, cfg.max_evals, 42, run_base=run_base, xyz=True)
         h2d = dd.upload_bytes
         dd.close()
@@ -385,7 +390,7 @@ def hts_oracle_sample(cfg, grid, ligs, threads, budget):
     out = [0] * threads
 
     def work(i):
-        P = oracle.Problem(grid, ligs[i % len(ligs)])
+        P = oracle.Problem(grid, ligs[i % len(ligs)], sf={} if SCORING else None)
         out[i] = oracle.dock_run(P, pp, cfg.pop, budget, 42, ligand_id=i, run=0)["evals"]
     ts = [threading.Thread(target=work, args=(i,)) for i in range(threads)]
     t0 = time.perf_counter()
@@ -415,7 +420,8 @@ def run_hts(args, cfg, grid):
     per_lig_evals = cfg.runs * cfg.max_evals
     sample_desc = (f"configs[4] sample: {args.n_ligs} of the 10k synthetic ligands (N ~ U{{10..70}}, "
                    f"T = clip(N/5 + U{{-1,0,1}}, 0, 15), 8 types), 64^3 receptor, pop {cfg.pop}, {cfg.runs} runs x "
-                   f"{cfg.max_evals} evals, ADADELTA ls_rate {cfg.ls_rate}, {cfg.ls_iters} iters")
+                   f"{cfg.max_evals} evals, ADADELTA ls_rate {cfg.ls_rate}, {cfg.ls_iters} iters"
+                   + (", AD4.1-calibrated scoring (NEXT-2)" if SCORING else ""))
     if args.impl == "reference":
         threads = os.cpu_count() or 1
         budget = 20_000
@@ -442,7 +448,7 @@ def run_hts(args, cfg, grid):
     costs = sched.ligand_cost([len(l.types) for l in ligs], n_pairs)
     mine = sched.lpt_partition(costs, world)[rank]
     my_ligs = [ligs[i] for i in mine]
-    kw = dict(ls_method=cfg.ls_method, ls_rate=cfg.ls_rate, ls_max_iters=cfg.ls_iters)
+    kw = dict(ls_method=cfg.ls_method, ls_rate=cfg.ls_rate, ls_max_iters=cfg.ls_iters, scoring=SCORING)
     for _ in range(args.warmup):   # warm-up on a slice: context, kernels, graphs
         dock.screen(grid, my_ligs[:8], cfg.pop, cfg.runs, cfg.max_evals // 10, 7, ligand_ids=mine[:8],
                     devices=[local], slots_per_device=args.slots, **kw)
@@ -518,7 +524,7 @@ def run_micro(args, cfg, lig, grid):
     from gen import random_genotypes
 
     dev = torch.device("cuda", 0)
-    d = dock.Docker.from_inputs(grid, lig, ls_method=0)
+    d = dock.Docker.from_inputs(grid, lig, ls_method=0, scoring=SCORING)
     n = cfg.runs * cfg.pop
     X = torch.from_numpy(random_genotypes(grid, d.T, n, seed=5, frac_out=0.0, shrink=0.2)).to(dev)
     out = torch.empty(n, dtype=torch.float32, device=dev)
@@ -553,7 +559,7 @@ def run_micro(args, cfg, lig, grid):
     t_in = res["inter"]
     pair_steps = n * iters * d.P
     t_pr = res["intra"]
-    fl = pair_steps * F_PAIR_EG / t_pr / 1e12
+    fl = pair_steps * (F_PAIR_EG_AD4 if SCORING else F_PAIR_EG) / t_pr / 1e12
     line = {"metric": "microbench", "config": {"workload": workload_desc(cfg), "genotypes": n, "iters": iters},
             "inter": {"kernel": "k_bench_part<kInter> (pose + trilinear E+G)", "ms": 1e3 * t_in,
                       "atom_lookups_per_s": lookups / t_in,
@@ -583,7 +589,11 @@ def main():
     ap.add_argument("--slots", type=int, default=4, help="hts: ligands in flight per GPU")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--scoring", default="d5", choices=["d5", "ad4"],
+                    help="intramolecular scoring: D5 (default) or the NEXT-2 AD4.1-calibrated variant")
     args = ap.parse_args()
+    global SCORING
+    SCORING = 1 if args.scoring == "ad4" else 0
     from gen import config_inputs
     cfg, lig, grid = config_inputs(args.config)
     if args.runs > 0:

@@ -37,6 +37,17 @@ extern "C" {
 typedef struct dock_ctx dock_ctx;
 enum { DOCK_OK = 0, DOCK_E_INPUT = 1, DOCK_E_INTERNAL = 2 };
 enum { DOCK_LS_ADADELTA = 0, DOCK_LS_SOLIS_WETS = 1 };
+/* Scoring function of the intramolecular pair energy.  DOCK_SF_D5: reading D5 (DESIGN.md
+   §3).  DOCK_SF_AD4: reading D5-AD4 (NEXT-2 of SURVEY.md
+   §8(f), the AutoDock4.1-calibrated forms SPEC S:219-223, 232 lists as D5's
+   simplifications): vdW/H-bond times w_vdw/w_hb at the 0.5 Å-smoothed distance for r < 8 Å;
+   electrostatics w_el 332.06363 q_i q_j / (r eps(r)) with the Mehler-Solmajer dielectric
+   eps(r) = A + B/(1 + k e^{-lambda B r}), A = -8.5525, B = 78.4 - A, k = 7.7839,
+   lambda = 0.003627; desolvation w_ds (S'_i V_j + S'_j V_i) exp(-r^2/(2 3.6^2)) with
+   S' = S + qasp |q|; electrostatics and desolvation for r < 20.48 Å.  The smoothing
+   window, cutoffs and dielectric constants are fixed; the weights and qasp are
+   dock_params fields.  The intermolecular grid term (D4) is the same in both. */
+enum { DOCK_SF_D5 = 0, DOCK_SF_AD4 = 1 };
 
 #define DOCK_MAX_ATOMS 256
 #define DOCK_MAX_TORSIONS 32
@@ -95,11 +106,16 @@ typedef struct {
                                     than 16 atoms: 0 = auto, 1 = none, 2 (with depth 2) or 4 (with
                                     depth 1) = cooperative evaluation.  Results identical up to the
                                     FP32 summation order of the energy parts (fixed per setting). */
+    int32_t scoring;             /* DOCK_SF_D5 (default) or DOCK_SF_AD4 */
+    float w_vdw, w_hb, w_el, w_ds, w_tors;   /* DOCK_SF_AD4 free-energy coefficients (finite, >= 0);
+                                    defaults AutoDock 4.1: .1662 .1209 .1406 .1322 .2983 */
+    float qasp;                  /* DOCK_SF_AD4 charge-dependent solvation parameter (default .01097) */
 } dock_params;
 
 /* Fills the defaults: p_tour .60, p_cross .80, p_mut .02, 2.0 Å / 0.523 rad, ADADELTA,
    ls_rate 1.0, 300 iterations, SW 1.0/0.01/2/0.5/4/4, ADADELTA rho .8 eps 1e-2,
-   27000 generations, device 0, l2_persist 1, gens_per_graph 16. */
+   27000 generations, device 0, l2_persist 1, gens_per_graph 16, scoring DOCK_SF_D5 with the
+   AD4.1 coefficients filled in (used only when scoring = DOCK_SF_AD4). */
 int dock_params_default(dock_params *p);
 
 /* Built-in type table by name ("C","A","N","NA","O","OA","H","HD").
@@ -149,6 +165,14 @@ int dock_eval(dock_ctx *ctx, int32_t n, const float *genotypes, float *energy, f
               float *xyz);
 int dock_eval_device(dock_ctx *ctx, int32_t n, const float *d_genotypes, float *d_energy,
                      float *d_grad, float *d_xyz, void *stream);   /* stream NULL = legacy default */
+
+/* The two energy terms of n genotypes separately (D4 intermolecular, D5 / D5-AD4
+   intramolecular; host arrays [n], each may be NULL) and the binding estimate
+   dG[n] = inter + w_tors * T (AutoDock4's "unbound = bound" model: the torsional
+   free-energy penalty of NEXT-2; w_tors = 0 under DOCK_SF_D5, so dG = inter).  Each term is
+   its own energy-only kernel launch. */
+int dock_eval_terms(dock_ctx *ctx, int32_t n, const float *genotypes, float *inter, float *intra,
+                    float *dG);
 
 /* Microbenchmark of one part of the evaluation, for roofline evidence:
    part 0 = pose + intermolecular grid interpolation with gradient (a3+a4), part 1 = pose

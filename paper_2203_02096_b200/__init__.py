@@ -19,6 +19,7 @@ LIB_PATH = os.environ.get("DOCK_LIB") or os.path.join(_HERE, "libdock.so")
 
 DOCK_OK, DOCK_E_INPUT, DOCK_E_INTERNAL = 0, 1, 2
 LS_ADADELTA, LS_SOLIS_WETS = 0, 1
+SF_D5, SF_AD4 = 0, 1          # dock_params.scoring (NEXT-2: D5-AD4)
 PURPOSE_INIT, PURPOSE_GA, PURPOSE_LS_PICK, PURPOSE_SW = 0, 1, 2, 3
 
 
@@ -51,7 +52,8 @@ class Params(C.Structure):
                 ("sw_cons_succ", C.c_int32), ("sw_cons_fail", C.c_int32), ("ad_rho", C.c_float),
                 ("ad_eps", C.c_float), ("max_generations", C.c_int32), ("device", C.c_int32),
                 ("l2_persist", C.c_int32), ("gens_per_graph", C.c_int32), ("profile", C.c_int32), ("sw_depth", C.c_int32),
-                ("sw_split", C.c_int32)]
+                ("sw_split", C.c_int32), ("scoring", C.c_int32), ("w_vdw", C.c_float), ("w_hb", C.c_float),
+                ("w_el", C.c_float), ("w_ds", C.c_float), ("w_tors", C.c_float), ("qasp", C.c_float)]
 
 
 class ScreenOpts(C.Structure):
@@ -87,6 +89,7 @@ def _load():
         "dock_run_device": (i32, [v, i32, i32, i32, u32, i64, u64, v, v, v, v, v]),
         "dock_eval": (i32, [v, i32, P(f), P(f), P(f), P(f)]),
         "dock_eval_device": (i32, [v, i32, v, v, v, v, v]),
+        "dock_eval_terms": (i32, [v, i32, P(f), P(f), P(f), P(f)]),
         "dock_bench_part": (i32, [v, i32, i32, i32, v, v, v]),
         "dock_get_pairs": (i32, [v, P(i32)]),
         "dock_get_torsions": (i32, [v, P(i32), P(C.c_uint8)]),
@@ -117,7 +120,7 @@ EXPORTED = ("dock_params_default", "dock_builtin_type_param", "dock_init", "dock
             "dock_run_device", "dock_eval", "dock_eval_device", "dock_get_pairs", "dock_get_torsions",
             "dock_philox", "dock_stream_words", "dock_ga_step", "dock_ls_step", "dock_launch_count",
             "dock_topology", "dock_kernel_stats", "dock_upload_bytes", "dock_screen", "dock_screen_last_error",
-            "dock_bench_part")
+            "dock_bench_part", "dock_eval_terms")
 
 
 def topology(types, charges, xyz, bonds, rotatable, type_params, roles):
@@ -365,6 +368,14 @@ class Docker:
         self._chk(lib.dock_eval(self._ctx, n, _ptr(x, C.c_float), _ptr(E, C.c_float), _ptr(gr, C.c_float),
                                 _ptr(xy, C.c_float)))
         return E, gr, xy
+
+    def eval_terms(self, genotypes):
+        """(inter [n], intra [n], dG [n]) through dock_eval_terms (dG = inter + w_tors T)."""
+        x = np.ascontiguousarray(genotypes, dtype=np.float32).reshape(-1, self.G)
+        n = x.shape[0]
+        out = [np.zeros(n, np.float32) for _ in range(3)]
+        self._chk(lib.dock_eval_terms(self._ctx, n, _ptr(x, C.c_float), *(_ptr(o, C.c_float) for o in out)))
+        return tuple(out)
 
     def eval_device(self, genotypes, energy, grad=None, xyz=None, stream=0):
         """torch CUDA tensors (float32, contiguous); stream = torch.cuda.Stream.cuda_stream or 0."""

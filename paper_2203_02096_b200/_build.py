@@ -32,10 +32,13 @@ def build(force: bool = False, verbose: bool = False, out: str | None = None, de
     obj_dir = os.path.join(ROOT, "build", "obj" if out is None else "obj_" + os.path.basename(out))
     os.makedirs(obj_dir, exist_ok=True)
     procs, objs = [], []
-    for src in SOURCES:
-        obj = os.path.join(obj_dir, src + ".o")
+    # kernels.cu is compiled twice: the D5 scoring function (dk::d5) and, with -DDK_AD4,
+    # the NEXT-2 AutoDock4.1-calibrated variant (dk::ad4); the objects build in parallel.
+    units = [(src, src + ".o", ()) for src in SOURCES] + [("kernels.cu", "kernels_ad4.cu.o", ("DK_AD4",))]
+    for src, oname, extra in units:
+        obj = os.path.join(obj_dir, oname)
         objs.append(obj)
-        cmd = [NVCC, *FLAGS, *[f"-D{d}" for d in defines], "-c", os.path.join(CSRC, src), "-o", obj]
+        cmd = [NVCC, *FLAGS, *[f"-D{d}" for d in (*defines, *extra)], "-c", os.path.join(CSRC, src), "-o", obj]
         if src.endswith(".cu") and verbose:
             cmd += ["-Xptxas", "-v"]
         procs.append((cmd, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT)))

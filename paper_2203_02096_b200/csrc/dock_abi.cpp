@@ -145,6 +145,9 @@ int validate_params(const dock_params &p, std::string *err) {
     if (p.gens_per_graph < 1 || p.gens_per_graph > 4096) { *err = "params.gens_per_graph: 1..4096"; return DOCK_E_INPUT; }
     if (p.sw_depth < 0 || p.sw_depth > 3) { *err = "params.sw_depth: 0..3"; return DOCK_E_INPUT; }
     if (p.sw_split != 0 && p.sw_split != 1 && p.sw_split != 2 && p.sw_split != 4) { *err = "params.sw_split: 0, 1, 2 or 4"; return DOCK_E_INPUT; }
+    if (p.scoring != DOCK_SF_D5 && p.scoring != DOCK_SF_AD4) { *err = "params.scoring: DOCK_SF_D5 or DOCK_SF_AD4"; return DOCK_E_INPUT; }
+    for (float w : {p.w_vdw, p.w_hb, p.w_el, p.w_ds, p.w_tors, p.qasp})
+        if (!std::isfinite(w) || w < 0.f) { *err = "params.w_* / qasp: must be finite and >= 0"; return DOCK_E_INPUT; }
     return DOCK_OK;
 }
 
@@ -316,6 +319,9 @@ int dock_params_default(dock_params *p) {
     p->ad_rho = 0.8f; p->ad_eps = 1e-2f;
     p->max_generations = 27000;
     p->device = 0; p->l2_persist = 1; p->gens_per_graph = 16;
+    p->scoring = DOCK_SF_D5;   // AD4.1 coefficients (Huey et al. 2007), used by DOCK_SF_AD4
+    p->w_vdw = 0.1662f; p->w_hb = 0.1209f; p->w_el = 0.1406f; p->w_ds = 0.1322f; p->w_tors = 0.2983f;
+    p->qasp = 0.01097f;
     return DOCK_OK;
 }
 
@@ -348,7 +354,7 @@ int dock_init(const dock_grids *grids, const dock_type_param *type_params, const
     dk::Prepared prep;
     {
         Trace tr("init.prepare_ligand");
-        if (dk::prepare_ligand(ligand, type_params, grids->n_types, &prep, &err) != DOCK_OK) { g_init_error = err; return DOCK_E_INPUT; }
+        if (dk::prepare_ligand(ligand, type_params, grids->n_types, dk::scoring_of(p), &prep, &err) != DOCK_OK) { g_init_error = err; return DOCK_E_INPUT; }
     }
     int ndev = 0;
     if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev < 1) {
@@ -605,11 +611,41 @@ int dock_eval(dock_ctx *c, int32_t n, const float *genotypes, float *energy, flo
     return DOCK_OK;
 }
 
+int dock_eval_terms(dock_ctx *c, int32_t n, const float *genotypes, float *inter, float *intra, float *dG) {
+    if (!c) return DOCK_E_INPUT;
+    if (n < 0) return input_error(c, "n: must be >= 0");
+    if (n == 0) return DOCK_OK;
+    if (!genotypes) return input_error(c, "genotypes: NULL");
+    for (long long i = 0; i < (long long)n * c->prep.G; ++i)
+        if (!std::isfinite(genotypes[i])) return input_error(c, "genotypes[" + std::to_string(i) + "]: non-finite");
+    CK(cudaSetDevice(c->device));
+    const int G = c->prep.G;
+    DevBuf dg(c->stream), dI(c->stream), dP(c->stream);
+    CK(dg.alloc(sizeof(float) * n * G));
+    CK(dI.alloc(sizeof(float) * n));
+    CK(dP.alloc(sizeof(float) * n));
+    CK(cudaMemcpyAsync(dg.p, genotypes, sizeof(float) * n * G, cudaMemcpyHostToDevice, c->stream));
+    CK(dk::launch_eval(c->lig, c->grid, n, (const float *)dg.p, (float *)dI.p, nullptr, nullptr, c->d_dfs2orig,
+                       c->stream, dk::kPartsInter));
+    CK(dk::launch_eval(c->lig, c->grid, n, (const float *)dg.p, (float *)dP.p, nullptr, nullptr, c->d_dfs2orig,
+                       c->stream, dk::kPartsIntra));
+    c->launches += 2;
+    std::vector<float> hi(n);
+    CK(cudaMemcpyAsync(hi.data(), dI.p, sizeof(float) * n, cudaMemcpyDeviceToHost, c->stream));
+    if (intra) CK(cudaMemcpyAsync(intra, dP.p, sizeof(float) * n, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    if (inter) std::copy(hi.begin(), hi.end(), inter);
+    // AD4 binding estimate: inter + w_tors * T (host: one multiply-add per genotype)
+    const float w_tors = c->params.scoring == DOCK_SF_AD4 ? c->params.w_tors : 0.0f;
+    if (dG) for (int i = 0; i < n; ++i) dG[i] = hi[i] + w_tors * (float)c->prep.T;
+    return DOCK_OK;
+}
+
 int dock_topology(const dock_ligand *ligand, const dock_type_param *type_params, int32_t n_types, int32_t *n_tors,
                   int32_t *axis, uint8_t *moved, int32_t *n_pairs, int32_t *pairs, int32_t pair_cap) {
     dk::Prepared p;
     std::string err;
-    if (dk::prepare_ligand(ligand, type_params, n_types, &p, &err) != DOCK_OK) { g_init_error = err; return DOCK_E_INPUT; }
+    if (dk::prepare_ligand(ligand, type_params, n_types, dk::Scoring(), &p, &err) != DOCK_OK) { g_init_error = err; return DOCK_E_INPUT; }
     if (n_tors) *n_tors = p.T;
     if (n_pairs) *n_pairs = p.P;
     for (int k = 0; k < p.T; ++k)

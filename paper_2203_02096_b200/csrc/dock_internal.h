@@ -57,6 +57,11 @@ struct LigDev {
     int off_ppar;     // float4[NC][2*Wg] partner params {R/2, sqrt(eps), S, V}, duplicated chunks;
                       //   R/2 negated for acceptors and sqrt(eps) negated for donors (role
                       //   in the sign bits; magnitudes via free |.| operand modifiers)
+    // scoring function (NEXT-2): 0 = D5, 1 = D5-AD4 (the kernels of namespace dk::ad4).
+    // AD4 runtime constants: vdW / H-bond coefficient factors (A x^12 - |B| x^n per unit
+    // eps_ij: w_vdw, 2 w_vdw / 5 w_hb, -6 w_hb) and the charge scale w_el 332.06363.
+    int sf;
+    float wA_v, wB_v, wA_h, wB_h, qscale;
     const uint8_t *blob;          // device pointer
 };
 

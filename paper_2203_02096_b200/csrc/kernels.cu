@@ -18,11 +18,13 @@
 // independently"; NS "one CTA or warp-group handles each individual").
 #include <math.h>
 
+#define DK_KERNELS_TU
 #include "kernels.cuh"
 #include "philox.cuh"
 #include "score.cuh"
 
 namespace dk {
+namespace DK_SF_NS {   // d5, or ad4 when compiled with -DDK_AD4 (score.cuh)
 
 static inline __host__ __device__ int a16(int x) { return (x + 15) & ~15; }
 
@@ -82,6 +84,7 @@ __device__ __forceinline__ LigSm stage_ligand(const LigDev &L, uint8_t *sm, int 
     v.slot4 = reinterpret_cast<const float4 *>(sm + L.off_slot4);
     v.slotq = reinterpret_cast<const float *>(sm + L.off_slotq);
     v.energy_tiles = L.energy_tiles;
+    v.wA_v = L.wA_v; v.wB_v = L.wB_v; v.wA_h = L.wA_h; v.wB_h = L.wB_h; v.qscale = L.qscale;
     return v;
 }
 
@@ -105,7 +108,7 @@ __device__ __forceinline__ float nan_inf(float v) { return isnan(v) ? INFINITY :
 // ---------------------------------------------------------------------------
 // k_eval: batched energy (+ gradient, + pose) of given genotypes.
 // ---------------------------------------------------------------------------
-template <int W, int MAXC, bool GRAD>
+template <int W, int MAXC, bool GRAD, int PARTS = kAll>
 __global__ void __launch_bounds__(256) k_eval(const LigDev L, const GridDev g, const ScratchLayout SL,
                                               int n, const float *__restrict__ genes, float *E,
                                               float *grad, float *xyz, const int *__restrict__ dfs2orig) {
@@ -120,7 +123,7 @@ __global__ void __launch_bounds__(256) k_eval(const LigDev L, const GridDev g, c
     const int G = L.G;
     for (int j = sub; j < G; j += W) S.genes[j] = genes[(size_t)gi * G + j];
     __syncwarp(mask);
-    const float e = eval_group<W, MAXC, GRAD>(Ls, g, S, sub, mask);
+    const float e = eval_group<W, MAXC, GRAD, PARTS>(Ls, g, S, sub, mask);
     if (sub == 0) E[gi] = e;
     if (GRAD && grad)
         for (int j = sub; j < G; j += W) grad[(size_t)gi * G + j] = S.grad[j];
@@ -821,6 +824,8 @@ cudaError_t setup_kernel_attributes() {
 #define DK_ATTR(W, MAXC)                                                             \
     if (e == cudaSuccess) e = allow_smem(k_eval<W, MAXC, false>);                    \
     if (e == cudaSuccess) e = allow_smem(k_eval<W, MAXC, true>);                     \
+    if (e == cudaSuccess) e = allow_smem(k_eval<W, MAXC, false, kInter>);            \
+    if (e == cudaSuccess) e = allow_smem(k_eval<W, MAXC, false, kIntra>);            \
     if (e == cudaSuccess) e = allow_smem(k_init<W, MAXC>);                           \
     if (e == cudaSuccess) e = allow_smem(k_ga<W, MAXC>);                             \
     if (e == cudaSuccess) e = allow_smem(k_ls_adadelta<W, MAXC>);                    \
@@ -838,7 +843,7 @@ cudaError_t setup_kernel_attributes() {
 static inline int ceil_div(long long a, long long b) { return (int)((a + b - 1) / b); }
 
 cudaError_t launch_eval(const LigDev &L, const GridDev &g, int n, const float *genes, float *E, float *grad,
-                        float *xyz, const int *dfs2orig, cudaStream_t s) {
+                        float *xyz, const int *dfs2orig, cudaStream_t s, int parts) {
     if (n <= 0) return cudaSuccess;
     const GroupCfg cfg = pick_group(L.N);
     const bool want_grad = grad != nullptr;
@@ -848,7 +853,12 @@ cudaError_t launch_eval(const LigDev &L, const GridDev &g, int n, const float *g
     if (smem > (size_t)kSmemMax) return cudaErrorInvalidConfiguration;
     const int blocks = ceil_div(n, groups);
     DK_DISPATCH(cfg, {
-        if (want_grad) k_eval<W, MAXC, true><<<blocks, kThreads, smem, s>>>(L, g, SL, n, genes, E, grad, xyz, dfs2orig);
+        // parts = one term only (dock_eval_terms): energy-only kernels of that term
+        if (parts == kInter && !want_grad)
+            k_eval<W, MAXC, false, kInter><<<blocks, kThreads, smem, s>>>(L, g, SL, n, genes, E, nullptr, xyz, dfs2orig);
+        else if (parts == kIntra && !want_grad)
+            k_eval<W, MAXC, false, kIntra><<<blocks, kThreads, smem, s>>>(L, g, SL, n, genes, E, nullptr, xyz, dfs2orig);
+        else if (want_grad) k_eval<W, MAXC, true><<<blocks, kThreads, smem, s>>>(L, g, SL, n, genes, E, grad, xyz, dfs2orig);
         else k_eval<W, MAXC, false><<<blocks, kThreads, smem, s>>>(L, g, SL, n, genes, E, grad, xyz, dfs2orig);
     });
     return cudaGetLastError();
@@ -1011,4 +1021,5 @@ cudaError_t launch_stream_words(uint32_t k0, uint32_t k1, uint32_t purpose, uint
     return cudaGetLastError();
 }
 
+}  // namespace DK_SF_NS
 }  // namespace dk

@@ -26,7 +26,17 @@ inline int a16(int x) { return (x + 15) & ~15; }
 
 }  // namespace
 
-int prepare_ligand(const dock_ligand *l, const dock_type_param *tp, int n_types, Prepared *out, std::string *err) {
+Scoring scoring_of(const dock_params &p) {
+    Scoring s;
+    s.sf = p.scoring;
+    if (s.sf == DOCK_SF_AD4) {
+        s.w_vdw = p.w_vdw; s.w_hb = p.w_hb; s.w_el = p.w_el; s.w_ds = p.w_ds; s.w_tors = p.w_tors; s.qasp = p.qasp;
+    }
+    return s;
+}
+
+int prepare_ligand(const dock_ligand *l, const dock_type_param *tp, int n_types, const Scoring &sf, Prepared *out,
+                   std::string *err) {
     auto fail = [&](const std::string &m) { *err = m; return (int)DOCK_E_INPUT; };
     if (!l) return fail("ligand: NULL");
     const int N = l->n_atoms;
@@ -206,6 +216,16 @@ int prepare_ligand(const dock_ligand *l, const dock_type_param *tp, int n_types,
     LigDev &L = o.layout;
     std::memset(&L, 0, sizeof(L));
     L.N = N; L.T = T; L.G = 6 + T; L.P = P;
+    // scoring function (NEXT-2): D5-AD4 folds its weights and charge-dependent solvation
+    // into the pair constants below; the tile kernels get the vdW / H-bond factors here.
+    const bool ad4 = sf.sf == DOCK_SF_AD4;
+    L.sf = ad4 ? 1 : 0;
+    L.wA_v = (float)sf.w_vdw; L.wB_v = (float)(2.0 * sf.w_vdw);
+    L.wA_h = (float)(5.0 * sf.w_hb); L.wB_h = (float)(-6.0 * sf.w_hb);
+    L.qscale = (float)(sf.w_el * 332.06363);
+    // D5-AD4 solvation parameter S' = S + qasp |q| and weighted volume V' = w_ds V of atom a
+    auto S_of = [&](int a) { const double S = tp[l->type[a]].S; return ad4 ? S + sf.qasp * std::fabs((double)l->charge[a]) : S; };
+    auto V_of = [&](int a) { const double V = tp[l->type[a]].V; return ad4 ? sf.w_ds * V : V; };
     int off = 0;
     L.off_lvl = off; off += a16(4 * (kMaxTors + 1));
     L.off_p = off; off += 16 * N;
@@ -293,6 +313,7 @@ int prepare_ligand(const dock_ligand *l, const dock_type_param *tp, int n_types,
                     const dock_type_param &t = tp[l->type[order[p]]];
                     const float h = 0.5f * t.R, e = (float)std::sqrt((double)t.eps);
                     v = make_float4(t.role == 2 ? -h : h, t.role == 1 ? -e : e, t.S, t.V);
+                    if (ad4) { v.z = (float)S_of(order[p]); v.w = (float)V_of(order[p]); }
                 }
                 pp[c * 2 * L.Wg + q] = v;
             }
@@ -311,7 +332,9 @@ int prepare_ligand(const dock_ligand *l, const dock_type_param *tp, int n_types,
         float4 *s4 = reinterpret_cast<float4 *>(bl + L.off_slot4);
         float *sq = reinterpret_cast<float *>(bl + L.off_slotq);
         auto fill = [&](int slot, int da, int db, bool on) {
-            s4[slot] = make_float4(0.f, 0.f, 0.f, 0.f);
+            // a non-pair slot contributes exactly 0 (A = B = SV = qq = 0); under D5-AD4 its
+            // r_eq operand is 1 Å so the smoothed distance stays >= 0.26 Å (x^2 finite, 0 * x^12 = 0)
+            s4[slot] = make_float4(ad4 ? 1.f : 0.f, 0.f, 0.f, 0.f);
             sq[slot] = 0.f;
             if (!on || da >= N || db >= N || !is_pair[(size_t)da * N + db]) return;
             const int ia = order[da], ib = order[db];
@@ -319,6 +342,13 @@ int prepare_ligand(const dock_ligand *l, const dock_type_param *tp, int n_types,
             const double req = 0.5 * ((double)ta.R + (double)tb.R);
             const double eps = std::sqrt((double)ta.eps * (double)tb.eps);
             const bool hb = hb_of(ia, ib);
+            if (ad4) {   // {r_eq, w A, w B, w_ds (S'_a V_b + S'_b V_a)}, w_el 332.06363 q_a q_b
+                s4[slot] = make_float4((float)req, (float)((hb ? 5.0 * sf.w_hb : sf.w_vdw) * eps),
+                                       hb ? -(float)(6.0 * sf.w_hb * eps) : (float)(2.0 * sf.w_vdw * eps),
+                                       (float)(S_of(ia) * V_of(ib) + S_of(ib) * V_of(ia)));
+                sq[slot] = (float)(sf.w_el * 332.06363 * (double)l->charge[ia] * (double)l->charge[ib]);
+                return;
+            }
             s4[slot] = make_float4((float)(req * req), (float)((hb ? 5.0 : 1.0) * eps),
                                    hb ? -(float)(6.0 * eps) : (float)(2.0 * eps),
                                    (float)((double)ta.S * tb.V + (double)tb.S * ta.V));
@@ -359,6 +389,12 @@ int prepare_ligand(const dock_ligand *l, const dock_type_param *tp, int n_types,
         const dock_type_param &ti = tp[l->type[i]], &tj = tp[l->type[j]];
         const double req = 0.5 * ((double)ti.R + (double)tj.R);
         const float eps_ij = (float)std::sqrt((double)ti.eps * (double)tj.eps);
+        if (ad4) {   // {r_eq, +-w eps_ij, w_ds (S'_i V_j + S'_j V_i), w_el 332.06363 q_i q_j}
+            const float we = (float)((hb ? sf.w_hb : sf.w_vdw) * std::sqrt((double)ti.eps * (double)tj.eps));
+            pprm[q] = make_float4((float)req, hb ? -we : we, (float)(S_of(i) * V_of(j) + S_of(j) * V_of(i)),
+                                  (float)(sf.w_el * 332.06363 * (double)l->charge[i] * (double)l->charge[j]));
+            continue;
+        }
         pprm[q] = make_float4((float)(req * req), hb ? -eps_ij : eps_ij,
                               (float)((double)ti.S * tj.V + (double)tj.S * ti.V),
                               (float)(332.06363 / 4.0 * (double)l->charge[i] * (double)l->charge[j]));

@@ -22,8 +22,17 @@ struct Prepared {
     std::vector<uint8_t> blob;                    // the constant block, layout.blob_bytes
 };
 
-// D1 + blob assembly.  Returns DOCK_OK or DOCK_E_INPUT with `err` naming the field/index.
-int prepare_ligand(const dock_ligand *l, const dock_type_param *tp, int n_types, Prepared *out, std::string *err);
+// Scoring function of a context (dock_params.scoring and the D5-AD4 coefficients, NEXT-2).
+struct Scoring {
+    int sf = 0;                   // DOCK_SF_D5 or DOCK_SF_AD4
+    double w_vdw = 1, w_hb = 1, w_el = 1, w_ds = 1, w_tors = 0, qasp = 0;
+};
+Scoring scoring_of(const dock_params &p);
+
+// D1 + blob assembly (pair constants in the form of `sf`).  Returns DOCK_OK or
+// DOCK_E_INPUT with `err` naming the field/index.
+int prepare_ligand(const dock_ligand *l, const dock_type_param *tp, int n_types, const Scoring &sf, Prepared *out,
+                   std::string *err);
 
 // Grid validation and packing into one float4 {M_type, M_E, M_D, 0} per (type, node).
 int pack_grid(const dock_grids *g, std::vector<float4> *packed, std::string *err);

@@ -12,12 +12,36 @@
 
 #include "dock_internal.h"
 
+// This header (and kernels.cu) is compiled twice: once for the D5 scoring function
+// (namespace dk::d5) and once with -DDK_AD4 for the NEXT-2 AutoDock4.1-calibrated variant
+// (namespace dk::ad4).  Only the pair arithmetic differs; the launchers in
+// kernels.cuh dispatch on LigDev::sf.
+#ifdef DK_AD4
+#define DK_SF_NS ad4
+#else
+#define DK_SF_NS d5
+#endif
+
 namespace dk {
+namespace DK_SF_NS {
 
 constexpr float kElec4 = 332.06363f * 0.25f;                  // D5: 332.06363 / (4 rho^2)
 constexpr float kInvTwoSigma2 = 1.0f / (2.0f * 3.6f * 3.6f);    // desolvation sigma 3.6 Å
 constexpr float kExpScale = -kInvTwoSigma2 * 1.4426950408889634f;   // exp(-x/2s^2) = 2^(x*kExpScale)
 constexpr float kOut = 1e5f;                                    // D4.5 out-of-grid penalty
+#ifdef DK_AD4
+// D5-AD4: smoothing half-window, cutoffs (compared on rho^2), and the
+// Mehler-Solmajer dielectric eps(r) = A + B / (1 + k e^{-lambda B r}), B = 78.4 - A.
+constexpr float kSmoothH = 0.25f;                               // smooth / 2 = 0.5 Å / 2
+constexpr float kCutVdw2 = 8.0f * 8.0f;                         // vdW / H-bond: r < 8 Å
+constexpr float kCutEl2 = 20.48f * 20.48f;                      // elec + desolv: r < 20.48 Å
+constexpr float kDielA = -8.5525f;
+constexpr float kDielB = 78.4f + 8.5525f;
+constexpr float kDielK = 7.7839f;
+constexpr float kDielLB = 0.003627f * (78.4f + 8.5525f);          // lambda B
+constexpr float kDielC = -kDielLB * 1.4426950408889634f;         // e^{-lambda B r} = 2^(kDielC r)
+constexpr float kDielLB2 = kDielLB * (78.4f + 8.5525f);           // lambda B^2
+#endif
 #ifndef DK_WALK_DEPTH
 #define DK_WALK_DEPTH 4
 #endif
@@ -40,6 +64,7 @@ struct LigSm {
     const float *slotq;           // pair-slot 332.06363/4 q_i q_j (slot_mode)
     int NC, tail_rot, slot_mode;
     int energy_tiles;             // energy-only evaluation through the pair tiles (no pair list)
+    float wA_v, wB_v, wA_h, wB_h, qscale;   // D5-AD4 constants (LigDev; unused by D5)
 };
 
 // Gradient-path pose index: chunk c = a / W lives at [c][2W], its copy at [c][2W] + W.
@@ -98,6 +123,12 @@ __device__ __forceinline__ float rcp_approx(float x) {
 #endif
 }
 
+__device__ __forceinline__ float rsqrt_approx(float x) {
+    float y;
+    asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
 // sin/cos of an unwrapped angle: two-constant Cody-Waite reduction to [-pi, pi], then the
 // SFU (__sincosf, |err| < 4e-7 there).  Genes are never wrapped (D3), so the reduction
 // matters; beyond |x| = 1e5 the accurate library path is used.
@@ -112,6 +143,31 @@ __device__ __forceinline__ void fast_sincos(float x, float &s, float &c) {
     }
 }
 
+#ifdef DK_AD4
+// D5-AD4 vdW / H-bond at the smoothed distance: the smoothed r_s (minimum of the potential
+// over [r - 0.25, r + 0.25] Å: r + 0.25 below r_eq - 0.25, r - 0.25 above r_eq + 0.25, r_eq
+// in between) and 1 / r_s^2.
+__device__ __forceinline__ float ad4_smooth(float r, float req) {
+    const float lo = r + kSmoothH;
+    return lo < req ? lo : fmaxf(r - kSmoothH, req);
+}
+
+// D5-AD4 pair energy from precomputed pair constants (energy-only path):
+// pp = {r_eq, +-w eps_ij (negative: H-bond pair), w_ds (S'_i V_j + S'_j V_i), w_el 332.06363 q_i q_j}.
+__device__ __forceinline__ float pair_e_pre(float rho2, float4 pp) {
+    const bool hb = __float_as_int(pp.y) < 0;
+    rho2 = fmaxf(rho2, 1e-4f);                           // 0.01 Å clamp
+    const float r = rho2 * rsqrt_approx(rho2);
+    const float rs = ad4_smooth(r, pp.x);
+    const float x2 = pp.x * pp.x * rcp_approx(rs * rs), x4 = x2 * x2, x6 = x4 * x2, x12 = x6 * x6;
+    const float vdw = hb ? fmaf(5.0f, x12, -6.0f * (x6 * x4)) : fmaf(-2.0f, x6, x12);
+    const float Ev = rho2 < kCutVdw2 ? fabsf(pp.y) * vdw : 0.0f;
+    const float u = kDielK * ex2_approx(kDielC * r), sg = 1.0f + u;
+    const float Eel = pp.w * sg * rcp_approx(r * fmaf(kDielA, sg, kDielB));   // qq / (r eps(r))
+    const float Eds = pp.z * ex2_approx(rho2 * kExpScale);
+    return Ev + (rho2 < kCutEl2 ? Eel + Eds : 0.0f);
+}
+#else
 // D5 pair energy from precomputed pair constants (energy-only path).
 __device__ __forceinline__ float pair_e_pre(float rho2, float4 pp) {
     const bool hb = __float_as_int(pp.y) < 0;            // H-bond pair: eps_ij stored negated
@@ -121,6 +177,7 @@ __device__ __forceinline__ float pair_e_pre(float rho2, float4 pp) {
     const float vdw = hb ? fmaf(5.0f, x12, -6.0f * (x6 * x4)) : fmaf(-2.0f, x6, x12);   // 12-10 / 12-6
     return fmaf(fabsf(pp.y), vdw, fmaf(pp.w, inv, pp.z * ex2_approx(rho2 * kExpScale)));
 }
+#endif
 
 // D5 pair energy and dE/d(rho^2) from per-atom parameters (gradient path).
 __device__ __forceinline__ float pair_eg(float rho2, float4 pi, float qi, float4 pj, float qj, bool hb, float &dE) {
@@ -156,6 +213,56 @@ __device__ __forceinline__ float vdw_ab(float x2, float A, float B, float &dvr) 
     return tA - tB;
 }
 
+#ifdef DK_AD4
+// D5-AD4 pair energy and dE/d(rho^2), given rq = r_eq, the weighted vdW coefficients, the
+// weighted desolvation product and qq = w_el 332.06363 q_i q_j:
+//   vdW at the smoothed r_s: dE/drho^2 = (dE/dr_s)(dr_s/dr) / 2r = dvr / (r_s r), 0 on the plateau;
+//   elec qq s / (r D), s = 1 + k e^{-lambda B r}, D = A s + B (eps = D / s):
+//     dE/drho^2 = -E (1/r + eps'/eps) / 2r, eps'/eps = lambda B^2 (s - 1) / (s D);
+//   desolvation as D5; cutoffs on rho^2; zero force inside the clamp.
+__device__ __forceinline__ float pair_eg_ab(float rho2, float rq, float A, float B, float sv, float qq, float &dE) {
+    const bool clamped = rho2 < 1e-4f;
+    rho2 = fmaxf(rho2, 1e-4f);                           // 0.01 Å clamp
+    const float ir = rsqrt_approx(rho2), r = rho2 * ir;
+    const float rs = ad4_smooth(r, rq);
+    const float irs2 = rcp_approx(rs * rs);
+    float dvr;
+    const float Ev = vdw_ab(rq * rq * irs2, A, B, dvr);
+    const float dv = rs == rq ? 0.0f : dvr * (rs * irs2) * ir;
+    const bool in_v = rho2 < kCutVdw2;
+    const float u = kDielK * ex2_approx(kDielC * r), sg = 1.0f + u;
+    const float isd = rcp_approx(sg * fmaf(kDielA, sg, kDielB));
+    const float Eel = qq * (sg * sg) * isd * ir;
+    const float del = -0.5f * Eel * ir * fmaf(kDielLB2 * u, isd, ir);
+    const float Eds = sv * ex2_approx(rho2 * kExpScale);
+    const bool in_e = rho2 < kCutEl2;
+    const float d = (in_v ? dv : 0.0f) + (in_e ? fmaf(-Eds, kInvTwoSigma2, del) : 0.0f);
+    dE = clamped ? 0.0f : d;
+    return (in_v ? Ev : 0.0f) + (in_e ? Eel + Eds : 0.0f);
+}
+
+// Energy only, from the same operands (large-ligand energy tiles).
+__device__ __forceinline__ float pair_e_ab(float rho2, float rq, float A, float B, float sv, float qq) {
+    rho2 = fmaxf(rho2, 1e-4f);
+    const float r = rho2 * rsqrt_approx(rho2);
+    const float rs = ad4_smooth(r, rq);
+    float dvr;
+    const float Ev = vdw_ab(rq * rq * rcp_approx(rs * rs), A, B, dvr);
+    const float u = kDielK * ex2_approx(kDielC * r), sg = 1.0f + u;
+    const float Eel = qq * sg * rcp_approx(r * fmaf(kDielA, sg, kDielB));
+    const float Eds = sv * ex2_approx(rho2 * kExpScale);
+    return (rho2 < kCutVdw2 ? Ev : 0.0f) + (rho2 < kCutEl2 ? Eel + Eds : 0.0f);
+}
+
+// pair-slot / tile operand for r_eq: r_eq itself (smoothing compares distances)
+__device__ __forceinline__ float sf_req(float req) { return req; }
+// own-charge scale (w_el 332.06363) and the vdW / H-bond coefficients per unit eps_ij
+__device__ __forceinline__ float sf_qscale(const LigSm &L) { return L.qscale; }
+__device__ __forceinline__ void sf_vdw_coeffs(const LigSm &L, bool hb, float eps, float &A, float &B) {
+    A = eps * (hb ? L.wA_h : L.wA_v);
+    B = eps * (hb ? L.wB_h : L.wB_v);
+}
+#else
 // D5 pair energy and dE/d(rho^2) on the gradient path, given the vdW coefficients:
 // E_el = qq / rho^2; E_ds = SV exp(-rho^2 / 2 sigma^2); zero force inside the clamp.
 __device__ __forceinline__ float pair_eg_ab(float rho2, float req2, float A, float B, float sv, float qq, float &dE) {
@@ -170,6 +277,23 @@ __device__ __forceinline__ float pair_eg_ab(float rho2, float req2, float A, flo
     dE = clamped ? 0.0f : d;
     return Evdw + Eel + Eds;
 }
+
+// Energy only, from the same operands (large-ligand energy tiles).
+__device__ __forceinline__ float pair_e_ab(float rho2, float req2, float A, float B, float sv, float qq) {
+    rho2 = fmaxf(rho2, 1e-4f);
+    const float inv = rcp_approx(rho2);
+    float dvr;
+    const float Ev = vdw_ab(req2 * inv, A, B, dvr);
+    return Ev + fmaf(qq, inv, sv * ex2_approx(rho2 * kExpScale));
+}
+
+__device__ __forceinline__ float sf_req(float req) { return req * req; }
+__device__ __forceinline__ float sf_qscale(const LigSm &) { return kElec4; }
+__device__ __forceinline__ void sf_vdw_coeffs(const LigSm &, bool hb, float eps, float &A, float &B) {
+    A = hb ? 5.0f * eps : eps;
+    B = hb ? -6.0f * eps : 2.0f * eps;
+}
+#endif
 
 // D4 intermolecular energy of one atom and its gradient.
 __device__ __forceinline__ float inter_atom(const GridDev &g, int type, float q, float rx, float ry,
@@ -226,7 +350,7 @@ struct OwnPair {
 // accumulator (+dE d) and the partner accumulator (-dE d); the factor 2 of
 // dE/dr_i = 2 dE/drho2 (r_i - r_j) is applied once per atom at the end.
 // Partner data: pose record rj (x, y, z, q) and signed params pj (role in the signs).
-__device__ __forceinline__ void tile_pair(bool on, float rxi, float ryi, float rzi, const OwnPair &o, float4 rj,
+__device__ __forceinline__ void tile_pair(const LigSm &L, bool on, float rxi, float ryi, float rzi, const OwnPair &o, float4 rj,
                                           float4 pj, float &e, float &gxi, float &gyi, float &gzi, float &fx,
                                           float &fy, float &fz) {
     const float dx = rxi - rj.x, dy = ryi - rj.y, dz = rzi - rj.z;
@@ -235,9 +359,9 @@ __device__ __forceinline__ void tile_pair(bool on, float rxi, float ryi, float r
     const float req = o.R + fabsf(pj.x);                 // (R_i + R_j) / 2
     const float eps = o.e * fabsf(pj.y);                 // sqrt(eps_i eps_j)
     const bool hb = o.hbc && __float_as_int(o.don ? pj.x : pj.y) < 0;   // donor-acceptor (role in sign bits)
-    const float A = hb ? 5.0f * eps : eps;
-    const float B = hb ? -6.0f * eps : 2.0f * eps;
-    E = pair_eg_ab(rho2, req * req, A, B, fmaf(o.S, pj.w, pj.z * o.V), o.q * rj.w, dE);
+    float A, B;
+    sf_vdw_coeffs(L, hb, eps, A, B);
+    E = pair_eg_ab(rho2, sf_req(req), A, B, fmaf(o.S, pj.w, pj.z * o.V), o.q * rj.w, dE);
     dE = on ? dE : 0.0f;
     e += on ? E : 0.0f;
     gxi = fmaf(dE, dx, gxi); gyi = fmaf(dE, dy, gyi); gzi = fmaf(dE, dz, gzi);
@@ -273,7 +397,7 @@ __device__ __forceinline__ void intra_tiles(const LigSm &L, const Scratch &S, in
     for (int c = 0; c < MAXC; ++c) {
         const int a = sub + W * c;
         const bool ok = a < N;
-        own[c].q = ok ? kElec4 * S.r[ridx<W>(a)].w : 0.0f;
+        own[c].q = ok ? sf_qscale(L) * S.r[ridx<W>(a)].w : 0.0f;
         const float4 pp = L.ppar[ridx<W>(a)];
         own[c].R = fabsf(pp.x); own[c].e = fabsf(pp.y); own[c].S = pp.z; own[c].V = pp.w;
         own[c].hbc = __float_as_int(pp.x) < 0 || __float_as_int(pp.y) < 0;   // sign bits: -0.0 counts
@@ -303,7 +427,7 @@ __device__ __forceinline__ void intra_tiles(const LigSm &L, const Scratch &S, in
             float fx = 0.f, fy = 0.f, fz = 0.f;
 #pragma unroll 4
             for (int s = s0; s <= s1; ++s) {
-                tile_pair((rot >> s) & 1u, rx[I], ry[I], rz[I], own[I], rrow[s], qrow[s], e, hx[I], hy[I], hz[I], fx,
+                tile_pair(L, (rot >> s) & 1u, rx[I], ry[I], rz[I], own[I], rrow[s], qrow[s], e, hx[I], hy[I], hz[I], fx,
                           fy, fz);
                 if (s < s1) {
                     const int src = (sub + 1) & (W - 1);
@@ -331,7 +455,7 @@ __device__ __forceinline__ void intra_tiles(const LigSm &L, const Scratch &S, in
                 if (I > Bf) break;
                 const int a = I * W + sub;
                 const bool on = (I < Bf || sub < k) && ((mrow[a >> 5] >> (a & 31)) & 1u);
-                tile_pair(on, rx[I], ry[I], rz[I], own[I], rj, pj, e, hx[I], hy[I], hz[I], fx, fy, fz);
+                tile_pair(L, on, rx[I], ry[I], rz[I], own[I], rj, pj, e, hx[I], hy[I], hz[I], fx, fy, fz);
             }
             fx = gsum<W>(fx, mask); fy = gsum<W>(fy, mask); fz = gsum<W>(fz, mask);
 #pragma unroll
@@ -448,7 +572,7 @@ __device__ __forceinline__ float intra_tiles_energy(const LigSm &L, const Scratc
         const int aI = I * W + sub;
         const bool okI = aI < N;
         const float4 po = L.ppar[ridx<W>(aI)];
-        const float qi = okI ? kElec4 * S.r[ridx<W>(aI)].w : 0.0f;
+        const float qi = okI ? sf_qscale(L) * S.r[ridx<W>(aI)].w : 0.0f;
         const float Ri = fabsf(po.x), ei = fabsf(po.y);
         const bool hbc = __float_as_int(po.x) < 0 || __float_as_int(po.y) < 0, don = __float_as_int(po.y) < 0;
 #pragma unroll
@@ -473,13 +597,12 @@ __device__ __forceinline__ float intra_tiles_energy(const LigSm &L, const Scratc
             for (int st = s0 + i0; st < s0 + i1; ++st) {
                 const float4 rj = rrow[st], pj = qrow[st];
                 const float dx = rx[I] - rj.x, dy = ry[I] - rj.y, dz = rz[I] - rj.z;
-                const float rho2 = fmaxf(fmaf(dx, dx, fmaf(dy, dy, dz * dz)), 1e-4f);
-                const float inv = rcp_approx(rho2);
+                const float rho2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
                 const float req = Ri + fabsf(pj.x), eps = ei * fabsf(pj.y);
                 const bool hb = hbc && __float_as_int(don ? pj.x : pj.y) < 0;
-                float dvr;
-                const float Ev = vdw_ab(req * req * inv, hb ? 5.0f * eps : eps, hb ? -6.0f * eps : 2.0f * eps, dvr);
-                const float E = Ev + fmaf(qi * rj.w, inv, o_sv(po, pj) * ex2_approx(rho2 * kExpScale));
+                float A, B;
+                sf_vdw_coeffs(L, hb, eps, A, B);
+                const float E = pair_e_ab(rho2, sf_req(req), A, B, o_sv(po, pj), qi * rj.w);
                 e += ((rot >> st) & 1u) ? E : 0.0f;
             }
         }
@@ -751,4 +874,5 @@ __device__ float eval_group(const LigSm &L, const GridDev &grid, const Scratch &
     }
 }
 
+}  // namespace DK_SF_NS
 }  // namespace dk

@@ -100,7 +100,7 @@ extern "C" int dock_screen(const dock_grids *grids, const dock_type_param *type_
         for (int t = 0; t < prep_threads; ++t)
             pool.emplace_back([&] {
                 for (int i; (i = next.fetch_add(1)) < n_ligands;)
-                    prep_rc[i] = dk::prepare_ligand(&ligands[i], type_params, grids->n_types, &prep[i], &prep_err[i]);
+                    prep_rc[i] = dk::prepare_ligand(&ligands[i], type_params, grids->n_types, dk::scoring_of(p), &prep[i], &prep_err[i]);
             });
         for (auto &t : pool) t.join();
     }

@@ -38,6 +38,19 @@ def test_params_default(dock):
     assert (p.p_tour, p.p_cross, p.p_mut) == (np.float32(0.6), np.float32(0.8), np.float32(0.02))
     assert p.ls_max_iters == 300 and p.max_generations == 27000 and p.gens_per_graph == 16
     assert abs(p.ad_rho - 0.8) < 1e-7 and abs(p.ad_eps - 1e-2) < 1e-9
+    # NEXT-2: D5 by default, AD4.1 coefficients filled in for DOCK_SF_AD4
+    assert p.scoring == dock.SF_D5
+    assert (p.w_vdw, p.w_hb, p.w_el, p.w_ds, p.w_tors, p.qasp) == tuple(
+        np.float32(v) for v in (0.1662, 0.1209, 0.1406, 0.1322, 0.2983, 0.01097))
+
+
+@pytest.mark.parametrize("bad", [dict(scoring=2), dict(scoring=1, w_el=-1.0), dict(scoring=1, qasp=float("nan"))])
+def test_scoring_params_validated_before_device(dock, bad):
+    from gen import config_inputs
+    cfg, lig, grid = config_inputs("tiny")
+    with pytest.raises(dock.DockError) as e:
+        dock.Docker.from_inputs(grid, lig, **bad)
+    assert e.value.code == dock.DOCK_E_INPUT
 
 
 def test_builtin_table_matches_input_table(dock):

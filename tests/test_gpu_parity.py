@@ -115,6 +115,7 @@ def test_energy_gradient_pose_parity(dock, name, n):
     X[:5, 6:] = 0.0
     E, Gd, xyz = d.eval(X, grad=True, xyz=True)
     E0, _, _ = d.eval(X, grad=False, xyz=False)            # energy-only kernel path
+    assert np.isfinite(E).all() and np.isfinite(E0).all() and np.isfinite(Gd).all()
     bad_e = bad_g = bad_x = ex_e = ex_g = 0
     hi = np.array(grid.n) - 1
     for i in range(n):
