@@ -127,6 +127,8 @@ def lib():
                                   P(i64), P(i), P(d)]
         L.or_dock_run.restype = i
         L.or_sum_evals.argtypes = [i, P(i64)]; L.or_sum_evals.restype = i64
+        L.or_rmsd.argtypes = [i, P(d), P(d)]; L.or_rmsd.restype = d
+        L.or_cluster.argtypes = [i, i, P(d), P(d), d, P(i), P(d), P(i)]; L.or_cluster.restype = i
         _lib = L
     return _lib
 
@@ -376,3 +378,22 @@ def dock_run(prob, pp, pop, max_evals, seed, ligand_id=0, run=0):
 def sum_evals(counters):
     c = np.ascontiguousarray(counters, dtype=np.int64)
     return int(lib().or_sum_evals(c.shape[0], _p(c, C.c_int64)))
+
+
+# ---------------------------------------------------------------------------
+# NEXT-3: clustering of per-run best poses
+# ---------------------------------------------------------------------------
+def rmsd(a, b):
+    a = _f64(a).reshape(-1); b = _f64(b).reshape(-1)
+    return float(lib().or_rmsd(a.shape[0] // 3, _p(a, C.c_double), _p(b, C.c_double)))
+
+
+def cluster(xyz, E, rmsd_tol=2.0):
+    """(n_clusters, cluster [n], rmsd_to_seed [n], rank [n]) of poses xyz [n, N, 3]."""
+    x = _f64(xyz)
+    n = x.shape[0]; N = x.shape[1] if x.ndim == 3 else x.reshape(n, -1).shape[1] // 3
+    e = _f64(E)
+    c = np.zeros(max(n, 1), np.int32); r = np.zeros(max(n, 1)); rk = np.zeros(max(n, 1), np.int32)
+    nc = lib().or_cluster(n, N, _p(x, C.c_double), _p(e, C.c_double), float(rmsd_tol), _p(c, C.c_int),
+                          _p(r, C.c_double), _p(rk, C.c_int))
+    return int(nc), c[:n], r[:n], rk[:n]

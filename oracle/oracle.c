@@ -753,3 +753,46 @@ int or_dock_run(const or_problem *P, const or_params *pp, int pop, int64_t max_e
     free(genes); free(ng); free(E); free(nE); free(cnt); free(perm);
     return 0;
 }
+
+/* ========================================================================
+ * NEXT-3 — clustering of the per-run best poses (DESIGN.md §12
+ * reading D12): AutoDock's cluster analysis with plain RMSD, written as its definition.
+ * ======================================================================== */
+double or_rmsd(int N, const double *a, const double *b) {
+    double s = 0.0;
+    for (int i = 0; i < 3 * N; ++i) s += (a[i] - b[i]) * (a[i] - b[i]);
+    return N > 0 ? sqrt(s / N) : 0.0;
+}
+
+int or_cluster(int n, int N, const double *xyz, const double *E, double rmsd_tol, int *cluster,
+               double *rmsd_to_seed, int *rank) {
+    int *order = (int *)malloc(sizeof(int) * (n > 0 ? n : 1));
+    int *seed = (int *)malloc(sizeof(int) * (n > 0 ? n : 1));
+    for (int i = 0; i < n; ++i) order[i] = i;
+    /* insertion sort by (key, index): key = E, NaN = +inf */
+    for (int i = 1; i < n; ++i) {
+        int v = order[i], j = i - 1;
+        while (j >= 0) {
+            double kj = key_of(E[order[j]]), kv = key_of(E[v]);
+            if (kj > kv || (kj == kv && order[j] > v)) { order[j + 1] = order[j]; --j; }
+            else break;
+        }
+        order[j + 1] = v;
+    }
+    int nc = 0;
+    for (int t = 0; t < n; ++t) {
+        int k = order[t];
+        if (rank) rank[k] = t;
+        int c = -1;
+        double r = 0.0;
+        for (int s = 0; s < nc; ++s) {
+            r = or_rmsd(N, xyz + (size_t)3 * N * k, xyz + (size_t)3 * N * seed[s]);
+            if (r < rmsd_tol) { c = s; break; }
+        }
+        if (c < 0) { c = nc; seed[nc++] = k; r = 0.0; }
+        cluster[k] = c;
+        rmsd_to_seed[k] = r;
+    }
+    free(order); free(seed);
+    return nc;
+}

@@ -142,6 +142,16 @@ int or_dock_run(const or_problem *P, const or_params *pp, int pop, int64_t max_e
                 double *best_E, double *best_genes, int64_t *evals_used, int *generations,
                 double *final_E /*[pop] nullable*/);
 
+/* ---- NEXT-3: RMSD clustering of per-run best poses ----
+   Poses sorted by energy (ascending; NaN last; ties -> lower index).  The first pose
+   seeds cluster 0; each next pose joins the lowest-numbered cluster whose seed is within
+   rmsd_tol (plain RMSD over the N atoms, no superposition: all poses share the receptor
+   frame), else seeds a new cluster.  Outputs per pose: cluster id, RMSD to its cluster's
+   seed (0 for a seed), rank in the energy order.  Returns the number of clusters. */
+int or_cluster(int n, int N, const double *xyz /*[n*N*3]*/, const double *E /*[n]*/, double rmsd_tol,
+               int *cluster /*[n]*/, double *rmsd_to_seed /*[n]*/, int *rank /*[n] nullable*/);
+double or_rmsd(int N, const double *a, const double *b);
+
 /* D11 / Listing 1: sum of per-individual evaluation counters. */
 int64_t or_sum_evals(int n, const int64_t *counters);
 
