@@ -257,6 +257,47 @@ int dock_screen(const dock_grids *grids, const dock_type_param *type_params,
                 int32_t *device_of, dock_screen_stats *stats);
 const char *dock_screen_last_error(void);
 
+/* ---------------- results: pose clustering and serialisation (NEXT-3) ----------------
+   SURVEY.md §8(f) rank 3; SPEC S:42-45 (DockingResult), S:66-74 (write_result).  The paper
+   removed file writing to time the kernels; these run after the search. */
+
+/* AutoDock-style cluster analysis of n poses of this context's ligand (reading D12): poses
+   in ascending energy order (NaN last, ties -> lower index); each joins the lowest-numbered
+   cluster whose seed (first pose) is within rmsd_tol Å, else seeds a new cluster.  RMSD is
+   plain (no superposition: all poses share the receptor frame), accumulated in FP64 on
+   the device.  Host arrays: xyz [n*N*3] (caller atom order, e.g. dock_run's best_xyz),
+   energy [n] -> cluster [n], rmsd_to_seed [n] (0 for seeds), rank [n] (energy order; may be
+   NULL), *n_clusters.  1 <= n <= 4096 (n = 0: *n_clusters = 0).  One CTA on the context's
+   device and stream; synchronous. */
+int dock_cluster(dock_ctx *ctx, int32_t n, const float *xyz, const float *energy, float rmsd_tol,
+                 int32_t *cluster, float *rmsd_to_seed, int32_t *rank, int32_t *n_clusters);
+
+/* A docking result to serialise (all host arrays; optional ones may be NULL). */
+typedef struct {
+    int32_t n_runs, n_atoms, n_genes;
+    const float *best_energy;     /* [n_runs] */
+    const float *best_genotype;   /* [n_runs*n_genes] */
+    const float *best_xyz;        /* [n_runs*n_atoms*3] or NULL */
+    const int64_t *evals;         /* [n_runs] or NULL */
+    const int32_t *generations;   /* [n_runs] or NULL */
+    const int32_t *cluster;       /* [n_runs] or NULL (dock_cluster) */
+    const float *rmsd_to_seed;    /* [n_runs] or NULL */
+    const float *dG;              /* [n_runs] binding estimates or NULL (dock_eval_terms) */
+    int32_t n_timings;            /* per-kernel timing table (may be 0) */
+    const char *const *timing_names;
+    const double *timing_ms;
+} dock_result_view;
+enum { DOCK_FMT_JSON = 0, DOCK_FMT_CSV = 1 };
+
+/* Serialise r as JSON ({best_energy, best_run, best_genotype, best_coordinates, per_run[],
+   clusters[], timings{}}; the overall best is the minimum over runs, NaN as +inf, lowest run
+   on ties) or CSV (header + one row per run: run, best_energy, evals, generations,
+   cluster, rmsd_to_seed, dG; absent columns empty).  Floats as %.9g (float32 round-trips
+   exactly), NaN -> JSON null / empty CSV field.  *len = bytes needed including the NUL;
+   returns DOCK_E_INPUT (text not written) if buf is NULL or cap < *len, so callers may size
+   the buffer with a first call.  Host only: no device needed. */
+int dock_write_result(const dock_result_view *r, int32_t format, char *buf, size_t cap, size_t *len);
+
 /* Kernel-launch counter of this context (for the benchmark's gpu_launches claim). */
 int64_t dock_launch_count(const dock_ctx *ctx);
 

@@ -66,6 +66,17 @@ class ScreenStats(C.Structure):
                 ("n_failed", C.c_int32), ("launches", C.c_int64)]
 
 
+class ResultView(C.Structure):
+    _fields_ = [("n_runs", C.c_int32), ("n_atoms", C.c_int32), ("n_genes", C.c_int32),
+                ("best_energy", C.POINTER(C.c_float)), ("best_genotype", C.POINTER(C.c_float)),
+                ("best_xyz", C.POINTER(C.c_float)), ("evals", C.POINTER(C.c_int64)),
+                ("generations", C.POINTER(C.c_int32)), ("cluster", C.POINTER(C.c_int32)),
+                ("rmsd_to_seed", C.POINTER(C.c_float)), ("dG", C.POINTER(C.c_float)),
+                ("n_timings", C.c_int32), ("timing_names", C.POINTER(C.c_char_p)),
+                ("timing_ms", C.POINTER(C.c_double))]
+
+
+FMT_JSON, FMT_CSV = 0, 1
 MAX_GENES = 38
 
 
@@ -90,6 +101,8 @@ def _load():
         "dock_eval": (i32, [v, i32, P(f), P(f), P(f), P(f)]),
         "dock_eval_device": (i32, [v, i32, v, v, v, v, v]),
         "dock_eval_terms": (i32, [v, i32, P(f), P(f), P(f), P(f)]),
+        "dock_cluster": (i32, [v, i32, P(f), P(f), f, P(i32), P(f), P(i32), P(i32)]),
+        "dock_write_result": (i32, [P(ResultView), i32, C.c_char_p, C.c_size_t, P(C.c_size_t)]),
         "dock_bench_part": (i32, [v, i32, i32, i32, v, v, v]),
         "dock_get_pairs": (i32, [v, P(i32)]),
         "dock_get_torsions": (i32, [v, P(i32), P(C.c_uint8)]),
@@ -120,7 +133,46 @@ EXPORTED = ("dock_params_default", "dock_builtin_type_param", "dock_init", "dock
             "dock_run_device", "dock_eval", "dock_eval_device", "dock_get_pairs", "dock_get_torsions",
             "dock_philox", "dock_stream_words", "dock_ga_step", "dock_ls_step", "dock_launch_count",
             "dock_topology", "dock_kernel_stats", "dock_upload_bytes", "dock_screen", "dock_screen_last_error",
-            "dock_bench_part", "dock_eval_terms")
+            "dock_bench_part", "dock_eval_terms", "dock_cluster", "dock_write_result")
+
+
+def write_result(res: dict, fmt: str = "json", timings: dict | None = None) -> str:
+    """dock_write_result (NEXT-3): res has best_E [R], best_genes [R, G] and optionally
+    best_xyz [R, N, 3], evals, generations, cluster, rmsd_to_seed, dG (arrays over runs)."""
+    keep = []
+
+    def arr(key, dt, ct):
+        v = res.get(key)
+        if v is None:
+            return None
+        a = np.ascontiguousarray(v, dtype=dt)
+        keep.append(a)
+        return _ptr(a, ct)
+    bE = np.ascontiguousarray(res["best_E"], dtype=np.float32)
+    bG = np.ascontiguousarray(res["best_genes"], dtype=np.float32)
+    bG = bG.reshape(bE.shape[0], bG.shape[-1] if bG.ndim > 1 else -1)
+    keep += [bE, bG]
+    r = ResultView()
+    r.n_runs = bE.shape[0]; r.n_genes = bG.shape[1]
+    xyz = res.get("best_xyz")
+    r.n_atoms = 0 if xyz is None else int(np.asarray(xyz).shape[1])
+    r.best_energy = _ptr(bE, C.c_float); r.best_genotype = _ptr(bG, C.c_float)
+    r.best_xyz = arr("best_xyz", np.float32, C.c_float)
+    r.evals = arr("evals", np.int64, C.c_int64)
+    r.generations = arr("generations", np.int32, C.c_int32)
+    r.cluster = arr("cluster", np.int32, C.c_int32)
+    r.rmsd_to_seed = arr("rmsd_to_seed", np.float32, C.c_float)
+    r.dG = arr("dG", np.float32, C.c_float)
+    timings = timings or {}
+    names = (C.c_char_p * max(1, len(timings)))(*[k.encode() for k in timings])
+    ms = np.ascontiguousarray(list(timings.values()) or [0.0], dtype=np.float64)
+    r.n_timings = len(timings); r.timing_names = names; r.timing_ms = _ptr(ms, C.c_double)
+    f = {"json": FMT_JSON, "csv": FMT_CSV}[fmt]
+    need = C.c_size_t(0)
+    lib.dock_write_result(C.byref(r), f, None, 0, C.byref(need))
+    buf = C.create_string_buffer(need.value)
+    _check(lib.dock_write_result(C.byref(r), f, buf, need.value, C.byref(need)))
+    return buf.value.decode()
 
 
 def topology(types, charges, xyz, bonds, rotatable, type_params, roles):
@@ -376,6 +428,18 @@ class Docker:
         out = [np.zeros(n, np.float32) for _ in range(3)]
         self._chk(lib.dock_eval_terms(self._ctx, n, _ptr(x, C.c_float), *(_ptr(o, C.c_float) for o in out)))
         return tuple(out)
+
+    # ---- NEXT-3 ----
+    def cluster(self, xyz, energy, rmsd_tol=2.0):
+        """dock_cluster: (n_clusters, cluster [n], rmsd_to_seed [n], rank [n]) of poses [n, N, 3]."""
+        x = np.ascontiguousarray(xyz, dtype=np.float32).reshape(-1, self.N, 3)
+        e = np.ascontiguousarray(energy, dtype=np.float32).reshape(-1)
+        n = x.shape[0]
+        c = np.zeros(max(n, 1), np.int32); r = np.zeros(max(n, 1), np.float32); rk = np.zeros(max(n, 1), np.int32)
+        nc = C.c_int32(0)
+        self._chk(lib.dock_cluster(self._ctx, n, _ptr(x, C.c_float), _ptr(e, C.c_float), float(rmsd_tol),
+                                   _ptr(c, C.c_int32), _ptr(r, C.c_float), _ptr(rk, C.c_int32), C.byref(nc)))
+        return int(nc.value), c[:n], r[:n], rk[:n]
 
     def eval_device(self, genotypes, energy, grad=None, xyz=None, stream=0):
         """torch CUDA tensors (float32, contiguous); stream = torch.cuda.Stream.cuda_stream or 0."""

@@ -9,8 +9,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libdock.so")
-SOURCES = ["kernels.cu", "prep.cpp", "dock_abi.cpp", "screen.cpp"]
-HEADERS = ["dock_internal.h", "engine.h", "kernels.cuh", "philox.cuh", "prep.h", "score.cuh"]
+SOURCES = ["kernels.cu", "prep.cpp", "dock_abi.cpp", "screen.cpp", "cluster.cu", "results.cpp"]
+HEADERS = ["dock_internal.h", "engine.h", "kernels.cuh", "philox.cuh", "prep.h", "score.cuh", "cluster.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc" if os.path.exists("/usr/local/cuda/bin/nvcc") else "nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC", "-diag-suppress", "177"]

@@ -18,6 +18,7 @@
 #include <string>
 #include <vector>
 
+#include "cluster.cuh"
 #include "engine.h"
 
 namespace {
@@ -638,6 +639,38 @@ int dock_eval_terms(dock_ctx *c, int32_t n, const float *genotypes, float *inter
     // AD4 binding estimate: inter + w_tors * T (host: one multiply-add per genotype)
     const float w_tors = c->params.scoring == DOCK_SF_AD4 ? c->params.w_tors : 0.0f;
     if (dG) for (int i = 0; i < n; ++i) dG[i] = hi[i] + w_tors * (float)c->prep.T;
+    return DOCK_OK;
+}
+
+int dock_cluster(dock_ctx *c, int32_t n, const float *xyz, const float *energy, float rmsd_tol, int32_t *cluster,
+                 float *rmsd_to_seed, int32_t *rank, int32_t *n_clusters) {
+    if (!c) return DOCK_E_INPUT;
+    if (!n_clusters) return input_error(c, "n_clusters: NULL");
+    if (n < 0 || n > dk::kClusterMaxPoses) return input_error(c, "n: must be in 0..4096");
+    if (n == 0) { *n_clusters = 0; return DOCK_OK; }
+    if (!xyz || !energy || !cluster || !rmsd_to_seed) return input_error(c, "xyz/energy/cluster/rmsd_to_seed: NULL");
+    if (!std::isfinite(rmsd_tol) || rmsd_tol < 0.f) return input_error(c, "rmsd_tol: must be finite and >= 0");
+    const int N = c->prep.N;
+    for (long long i = 0; i < (long long)n * N * 3; ++i)
+        if (!std::isfinite(xyz[i])) return input_error(c, "xyz[" + std::to_string(i) + "]: non-finite");
+    CK(cudaSetDevice(c->device));
+    DevBuf dx(c->stream), dE(c->stream), dc(c->stream), dr(c->stream), dk_(c->stream), dn(c->stream);
+    CK(dx.alloc(sizeof(float) * n * N * 3));
+    CK(dE.alloc(sizeof(float) * n));
+    CK(dc.alloc(sizeof(int) * n));
+    CK(dr.alloc(sizeof(float) * n));
+    CK(dk_.alloc(sizeof(int) * n));
+    CK(dn.alloc(sizeof(int)));
+    CK(cudaMemcpyAsync(dx.p, xyz, sizeof(float) * n * N * 3, cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemcpyAsync(dE.p, energy, sizeof(float) * n, cudaMemcpyHostToDevice, c->stream));
+    CK(dk::launch_cluster(n, N, (const float *)dx.p, (const float *)dE.p, rmsd_tol, (int *)dc.p, (float *)dr.p,
+                          (int *)dk_.p, (int *)dn.p, c->stream));
+    c->launches += 1;
+    CK(cudaMemcpyAsync(cluster, dc.p, sizeof(int) * n, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaMemcpyAsync(rmsd_to_seed, dr.p, sizeof(float) * n, cudaMemcpyDeviceToHost, c->stream));
+    if (rank) CK(cudaMemcpyAsync(rank, dk_.p, sizeof(int) * n, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaMemcpyAsync(n_clusters, dn.p, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
     return DOCK_OK;
 }
 

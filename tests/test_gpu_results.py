@@ -1,0 +1,92 @@
+"""GPU parity of NEXT-3 clustering (dock_cluster, k_cluster) against the oracle's
+or_cluster, and the end-to-end result path: run -> cluster -> dG -> write_result.
+
+Cluster ids and energy ranks are integers: bit-exact.  The RMSD threshold decision is
+taken in FP64 on both sides (only the summation order differs), so the fixtures assert
+that no pose-seed RMSD lies within 1e-9 Å of the tolerance."""
+import json
+
+import numpy as np
+import pytest
+
+import oracle
+from gen import config_inputs
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def dock():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    from paper_2203_02096_b200._build import build
+    build()
+    import paper_2203_02096_b200 as d
+    return d
+
+
+def min_threshold_margin(poses, tol):
+    n = poses.shape[0]
+    x = poses.reshape(n, -1).astype(np.float64)
+    d2 = ((x[:, None, :] - x[None, :, :]) ** 2).sum(-1) / poses.shape[1]
+    return np.abs(np.sqrt(d2) - tol).min()
+
+
+@pytest.mark.parametrize("n,spread,tol,seed", [(1, 1.0, 2.0, 0), (37, 1.5, 2.0, 1), (500, 1.2, 2.0, 2),
+                                               (2000, 3.0, 1.5, 3), (4096, 0.8, 2.0, 4), (300, 1.0, 0.0, 5)])
+def test_cluster_parity(dock, n, spread, tol, seed):
+    cfg, lig, grid = config_inputs("3ce3")
+    d = dock.Docker.from_inputs(grid, lig)
+    rng = np.random.default_rng(seed)
+    base = np.stack([rng.normal(0, 3, (d.N, 3)) for _ in range(6)])           # 6 "binding modes"
+    poses = (base[rng.integers(0, 6, n)] + rng.normal(0, spread, (n, 1, 3)) +
+             rng.normal(0, 0.3 * spread, (n, d.N, 3))).astype(np.float32)
+    E = rng.normal(-6, 2, n).astype(np.float32)
+    E[rng.integers(0, n, max(1, n // 50))] = np.float32(-6.0)                 # ties
+    if n > 10:
+        E[3] = np.nan
+    if n <= 2000 and n > 1 and tol > 0:
+        assert min_threshold_margin(poses, tol) > 1e-9
+    nc, c, r, rk = d.cluster(poses, E, tol)
+    onc, oc, orr, ork = oracle.cluster(poses.astype(np.float64), E.astype(np.float64), float(np.float32(tol)))
+    assert nc == onc
+    np.testing.assert_array_equal(c, oc)
+    np.testing.assert_array_equal(rk, ork)
+    np.testing.assert_allclose(r, orr, rtol=1e-6, atol=1e-6)
+    if tol > 0 and n > 37:
+        assert 1 < nc < n                                                      # non-degenerate fixture
+
+
+def test_cluster_rejects_bad_input(dock):
+    cfg, lig, grid = config_inputs("tiny")
+    d = dock.Docker.from_inputs(grid, lig)
+    with pytest.raises(dock.DockError):
+        d.cluster(np.zeros((4097, d.N, 3)), np.zeros(4097), 2.0)
+    with pytest.raises(dock.DockError):
+        d.cluster(np.zeros((3, d.N, 3)), np.zeros(3), -1.0)
+    x = np.zeros((3, d.N, 3)); x[1, 0, 0] = np.nan
+    with pytest.raises(dock.DockError):
+        d.cluster(x, np.zeros(3), 2.0)
+
+
+@pytest.mark.parametrize("scoring", [0, 1])
+def test_run_cluster_write_end_to_end(dock, scoring):
+    cfg, lig, grid = config_inputs("1stp")
+    d = dock.Docker.from_inputs(grid, lig, ls_method=1, ls_rate=0.06, scoring=scoring)
+    res = d.run(cfg.pop, 20, 60_000, 42)
+    nc, c, r, rk = d.cluster(res["best_xyz"], res["best_E"], 2.0)
+    onc, oc, orr, _ = oracle.cluster(res["best_xyz"].astype(np.float64), res["best_E"].astype(np.float64), 2.0)
+    assert nc == onc and np.array_equal(c, oc)
+    inter, intra, dG = d.eval_terms(res["best_genes"])
+    P = oracle.Problem(grid, lig, sf={} if scoring else None)
+    for i in range(20):
+        ref = P.energy(res["best_genes"][i].astype(np.float64), grad=False)
+        assert abs(dG[i] - P.binding_dG(ref["inter"])) <= max(1e-3, 1e-4 * abs(ref["inter"]))
+    res.update(cluster=c, rmsd_to_seed=r, dG=dG)
+    j = json.loads(dock.write_result(res, "json"))
+    b = int(np.argmin(res["best_E"]))
+    assert j["best_run"] == b and np.float32(j["best_energy"]) == res["best_E"][b]
+    assert np.array_equal(np.array(j["best_coordinates"], np.float32), res["best_xyz"][b])
+    assert sum(cl["size"] for cl in j["clusters"]) == 20 and len(j["clusters"]) == nc
+    assert j["clusters"][0]["best_run"] == b                  # cluster 0 is seeded by the best pose
