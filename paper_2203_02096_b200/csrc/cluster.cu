@@ -29,7 +29,7 @@ __global__ void __launch_bounds__(kClusterThreads) k_cluster(int n, int N, const
     extern __shared__ uint8_t cl_smem[];
     int *order = reinterpret_cast<int *>(cl_smem);               // [n] pose of energy rank t
     int *seed = order + n;                                       // [n] seed pose of cluster c
-    double *rs = reinterpret_cast<double *>(seed + n + (n & 1)); // [n] RMSD to seed c of the current pose
+    double *rs = reinterpret_cast<double *>(seed + n);          // [n] RMSD to seed c (byte 8n: aligned)
     __shared__ int s_nc, s_hit;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
     // energy ranks: (key, index) order, NaN = +inf, ties -> lower index
@@ -83,7 +83,7 @@ __global__ void __launch_bounds__(kClusterThreads) k_cluster(int n, int N, const
 
 }  // namespace
 
-size_t cluster_smem_bytes(int n) { return (size_t)8 * n + 8 + (size_t)8 * n; }
+size_t cluster_smem_bytes(int n) { return (size_t)16 * n; }
 
 cudaError_t launch_cluster(int n, int N, const float *xyz, const float *E, float tol, int *cluster, float *rmsd,
                            int *rank, int *n_clusters, cudaStream_t s) {
