@@ -43,7 +43,9 @@ struct LigDev {
     int Wg;           // lanes per group of the gradient kernels (16 if N <= 16, else 32)
     int NC;           // chunks = ceil(N / Wg)
     int energy_tiles; // 1: energy-only kernels also use the pair tiles (pair list too large to stage)
-    int tail_rot;     // 1: the partial last chunk is rotated as a padded chunk, 0: broadcast
+    int tail_rot;     // 1: the partial last chunk is rotated as a padded chunk, 0: broadcast or segments
+    int tail_seg;     // > 0 (slot mode): the tail rotated inside lane segments of power-of-two width tp:
+                      //   tp | log2(tp) << 8 | tail x tail rounds << 16
     // Gradient-path pair-slot tables (slot_mode = 1, small and mid-size ligands): every
     // (tile, step, lane) of intra_tiles and every (tail atom, chunk, lane) of the broadcast
     // tail gets its D5 pair constants precomputed in double on the host --

@@ -80,6 +80,7 @@ __device__ __forceinline__ LigSm stage_ligand(const LigDev &L, uint8_t *sm, int 
     v.ppar = reinterpret_cast<const float4 *>(sm + L.off_ppar);
     v.NC = L.NC;
     v.tail_rot = L.tail_rot;
+    v.tail_seg = L.tail_seg;
     v.slot_mode = L.slot_mode;
     v.slot4 = reinterpret_cast<const float4 *>(sm + L.off_slot4);
     v.slotq = reinterpret_cast<const float *>(sm + L.off_slotq);

@@ -241,12 +241,42 @@ int prepare_ligand(const dock_ligand *l, const dock_type_param *tp, int n_types,
     L.off_ppar = off; off += 16 * L.NC * 2 * L.Wg;
     // tile schedule of the gradient path (must match score.cuh intra_tiles)
     const int Wg = L.Wg, Bf = N / Wg, tail = N - Bf * Wg;
+    // Partial last chunk (tail of t atoms), three schedules (score.cuh), by a cost model in
+    // pair evaluations (~40 instructions each) and shuffles:
+    //   rot:  a padded rotated chunk: W/2 + Bf*W steps;
+    //   bcast: every lane meets tail atom k at once, k = 0..t-1: t*(Bf+1) evaluations + 3 sums each;
+    //   seg (slot mode only): the tail padded to tp = 2^ceil(log2 t) <= W/2, rotated inside
+    //     W/tp lane segments: Bf*tp steps against the full chunks, then the tail x tail
+    //     steps 1..tp/2 shared round-robin by the segments, and a butterfly over segments.
+    L.tail_seg = 0;
     L.tail_rot = (tail > 0 && (Wg / 2 + Bf * Wg) * 40 < tail * ((Bf + 1) * 40 + 3 * 5)) ? 1 : 0;
-    const int Bt = Bf + L.tail_rot;
-    const int tile_steps = Bt * (Wg / 2) + (Bt * (Bt - 1) / 2) * Wg;
-    const int bcast_slots = (tail > 0 && !L.tail_rot) ? tail * (Bf + 1) * Wg : 0;
-    L.n_slots = tile_steps * Wg + bcast_slots;
+    int tpw = 1;   // segment width
+    while (tpw < tail) tpw <<= 1;
+    const int seg_rounds = (tpw / 2 + (Wg / tpw) - 1) / (Wg / tpw);
+    auto seg_lg = [&]() { int l = 0; for (int m = tpw; m < Wg; m <<= 1) ++l; return l; };
+    if (tail > 0 && tpw <= Wg / 2) {
+        const int c_seg = (Bf * tpw + seg_rounds) * 40 + (tpw + seg_rounds) * 6 + 6 * seg_lg();
+        const int c_rot = (Wg / 2 + Bf * Wg) * 40;
+        const int c_bc = tail * ((Bf + 1) * 40 + 3 * 10);
+        int lg = 0;
+        while ((1 << lg) < tpw) ++lg;
+        if (c_seg < c_rot && c_seg < c_bc) { L.tail_seg = tpw | (lg << 8) | (seg_rounds << 16); L.tail_rot = 0; }
+    }
+    auto slot_count = [&]() {
+        const int Bt_ = Bf + L.tail_rot;
+        const int steps = Bt_ * (Wg / 2) + (Bt_ * (Bt_ - 1) / 2) * Wg;
+        int extra = 0;
+        if (tail > 0 && !L.tail_rot) extra = L.tail_seg ? (Bf * tpw + seg_rounds) * Wg : tail * (Bf + 1) * Wg;
+        return steps * Wg + extra;
+    };
+    L.n_slots = slot_count();
     L.slot_mode = (20 * L.n_slots <= 64 * 1024) ? 1 : 0;      // beyond: per-atom params + bits
+    if (!L.slot_mode && L.tail_seg) {                          // seg needs the slot tables
+        L.tail_seg = 0;
+        L.tail_rot = (tail > 0 && (Wg / 2 + Bf * Wg) * 40 < tail * ((Bf + 1) * 40 + 3 * 5)) ? 1 : 0;
+        L.n_slots = slot_count();
+    }
+    const int Bt = Bf + L.tail_rot;
     L.off_slot4 = off; off += L.slot_mode ? 16 * L.n_slots : 0;
     L.off_slotq = off; off += L.slot_mode ? a16(4 * L.n_slots) : 0;
     L.grad_bytes = off;              // the gradient kernels stage only up to here
@@ -364,7 +394,23 @@ int prepare_ligand(const dock_ligand *l, const dock_type_param *tp, int n_types,
                         fill(slot, I * Wg + ln, J * Wg + ((ln + st) & (Wg - 1)), once);
                     }
             }
-        if (tail > 0 && !L.tail_rot)
+        if (tail > 0 && L.tail_seg) {
+            // own chunks x tail: step s, chunk I, lane ln -> tail position ((ln mod tpw) + s) mod tpw
+            for (int st = 0; st < tpw; ++st)
+                for (int I = 0; I < Bf; ++I)
+                    for (int ln = 0; ln < Wg; ++ln, ++slot) {
+                        const int k = ((ln & (tpw - 1)) + st) & (tpw - 1);
+                        fill(slot, I * Wg + ln, Bf * Wg + k, k < tail);
+                    }
+            // tail x tail: round r, segment g = ln / tpw takes step 1 + g + r * (Wg / tpw)
+            for (int r = 0; r < seg_rounds; ++r)
+                for (int ln = 0; ln < Wg; ++ln, ++slot) {
+                    const int sl = ln & (tpw - 1), st = 1 + ln / tpw + r * (Wg / tpw);
+                    const int k = (sl + st) & (tpw - 1);
+                    const bool once = st < tpw / 2 || (st == tpw / 2 && sl < tpw / 2);
+                    fill(slot, Bf * Wg + sl, Bf * Wg + k, once && sl < tail && k < tail);
+                }
+        } else if (tail > 0 && !L.tail_rot)
             for (int k = 0; k < tail; ++k)
                 for (int I = 0; I <= Bf; ++I)
                     for (int ln = 0; ln < Wg; ++ln, ++slot)

@@ -62,7 +62,7 @@ struct LigSm {
     const float4 *ppar;           // [NC][2W] signed partner params (duplicated chunks)
     const float4 *slot4;          // pair-slot constants {r_eq^2, A, B, SV} (slot_mode)
     const float *slotq;           // pair-slot 332.06363/4 q_i q_j (slot_mode)
-    int NC, tail_rot, slot_mode;
+    int NC, tail_rot, slot_mode, tail_seg;
     int energy_tiles;             // energy-only evaluation through the pair tiles (no pair list)
     float wA_v, wB_v, wA_h, wB_h, qscale;   // D5-AD4 constants (LigDev; unused by D5)
 };
@@ -527,7 +527,54 @@ __device__ __forceinline__ void intra_tiles_slots(const LigSm &L, const Scratch 
             hx[J] += fx; hy[J] += fy; hz[J] += fz;
         }
     }
-    if (t > 0 && !tail_rot) {
+    if (t > 0 && L.tail_seg > 0) {
+        // Segmented tail (prep.cpp): the tail, padded to tp lanes, is rotated inside the W/tp
+        // lane segments.  (a) step s pairs own chunk atoms I*W+sub (I < Bf) with tail atom
+        // (sl + s) mod tp; the partner accumulator travels one lane per step inside the
+        // segment (as in the tiles) and returns to its owner after step tp-1.  (b) tail x
+        // tail: segment g takes steps 1 + g + r*(W/tp) of the diagonal schedule (zero slots
+        // beyond tp/2); the partner force goes back by one segment shuffle.  A butterfly over
+        // the segments then sums each tail atom's force.  Fixed order: deterministic.
+        // tail_seg packs tp | log2(tp) << 8 | rounds << 16 (no integer divisions here)
+        const int tp = L.tail_seg & 0xff, lg = (L.tail_seg >> 8) & 0xff, rounds = L.tail_seg >> 16;
+        const int sl = sub & (tp - 1), nseg = W >> lg, g = sub >> lg;
+        const float4 *trow = S.r + Bf * 2 * W;                  // tail chunk (positions 0..tp-1)
+        float fx = 0.f, fy = 0.f, fz = 0.f;
+        for (int st = 0; st < tp; ++st) {
+            const float4 rj = trow[(sl + st) & (tp - 1)];
+#pragma unroll
+            for (int I = 0; I < MAXC; ++I) {
+                if (I >= Bf) break;
+                const int q = slot0 + (st * Bf + I) * W + sub;
+                slot_pair(rx[I], ry[I], rz[I], rj, L.slot4[q], L.slotq[q], e, hx[I], hy[I], hz[I], fx, fy, fz);
+            }
+            const int src = (sl + 1) & (tp - 1);               // after the last step: back to the owner
+            fx = __shfl_sync(mask, fx, src, tp);
+            fy = __shfl_sync(mask, fy, src, tp);
+            fz = __shfl_sync(mask, fz, src, tp);
+        }
+        slot0 += tp * Bf * W;
+        const float4 ro = trow[sl];
+        for (int r = 0; r < rounds; ++r) {
+            const int st = 1 + g + r * nseg;
+            const int q = slot0 + r * W + sub;
+            float px = 0.f, py = 0.f, pz = 0.f;
+            slot_pair(ro.x, ro.y, ro.z, trow[(sl + st) & (tp - 1)], L.slot4[q], L.slotq[q], e, fx, fy, fz, px, py,
+                      pz);
+            const int src = (sl - st) & (tp - 1);              // lane m receives the force on m from m - st
+            fx += __shfl_sync(mask, px, src, tp);
+            fy += __shfl_sync(mask, py, src, tp);
+            fz += __shfl_sync(mask, pz, src, tp);
+        }
+        for (int m = tp; m < W; m <<= 1) {
+            fx += __shfl_xor_sync(mask, fx, m, W);
+            fy += __shfl_xor_sync(mask, fy, m, W);
+            fz += __shfl_xor_sync(mask, fz, m, W);
+        }
+#pragma unroll
+        for (int c = 0; c < MAXC; ++c)
+            if (c == Bf && sub < t) { hx[c] += fx; hy[c] += fy; hz[c] += fz; }
+    } else if (t > 0 && !tail_rot) {
         for (int k = 0; k < t; ++k) {
             const int j = Bf * W + k;                       // uniform: shared-memory broadcast
             const float4 rj = S.r[ridx<W>(j)];
