@@ -9,6 +9,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <numeric>
 
@@ -255,12 +256,15 @@ int prepare_ligand(const dock_ligand *l, const dock_type_param *tp, int n_types,
     const int seg_rounds = (tpw / 2 + (Wg / tpw) - 1) / (Wg / tpw);
     auto seg_lg = [&]() { int l = 0; for (int m = tpw; m < Wg; m <<= 1) ++l; return l; };
     if (tail > 0 && tpw <= Wg / 2) {
-        const int c_seg = (Bf * tpw + seg_rounds) * 40 + (tpw + seg_rounds) * 6 + 6 * seg_lg();
+        // (per-evaluation weights from the A/B in profiles/r01r: 3ce3 seg 1.11x, 7cpa bcast 1.04x)
+        const int c_seg = (Bf * tpw + seg_rounds) * 46 + (tpw + seg_rounds) * 6 + 6 * seg_lg();
         const int c_rot = (Wg / 2 + Bf * Wg) * 40;
-        const int c_bc = tail * ((Bf + 1) * 40 + 3 * 10);
+        const int c_bc = tail * ((Bf + 1) * 40 + 3 * 5);
         int lg = 0;
         while ((1 << lg) < tpw) ++lg;
-        if (c_seg < c_rot && c_seg < c_bc) { L.tail_seg = tpw | (lg << 8) | (seg_rounds << 16); L.tail_rot = 0; }
+        bool use_seg = c_seg < c_rot && c_seg < c_bc;
+        if (const char *f = std::getenv("DOCK_TAIL")) use_seg = std::strcmp(f, "seg") == 0;   // A/B experiments
+        if (use_seg) { L.tail_seg = tpw | (lg << 8) | (seg_rounds << 16); L.tail_rot = 0; }
     }
     auto slot_count = [&]() {
         const int Bt_ = Bf + L.tail_rot;
