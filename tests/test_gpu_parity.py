@@ -558,3 +558,36 @@ def test_sw_cooperative_split(dock, split, depth):
     tol, _ = pose_tols(P, ref)
     assert abs(ref["E"] - r["best_E"][0]) <= tol
     d.close()
+
+
+# ---------------------------------------------------------------------------
+# Tail schedules of the gradient pair tiles (prep.cpp cost model): the last
+# partial chunk is rotated as a padded chunk, broadcast atom by atom, or rotated inside
+# power-of-two lane segments.  Every schedule must give the oracle's energy and gradient
+# for every tail size; DOCK_TAIL forces the segment schedule (seg) or the cost model's
+# choice between the other two (bcast).
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("n_atoms", [9, 13, 24, 33, 36, 40, 41, 47, 50, 57, 63, 65, 70, 72, 80])
+@pytest.mark.parametrize("mode", ["seg", "bcast"])
+def test_tail_schedules_parity(dock, n_atoms, mode, monkeypatch):
+    from gen import make_ligand
+    from gen.synth import TYPE_NAMES, make_grid
+    monkeypatch.setenv("DOCK_TAIL", mode)
+    lig = make_ligand(n_atoms, min(15, n_atoms // 5), seed=100 + n_atoms, type_names=list(TYPE_NAMES))
+    grid = make_grid(40, 0.5, list(TYPE_NAMES), seed=3)
+    d = dock.Docker.from_inputs(grid, lig)
+    P = oracle.Problem(grid, lig)
+    X = near_reference_genotypes(grid, lig, d.T, 48, seed=n_atoms)
+    E, Gd, _ = d.eval(X, grad=True)
+    assert np.isfinite(E).all() and np.isfinite(Gd).all()
+    bad = []
+    for i in range(X.shape[0]):
+        ref = P.energy(X[i].astype(np.float64))
+        fm, cm = P.margins(ref["xyz"])
+        tol, gtol = pose_tols(P, ref)
+        if abs(E[i] - ref["E"]) > tol:
+            bad.append(("E", i, float(E[i]), ref["E"]))
+        if fm >= 1e-4 and cm >= 1e-4 and np.abs(Gd[i] - ref["grad"]).max() > gtol:
+            bad.append(("g", i))
+    assert not bad, bad[:5]
+    d.close()
