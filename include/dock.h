@@ -110,6 +110,12 @@ typedef struct {
     float w_vdw, w_hb, w_el, w_ds, w_tors;   /* DOCK_SF_AD4 free-energy coefficients (finite, >= 0);
                                     defaults AutoDock 4.1: .1662 .1209 .1406 .1322 .2983 */
     float qasp;                  /* DOCK_SF_AD4 charge-dependent solvation parameter (default .01097) */
+    int32_t run_branches;        /* 0 = auto (Solis-Wets jobs with several runs: 2), 1 = all runs step
+                                    through each generation together (one GA / LS / sum_evals launch per
+                                    generation), 2 = every run is its own branch of the generation graph
+                                    (its own launches on its own stream), so a run's next generation does
+                                    not wait for the longest Solis-Wets chain of the other runs.  Results
+                                    are identical (per-run state and RNG streams). */
 } dock_params;
 
 /* Fills the defaults: p_tour .60, p_cross .80, p_mut .02, 2.0 Å / 0.523 rad, ADADELTA,
@@ -306,6 +312,9 @@ int64_t dock_launch_count(const dock_ctx *ctx);
    0 = k_ga (offspring; profile >= 2 only), 1 = k_ls_* (local search), 2 = k_init.
    Arrays of 3. */
 int dock_kernel_stats(const dock_ctx *ctx, double *ms, int64_t *launches);
+
+/* Concurrent run branches of the last dock_run* call (1 = lockstep generations). */
+int dock_run_branches(const dock_ctx *ctx);
 
 /* Bytes dock_init copied host -> device (packed grid + ligand block + atom map). */
 int64_t dock_upload_bytes(const dock_ctx *ctx);

@@ -53,7 +53,8 @@ class Params(C.Structure):
                 ("ad_eps", C.c_float), ("max_generations", C.c_int32), ("device", C.c_int32),
                 ("l2_persist", C.c_int32), ("gens_per_graph", C.c_int32), ("profile", C.c_int32), ("sw_depth", C.c_int32),
                 ("sw_split", C.c_int32), ("scoring", C.c_int32), ("w_vdw", C.c_float), ("w_hb", C.c_float),
-                ("w_el", C.c_float), ("w_ds", C.c_float), ("w_tors", C.c_float), ("qasp", C.c_float)]
+                ("w_el", C.c_float), ("w_ds", C.c_float), ("w_tors", C.c_float), ("qasp", C.c_float),
+                ("run_branches", C.c_int32)]
 
 
 class ScreenOpts(C.Structure):
@@ -113,6 +114,7 @@ def _load():
         "dock_launch_count": (i64, [v]),
         "dock_kernel_stats": (i32, [v, P(C.c_double), P(i64)]),
         "dock_upload_bytes": (i64, [v]),
+        "dock_run_branches": (i32, [v]),
         "dock_screen": (i32, [P(Grids), P(TypeParam), P(Ligand), i32, P(u32), P(Params), P(ScreenOpts), i32, i32,
                               i64, u64, P(f), P(i32), P(f), P(i64), P(i32), P(i32), P(ScreenStats)]),
         "dock_screen_last_error": (C.c_char_p, []),
@@ -133,7 +135,7 @@ EXPORTED = ("dock_params_default", "dock_builtin_type_param", "dock_init", "dock
             "dock_run_device", "dock_eval", "dock_eval_device", "dock_get_pairs", "dock_get_torsions",
             "dock_philox", "dock_stream_words", "dock_ga_step", "dock_ls_step", "dock_launch_count",
             "dock_topology", "dock_kernel_stats", "dock_upload_bytes", "dock_screen", "dock_screen_last_error",
-            "dock_bench_part", "dock_eval_terms", "dock_cluster", "dock_write_result")
+            "dock_bench_part", "dock_eval_terms", "dock_cluster", "dock_write_result", "dock_run_branches")
 
 
 def write_result(res: dict, fmt: str = "json", timings: dict | None = None) -> str:
@@ -386,6 +388,11 @@ class Docker:
     @property
     def launches(self) -> int:
         return int(lib.dock_launch_count(self._ctx))
+
+    @property
+    def run_branches(self) -> int:
+        """Concurrent run branches of the last run (1 = lockstep generations)."""
+        return int(lib.dock_run_branches(self._ctx))
 
     @property
     def upload_bytes(self) -> int:

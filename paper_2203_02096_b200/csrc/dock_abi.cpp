@@ -75,7 +75,7 @@ dk::SearchDev make_search(const dock_ctx *c, int pop, int runs, int run_base, ui
     s.ad_rho = p.ad_rho; s.ad_eps = p.ad_eps;
     s.max_generations = p.max_generations;
     s.max_evals = max_evals;
-    s.pop = pop; s.runs = runs; s.run_base = run_base;
+    s.pop = pop; s.runs = runs; s.run_base = run_base; s.rstride = runs;
     const uint64_t k = seed + (uint64_t)ligand_id * 0x9E3779B97F4A7C15ull;   // D2 key
     s.key0 = (uint32_t)k; s.key1 = (uint32_t)(k >> 32);
     return s;
@@ -146,6 +146,7 @@ int validate_params(const dock_params &p, std::string *err) {
     if (p.gens_per_graph < 1 || p.gens_per_graph > 4096) { *err = "params.gens_per_graph: 1..4096"; return DOCK_E_INPUT; }
     if (p.sw_depth < 0 || p.sw_depth > 3) { *err = "params.sw_depth: 0..3"; return DOCK_E_INPUT; }
     if (p.sw_split != 0 && p.sw_split != 1 && p.sw_split != 2 && p.sw_split != 4) { *err = "params.sw_split: 0, 1, 2 or 4"; return DOCK_E_INPUT; }
+    if (p.run_branches < 0 || p.run_branches > 2) { *err = "params.run_branches: 0, 1 or 2"; return DOCK_E_INPUT; }
     if (p.scoring != DOCK_SF_D5 && p.scoring != DOCK_SF_AD4) { *err = "params.scoring: DOCK_SF_D5 or DOCK_SF_AD4"; return DOCK_E_INPUT; }
     for (float w : {p.w_vdw, p.w_hb, p.w_el, p.w_ds, p.w_tors, p.qasp})
         if (!std::isfinite(w) || w < 0.f) { *err = "params.w_* / qasp: must be finite and >= 0"; return DOCK_E_INPUT; }
@@ -398,6 +399,8 @@ void dock_free(dock_ctx *c) {
     {
         Trace t3("free.events_and_stream");
         for (cudaEvent_t e : c->events) cudaEventDestroy(e);
+        for (cudaEvent_t e : c->branch_events) cudaEventDestroy(e);
+        for (cudaStream_t b : c->branch_streams) cudaStreamDestroy(b);
         if (c->stream) cudaStreamDestroy(c->stream);
     }
     cudaGetLastError();
@@ -411,6 +414,8 @@ int dock_n_torsions(const dock_ctx *c) { return c ? c->prep.T : -1; }
 int dock_n_genes(const dock_ctx *c) { return c ? c->prep.G : -1; }
 int dock_n_pairs(const dock_ctx *c) { return c ? c->prep.P : -1; }
 int64_t dock_launch_count(const dock_ctx *c) { return c ? c->launches : -1; }
+
+int dock_run_branches(const dock_ctx *c) { return c ? c->last_branches : -1; }
 
 int64_t dock_upload_bytes(const dock_ctx *c) {
     return c ? (int64_t)(c->rec->bytes + c->prep.blob.size() + sizeof(int) * c->prep.N) : -1;
@@ -444,42 +449,95 @@ int dock_run_device(dock_ctx *c, int32_t pop, int32_t runs, int32_t run_base, ui
         const long long need = per_gen > 0 ? (max_evals - pop + per_gen - 1) / per_gen : 1;
         K = (int)std::max(1LL, std::min<long long>(K, std::min<long long>(need, c->params.max_generations)));
     }
+    // Run branches (dock_params.run_branches): with Solis-Wets the LS launch of a generation
+    // lasts as long as its longest chain, so runs stepping together wait for the slowest of
+    // all runs' chains every generation (1stp: max over 180 chains).  As independent graph
+    // branches, each run waits only for its own chains; the termination poll stays per
+    // graph batch.  ADADELTA chains all have the same length: lockstep (fewer launches).
+    const bool do_ls = sp.n_ls > 0 && sp.ls_iters > 0;
+    const int mode = c->params.run_branches;
+    const bool branched = runs > 1 && do_ls && (mode == 2 || (mode == 0 && sp.ls_method == DOCK_LS_SOLIS_WETS));
+    const int NB = branched ? runs : 1;
+    c->last_branches = NB;
     const bool prof = c->params.profile != 0;
     for (int i = 0; i < 3; ++i) { c->prof_ms[i] = 0; c->prof_n[i] = 0; }
-    if (prof && (int)c->events.size() < 3 * K + 2) {
-        while ((int)c->events.size() < 3 * K + 2) {
+    // events: lockstep 3 per generation (GA start, LS start, LS end) + 2 for init;
+    // branched 2 per generation around run 0's LS node (every run's branch is the same
+    // work; events on all branches, 2 x runs x K graph nodes, slowed 1stp 2.6x) + 2 for init
+    const int n_ev = branched ? 2 * K + 2 : 3 * K + 2;
+    const int ev_init = n_ev - 2;
+    if (prof && (int)c->events.size() < n_ev) {
+        while ((int)c->events.size() < n_ev) {
             cudaEvent_t ev;
             CK(cudaEventCreate(&ev));
             c->events.push_back(ev);
         }
     }
+    if (branched) {
+        while ((int)c->branch_streams.size() < NB) {
+            cudaStream_t b;
+            CK(cudaStreamCreateWithFlags(&b, cudaStreamNonBlocking));
+            c->branch_streams.push_back(b);
+        }
+        while ((int)c->branch_events.size() < NB + 1) {
+            cudaEvent_t e;
+            CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+            c->branch_events.push_back(e);
+        }
+    }
     cudaEvent_t *ev = c->events.data();
-    if (prof) CK(cudaEventRecord(ev[3 * K], s));
+    if (prof) CK(cudaEventRecord(ev[ev_init], s));
     CK(dk::launch_init(c->lig, c->grid, sp, pd, s));
-    if (prof) CK(cudaEventRecord(ev[3 * K + 1], s));
+    if (prof) CK(cudaEventRecord(ev[ev_init + 1], s));
     c->launches += 1;
     dk::LsArgs la{};
     la.use_state = 1; la.n_per_run = sp.n_ls; la.iters = sp.ls_iters;
-    const bool do_ls = sp.n_ls > 0 && sp.ls_iters > 0;
+    la.wave_total = runs * sp.n_ls;      // the speculation-depth rule sees every run's chains
     // capture K generations once; the kernels read the generation from device state
     cudaGraph_t graph = nullptr;
     cudaGraphExec_t exec = nullptr;
     auto t_cap = std::chrono::steady_clock::now();
     CK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
     cudaError_t ce = cudaSuccess;
-    for (int k = 0; k < K && ce == cudaSuccess; ++k) {
-        // profile 1: events around the LS node only (2 graph nodes per generation);
-        // profile 2: also around the GA node
-        if (prof && c->params.profile >= 2) ce = cudaEventRecordWithFlags(ev[3 * k], s, cudaEventRecordExternal);
-        if (ce == cudaSuccess) ce = dk::launch_ga(c->lig, c->grid, sp, pd, nullptr, s);
-        if (ce == cudaSuccess && prof) ce = cudaEventRecordWithFlags(ev[3 * k + 1], s, cudaEventRecordExternal);
-        if (ce == cudaSuccess && do_ls) ce = dk::launch_ls(c->lig, c->grid, sp, pd, la, runs * sp.n_ls, s);
-        if (ce == cudaSuccess && prof) ce = cudaEventRecordWithFlags(ev[3 * k + 2], s, cudaEventRecordExternal);
-        if (ce == cudaSuccess) ce = dk::launch_gen_end(sp, pd, s);
+    if (!branched) {
+        for (int k = 0; k < K && ce == cudaSuccess; ++k) {
+            // profile 1: events around the LS node only (2 graph nodes per generation);
+            // profile 2: also around the GA node
+            if (prof && c->params.profile >= 2) ce = cudaEventRecordWithFlags(ev[3 * k], s, cudaEventRecordExternal);
+            if (ce == cudaSuccess) ce = dk::launch_ga(c->lig, c->grid, sp, pd, nullptr, s);
+            if (ce == cudaSuccess && prof) ce = cudaEventRecordWithFlags(ev[3 * k + 1], s, cudaEventRecordExternal);
+            if (ce == cudaSuccess && do_ls) ce = dk::launch_ls(c->lig, c->grid, sp, pd, la, runs * sp.n_ls, s);
+            if (ce == cudaSuccess && prof) ce = cudaEventRecordWithFlags(ev[3 * k + 2], s, cudaEventRecordExternal);
+            if (ce == cudaSuccess) ce = dk::launch_gen_end(sp, pd, s);
+        }
+    } else {
+        // fork: every run's K generations on its own stream, on a one-run view of the
+        // population buffers (rstride keeps the parity blocks' stride), then join
+        const size_t G = (size_t)c->prep.G, P = (size_t)pop;
+        ce = cudaEventRecord(c->branch_events[0], s);
+        for (int r = 0; r < NB && ce == cudaSuccess; ++r) {
+            cudaStream_t b = c->branch_streams[r];
+            ce = cudaStreamWaitEvent(b, c->branch_events[0], 0);
+            dk::SearchDev spr = sp;
+            spr.runs = 1; spr.run_base = sp.run_base + r;
+            dk::PopDev pr = pd;
+            pr.genes = pd.genes + (size_t)r * P * G; pr.E = pd.E + (size_t)r * P; pr.state = pd.state + r;
+            pr.perm = pd.perm + (size_t)r * P; pr.ls_evals = pd.ls_evals + (size_t)r * P;
+            for (int k = 0; k < K && ce == cudaSuccess; ++k) {
+                ce = dk::launch_ga(c->lig, c->grid, spr, pr, nullptr, b);
+                if (ce == cudaSuccess && prof && r == 0) ce = cudaEventRecordWithFlags(ev[2 * k], b, cudaEventRecordExternal);
+                if (ce == cudaSuccess) ce = dk::launch_ls(c->lig, c->grid, spr, pr, la, sp.n_ls, b);
+                if (ce == cudaSuccess && prof && r == 0) ce = cudaEventRecordWithFlags(ev[2 * k + 1], b, cudaEventRecordExternal);
+                if (ce == cudaSuccess) ce = dk::launch_gen_end(spr, pr, b);
+            }
+            if (ce == cudaSuccess) ce = cudaEventRecord(c->branch_events[1 + r], b);
+            if (ce == cudaSuccess) ce = cudaStreamWaitEvent(s, c->branch_events[1 + r], 0);
+        }
     }
     cudaError_t ee = cudaStreamEndCapture(s, &graph);
     if (ce != cudaSuccess || ee != cudaSuccess) {
         if (graph) cudaGraphDestroy(graph);
+        cudaGetLastError();
         c->err = std::string("graph capture: ") + cudaGetErrorString(ce != cudaSuccess ? ce : ee);
         return DOCK_E_INTERNAL;
     }
@@ -489,9 +547,9 @@ int dock_run_device(dock_ctx *c, int32_t pop, int32_t runs, int32_t run_base, ui
         return DOCK_E_INTERNAL;
     }
     if (Trace::on())
-        std::fprintf(stderr, "[dock] run.graph_capture+instantiate %.3f ms\n",
-                     std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_cap).count());
-    const int per_graph = K * (do_ls ? 3 : 2);
+        std::fprintf(stderr, "[dock] run.graph_capture+instantiate %.3f ms (%d branches)\n",
+                     std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_cap).count(), NB);
+    const int per_graph = NB * K * (do_ls ? 3 : 2);
     const long long max_batches = (long long)c->params.max_generations / K + 2;
     int rc = DOCK_OK;
     for (long long b = 0; b < max_batches; ++b) {
@@ -503,10 +561,15 @@ int dock_run_device(dock_ctx *c, int32_t pop, int32_t runs, int32_t run_base, ui
         if (prof) {
             float t;
             cudaError_t pe = cudaSuccess;
-            if (b == 0 && (pe = cudaEventElapsedTime(&t, ev[3 * K], ev[3 * K + 1])) == cudaSuccess) { c->prof_ms[2] += t; c->prof_n[2] += 1; }
-            for (int k = 0; k < K && pe == cudaSuccess; ++k) {
-                if (c->params.profile >= 2 && (pe = cudaEventElapsedTime(&t, ev[3 * k], ev[3 * k + 1])) == cudaSuccess) { c->prof_ms[0] += t; c->prof_n[0] += 1; }
-                if (pe == cudaSuccess && do_ls && (pe = cudaEventElapsedTime(&t, ev[3 * k + 1], ev[3 * k + 2])) == cudaSuccess) { c->prof_ms[1] += t; c->prof_n[1] += 1; }
+            if (b == 0 && (pe = cudaEventElapsedTime(&t, ev[ev_init], ev[ev_init + 1])) == cudaSuccess) { c->prof_ms[2] += t; c->prof_n[2] += 1; }
+            if (branched) {
+                for (int q = 0; q < K && pe == cudaSuccess; ++q)
+                    if ((pe = cudaEventElapsedTime(&t, ev[2 * q], ev[2 * q + 1])) == cudaSuccess) { c->prof_ms[1] += t; c->prof_n[1] += 1; }
+            } else {
+                for (int k = 0; k < K && pe == cudaSuccess; ++k) {
+                    if (c->params.profile >= 2 && (pe = cudaEventElapsedTime(&t, ev[3 * k], ev[3 * k + 1])) == cudaSuccess) { c->prof_ms[0] += t; c->prof_n[0] += 1; }
+                    if (pe == cudaSuccess && do_ls && (pe = cudaEventElapsedTime(&t, ev[3 * k + 1], ev[3 * k + 2])) == cudaSuccess) { c->prof_ms[1] += t; c->prof_n[1] += 1; }
+                }
             }
             if (pe != cudaSuccess) {
                 c->err = std::string("profiling (ignored): cudaEventElapsedTime: ") + cudaGetErrorString(pe);

@@ -92,10 +92,13 @@ struct SearchDev {
     int max_generations;
     long long max_evals;
     int pop, runs, run_base;
+    int rstride;                  // runs of the population allocation: stride of the generation-parity
+                                  // blocks (= runs; larger for a one-run view of a multi-run job)
     uint32_t key0, key1;          // Philox key from (seed, ligand_id) (D2)
 };
 
-// Population buffers (double-buffered by generation parity).
+// Population buffers (double-buffered by generation parity): genes [2][rstride][pop][G],
+// E [2][rstride][pop], state [rstride], perm / ls_evals [rstride][pop].
 struct PopDev {
     float *genes;                 // [2][runs][pop][G]
     float *E;                     // [2][runs][pop]

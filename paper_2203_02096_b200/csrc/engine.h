@@ -93,6 +93,9 @@ struct dock_ctx {
     double prof_ms[3] = {0, 0, 0};
     long long prof_n[3] = {0, 0, 0};
     std::vector<cudaEvent_t> events;   // profiling: 3 per captured generation + 2 for init
+    std::vector<cudaStream_t> branch_streams;   // run branches of the generation graph (run_branches)
+    std::vector<cudaEvent_t> branch_events;     // fork + one join per branch (timing disabled)
+    int last_branches = 1;
 };
 
 namespace dk {

@@ -213,10 +213,10 @@ __global__ void __launch_bounds__(256) k_ga(const LigDev L, const GridDev g, con
     const uint32_t gen = act ? (uint32_t)st.gen + 1u : 1u;
     const int cur = act ? (st.gen & 1) : 0, nxt = gen & 1;
     const int rr = act ? r : 0;
-    const float *oldG = pop.genes + ((size_t)cur * sp.runs + rr) * P * G;
-    const float *oldE = pop.E + ((size_t)cur * sp.runs + rr) * P;
-    float *newG = pop.genes + ((size_t)nxt * sp.runs + rr) * P * G;
-    float *newE = pop.E + ((size_t)nxt * sp.runs + rr) * P;
+    const float *oldG = pop.genes + ((size_t)cur * sp.rstride + rr) * P * G;
+    const float *oldE = pop.E + ((size_t)cur * sp.rstride + rr) * P;
+    float *newG = pop.genes + ((size_t)nxt * sp.rstride + rr) * P * G;
+    float *newE = pop.E + ((size_t)nxt * sp.rstride + rr) * P;
     const uint32_t run_g = (uint32_t)(sp.run_base + rr);
     bool child = false;                 // this group scores a real offspring
     int A = 0, B = 0, c1 = 0, c2 = 0;
@@ -329,8 +329,8 @@ __device__ __forceinline__ LsTarget ls_target(const SearchDev &sp, const PopDev 
         if (!run_active(st, sp)) return t;
         const int gen = st.gen + 1, nxt = gen & 1;
         const int i = pop.perm[(size_t)r * sp.pop + s];
-        t.row = pop.genes + (((size_t)nxt * sp.runs + r) * sp.pop + i) * G;
-        t.E = pop.E + ((size_t)nxt * sp.runs + r) * sp.pop + i;
+        t.row = pop.genes + (((size_t)nxt * sp.rstride + r) * sp.pop + i) * G;
+        t.E = pop.E + ((size_t)nxt * sp.rstride + r) * sp.pop + i;
         t.evals = pop.ls_evals + (size_t)r * sp.pop + s;
         t.slot = (uint32_t)i; t.gen = (uint32_t)gen; t.run_g = (uint32_t)(sp.run_base + r);
         t.act = true;
@@ -723,7 +723,7 @@ __global__ void __launch_bounds__(256) k_best(const int G, const SearchDev sp, c
     if (r >= sp.runs) return;
     const RunState st = pop.state[r];
     const int buf = st.gen & 1;
-    const float *E = pop.E + ((size_t)buf * sp.runs + r) * sp.pop;
+    const float *E = pop.E + ((size_t)buf * sp.rstride + r) * sp.pop;
     float bv = INFINITY;
     int bi = 0x7fffffff;
     for (int i = lane; i < sp.pop; i += 32) {
@@ -736,7 +736,7 @@ __global__ void __launch_bounds__(256) k_best(const int G, const SearchDev sp, c
         const int oi = __shfl_xor_sync(0xffffffffu, bi, m);
         if (ov < bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; }
     }
-    const float *row = pop.genes + (((size_t)buf * sp.runs + r) * sp.pop + bi) * G;
+    const float *row = pop.genes + (((size_t)buf * sp.rstride + r) * sp.pop + bi) * G;
     for (int j = lane; j < G; j += 32) bestG[(size_t)r * G + j] = row[j];
     if (lane == 0) {
         bestE[r] = E[bi];
@@ -927,7 +927,8 @@ cudaError_t launch_ls(const LigDev &L, const GridDev &g, const SearchDev &sp, co
                 });
                 cudaGetLastError();
                 const long long waves = L.P >= 2000 ? 4 : 1;
-                if (sm_b <= (size_t)kSmemMax && per_sm > 0 && (long long)n_total <= waves * per_sm * nsm) depth = D;
+                const long long in_flight = a.wave_total > 0 ? a.wave_total : n_total;
+                if (sm_b <= (size_t)kSmemMax && per_sm > 0 && in_flight <= waves * per_sm * nsm) depth = D;
             }
         }
         // Cooperative evaluation (several warps per trial point) for large ligands, whose one
@@ -965,7 +966,7 @@ cudaError_t launch_ls(const LigDev &L, const GridDev &g, const SearchDev &sp, co
         // depth 1: one warp per individual; few individuals -> one warp per CTA so they
         // spread over all SMs.
         const int ng = cfg.W <= 16 ? 2 : 1;
-        const int warps = n_total >= 148 * 8 ? 8 : 1;
+        const int warps = (a.wave_total > 0 ? a.wave_total : n_total) >= 148 * 8 ? 8 : 1;
         const size_t smem = (size_t)staged_bytes(L, false) + (size_t)warps * ng * SL.bytes;
         if (smem > (size_t)kSmemMax) return cudaErrorInvalidConfiguration;
         const int blocks = ceil_div(n_total, warps);

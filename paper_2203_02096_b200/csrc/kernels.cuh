@@ -23,6 +23,8 @@ struct LsArgs {
     int *evals;             // hook mode: [n] evaluation counts (engine: PopDev.ls_evals)
     const int *rng_slot;    // hook mode: [n] population index used as SW RNG slot
     int gen, run;           // hook mode: generation and global run index
+    int wave_total;         // LS individuals in flight on the device for the speculation-depth rule
+                            // (per-run launches of concurrent branches: all runs'); 0 = this launch's
 };
 
 struct GroupCfg {

@@ -591,3 +591,26 @@ def test_tail_schedules_parity(dock, n_atoms, mode, monkeypatch):
             bad.append(("g", i))
     assert not bad, bad[:5]
     d.close()
+
+
+# ---------------------------------------------------------------------------
+# Run branches (dock_params.run_branches): every run stepping through its
+# generations as its own graph branch gives exactly the lockstep results.
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("name,method,runs,budget", [("1stp", 1, 20, 120_000), ("tiny", 1, 6, 2000),
+                                                     ("3ce3", 0, 4, 40_000)])
+def test_run_branches_identical_to_lockstep(dock, name, method, runs, budget):
+    cfg, lig, grid = config_inputs(name)
+    kw = dict(ls_method=method, ls_rate=0.06 if method == 1 else 1.0,
+              ls_max_iters=cfg.ls_iters if name != "tiny" else 30, gens_per_graph=4)
+    a = dock.Docker.from_inputs(grid, lig, run_branches=1, **kw)
+    b = dock.Docker.from_inputs(grid, lig, run_branches=2, **kw)
+    ra = a.run(cfg.pop, runs, budget, 77, run_base=3, ligand_id=5)
+    rb = b.run(cfg.pop, runs, budget, 77, run_base=3, ligand_id=5)
+    assert a.run_branches == 1 and b.run_branches == runs
+    for k in ("best_E", "best_genes", "evals", "generations", "best_xyz"):
+        assert np.array_equal(ra[k], rb[k]), k
+    if method == 1:                        # auto picks branches for Solis-Wets
+        c = dock.Docker.from_inputs(grid, lig, **kw)
+        rc = c.run(cfg.pop, runs, budget, 77, run_base=3, ligand_id=5)
+        assert c.run_branches == runs and np.array_equal(rc["best_E"], ra["best_E"])
