@@ -84,6 +84,7 @@ dk::SearchDev make_search(const dock_ctx *c, int pop, int runs, int run_base, ui
 dk::PopDev pop_of(const dock_ctx *c) {
     dk::PopDev d;
     d.genes = c->d_genes; d.E = c->d_E; d.state = c->d_state; d.perm = c->d_perm; d.ls_evals = c->d_ls_evals;
+    d.ls_count = c->d_ls_count;
     return d;
 }
 
@@ -92,8 +93,9 @@ int ensure_buffers(dock_ctx *c, int runs, int pop) {
     const int R = std::max(runs, c->cap_runs), P = std::max(pop, c->cap_pop);
     CK(cudaStreamSynchronize(c->stream));
     dk::dfree(c->d_genes, c->stream); dk::dfree(c->d_E, c->stream); dk::dfree(c->d_state, c->stream);
-    dk::dfree(c->d_perm, c->stream); dk::dfree(c->d_ls_evals, c->stream);
+    dk::dfree(c->d_perm, c->stream); dk::dfree(c->d_ls_evals, c->stream); dk::dfree(c->d_ls_count, c->stream);
     c->d_genes = nullptr; c->d_E = nullptr; c->d_state = nullptr; c->d_perm = nullptr; c->d_ls_evals = nullptr;
+    c->d_ls_count = nullptr;
     c->cap_runs = c->cap_pop = 0;
     // rows are strided by the ligand's G, but sized for the largest G so a context can be
     // reused for any ligand (dock_screen slots)
@@ -104,6 +106,8 @@ int ensure_buffers(dock_ctx *c, int runs, int pop) {
     CK(dk::dmalloc((void **)&c->d_state, (size_t)R * sizeof(dk::RunState), s));
     CK(dk::dmalloc((void **)&c->d_perm, (size_t)R * P * sizeof(int), s));
     CK(dk::dmalloc((void **)&c->d_ls_evals, (size_t)R * P * sizeof(int), s));
+    CK(dk::dmalloc((void **)&c->d_ls_count, (size_t)R * sizeof(int), s));
+    CK(cudaMemsetAsync(c->d_ls_count, 0, (size_t)R * sizeof(int), s));
     CK(cudaStreamSynchronize(s));   // usable from any stream (dock_run_device's) from here on
     if (!c->h_state.reserve(R)) { c->err = "pinned host allocation failed"; return DOCK_E_INTERNAL; }
     c->cap_runs = R; c->cap_pop = P;
@@ -394,7 +398,7 @@ void dock_free(dock_ctx *c) {
         cudaStream_t s = c->stream;
         dk::dfree(c->d_blob, s); dk::dfree(c->d_dfs2orig, s);
         dk::dfree(c->d_genes, s); dk::dfree(c->d_E, s); dk::dfree(c->d_state, s); dk::dfree(c->d_perm, s);
-        dk::dfree(c->d_ls_evals, s);
+        dk::dfree(c->d_ls_evals, s); dk::dfree(c->d_ls_count, s);
     }
     {
         Trace t3("free.events_and_stream");
@@ -508,7 +512,7 @@ int dock_run_device(dock_ctx *c, int32_t pop, int32_t runs, int32_t run_base, ui
             if (ce == cudaSuccess && prof) ce = cudaEventRecordWithFlags(ev[3 * k + 1], s, cudaEventRecordExternal);
             if (ce == cudaSuccess && do_ls) ce = dk::launch_ls(c->lig, c->grid, sp, pd, la, runs * sp.n_ls, s);
             if (ce == cudaSuccess && prof) ce = cudaEventRecordWithFlags(ev[3 * k + 2], s, cudaEventRecordExternal);
-            if (ce == cudaSuccess) ce = dk::launch_gen_end(sp, pd, s);
+            if (ce == cudaSuccess && !do_ls) ce = dk::launch_gen_end(sp, pd, s);   // else fused into k_ls_*
         }
     } else {
         // fork: every run's K generations on its own stream, on a one-run view of the
@@ -523,12 +527,12 @@ int dock_run_device(dock_ctx *c, int32_t pop, int32_t runs, int32_t run_base, ui
             dk::PopDev pr = pd;
             pr.genes = pd.genes + (size_t)r * P * G; pr.E = pd.E + (size_t)r * P; pr.state = pd.state + r;
             pr.perm = pd.perm + (size_t)r * P; pr.ls_evals = pd.ls_evals + (size_t)r * P;
+            pr.ls_count = pd.ls_count + r;
             for (int k = 0; k < K && ce == cudaSuccess; ++k) {
                 ce = dk::launch_ga(c->lig, c->grid, spr, pr, nullptr, b);
                 if (ce == cudaSuccess && prof && r == 0) ce = cudaEventRecordWithFlags(ev[2 * k], b, cudaEventRecordExternal);
                 if (ce == cudaSuccess) ce = dk::launch_ls(c->lig, c->grid, spr, pr, la, sp.n_ls, b);
                 if (ce == cudaSuccess && prof && r == 0) ce = cudaEventRecordWithFlags(ev[2 * k + 1], b, cudaEventRecordExternal);
-                if (ce == cudaSuccess) ce = dk::launch_gen_end(spr, pr, b);
             }
             if (ce == cudaSuccess) ce = cudaEventRecord(c->branch_events[1 + r], b);
             if (ce == cudaSuccess) ce = cudaStreamWaitEvent(s, c->branch_events[1 + r], 0);
@@ -549,7 +553,7 @@ int dock_run_device(dock_ctx *c, int32_t pop, int32_t runs, int32_t run_base, ui
     if (Trace::on())
         std::fprintf(stderr, "[dock] run.graph_capture+instantiate %.3f ms (%d branches)\n",
                      std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_cap).count(), NB);
-    const int per_graph = NB * K * (do_ls ? 3 : 2);
+    const int per_graph = NB * K * 2;   // GA + LS (gen end fused), or GA + gen end
     const long long max_batches = (long long)c->params.max_generations / K + 2;
     int rc = DOCK_OK;
     for (long long b = 0; b < max_batches; ++b) {

@@ -105,6 +105,7 @@ struct PopDev {
     RunState *state;              // [runs]
     int *perm;                    // [runs][pop] LS pick order
     int *ls_evals;                // [runs][pop] per-LS evaluation counts
+    int *ls_count;                // [runs] LS individuals finished this generation (fused gen end)
 };
 
 }  // namespace dk

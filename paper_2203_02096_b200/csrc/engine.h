@@ -86,7 +86,7 @@ struct dock_ctx {
     int cap_runs = 0, cap_pop = 0;
     float *d_genes = nullptr, *d_E = nullptr;
     dk::RunState *d_state = nullptr;
-    int *d_perm = nullptr, *d_ls_evals = nullptr;
+    int *d_perm = nullptr, *d_ls_evals = nullptr, *d_ls_count = nullptr;
     dk::PinnedBuf<dk::RunState> h_state;   // termination poll target
     std::string err;
     long long launches = 0;

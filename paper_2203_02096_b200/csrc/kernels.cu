@@ -169,7 +169,7 @@ __global__ void __launch_bounds__(256) k_init(const LigDev L, const GridDev g, c
     const float e = eval_group<W, MAXC, false>(Ls, g, S, sub, mask);
     if (sub == 0) {
         pop.E[(size_t)r * sp.pop + k] = e;
-        if (k == 0) { pop.state[r].evals = sp.pop; pop.state[r].gen = 0; }
+        if (k == 0) { pop.state[r].evals = sp.pop; pop.state[r].gen = 0; pop.ls_count[r] = 0; }
     }
 }
 
@@ -316,12 +316,14 @@ struct LsTarget {
     float *E;
     int *evals;
     uint32_t slot, gen, run_g;
+    int run_l;                    // engine mode: run index in the launch (for the fused gen end); -1: hook
 };
 
 __device__ __forceinline__ LsTarget ls_target(const SearchDev &sp, const PopDev &pop, const LsArgs &a, int gi,
                                               int G) {
     LsTarget t;
     t.act = false;
+    t.run_l = -1;
     if (a.use_state) {
         if (gi >= sp.runs * a.n_per_run) return t;
         const int r = gi / a.n_per_run, s = gi % a.n_per_run;
@@ -333,6 +335,7 @@ __device__ __forceinline__ LsTarget ls_target(const SearchDev &sp, const PopDev 
         t.E = pop.E + ((size_t)nxt * sp.rstride + r) * sp.pop + i;
         t.evals = pop.ls_evals + (size_t)r * sp.pop + s;
         t.slot = (uint32_t)i; t.gen = (uint32_t)gen; t.run_g = (uint32_t)(sp.run_base + r);
+        t.run_l = r;
         t.act = true;
     } else {
         if (gi >= a.n_per_run) return t;
@@ -343,6 +346,26 @@ __device__ __forceinline__ LsTarget ls_target(const SearchDev &sp, const PopDev 
         t.act = true;
     }
     return t;
+}
+
+// Generation end fused into the LS kernels (D11 sum_evals, and the generation
+// counter; formerly the k_gen_end launch): every LS individual of a run bumps the run's
+// counter after writing its evaluation count, and the run's last one (classic last-block
+// pattern) sums the counts and advances the run state.  Integer sum: order-free, so the
+// result equals k_gen_end's.
+__device__ __forceinline__ void ls_finish(const SearchDev &sp, const PopDev &pop, const LsTarget &t) {
+    if (t.run_l < 0) return;
+    const int r = t.run_l;
+    __threadfence();
+    if (atomicAdd(&pop.ls_count[r], 1) != sp.n_ls - 1) return;
+    __threadfence();
+    long long s = 0;
+    for (int i = 0; i < sp.n_ls; ++i) s += __ldcg(pop.ls_evals + (size_t)r * sp.pop + i);
+    const long long ev = __ldcg(&pop.state[r].evals);
+    const int gen = __ldcg(&pop.state[r].gen);
+    pop.state[r].evals = ev + (long long)(sp.pop - 1) + s;   // offspring + local search
+    pop.state[r].gen = gen + 1;
+    pop.ls_count[r] = 0;
 }
 
 // ---------------------------------------------------------------------------
@@ -407,7 +430,7 @@ __global__ void __launch_bounds__(256, (MAXC <= 4 ? DK_ADA_MINB : 1)) k_ls_adade
         const int j = sub + W * s;
         if (j < G) t.row[j] = bx[s];
     }
-    if (sub == 0) { *t.E = Ebest; *t.evals = a.iters; }
+    if (sub == 0) { *t.E = Ebest; *t.evals = a.iters; ls_finish(sp, pop, t); }
 }
 
 // ---------------------------------------------------------------------------
@@ -542,7 +565,7 @@ __global__ void __launch_bounds__(256) k_ls_sw(const LigDev L, const GridDev g, 
         const int j = lane + 32 * s;
         if (j < G) t.row[j] = x[s];
     }
-    if (lane == 0) { *t.E = Ex; *t.evals = ne; }
+    if (lane == 0) { *t.E = Ex; *t.evals = ne; ls_finish(sp, pop, t); }
 }
 
 // ---------------------------------------------------------------------------
@@ -693,7 +716,7 @@ __global__ void __launch_bounds__(tree_threads<W, D, KP>(), (W == 16 && D == 3) 
         __syncthreads();
     }
     for (int j = threadIdx.x; j < G; j += blockDim.x) t.row[j] = sx[j];
-    if (threadIdx.x == 0) { *t.E = Ex; *t.evals = ne; }
+    if (threadIdx.x == 0) { *t.E = Ex; *t.evals = ne; ls_finish(sp, pop, t); }
 }
 
 // ---------------------------------------------------------------------------
