@@ -110,12 +110,15 @@ typedef struct {
     float w_vdw, w_hb, w_el, w_ds, w_tors;   /* DOCK_SF_AD4 free-energy coefficients (finite, >= 0);
                                     defaults AutoDock 4.1: .1662 .1209 .1406 .1322 .2983 */
     float qasp;                  /* DOCK_SF_AD4 charge-dependent solvation parameter (default .01097) */
-    int32_t run_branches;        /* 0 = auto (Solis-Wets jobs with several runs: 2), 1 = all runs step
+    int32_t run_branches;        /* 0 = auto (Solis-Wets: 3 where eligible, else 2), 1 = all runs step
                                     through each generation together (one GA / LS / sum_evals launch per
                                     generation), 2 = every run is its own branch of the generation graph
                                     (its own launches on its own stream), so a run's next generation does
-                                    not wait for the longest Solis-Wets chain of the other runs.  Results
-                                    are identical (per-run state and RNG streams). */
+                                    not wait for the longest Solis-Wets chain of the other runs, 3 = one
+                                    persistent thread-block cluster per run (Solis-Wets, <= 16 LS
+                                    individuals per run, speculation depth 2) loops over the run's
+                                    generations on the device: one launch per job, no host polling.
+                                    Results are identical in every mode (per-run state and RNG streams). */
 } dock_params;
 
 /* Fills the defaults: p_tour .60, p_cross .80, p_mut .02, 2.0 Å / 0.523 rad, ADADELTA,

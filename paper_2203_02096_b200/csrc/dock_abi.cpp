@@ -150,7 +150,7 @@ int validate_params(const dock_params &p, std::string *err) {
     if (p.gens_per_graph < 1 || p.gens_per_graph > 4096) { *err = "params.gens_per_graph: 1..4096"; return DOCK_E_INPUT; }
     if (p.sw_depth < 0 || p.sw_depth > 3) { *err = "params.sw_depth: 0..3"; return DOCK_E_INPUT; }
     if (p.sw_split != 0 && p.sw_split != 1 && p.sw_split != 2 && p.sw_split != 4) { *err = "params.sw_split: 0, 1, 2 or 4"; return DOCK_E_INPUT; }
-    if (p.run_branches < 0 || p.run_branches > 2) { *err = "params.run_branches: 0, 1 or 2"; return DOCK_E_INPUT; }
+    if (p.run_branches < 0 || p.run_branches > 3) { *err = "params.run_branches: 0..3"; return DOCK_E_INPUT; }
     if (p.scoring != DOCK_SF_D5 && p.scoring != DOCK_SF_AD4) { *err = "params.scoring: DOCK_SF_D5 or DOCK_SF_AD4"; return DOCK_E_INPUT; }
     for (float w : {p.w_vdw, p.w_hb, p.w_el, p.w_ds, p.w_tors, p.qasp})
         if (!std::isfinite(w) || w < 0.f) { *err = "params.w_* / qasp: must be finite and >= 0"; return DOCK_E_INPUT; }
@@ -398,7 +398,7 @@ void dock_free(dock_ctx *c) {
         cudaStream_t s = c->stream;
         dk::dfree(c->d_blob, s); dk::dfree(c->d_dfs2orig, s);
         dk::dfree(c->d_genes, s); dk::dfree(c->d_E, s); dk::dfree(c->d_state, s); dk::dfree(c->d_perm, s);
-        dk::dfree(c->d_ls_evals, s); dk::dfree(c->d_ls_count, s);
+        dk::dfree(c->d_ls_evals, s); dk::dfree(c->d_ls_count, s); dk::dfree(c->d_prof, s);
     }
     {
         Trace t3("free.events_and_stream");
@@ -460,6 +460,26 @@ int dock_run_device(dock_ctx *c, int32_t pop, int32_t runs, int32_t run_base, ui
     // graph batch.  ADADELTA chains all have the same length: lockstep (fewer launches).
     const bool do_ls = sp.n_ls > 0 && sp.ls_iters > 0;
     const int mode = c->params.run_branches;
+    // Persistent clusters (k_run_sw): the whole Solis-Wets job in one launch,
+    // one thread-block cluster per run looping over its generations on the device.
+    if (do_ls && (mode == 3 || (mode == 0 && sp.ls_method == DOCK_LS_SOLIS_WETS)) && dk::run_sw_eligible(c->lig, sp)) {
+        c->last_branches = runs;
+        const bool prof = c->params.profile != 0;
+        for (int i = 0; i < 3; ++i) { c->prof_ms[i] = 0; c->prof_n[i] = 0; }
+        if (prof && !c->d_prof) CK(dk::dmalloc((void **)&c->d_prof, 2 * sizeof(unsigned long long), s));
+        if (prof) CK(cudaMemsetAsync(c->d_prof, 0, 2 * sizeof(unsigned long long), s));
+        CK(dk::launch_init(c->lig, c->grid, sp, pd, s));
+        CK(dk::launch_run_sw(c->lig, c->grid, sp, pd, prof ? c->d_prof : nullptr, s));
+        CK(dk::launch_best(c->lig, sp, pd, d_best_energy, d_best_genotype, (long long *)d_evals_used, d_generations, s));
+        c->launches += 3;
+        if (prof) {
+            unsigned long long h[2] = {0, 0};
+            CK(cudaMemcpyAsync(h, c->d_prof, sizeof h, cudaMemcpyDeviceToHost, s));
+            CK(cudaStreamSynchronize(s));
+            c->prof_ms[1] = (double)h[0] * 1e-6; c->prof_n[1] = (long long)h[1];
+        }
+        return DOCK_OK;
+    }
     const bool branched = runs > 1 && do_ls && (mode == 2 || (mode == 0 && sp.ls_method == DOCK_LS_SOLIS_WETS));
     const int NB = branched ? runs : 1;
     c->last_branches = NB;

@@ -96,6 +96,7 @@ struct dock_ctx {
     std::vector<cudaStream_t> branch_streams;   // run branches of the generation graph (run_branches)
     std::vector<cudaEvent_t> branch_events;     // fork + one join per branch (timing disabled)
     int last_branches = 1;
+    unsigned long long *d_prof = nullptr;       // k_run_sw LS-phase timer (profile)
 };
 
 namespace dk {

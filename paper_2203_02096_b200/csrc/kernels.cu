@@ -18,6 +18,8 @@
 // independently"; NS "one CTA or warp-group handles each individual").
 #include <math.h>
 
+#include <cooperative_groups.h>
+
 #define DK_KERNELS_TU
 #include "kernels.cuh"
 #include "philox.cuh"
@@ -179,7 +181,7 @@ __device__ __forceinline__ int tournament(const float *E, int pop, uint32_t wa, 
     const int i = (int)below(wa, (uint32_t)pop);
     int j = (int)below(wb, (uint32_t)(pop - 1));
     if (j >= i) j += 1;
-    const float ei = nan_inf(E[i]), ej = nan_inf(E[j]);
+    const float ei = nan_inf(__ldcg(E + i)), ej = nan_inf(__ldcg(E + j));   // L2: written by other CTAs (k_run_sw)
     const int better = (ei < ej || (ei == ej && i < j)) ? i : j;
     const int other = better == i ? j : i;
     return u01(wc) < p_tour ? better : other;
@@ -188,26 +190,16 @@ __device__ __forceinline__ int tournament(const float *E, int pop, uint32_t wa, 
 // ---------------------------------------------------------------------------
 // k_ga: one generation of the GA for every (run, slot) (D8).
 // ---------------------------------------------------------------------------
+// One GA slot (D8) of run r, generation st.gen + 1, on one lane group: slot 0 =
+// elitism + the LS sample (partial Fisher-Yates), slot k >= 1 = tournaments, two-point
+// crossover, mutation and the offspring energy.  act = false: a shadow evaluation of a
+// dummy genotype keeps the warp converged and writes nothing.  Used by k_ga (one launch
+// per generation) and by k_run_sw (the persistent cluster kernel).
 template <int W, int MAXC>
-__global__ void __launch_bounds__(256) k_ga(const LigDev L, const GridDev g, const ScratchLayout SL,
-                                            const SearchDev sp, const PopDev pop, int *dbg) {
-    extern __shared__ uint4 smem_u4[];
-    uint8_t *sm = reinterpret_cast<uint8_t *>(smem_u4);
-    const int gl = threadIdx.x / W, sub = threadIdx.x % W;
-    const int gi = blockIdx.x * (blockDim.x / W) + gl;
-    const int P = sp.pop, G = L.G;
-    bool act = false;
-    RunState st;
-    const int r = gi / P;
-    if (gi < sp.runs * P) { st = pop.state[r]; act = run_active(st, sp); }
-    if (!__syncthreads_or(act)) return;            // finished runs cost one state read
-    const LigSm Ls = stage_ligand(L, sm, staged_bytes(L, false));
-    // Both lane groups of a warp stay converged through the evaluation (the elite slot and
-    // inactive groups evaluate a dummy genotype and write nothing), so its shuffles take a
-    // constant full-warp mask.
-    if (!__any_sync(0xffffffffu, act)) return;
-    const int k = gi % P;
-    const Scratch S = scratch_at(sm + staged_bytes(L, false) + gl * SL.bytes, SL);
+__device__ __forceinline__ void ga_slot_group(const LigSm &Ls, const GridDev &g, const Scratch &S, int *perm_scratch,
+                                              const SearchDev &sp, const PopDev &pop, const int G, bool act,
+                                              const RunState st, int r, int k, int sub, int *dbg) {
+    const int P = sp.pop;
     const unsigned mask = group_mask<W>();
     const uint2 key = make_uint2(sp.key0, sp.key1);
     const uint32_t gen = act ? (uint32_t)st.gen + 1u : 1u;
@@ -230,7 +222,7 @@ __global__ void __launch_bounds__(256) k_ga(const LigDev L, const GridDev g, con
         float bv = INFINITY;
         int bi = 0x7fffffff;
         for (int i = sub; i < P; i += W) {
-            const float v = nan_inf(oldE[i]);
+            const float v = nan_inf(__ldcg(oldE + i));
             if (v < bv || (v == bv && i < bi)) { bv = v; bi = i; }
         }
 #pragma unroll
@@ -240,13 +232,13 @@ __global__ void __launch_bounds__(256) k_ga(const LigDev L, const GridDev g, con
             if (ov < bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; }
         }
         for (int j = sub; j < G; j += W) {
-            const float v = oldG[(size_t)bi * G + j];
+            const float v = __ldcg(oldG + (size_t)bi * G + j);
             newG[j] = v;
             S.genes[j] = v;                 // shadow evaluation only
         }
-        if (sub == 0) newE[0] = oldE[bi];
+        if (sub == 0) newE[0] = __ldcg(oldE + bi);
         // local-search sample: partial Fisher-Yates over the new population (D8.3)
-        int *perm = reinterpret_cast<int *>(sm + staged_bytes(L, false) + gl * SL.bytes + SL.off_extra);
+        int *perm = perm_scratch;
         for (int i = sub; i < P; i += W) perm[i] = i;
         __syncwarp(mask);
         if (sub == 0) {
@@ -260,7 +252,7 @@ __global__ void __launch_bounds__(256) k_ga(const LigDev L, const GridDev g, con
         __syncwarp(mask);
         for (int s = sub; s < P; s += W) pop.perm[(size_t)r * P + s] = perm[s];
         if (dbg && sub == 0) {
-            int *d = dbg + (size_t)gi * 8;
+            int *d = dbg + (size_t)(r * P + k) * 8;
             d[0] = bi; d[1] = bi; d[2] = 0; d[3] = 0; d[4] = 0; d[5] = 0; d[6] = 0; d[7] = bi;
         }
     } else {
@@ -284,7 +276,7 @@ __global__ void __launch_bounds__(256) k_ga(const LigDev L, const GridDev g, con
             const uint32_t md = m + 1u;
             const uint32_t wd = ((md >> 2) == (m >> 2)) ? lane_of(bc, md & 3)
                                                         : lane_of(stream_block(key, kGA, (uint32_t)k, gen, run_g, md >> 2), md & 3);
-            float v = (cross && c1 <= j && j < c2) ? oldG[(size_t)B * G + j] : oldG[(size_t)A * G + j];
+            float v = __ldcg(oldG + (size_t)((cross && c1 <= j && j < c2) ? B : A) * G + j);
             if (u01(wc) < sp.p_mut) {
                 const float mag = j < 3 ? sp.mut_trans : sp.mut_angle;
                 v += (2.0f * u01(wd) - 1.0f) * mag;
@@ -302,11 +294,37 @@ __global__ void __launch_bounds__(256) k_ga(const LigDev L, const GridDev g, con
 #pragma unroll
         for (int m = W / 2; m >= 1; m >>= 1) mbits |= __shfl_xor_sync(mask, mbits, m, W);
         if (sub == 0) {
-            int *d = dbg + (size_t)gi * 8;
+            int *d = dbg + (size_t)(r * P + k) * 8;
             d[0] = A; d[1] = B; d[2] = cross ? 1 : 0; d[3] = c1; d[4] = c2;
             d[5] = (int)(uint32_t)mbits; d[6] = (int)(uint32_t)(mbits >> 32); d[7] = -1;
         }
     }
+}
+
+// ---------------------------------------------------------------------------
+// k_ga: one generation of the GA for every (run, slot) (D8).
+// ---------------------------------------------------------------------------
+template <int W, int MAXC>
+__global__ void __launch_bounds__(256) k_ga(const LigDev L, const GridDev g, const ScratchLayout SL,
+                                            const SearchDev sp, const PopDev pop, int *dbg) {
+    extern __shared__ uint4 smem_u4[];
+    uint8_t *sm = reinterpret_cast<uint8_t *>(smem_u4);
+    const int gl = threadIdx.x / W, sub = threadIdx.x % W;
+    const int gi = blockIdx.x * (blockDim.x / W) + gl;
+    const int P = sp.pop, G = L.G;
+    bool act = false;
+    RunState st;
+    const int r = gi / P;
+    if (gi < sp.runs * P) { st = pop.state[r]; act = run_active(st, sp); }
+    if (!__syncthreads_or(act)) return;            // finished runs cost one state read
+    const LigSm Ls = stage_ligand(L, sm, staged_bytes(L, false));
+    // Both lane groups of a warp stay converged through the evaluation (the elite slot and
+    // inactive groups evaluate a dummy genotype and write nothing), so its shuffles take a
+    // constant full-warp mask.
+    if (!__any_sync(0xffffffffu, act)) return;
+    uint8_t *gbase = sm + staged_bytes(L, false) + gl * SL.bytes;
+    ga_slot_group<W, MAXC>(Ls, g, scratch_at(gbase, SL), reinterpret_cast<int *>(gbase + SL.off_extra), sp, pop, G,
+                           act, st, r, gi % P, sub, dbg);
 }
 
 // Resolve the row a local-search group works on (engine or hook mode).
@@ -327,10 +345,11 @@ __device__ __forceinline__ LsTarget ls_target(const SearchDev &sp, const PopDev 
     if (a.use_state) {
         if (gi >= sp.runs * a.n_per_run) return t;
         const int r = gi / a.n_per_run, s = gi % a.n_per_run;
-        const RunState st = pop.state[r];
+        RunState st;
+        st.evals = __ldcg(&pop.state[r].evals); st.gen = __ldcg(&pop.state[r].gen);   // L2: k_run_sw
         if (!run_active(st, sp)) return t;
         const int gen = st.gen + 1, nxt = gen & 1;
-        const int i = pop.perm[(size_t)r * sp.pop + s];
+        const int i = __ldcg(pop.perm + (size_t)r * sp.pop + s);
         t.row = pop.genes + (((size_t)nxt * sp.rstride + r) * sp.pop + i) * G;
         t.E = pop.E + ((size_t)nxt * sp.rstride + r) * sp.pop + i;
         t.evals = pop.ls_evals + (size_t)r * sp.pop + s;
@@ -586,18 +605,15 @@ constexpr int tree_threads() { return ((ipow3(D) - 1) * KP * W + 31) / 32 * 32; 
 // KP > 1: every node is evaluated cooperatively by KP lane groups (large ligands, whose
 // single evaluation is the latency of the chain): each computes a part of the grid and
 // pair sums, the partials are added in a fixed order in the resolution step.
-template <int W, int MAXC, int D, int KP = 1>
-__global__ void __launch_bounds__(tree_threads<W, D, KP>(), (W == 16 && D == 3) ? 2 : 1) k_ls_sw_tree(const LigDev L, const GridDev g,
-                                                                     const ScratchLayout SL, const SearchDev sp,
-                                                                     const PopDev pop, const LsArgs a) {
+// The speculative Solis-Wets chain of one individual (t) on one CTA of (3^D - 1) * KP lane
+// groups, ligand already staged (k_ls_sw_tree, and the LS phase of k_run_sw).  Shared
+// memory after the ligand block: the groups' scratch, then x, b, partial energies and the
+// double-buffered deviate shapes (tree_smem).
+template <int W, int MAXC, int D, int KP>
+__device__ __forceinline__ void sw_tree_chain(const LigSm &Ls, const GridDev &g, const ScratchLayout &SL,
+                                              const SearchDev &sp, const PopDev &pop, const LsArgs &a,
+                                              const LsTarget &t, uint8_t *sm, const int staged, const int G) {
     constexpr int NGR = ipow3(D) - 1;
-    extern __shared__ uint4 smem_u4[];
-    uint8_t *sm = reinterpret_cast<uint8_t *>(smem_u4);
-    const int G = L.G;
-    const LsTarget t = ls_target(sp, pop, a, blockIdx.x, G);
-    if (!t.act) return;                                      // uniform: one individual per CTA
-    const int staged = staged_bytes(L, false);
-    const LigSm Ls = stage_ligand(L, sm, staged);
     float *sx = reinterpret_cast<float *>(sm + staged + NGR * KP * SL.bytes);
     float *sb = sx + kMaxGenes;
     float *sE = sb + kMaxGenes;                              // [NGR][KP] partial energies
@@ -610,7 +626,7 @@ __global__ void __launch_bounds__(tree_threads<W, D, KP>(), (W == 16 && D == 3) 
     // the warps stay converged and the group shuffles take a constant full-warp mask
     constexpr unsigned gmask = 0xffffffffu;
     const uint2 key = make_uint2(sp.key0, sp.key1);
-    for (int j = threadIdx.x; j < G; j += blockDim.x) { sx[j] = t.row[j]; sb[j] = 0.0f; }
+    for (int j = threadIdx.x; j < G; j += blockDim.x) { sx[j] = __ldcg(t.row + j); sb[j] = 0.0f; }
     for (int j = sub; j < G; j += W) S.genes[j] = 0.0f;      // finite genes for a moot first round
     // this group's node: level lvl, parent state sigma (base-3 outcome digits), candidate
     int lvl = 0;
@@ -631,7 +647,7 @@ __global__ void __launch_bounds__(tree_threads<W, D, KP>(), (W == 16 && D == 3) 
         stri0[q] = sw_tri(key, t.slot, t.gen, t.run_g, G, k, j);
     }
     __syncthreads();
-    float Ex = *t.E, rho = sp.sw_rho;
+    float Ex = __ldcg(t.E), rho = sp.sw_rho;
     int succ = 0, fail = 0, ne = 0, it = 0, cur = 0;
     while (it < a.iters && !(rho < sp.sw_rho_min)) {
         const float *stri = stri0 + cur * D * kMaxGenes;
@@ -717,6 +733,83 @@ __global__ void __launch_bounds__(tree_threads<W, D, KP>(), (W == 16 && D == 3) 
     }
     for (int j = threadIdx.x; j < G; j += blockDim.x) t.row[j] = sx[j];
     if (threadIdx.x == 0) { *t.E = Ex; *t.evals = ne; ls_finish(sp, pop, t); }
+}
+
+template <int W, int MAXC, int D, int KP = 1>
+__global__ void __launch_bounds__(tree_threads<W, D, KP>(), (W == 16 && D == 3) ? 2 : 1) k_ls_sw_tree(const LigDev L, const GridDev g,
+                                                                     const ScratchLayout SL, const SearchDev sp,
+                                                                     const PopDev pop, const LsArgs a) {
+    constexpr int NGR = ipow3(D) - 1;
+    extern __shared__ uint4 smem_u4[];
+    uint8_t *sm = reinterpret_cast<uint8_t *>(smem_u4);
+    const int G = L.G;
+    const LsTarget t = ls_target(sp, pop, a, blockIdx.x, G);
+    if (!t.act) return;                                      // uniform: one individual per CTA
+    const int staged = staged_bytes(L, false);
+    const LigSm Ls = stage_ligand(L, sm, staged);
+    sw_tree_chain<W, MAXC, D, KP>(Ls, g, SL, sp, pop, a, t, sm, staged, G);
+}
+
+// ---------------------------------------------------------------------------
+// k_run_sw: a whole Solis-Wets docking run per thread-block cluster, persistent over its
+// generations.  One cluster of n_ls CTAs per run (n_ls <= 16: non-portable
+// cluster size); CTA q of the cluster owns the run's q-th LS individual.  Per generation:
+//   GA phase: the cluster's n_ls x 8 lane groups deal the pop GA slots (ga_slot_group: the
+//     same per-slot arithmetic and Philox words as k_ga), cluster barrier;
+//   LS phase: every CTA runs its individual's speculative depth-2 chain (sw_tree_chain),
+//     the run's last chain advances the run state (ls_finish), cluster barrier;
+// until the run's budget is spent (D8.5 per run, on the device).  Results equal the
+// lockstep and branched engines'.  No launch, graph node or host poll per generation, and
+// no run waits for another run's chains.  Population data written by other CTAs of the
+// cluster is read through L2 (__ldcg); the barriers order it (release / acquire).
+// prof != null: CTA 0 of run 0 accumulates the LS-phase duration (GA barrier -> LS
+// barrier, %globaltimer ns) and the phase count.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ unsigned long long global_ns() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+
+template <int W, int MAXC>
+__global__ void __launch_bounds__(tree_threads<W, 2, 1>(), 1) k_run_sw(const LigDev L, const GridDev g,
+                                                                      const ScratchLayout SL, const SearchDev sp,
+                                                                      const PopDev pop, const LsArgs a,
+                                                                      unsigned long long *prof) {
+    namespace cg = cooperative_groups;
+    constexpr int NGR = ipow3(2) - 1;
+    cg::cluster_group cl = cg::this_cluster();
+    const int nq = (int)cl.num_blocks(), q = (int)cl.block_rank();
+    const int r = blockIdx.x / nq;
+    extern __shared__ uint4 smem_u4[];
+    uint8_t *sm = reinterpret_cast<uint8_t *>(smem_u4);
+    const int G = L.G, P = sp.pop;
+    const int staged = staged_bytes(L, false);
+    const LigSm Ls = stage_ligand(L, sm, staged);
+    const int gidx = threadIdx.x / W, sub = threadIdx.x % W;
+    uint8_t *gbase = sm + staged + gidx * SL.bytes;
+    const Scratch S = scratch_at(gbase, SL);
+    const bool timer = prof != nullptr && r == 0 && q == 0 && threadIdx.x == 0;
+    for (;;) {
+        RunState st;
+        st.evals = __ldcg(&pop.state[r].evals); st.gen = __ldcg(&pop.state[r].gen);
+        if (!run_active(st, sp)) break;                   // uniform over the cluster
+        // ---- GA phase ----
+        for (int base = 0; base < P; base += nq * NGR) {
+            const int k = base + q * NGR + gidx;
+            ga_slot_group<W, MAXC>(Ls, g, S, reinterpret_cast<int *>(gbase + SL.off_extra), sp, pop, G, k < P, st, r,
+                                   k < P ? k : 0, sub, nullptr);
+        }
+        __threadfence();
+        cl.sync();
+        const unsigned long long t0 = timer ? global_ns() : 0ull;
+        // ---- LS phase ----
+        const LsTarget t = ls_target(sp, pop, a, r * nq + q, G);
+        sw_tree_chain<W, MAXC, 2, 1>(Ls, g, SL, sp, pop, a, t, sm, staged, G);
+        __threadfence();
+        cl.sync();
+        if (timer) { prof[0] += global_ns() - t0; prof[1] += 1ull; }
+    }
 }
 
 // ---------------------------------------------------------------------------
@@ -857,6 +950,8 @@ cudaError_t setup_kernel_attributes() {
     if (e == cudaSuccess) e = allow_smem(k_ls_sw_tree<W, MAXC, 2>);                  \
     if (e == cudaSuccess) e = allow_smem(k_ls_sw_tree<W, MAXC, 3>);                  \
     if (e == cudaSuccess) e = allow_split<W, MAXC>();                                 \
+    if (e == cudaSuccess) e = allow_smem(k_run_sw<W, MAXC>);                         \
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(k_run_sw<W, MAXC>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1); \
     if (e == cudaSuccess) e = allow_smem(k_bench_part<W, MAXC, kInter>);             \
     if (e == cudaSuccess) e = allow_smem(k_bench_part<W, MAXC, kIntra>);
     DK_ATTR(16, 1) DK_ATTR(32, 1) DK_ATTR(32, 2) DK_ATTR(32, 3) DK_ATTR(32, 4) DK_ATTR(32, 8)
@@ -1003,6 +1098,55 @@ cudaError_t launch_ls(const LigDev &L, const GridDev &g, const SearchDev &sp, co
         DK_DISPATCH(cfg, { k_ls_adadelta<W, MAXC><<<blocks, kThreads, smem, s>>>(L, g, SL, sp, pop, a); });
     }
     return cudaGetLastError();
+}
+
+// Persistent cluster engine (k_run_sw): eligible when the run's LS individuals fit one
+// cluster (n_ls <= 16), no cooperative split is wanted, and the speculation-depth rule
+// would pick depth 2 for all runs' chains (so the results and the tree are those of the
+// lockstep engine).  Returns 0 if not eligible.
+int run_sw_eligible(const LigDev &L, const SearchDev &sp) {
+    if (sp.ls_method != 1 || sp.n_ls < 1 || sp.n_ls > 16 || sp.ls_iters < 1) return 0;
+    if (sp.sw_depth != 0 && sp.sw_depth != 2) return 0;
+    if (sp.sw_split == 2 || sp.sw_split == 4 || (sp.sw_split == 0 && L.P >= 2000 && pick_group(L.N).W == 32)) return 0;
+    const GroupCfg cfg = pick_group(L.N);
+    const ScratchLayout SL = scratch_layout(L, false, 4 * sp.pop);
+    const size_t smem = tree_smem(L, SL, 2, 1);
+    if (smem > (size_t)kSmemMax) return 0;
+    if (sp.sw_depth == 0) {   // the auto depth rule of launch_ls, on all runs' chains
+        int dev = 0, nsm = 148, per_sm = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+        const size_t sm_b = tree_smem(L, scratch_layout(L, false, 0), 2, 1);
+        DK_DISPATCH(cfg, { cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_ls_sw_tree<W, MAXC, 2>, tree_threads<W, 2>(), sm_b); });
+        cudaGetLastError();
+        const long long waves = L.P >= 2000 ? 4 : 1;
+        if (!(per_sm > 0 && (long long)sp.runs * sp.n_ls <= waves * per_sm * nsm)) return 0;
+    }
+    return 1;
+}
+
+cudaError_t launch_run_sw(const LigDev &L, const GridDev &g, const SearchDev &sp, const PopDev &pop,
+                          unsigned long long *prof, cudaStream_t s) {
+    const GroupCfg cfg = pick_group(L.N);
+    const ScratchLayout SL = scratch_layout(L, false, 4 * sp.pop);
+    const size_t smem = tree_smem(L, SL, 2, 1);
+    LsArgs a{};
+    a.use_state = 1; a.n_per_run = sp.n_ls; a.iters = sp.ls_iters;
+    cudaError_t e = cudaSuccess;
+    DK_DISPATCH(cfg, {
+        auto kern = k_run_sw<W, MAXC>;
+        cudaLaunchConfig_t lc = {};
+        lc.gridDim = dim3((unsigned)(sp.runs * sp.n_ls));
+        lc.blockDim = dim3(tree_threads<W, 2>());
+        lc.dynamicSmemBytes = smem;
+        lc.stream = s;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = (unsigned)sp.n_ls; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
+        lc.attrs = at; lc.numAttrs = 1;
+        e = cudaLaunchKernelEx(&lc, kern, L, g, SL, sp, pop, a, prof);
+    });
+    return e != cudaSuccess ? e : cudaGetLastError();
 }
 
 cudaError_t launch_bench_part(const LigDev &L, const GridDev &g, int part, int n, int iters, const float *genes,

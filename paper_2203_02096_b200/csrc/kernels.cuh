@@ -46,6 +46,9 @@ struct GroupCfg {
                           int *dbg, cudaStream_t s);                                                         \
     cudaError_t launch_ls(const LigDev &L, const GridDev &g, const SearchDev &sp, const PopDev &pop,         \
                           const LsArgs &a, int n_total, cudaStream_t s);                                     \
+    int run_sw_eligible(const LigDev &L, const SearchDev &sp);                                               \
+    cudaError_t launch_run_sw(const LigDev &L, const GridDev &g, const SearchDev &sp, const PopDev &pop,     \
+                              unsigned long long *prof, cudaStream_t s);                                     \
     cudaError_t launch_bench_part(const LigDev &L, const GridDev &g, int part, int n, int iters,             \
                                   const float *genes, float *E, cudaStream_t s);                             \
     cudaError_t launch_gen_end(const SearchDev &sp, const PopDev &pop, cudaStream_t s);                      \
@@ -94,6 +97,13 @@ inline cudaError_t launch_bench_part(const LigDev &L, const GridDev &g, int part
                                      const float *genes, float *E, cudaStream_t s) {
     return L.sf == kScoreAD4 ? ad4::launch_bench_part(L, g, part, n, iters, genes, E, s)
                              : d5::launch_bench_part(L, g, part, n, iters, genes, E, s);
+}
+inline int run_sw_eligible(const LigDev &L, const SearchDev &sp) {
+    return L.sf == kScoreAD4 ? ad4::run_sw_eligible(L, sp) : d5::run_sw_eligible(L, sp);
+}
+inline cudaError_t launch_run_sw(const LigDev &L, const GridDev &g, const SearchDev &sp, const PopDev &pop,
+                                 unsigned long long *prof, cudaStream_t s) {
+    return L.sf == kScoreAD4 ? ad4::launch_run_sw(L, g, sp, pop, prof, s) : d5::launch_run_sw(L, g, sp, pop, prof, s);
 }
 inline cudaError_t launch_gen_end(const SearchDev &sp, const PopDev &pop, cudaStream_t s) {
     return d5::launch_gen_end(sp, pop, s);

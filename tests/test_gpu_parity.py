@@ -598,7 +598,8 @@ def test_tail_schedules_parity(dock, n_atoms, mode, monkeypatch):
 # generations as its own graph branch gives exactly the lockstep results.
 # ---------------------------------------------------------------------------
 @pytest.mark.parametrize("name,method,runs,budget", [("1stp", 1, 20, 120_000), ("tiny", 1, 6, 2000),
-                                                     ("3ce3", 0, 4, 40_000)])
+                                                     ("3ce3", 0, 4, 40_000), ("pm", 1, 5, 60_000),
+                                                     ("1stp", 1, 1, 30_000)])
 def test_run_branches_identical_to_lockstep(dock, name, method, runs, budget):
     cfg, lig, grid = config_inputs(name)
     kw = dict(ls_method=method, ls_rate=0.06 if method == 1 else 1.0,
@@ -610,7 +611,11 @@ def test_run_branches_identical_to_lockstep(dock, name, method, runs, budget):
     assert a.run_branches == 1 and b.run_branches == runs
     for k in ("best_E", "best_genes", "evals", "generations", "best_xyz"):
         assert np.array_equal(ra[k], rb[k]), k
-    if method == 1:                        # auto picks branches for Solis-Wets
-        c = dock.Docker.from_inputs(grid, lig, **kw)
-        rc = c.run(cfg.pop, runs, budget, 77, run_base=3, ligand_id=5)
-        assert c.run_branches == runs and np.array_equal(rc["best_E"], ra["best_E"])
+    if method == 1:                        # persistent clusters (auto for Solis-Wets where eligible)
+        for mode in (3, 0):
+            c = dock.Docker.from_inputs(grid, lig, run_branches=mode, **kw)
+            rc = c.run(cfg.pop, runs, budget, 77, run_base=3, ligand_id=5)
+            assert c.run_branches == runs
+            for k in ("best_E", "best_genes", "evals", "generations", "best_xyz"):
+                assert np.array_equal(ra[k], rc[k]), (mode, k)
+            c.close()
