@@ -480,7 +480,7 @@ int dock_run_device(dock_ctx *c, int32_t pop, int32_t runs, int32_t run_base, ui
         }
         return DOCK_OK;
     }
-    const bool branched = runs > 1 && do_ls && (mode == 2 || (mode == 0 && sp.ls_method == DOCK_LS_SOLIS_WETS));
+    const bool branched = runs > 1 && do_ls && (mode >= 2 || (mode == 0 && sp.ls_method == DOCK_LS_SOLIS_WETS));
     const int NB = branched ? runs : 1;
     c->last_branches = NB;
     const bool prof = c->params.profile != 0;

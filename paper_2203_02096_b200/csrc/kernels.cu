@@ -17,6 +17,7 @@
 // group (16 or 32 lanes) handles one individual ("each local optimization occurs
 // independently"; NS "one CTA or warp-group handles each individual").
 #include <math.h>
+#include <cstdlib>
 
 #include <cooperative_groups.h>
 
@@ -1112,7 +1113,7 @@ int run_sw_eligible(const LigDev &L, const SearchDev &sp) {
     const ScratchLayout SL = scratch_layout(L, false, 4 * sp.pop);
     const size_t smem = tree_smem(L, SL, 2, 1);
     if (smem > (size_t)kSmemMax) return 0;
-    if (sp.sw_depth == 0) {   // the auto depth rule of launch_ls, on all runs' chains
+    if (sp.sw_depth == 0 && !std::getenv("DOCK_RUNSW_ANY")) {   // the auto depth rule of launch_ls, on all runs' chains
         int dev = 0, nsm = 148, per_sm = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
