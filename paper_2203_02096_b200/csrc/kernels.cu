@@ -610,15 +610,16 @@ constexpr int tree_threads() { return ((ipow3(D) - 1) * KP * W + 31) / 32 * 32; 
 // groups, ligand already staged (k_ls_sw_tree, and the LS phase of k_run_sw).  Shared
 // memory after the ligand block: the groups' scratch, then x, b, partial energies and the
 // double-buffered deviate shapes (tree_smem).
+constexpr int kTriAhead = 16;   // SW iterations whose deviate shapes are precomputed at a time (>= D)
+
 template <int W, int MAXC, int D, int KP>
 __device__ __forceinline__ void sw_tree_chain(const LigSm &Ls, const GridDev &g, const ScratchLayout &SL,
                                               const SearchDev &sp, const PopDev &pop, const LsArgs &a,
                                               const LsTarget &t, uint8_t *sm, const int staged, const int G) {
     constexpr int NGR = ipow3(D) - 1;
-    float *sx = reinterpret_cast<float *>(sm + staged + NGR * KP * SL.bytes);
-    float *sb = sx + kMaxGenes;
-    float *sE = sb + kMaxGenes;                              // [NGR][KP] partial energies
-    float *stri0 = sE + NGR * KP;                            // [2][D][G] deviate shapes, double-buffered by round
+    constexpr int NS = (kMaxGenes + W - 1) / W;              // genes per lane: j = sub + W s
+    float *sE = reinterpret_cast<float *>(sm + staged + NGR * KP * SL.bytes);   // [2][NGR][KP], by round parity
+    float *stri = sE + 2 * NGR * KP;                         // [kTriAhead][G] deviate shapes of iterations sbase..
     const int gidx = threadIdx.x / W, sub = threadIdx.x % W;  // lane group
     const int grp = gidx / KP, part = gidx % KP;             // node, part of its evaluation
     const bool in_grp = grp < NGR;
@@ -627,7 +628,16 @@ __device__ __forceinline__ void sw_tree_chain(const LigSm &Ls, const GridDev &g,
     // the warps stay converged and the group shuffles take a constant full-warp mask
     constexpr unsigned gmask = 0xffffffffu;
     const uint2 key = make_uint2(sp.key0, sp.key1);
-    for (int j = threadIdx.x; j < G; j += blockDim.x) { sx[j] = __ldcg(t.row + j); sb[j] = 0.0f; }
+    // x and b live in registers: every thread holds genes sub + W s and advances them along
+    // the resolved path itself (all threads resolve identically), so a round needs one
+    // barrier; sE is double-buffered by round parity for the same reason.
+    float x[NS], b[NS];
+#pragma unroll
+    for (int s2 = 0; s2 < NS; ++s2) {
+        const int j = sub + W * s2;
+        x[s2] = j < G ? __ldcg(t.row + j) : 0.0f;
+        b[s2] = 0.0f;
+    }
     for (int j = sub; j < G; j += W) S.genes[j] = 0.0f;      // finite genes for a moot first round
     // this group's node: level lvl, parent state sigma (base-3 outcome digits), candidate
     int lvl = 0;
@@ -642,16 +652,29 @@ __device__ __forceinline__ void sw_tree_chain(const LigSm &Ls, const GridDev &g,
             if (k < lvl) { digit[k] = v % 3; v /= 3; }
         }
     }
-    // deviate shapes of the first round (one Philox block per (iteration, gene))
-    for (int q = threadIdx.x; q < D * G; q += blockDim.x) {
+    // deviate shapes of kTriAhead iterations at a time (one Philox block per (iteration,
+    // gene)), refilled when a round would run past them: the Philox work leaves the
+    // per-round critical path
+    int sbase = 0;
+    for (int q = threadIdx.x; q < kTriAhead * G; q += blockDim.x) {
         const int k = q / G, j = q - k * G;
-        stri0[q] = sw_tri(key, t.slot, t.gen, t.run_g, G, k, j);
+        stri[q] = sw_tri(key, t.slot, t.gen, t.run_g, G, k, j);
     }
     __syncthreads();
     float Ex = __ldcg(t.E), rho = sp.sw_rho;
     int succ = 0, fail = 0, ne = 0, it = 0, cur = 0;
     while (it < a.iters && !(rho < sp.sw_rho_min)) {
-        const float *stri = stri0 + cur * D * kMaxGenes;
+        if (it + D > sbase + kTriAhead) {                     // uniform: refill the deviate window
+            __syncthreads();                                  // the previous round's path reads are done
+            sbase = it;
+            for (int q = threadIdx.x; q < kTriAhead * G; q += blockDim.x) {
+                const int k = q / G, j = q - k * G;
+                stri[q] = sw_tri(key, t.slot, t.gen, t.run_g, G, sbase + k, j);
+            }
+            __syncthreads();
+        }
+        const float *tri = stri + (it - sbase) * G;           // iteration it + k: tri[k * G + j]
+        float *sEc = sE + cur * NGR * KP;
         // ---- 1. every live node's trial genotype, then its energy ----
         if (in_grp) {
             float rl[D];
@@ -668,22 +691,26 @@ __device__ __forceinline__ void sw_tree_chain(const LigSm &Ls, const GridDev &g,
             }
             if (r < sp.sw_rho_min || it + lvl >= a.iters) live = false;
             if (live) {
-                for (int j = sub; j < G; j += W) {
-                    float x = sx[j], b = sb[j];
 #pragma unroll
-                    for (int k = 0; k < D; ++k)
-                        if (k < lvl) sw_gene_step(digit[k], sw_dev(rl[k], stri[k * G + j]), x, b);
-                    const float d = sw_dev(r, stri[lvl * G + j]);
-                    S.genes[j] = cand ? sw_c2(x, b, d) : sw_c1(x, b, d);
+                for (int s2 = 0; s2 < NS; ++s2) {
+                    const int j = sub + W * s2;
+                    if (j < G) {
+                        float xx = x[s2], bb = b[s2];
+#pragma unroll
+                        for (int k = 0; k < D; ++k)
+                            if (k < lvl) sw_gene_step(digit[k], sw_dev(rl[k], tri[k * G + j]), xx, bb);
+                        const float d = sw_dev(r, tri[lvl * G + j]);
+                        S.genes[j] = cand ? sw_c2(xx, bb, d) : sw_c1(xx, bb, d);
+                    }
                 }
             }
             __syncwarp(gmask);
             const float e = eval_group<W, MAXC, false, kAll, KP>(Ls, g, S, sub, gmask, part);
-            if (sub == 0) sE[gidx] = live ? e : INFINITY;
+            if (sub == 0) sEc[gidx] = live ? e : INFINITY;
         }
         __syncthreads();
         // ---- 2. resolve the actual path (every thread, identical scalar logic) ----
-        int path[D], rho_steps = 0, it0 = it;
+        int path[D], rho_steps = 0;
         float rl[D];
         int sg = 0;
 #pragma unroll
@@ -695,9 +722,9 @@ __device__ __forceinline__ void sw_tree_chain(const LigSm &Ls, const GridDev &g,
             if (it >= a.iters || rho < sp.sw_rho_min) break;
             rl[k] = rho;
             const int id = ipow3(k) - 1 + 2 * sg;
-            float E1 = sE[id * KP], E2 = sE[(id + 1) * KP];          // partials: fixed order
+            float E1 = sEc[id * KP], E2 = sEc[(id + 1) * KP];          // partials: fixed order
 #pragma unroll
-            for (int p = 1; p < KP; ++p) { E1 += sE[id * KP + p]; E2 += sE[(id + 1) * KP + p]; }
+            for (int p = 1; p < KP; ++p) { E1 += sEc[id * KP + p]; E2 += sEc[(id + 1) * KP + p]; }
             int o;
             ++ne;
             if (E1 < Ex) { o = 0; Ex = E1; }
@@ -712,27 +739,25 @@ __device__ __forceinline__ void sw_tree_chain(const LigSm &Ls, const GridDev &g,
             ++it;
             ++rho_steps;
         }
-        // ---- 3. advance x and b along the resolved path (warp 0), and meanwhile the next
-        // round's deviate shapes (iterations it..it+D-1; the other warps) ----
-        if (threadIdx.x < 32) {
-            for (int j = threadIdx.x; j < G; j += 32) {
-                float x = sx[j], b = sb[j];
+        // ---- 3. advance this thread's x and b along the resolved path ----
+#pragma unroll
+        for (int s2 = 0; s2 < NS; ++s2) {
+            const int j = sub + W * s2;
+            if (j < G) {
 #pragma unroll
                 for (int k = 0; k < D; ++k)
-                    if (k < rho_steps) sw_gene_step(path[k], sw_dev(rl[k], stri[k * G + j]), x, b);
-                sx[j] = x; sb[j] = b;
-            }
-        } else {
-            float *nxt = stri0 + (cur ^ 1) * D * kMaxGenes;
-            for (int q = threadIdx.x - 32; q < D * G; q += blockDim.x - 32) {
-                const int k = q / G, j = q - k * G;
-                nxt[q] = sw_tri(key, t.slot, t.gen, t.run_g, G, it + k, j);
+                    if (k < rho_steps) sw_gene_step(path[k], sw_dev(rl[k], tri[k * G + j]), x[s2], b[s2]);
             }
         }
         cur ^= 1;
-        __syncthreads();
     }
-    for (int j = threadIdx.x; j < G; j += blockDim.x) t.row[j] = sx[j];
+    if (gidx == 0) {
+#pragma unroll
+        for (int s2 = 0; s2 < NS; ++s2) {
+            const int j = sub + W * s2;
+            if (j < G) t.row[j] = x[s2];
+        }
+    }
     if (threadIdx.x == 0) { *t.E = Ex; *t.evals = ne; ls_finish(sp, pop, t); }
 }
 
@@ -1011,7 +1036,7 @@ cudaError_t launch_ga(const LigDev &L, const GridDev &g, const SearchDev &sp, co
 // group, x and b, the partial energies and the double-buffered deviate shapes
 static size_t tree_smem(const LigDev &L, const ScratchLayout &SL, int D, int KP) {
     const int ngr = (D == 3 ? 26 : (D == 2 ? 8 : 2)) * KP;
-    return (size_t)staged_bytes(L, false) + (size_t)ngr * SL.bytes + 4 * (2 * kMaxGenes + ngr + 2 * D * kMaxGenes);
+    return (size_t)staged_bytes(L, false) + (size_t)ngr * SL.bytes + 4 * (2 * ngr + kTriAhead * kMaxGenes);
 }
 
 cudaError_t launch_ls(const LigDev &L, const GridDev &g, const SearchDev &sp, const PopDev &pop, const LsArgs &a,
