@@ -10,7 +10,7 @@ timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 600 --c
     --log-file $OUT/launches_${CFG}.csv python bench.py --config $CFG --steps 1 --warmup 0 --no-cpu "$@" \
     > $OUT/ncu_launch_${CFG}.log 2>&1
 python scripts/ncu_summary.py launches $OUT/launches_${CFG}.csv > $OUT/launch_share_${CFG}.txt 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:${KRE} -s 20 -c 1 \
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:${KRE} -s ${SKIP:-20} -c 1 \
     -o /tmp/prof_${CFG}_${TAG} python bench.py --config $CFG --steps 1 --warmup 0 --no-cpu "$@" \
     > $OUT/ncu_full_${CFG}.log 2>&1
 python scripts/ncu_summary.py full /tmp/prof_${CFG}_${TAG}.ncu-rep > $OUT/full_ls_${CFG}.txt 2>&1

@@ -14,7 +14,7 @@ for C in $CFGS; do
   timeout 900 python bench.py --config $C > $OUT/bench_$C.json 2> $OUT/bench_$C.err; echo "bench $C rc=$?"; tail -c 600 $OUT/bench_$C.json
 done
 if [ "${PROFILE:-1}" = "1" ]; then
-  bash scripts/gpu_profile.sh 1stp k_ls_sw_tree $TAG
+  SKIP=1 bash scripts/gpu_profile.sh 1stp k_run_sw $TAG
   bash scripts/gpu_profile.sh 7cpa k_ls_adadelta $TAG
   ls -la gpurun_out/
 fi
