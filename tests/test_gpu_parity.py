@@ -619,3 +619,22 @@ def test_run_branches_identical_to_lockstep(dock, name, method, runs, budget):
             for k in ("best_E", "best_genes", "evals", "generations", "best_xyz"):
                 assert np.array_equal(ra[k], rc[k]), (mode, k)
             c.close()
+
+
+@pytest.mark.parametrize("ls_rate,max_gen", [(16 / 150, 27000), (17 / 150, 27000), (1 / 150, 27000), (0.06, 7)])
+def test_cluster_engine_edges(dock, ls_rate, max_gen):
+    """k_run_sw at its eligibility edges (n_ls = 16 clusters, 17 falls back to branches,
+    n_ls = 1) and with a generation cap: identical to lockstep."""
+    cfg, lig, grid = config_inputs("1stp")
+    kw = dict(ls_method=1, ls_rate=ls_rate, ls_max_iters=60, max_generations=max_gen)
+    a = dock.Docker.from_inputs(grid, lig, run_branches=1, **kw)
+    b = dock.Docker.from_inputs(grid, lig, run_branches=0, **kw)
+    ra = a.run(150, 4, 40_000, 5, xyz=False)
+    rb = b.run(150, 4, 40_000, 5, xyz=False)
+    n_ls = int(np.ceil(np.float64(np.float32(ls_rate)) * 150 - 1e-4))
+    assert b.run_branches == 4 and (n_ls <= 16) == (n_ls != 17)
+    for k in ("best_E", "best_genes", "evals", "generations"):
+        assert np.array_equal(ra[k], rb[k]), k
+    if max_gen < 27000:
+        assert (ra["generations"] == max_gen).all()
+    a.close(); b.close()
