@@ -307,6 +307,17 @@ enum { DOCK_FMT_JSON = 0, DOCK_FMT_CSV = 1 };
    the buffer with a first call.  Host only: no device needed. */
 int dock_write_result(const dock_result_view *r, int32_t format, char *buf, size_t cap, size_t *len);
 
+/* Serialise a dock_screen result table (one row per ligand): JSON {ligands: [{ligand,
+   id, status, best_energy, best_run, evals, device, best_genotype[n_genes[i]]}], best:
+   {ligand, best_energy}} (best = lowest energy over ligands with status DOCK_OK, NaN as
+   +inf, lowest index on ties) or CSV (ligand,id,status,best_energy,best_run,evals,device).
+   Arrays are dock_screen's outputs; ids, best_run, best_genotype (stride DOCK_MAX_GENES),
+   n_genes, evals, status and device_of may be NULL.  Size protocol as dock_write_result. */
+int dock_write_screen(int32_t n_ligands, const uint32_t *ids, const float *best_energy,
+                      const int32_t *best_run, const float *best_genotype, const int32_t *n_genes,
+                      const int64_t *evals, const int32_t *status, const int32_t *device_of,
+                      int32_t format, char *buf, size_t cap, size_t *len);
+
 /* Kernel-launch counter of this context (for the benchmark's gpu_launches claim). */
 int64_t dock_launch_count(const dock_ctx *ctx);
 

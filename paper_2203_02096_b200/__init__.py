@@ -104,6 +104,8 @@ def _load():
         "dock_eval_terms": (i32, [v, i32, P(f), P(f), P(f), P(f)]),
         "dock_cluster": (i32, [v, i32, P(f), P(f), f, P(i32), P(f), P(i32), P(i32)]),
         "dock_write_result": (i32, [P(ResultView), i32, C.c_char_p, C.c_size_t, P(C.c_size_t)]),
+        "dock_write_screen": (i32, [i32, P(u32), P(f), P(i32), P(f), P(i32), P(i64), P(i32), P(i32), i32, C.c_char_p,
+                                    C.c_size_t, P(C.c_size_t)]),
         "dock_bench_part": (i32, [v, i32, i32, i32, v, v, v]),
         "dock_get_pairs": (i32, [v, P(i32)]),
         "dock_get_torsions": (i32, [v, P(i32), P(C.c_uint8)]),
@@ -135,7 +137,8 @@ EXPORTED = ("dock_params_default", "dock_builtin_type_param", "dock_init", "dock
             "dock_run_device", "dock_eval", "dock_eval_device", "dock_get_pairs", "dock_get_torsions",
             "dock_philox", "dock_stream_words", "dock_ga_step", "dock_ls_step", "dock_launch_count",
             "dock_topology", "dock_kernel_stats", "dock_upload_bytes", "dock_screen", "dock_screen_last_error",
-            "dock_bench_part", "dock_eval_terms", "dock_cluster", "dock_write_result", "dock_run_branches")
+            "dock_bench_part", "dock_eval_terms", "dock_cluster", "dock_write_result", "dock_run_branches",
+            "dock_write_screen")
 
 
 def write_result(res: dict, fmt: str = "json", timings: dict | None = None) -> str:
@@ -174,6 +177,32 @@ def write_result(res: dict, fmt: str = "json", timings: dict | None = None) -> s
     lib.dock_write_result(C.byref(r), f, None, 0, C.byref(need))
     buf = C.create_string_buffer(need.value)
     _check(lib.dock_write_result(C.byref(r), f, buf, need.value, C.byref(need)))
+    return buf.value.decode()
+
+
+def write_screen(out: dict, fmt: str = "json", ids=None, n_genes=None) -> str:
+    """dock_write_screen (NEXT-3): a screen() result dict -> JSON / CSV text."""
+    bE = np.ascontiguousarray(out["best_E"], dtype=np.float32)
+    n = bE.shape[0]
+    keep = []
+
+    def arr(v, dt, ct):
+        if v is None:
+            return None
+        a = np.ascontiguousarray(v, dtype=dt)
+        keep.append(a)
+        return _ptr(a, ct)
+    f = {"json": FMT_JSON, "csv": FMT_CSV}[fmt]
+    args = [n, arr(ids, np.uint32, C.c_uint32), _ptr(bE, C.c_float), arr(out.get("best_run"), np.int32, C.c_int32),
+            arr(out.get("best_genes"), np.float32, C.c_float), arr(n_genes, np.int32, C.c_int32),
+            arr(out.get("evals"), np.int64, C.c_int64), arr(out.get("status"), np.int32, C.c_int32),
+            arr(out.get("device"), np.int32, C.c_int32), f]
+    need = C.c_size_t(0)
+    lib.dock_write_screen(*args, None, 0, C.byref(need))
+    buf = C.create_string_buffer(need.value)
+    rc = lib.dock_write_screen(*args, buf, need.value, C.byref(need))
+    if rc != DOCK_OK:
+        raise DockError(rc, "dock_write_screen")
     return buf.value.decode()
 
 

@@ -137,3 +137,59 @@ extern "C" int dock_write_result(const dock_result_view *r, int32_t format, char
     std::memcpy(buf, o.c_str(), o.size() + 1);
     return DOCK_OK;
 }
+
+extern "C" int dock_write_screen(int32_t n, const uint32_t *ids, const float *best_energy, const int32_t *best_run,
+                                 const float *best_genotype, const int32_t *n_genes, const int64_t *evals,
+                                 const int32_t *status, const int32_t *device_of, int32_t format, char *buf,
+                                 size_t cap, size_t *len) {
+    if (n < 0 || (n > 0 && !best_energy) || (format != DOCK_FMT_JSON && format != DOCK_FMT_CSV)) return DOCK_E_INPUT;
+    auto ok = [&](int i) { return !status || status[i] == DOCK_OK; };
+    int best = -1;
+    for (int i = 0; i < n; ++i)
+        if (ok(i) && (best < 0 || key(best_energy[i]) < key(best_energy[best]))) best = i;
+    std::string o;
+    if (format == DOCK_FMT_CSV) {
+        o += "ligand,id,status,best_energy,best_run,evals,device\n";
+        for (int i = 0; i < n; ++i) {
+            put_i(o, i); o += ',';
+            put_i(o, ids ? (long long)ids[i] : i); o += ',';
+            put_i(o, status ? status[i] : 0); o += ',';
+            put_f(o, best_energy[i], false); o += ',';
+            if (best_run) put_i(o, best_run[i]);
+            o += ',';
+            if (evals) put_i(o, evals[i]);
+            o += ',';
+            if (device_of) put_i(o, device_of[i]);
+            o += '\n';
+        }
+    } else {
+        o += "{\"ligands\": [";
+        for (int i = 0; i < n; ++i) {
+            if (i) o += ", ";
+            o += "{\"ligand\": "; put_i(o, i);
+            o += ", \"id\": "; put_i(o, ids ? (long long)ids[i] : i);
+            o += ", \"status\": "; put_i(o, status ? status[i] : 0);
+            o += ", \"best_energy\": "; put_f(o, best_energy[i], true);
+            if (best_run) { o += ", \"best_run\": "; put_i(o, best_run[i]); }
+            if (evals) { o += ", \"evals\": "; put_i(o, evals[i]); }
+            if (device_of) { o += ", \"device\": "; put_i(o, device_of[i]); }
+            if (best_genotype && n_genes && ok(i)) {
+                o += ", \"best_genotype\": [";
+                for (int j = 0; j < n_genes[i] && j < DOCK_MAX_GENES; ++j) {
+                    if (j) o += ", ";
+                    put_f(o, best_genotype[(size_t)i * DOCK_MAX_GENES + j], true);
+                }
+                o += ']';
+            }
+            o += '}';
+        }
+        o += "], \"best\": {\"ligand\": "; put_i(o, best);
+        o += ", \"best_energy\": ";
+        if (best >= 0) put_f(o, best_energy[best], true); else o += "null";
+        o += "}}\n";
+    }
+    if (len) *len = o.size() + 1;
+    if (!buf || cap < o.size() + 1) return DOCK_E_INPUT;
+    std::memcpy(buf, o.c_str(), o.size() + 1);
+    return DOCK_OK;
+}

@@ -80,3 +80,24 @@ def test_float32_values_round_trip_through_text(dock):
     j = json.loads(dock.write_result(r, "json"))
     got = np.array([p["best_energy"] for p in j["per_run"]], np.float32)
     assert np.array_equal(got.view(np.uint32)[:5], vals.view(np.uint32)[:5]) and got[5] == 0.0
+
+
+def test_screen_table_json_csv(dock):
+    rng = np.random.default_rng(2)
+    n = 7
+    out = dict(best_E=rng.normal(-5, 2, n).astype(np.float32), best_run=rng.integers(0, 10, n).astype(np.int32),
+               best_genes=rng.normal(0, 1, (n, 38)).astype(np.float32), evals=rng.integers(1000, 9000, n),
+               status=np.array([0, 0, 1, 0, 0, 0, 0], np.int32), device=np.zeros(n, np.int32))
+    out["best_E"][2] = np.nan
+    out["best_E"][5] = -20.0
+    out["status"][5] = 1                                   # rejected ligand: never the best
+    ng = np.full(n, 11, np.int32)
+    j = json.loads(dock.write_screen(out, "json", ids=np.arange(100, 107), n_genes=ng))
+    ok = [i for i in range(n) if out["status"][i] == 0]
+    b = ok[int(np.argmin(out["best_E"][ok]))]
+    assert j["best"]["ligand"] == b and np.float32(j["best"]["best_energy"]) == out["best_E"][b]
+    assert [r["id"] for r in j["ligands"]] == list(range(100, 107))
+    assert j["ligands"][2]["best_energy"] is None and "best_genotype" not in j["ligands"][2]
+    assert np.array_equal(np.array(j["ligands"][0]["best_genotype"], np.float32), out["best_genes"][0, :11])
+    rows = list(csv.DictReader(io.StringIO(dock.write_screen(out, "csv"))))
+    assert len(rows) == n and rows[2]["best_energy"] == "" and int(rows[3]["evals"]) == out["evals"][3]
