@@ -9,6 +9,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <numeric>
@@ -420,6 +421,20 @@ int prepare_ligand(const dock_ligand *l, const dock_type_param *tp, int n_types,
                     for (int ln = 0; ln < Wg; ++ln, ++slot)
                         fill(slot, I * Wg + ln, Bf * Wg + k, I < Bf || ln < k);
         if (slot != L.n_slots) return fail("internal: pair-slot count mismatch");
+        if (std::getenv("DOCK_SLOT_STATS")) {   // diagnostics: steps (W slots) holding no pair at all
+            const float4 *s4c = reinterpret_cast<const float4 *>(bl + L.off_slot4);
+            int empty = 0, steps = L.n_slots / Wg, real = 0;
+            for (int st = 0; st < steps; ++st) {
+                bool any = false;
+                for (int ln = 0; ln < Wg; ++ln) {
+                    const float4 v = s4c[st * Wg + ln];
+                    if (v.y != 0.f || v.z != 0.f || v.w != 0.f || sq[st * Wg + ln] != 0.f) { any = true; ++real; }
+                }
+                if (!any) ++empty;
+            }
+            std::fprintf(stderr, "[slots] N %d P %d steps %d empty %d real-slots %d of %d\n", N, P, steps, empty, real,
+                         L.n_slots);
+        }
     }
     uint32_t *bpairs = reinterpret_cast<uint32_t *>(bl + L.off_pairs);
     float4 *pprm = reinterpret_cast<float4 *>(bl + L.off_pprm);
