@@ -797,13 +797,13 @@ __device__ __forceinline__ unsigned long long global_ns() {
     return t;
 }
 
-template <int W, int MAXC>
-__global__ void __launch_bounds__(tree_threads<W, 2, 1>(), 1) k_run_sw(const LigDev L, const GridDev g,
+template <int W, int MAXC, int D = 2>
+__global__ void __launch_bounds__(tree_threads<W, D, 1>(), 1) k_run_sw(const LigDev L, const GridDev g,
                                                                       const ScratchLayout SL, const SearchDev sp,
                                                                       const PopDev pop, const LsArgs a,
                                                                       unsigned long long *prof) {
     namespace cg = cooperative_groups;
-    constexpr int NGR = ipow3(2) - 1;
+    constexpr int NGR = ipow3(D) - 1;
     cg::cluster_group cl = cg::this_cluster();
     const int nq = (int)cl.num_blocks(), q = (int)cl.block_rank();
     const int r = blockIdx.x / nq;
@@ -831,7 +831,7 @@ __global__ void __launch_bounds__(tree_threads<W, 2, 1>(), 1) k_run_sw(const Lig
         const unsigned long long t0 = timer ? global_ns() : 0ull;
         // ---- LS phase ----
         const LsTarget t = ls_target(sp, pop, a, r * nq + q, G);
-        sw_tree_chain<W, MAXC, 2, 1>(Ls, g, SL, sp, pop, a, t, sm, staged, G);
+        sw_tree_chain<W, MAXC, D, 1>(Ls, g, SL, sp, pop, a, t, sm, staged, G);
         __threadfence();
         cl.sync();
         if (timer) { prof[0] += global_ns() - t0; prof[1] += 1ull; }
@@ -976,8 +976,10 @@ cudaError_t setup_kernel_attributes() {
     if (e == cudaSuccess) e = allow_smem(k_ls_sw_tree<W, MAXC, 2>);                  \
     if (e == cudaSuccess) e = allow_smem(k_ls_sw_tree<W, MAXC, 3>);                  \
     if (e == cudaSuccess) e = allow_split<W, MAXC>();                                 \
-    if (e == cudaSuccess) e = allow_smem(k_run_sw<W, MAXC>);                         \
-    if (e == cudaSuccess) e = cudaFuncSetAttribute(k_run_sw<W, MAXC>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1); \
+    if (e == cudaSuccess) e = allow_smem(k_run_sw<W, MAXC, 2>);                      \
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(k_run_sw<W, MAXC, 2>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1); \
+    if (e == cudaSuccess) e = allow_smem(k_run_sw<W, MAXC, 3>);                      \
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(k_run_sw<W, MAXC, 3>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1); \
     if (e == cudaSuccess) e = allow_smem(k_bench_part<W, MAXC, kInter>);             \
     if (e == cudaSuccess) e = allow_smem(k_bench_part<W, MAXC, kIntra>);
     DK_ATTR(16, 1) DK_ATTR(32, 1) DK_ATTR(32, 2) DK_ATTR(32, 3) DK_ATTR(32, 4) DK_ATTR(32, 8)
@@ -1132,11 +1134,11 @@ cudaError_t launch_ls(const LigDev &L, const GridDev &g, const SearchDev &sp, co
 // lockstep engine).  Returns 0 if not eligible.
 int run_sw_eligible(const LigDev &L, const SearchDev &sp) {
     if (sp.ls_method != 1 || sp.n_ls < 1 || sp.n_ls > 16 || sp.ls_iters < 1) return 0;
-    if (sp.sw_depth != 0 && sp.sw_depth != 2) return 0;
+    if (sp.sw_depth != 0 && sp.sw_depth != 2 && sp.sw_depth != 3) return 0;
     if (sp.sw_split == 2 || sp.sw_split == 4 || (sp.sw_split == 0 && L.P >= 2000 && pick_group(L.N).W == 32)) return 0;
     const GroupCfg cfg = pick_group(L.N);
     const ScratchLayout SL = scratch_layout(L, false, 4 * sp.pop);
-    const size_t smem = tree_smem(L, SL, 2, 1);
+    const size_t smem = tree_smem(L, SL, sp.sw_depth == 3 ? 3 : 2, 1);
     if (smem > (size_t)kSmemMax) return 0;
     if (sp.sw_depth == 0 && !std::getenv("DOCK_RUNSW_ANY")) {   // the auto depth rule of launch_ls, on all runs' chains
         int dev = 0, nsm = 148, per_sm = 0;
@@ -1155,15 +1157,16 @@ cudaError_t launch_run_sw(const LigDev &L, const GridDev &g, const SearchDev &sp
                           unsigned long long *prof, cudaStream_t s) {
     const GroupCfg cfg = pick_group(L.N);
     const ScratchLayout SL = scratch_layout(L, false, 4 * sp.pop);
-    const size_t smem = tree_smem(L, SL, 2, 1);
+    const int D = sp.sw_depth == 3 ? 3 : 2;   // depth 3 only on request (sw_depth = 3)
+    const size_t smem = tree_smem(L, SL, D, 1);
     LsArgs a{};
     a.use_state = 1; a.n_per_run = sp.n_ls; a.iters = sp.ls_iters;
     cudaError_t e = cudaSuccess;
     DK_DISPATCH(cfg, {
-        auto kern = k_run_sw<W, MAXC>;
+        auto kern = D == 3 ? k_run_sw<W, MAXC, 3> : k_run_sw<W, MAXC, 2>;
         cudaLaunchConfig_t lc = {};
         lc.gridDim = dim3((unsigned)(sp.runs * sp.n_ls));
-        lc.blockDim = dim3(tree_threads<W, 2>());
+        lc.blockDim = dim3(D == 3 ? tree_threads<W, 3>() : tree_threads<W, 2>());
         lc.dynamicSmemBytes = smem;
         lc.stream = s;
         cudaLaunchAttribute at[1];
