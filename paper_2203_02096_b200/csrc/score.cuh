@@ -45,7 +45,11 @@ constexpr float kDielLB2 = kDielLB * (78.4f + 8.5525f);           // lambda B^2
 #ifndef DK_WALK_DEPTH
 #define DK_WALK_DEPTH 4
 #endif
-constexpr int kWalkDepth = DK_WALK_DEPTH;   // torsion trees up to this depth: per-atom chain walk, no composites
+constexpr int kWalkDepth = DK_WALK_DEPTH;
+#ifndef DK_TILE_UNROLL
+#define DK_TILE_UNROLL 4   // steps unrolled in the pair-slot tile loop (A/B: scripts/variants.py)
+#endif
+constexpr int kTileUnroll = DK_TILE_UNROLL;   // torsion trees up to this depth: per-atom chain walk, no composites
 
 // Shared-memory view of the staged ligand block.
 struct LigSm {
@@ -509,7 +513,7 @@ __device__ __forceinline__ void intra_tiles_slots(const LigSm &L, const Scratch 
             const float *qrow = L.slotq + slot0 + sub - s0 * W;
             slot0 += (s1 - s0 + 1) * W;
             float fx = 0.f, fy = 0.f, fz = 0.f;
-#pragma unroll 4
+#pragma unroll kTileUnroll
             for (int s = s0; s <= s1; ++s) {
                 slot_pair(rx[I], ry[I], rz[I], rrow[s], crow[s * W], qrow[s * W], e, hx[I], hy[I], hz[I], fx, fy,
                           fz);
