@@ -638,3 +638,21 @@ def test_cluster_engine_edges(dock, ls_rate, max_gen):
     if max_gen < 27000:
         assert (ra["generations"] == max_gen).all()
     a.close(); b.close()
+
+
+def test_screen_solis_wets_cluster_engine(dock):
+    """dock_screen with Solis-Wets: several contexts run k_run_sw concurrently on one
+    device; every ligand equals its standalone run."""
+    from gen import hts_ligands
+    from gen.synth import TYPE_NAMES, make_grid
+    ligs = hts_ligands(5, seed=21)
+    grid = make_grid(24, 0.5, list(TYPE_NAMES), seed=77)
+    kw = dict(ls_method=1, ls_rate=0.06, ls_max_iters=60)
+    out = dock.screen(grid, ligs, 100, 4, 20_000, 9, devices=[0], slots_per_device=3, **kw)
+    assert (out["status"] == 0).all()
+    for i, lig in enumerate(ligs):
+        d = dock.Docker.from_inputs(grid, lig, **kw)
+        r = d.run(100, 4, 20_000, 9, ligand_id=i, xyz=False)
+        assert d.run_branches == 4
+        assert out["best_E"][i] == np.nanmin(r["best_E"]) and out["evals"][i] == r["evals"].sum()
+        d.close()
