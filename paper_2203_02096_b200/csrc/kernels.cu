@@ -1150,7 +1150,24 @@ int run_sw_eligible(const LigDev &L, const SearchDev &sp) {
         const long long waves = L.P >= 2000 ? 4 : 1;
         if (!(per_sm > 0 && (long long)sp.runs * sp.n_ls <= waves * per_sm * nsm)) return 0;
     }
-    return 1;
+    // the cluster shape must be schedulable at all (n_ls CTAs of this size in one GPC)
+    int clusters = 0;
+    DK_DISPATCH(cfg, {
+        cudaLaunchConfig_t lc = {};
+        lc.gridDim = dim3((unsigned)sp.n_ls);
+        const bool d3 = sp.sw_depth == 3;
+        lc.blockDim = dim3(d3 ? tree_threads<W, 3>() : tree_threads<W, 2>());
+        lc.dynamicSmemBytes = smem;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = (unsigned)sp.n_ls; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
+        lc.attrs = at; lc.numAttrs = 1;
+        if (cudaOccupancyMaxActiveClusters(&clusters, d3 ? k_run_sw<W, MAXC, 3> : k_run_sw<W, MAXC, 2>, &lc) !=
+            cudaSuccess)
+            clusters = 0;
+    });
+    cudaGetLastError();
+    return clusters > 0 ? 1 : 0;
 }
 
 cudaError_t launch_run_sw(const LigDev &L, const GridDev &g, const SearchDev &sp, const PopDev &pop,
