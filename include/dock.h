@@ -158,9 +158,12 @@ int dock_run_ex(dock_ctx *ctx, int32_t pop_size, int32_t num_runs, int32_t run_b
                 float *best_energy, float *best_genotype, float *best_xyz,
                 int64_t *evals_used, int32_t *generations);
 /* Device-resident variant: outputs are DEVICE pointers, work is enqueued on `stream`
-   (a cudaStream_t, NULL = the context's own stream).  Returns after the last generation batch has
-   been enqueued and the termination flags were polled (it syncs on `stream` once per
-   gens_per_graph generations to read 4*num_runs bytes). */
+   (a cudaStream_t, NULL = the context's own stream).  Graph engines (run_branches 1, 2):
+   returns after the last generation batch has been enqueued and the termination flags were
+   polled (it syncs on `stream` once per gens_per_graph generations to read 16*num_runs
+   bytes).  Persistent-cluster engine (Solis-Wets, run_branches 0 / 3 where eligible):
+   termination is decided on the device, and the call returns once the job is enqueued
+   (it syncs only with params.profile set). */
 int dock_run_device(dock_ctx *ctx, int32_t pop_size, int32_t num_runs, int32_t run_base,
                     uint32_t ligand_id, int64_t max_evals, uint64_t seed,
                     float *d_best_energy, float *d_best_genotype, int64_t *d_evals_used,
