@@ -275,6 +275,7 @@ def run_ours(args, cfg, lig, grid):
     # graph perturb it (1stp 455 vs 302 ms per step), so the timed region runs an
     # unprofiled context and the LS launch times come from one extra profiled step after it.
     branches = d.run_branches
+    engine = d.engine
     dt = d
     if branches > 1:
         dt = make(0)
@@ -337,7 +338,13 @@ def run_ours(args, cfg, lig, grid):
     peak = fp32_peak_tflops(sm_mhz)
     ls_tflops = ls_flops / (ls_ms / 1e3) / 1e12 if ls_ms > 0 else 0.0
     tr = ncu_traffic().get(cfg.name) or {}
-    roofline = {"kernel": ("k_ls_sw_tree / k_ls_sw (Solis-Wets LS, depth auto)" if not grad else "k_ls_adadelta"),
+    if grad:
+        kname = "k_ls_adadelta"
+    elif engine == "clusters":
+        kname = "k_run_sw (persistent cluster engine; timed unit: one LS phase of run 0, GA barrier -> LS barrier)"
+    else:
+        kname = "k_ls_sw_tree / k_ls_sw (Solis-Wets LS, depth auto)"
+    roofline = {"kernel": kname, "engine": engine,
                 "bound": "alu", "achieved": ls_tflops,
                 "peak": peak, "unit": "TFLOP/s", "frac": ls_tflops / peak,
                 "traffic": tr.get("dram_bytes_per_launch"),
@@ -350,8 +357,8 @@ def run_ours(args, cfg, lig, grid):
                 "note": ("Solis-Wets chains are a dependent sequence of energy evaluations and only "
                          f"{runs * int(cfg.ls_rate * cfg.pop + 0.9999)} chains run per generation: the kernel is "
                          "latency-bound (DESIGN.md §7), so this ALU fraction is low by construction"
-                         + (f"; {branches} run branches: achieved = all runs' LS flops / run 0's LS time "
-                            "(the branches run concurrently), share_of_step = run 0's LS time / step"
+                         + (f"; {branches} concurrent runs ({engine}): achieved = all runs' LS flops / run 0's "
+                            "LS time (the runs execute concurrently), share_of_step = run 0's LS time / step"
                             if branches > 1 else ""))
                 if not grad else "issue-bound pair tiles (ncu: profiles/)"}
 

@@ -333,6 +333,12 @@ int dock_kernel_stats(const dock_ctx *ctx, double *ms, int64_t *launches);
 /* Concurrent run branches of the last dock_run* call (1 = lockstep generations). */
 int dock_run_branches(const dock_ctx *ctx);
 
+/* Generation engine of the last dock_run* call: 0 = lockstep graph
+   (k_ga + k_ls_* per generation), 1 = run branches (one graph branch per run),
+   2 = persistent cluster engine (one k_run_sw launch for the whole job).
+   0 before the first run; -1 for a NULL context. */
+int dock_last_engine(const dock_ctx *ctx);
+
 /* Bytes dock_init copied host -> device (packed grid + ligand block + atom map). */
 int64_t dock_upload_bytes(const dock_ctx *ctx);
 

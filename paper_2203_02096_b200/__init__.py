@@ -117,6 +117,7 @@ def _load():
         "dock_kernel_stats": (i32, [v, P(C.c_double), P(i64)]),
         "dock_upload_bytes": (i64, [v]),
         "dock_run_branches": (i32, [v]),
+        "dock_last_engine": (i32, [v]),
         "dock_screen": (i32, [P(Grids), P(TypeParam), P(Ligand), i32, P(u32), P(Params), P(ScreenOpts), i32, i32,
                               i64, u64, P(f), P(i32), P(f), P(i64), P(i32), P(i32), P(ScreenStats)]),
         "dock_screen_last_error": (C.c_char_p, []),
@@ -138,7 +139,7 @@ EXPORTED = ("dock_params_default", "dock_builtin_type_param", "dock_init", "dock
             "dock_philox", "dock_stream_words", "dock_ga_step", "dock_ls_step", "dock_launch_count",
             "dock_topology", "dock_kernel_stats", "dock_upload_bytes", "dock_screen", "dock_screen_last_error",
             "dock_bench_part", "dock_eval_terms", "dock_cluster", "dock_write_result", "dock_run_branches",
-            "dock_write_screen")
+            "dock_write_screen", "dock_last_engine")
 
 
 def write_result(res: dict, fmt: str = "json", timings: dict | None = None) -> str:
@@ -422,6 +423,13 @@ class Docker:
     def run_branches(self) -> int:
         """Concurrent run branches of the last run (1 = lockstep generations)."""
         return int(lib.dock_run_branches(self._ctx))
+
+    ENGINES = ("lockstep", "branches", "clusters")
+
+    @property
+    def engine(self) -> str:
+        """Generation engine of the last run (dock_last_engine): lockstep, branches or clusters."""
+        return self.ENGINES[int(lib.dock_last_engine(self._ctx))]
 
     @property
     def upload_bytes(self) -> int:

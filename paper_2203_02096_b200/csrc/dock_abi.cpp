@@ -420,6 +420,7 @@ int dock_n_pairs(const dock_ctx *c) { return c ? c->prep.P : -1; }
 int64_t dock_launch_count(const dock_ctx *c) { return c ? c->launches : -1; }
 
 int dock_run_branches(const dock_ctx *c) { return c ? c->last_branches : -1; }
+int dock_last_engine(const dock_ctx *c) { return c ? c->last_engine : -1; }
 
 int64_t dock_upload_bytes(const dock_ctx *c) {
     return c ? (int64_t)(c->rec->bytes + c->prep.blob.size() + sizeof(int) * c->prep.N) : -1;
@@ -464,6 +465,7 @@ int dock_run_device(dock_ctx *c, int32_t pop, int32_t runs, int32_t run_base, ui
     // one thread-block cluster per run looping over its generations on the device.
     if (do_ls && (mode == 3 || (mode == 0 && sp.ls_method == DOCK_LS_SOLIS_WETS)) && dk::run_sw_eligible(c->lig, sp)) {
         c->last_branches = runs;
+        c->last_engine = 2;
         const bool prof = c->params.profile != 0;
         for (int i = 0; i < 3; ++i) { c->prof_ms[i] = 0; c->prof_n[i] = 0; }
         if (prof && !c->d_prof) CK(dk::dmalloc((void **)&c->d_prof, 2 * sizeof(unsigned long long), s));
@@ -483,6 +485,7 @@ int dock_run_device(dock_ctx *c, int32_t pop, int32_t runs, int32_t run_base, ui
     const bool branched = runs > 1 && do_ls && (mode >= 2 || (mode == 0 && sp.ls_method == DOCK_LS_SOLIS_WETS));
     const int NB = branched ? runs : 1;
     c->last_branches = NB;
+    c->last_engine = branched ? 1 : 0;
     const bool prof = c->params.profile != 0;
     for (int i = 0; i < 3; ++i) { c->prof_ms[i] = 0; c->prof_n[i] = 0; }
     // events: lockstep 3 per generation (GA start, LS start, LS end) + 2 for init;

@@ -96,6 +96,7 @@ struct dock_ctx {
     std::vector<cudaStream_t> branch_streams;   // run branches of the generation graph (run_branches)
     std::vector<cudaEvent_t> branch_events;     // fork + one join per branch (timing disabled)
     int last_branches = 1;
+    int last_engine = 0;        // dock_last_engine: 0 lockstep, 1 run branches, 2 persistent clusters
     unsigned long long *d_prof = nullptr;       // k_run_sw LS-phase timer (profile)
 };
 

@@ -609,6 +609,7 @@ def test_run_branches_identical_to_lockstep(dock, name, method, runs, budget):
     ra = a.run(cfg.pop, runs, budget, 77, run_base=3, ligand_id=5)
     rb = b.run(cfg.pop, runs, budget, 77, run_base=3, ligand_id=5)
     assert a.run_branches == 1 and b.run_branches == runs
+    assert a.engine == "lockstep" and b.engine == ("branches" if runs > 1 else "lockstep")
     for k in ("best_E", "best_genes", "evals", "generations", "best_xyz"):
         assert np.array_equal(ra[k], rb[k]), k
     if method == 1:                        # persistent clusters (auto for Solis-Wets where eligible)
@@ -616,6 +617,8 @@ def test_run_branches_identical_to_lockstep(dock, name, method, runs, budget):
             c = dock.Docker.from_inputs(grid, lig, run_branches=mode, **kw)
             rc = c.run(cfg.pop, runs, budget, 77, run_base=3, ligand_id=5)
             assert c.run_branches == runs
+            if name == "1stp":             # the headline shape runs in one wave: clusters
+                assert c.engine == "clusters", mode
             for k in ("best_E", "best_genes", "evals", "generations", "best_xyz"):
                 assert np.array_equal(ra[k], rc[k]), (mode, k)
             c.close()
@@ -633,6 +636,9 @@ def test_cluster_engine_edges(dock, ls_rate, max_gen):
     rb = b.run(150, 4, 40_000, 5, xyz=False)
     n_ls = int(np.ceil(np.float64(np.float32(ls_rate)) * 150 - 1e-4))
     assert b.run_branches == 4 and (n_ls <= 16) == (n_ls != 17)
+    assert a.engine == "lockstep"
+    if n_ls <= 8 or n_ls > 16:             # 9..16 also need the non-portable cluster size to fit
+        assert b.engine == ("clusters" if n_ls <= 16 else "branches")
     for k in ("best_E", "best_genes", "evals", "generations"):
         assert np.array_equal(ra[k], rb[k]), k
     if max_gen < 27000:
