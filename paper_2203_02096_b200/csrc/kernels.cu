@@ -797,13 +797,30 @@ __device__ __forceinline__ unsigned long long global_ns() {
     return t;
 }
 
+// Extra warps per k_run_sw CTA that work only in the GA phase: with
+// n_ls x (3^D - 1) lane groups the 1stp cluster (9 x 8 groups) deals its 150 GA slots in
+// 3 rounds, with one more warp (9 x 10 groups) in 2.  In the LS phase they are idle
+// (not in the tree).  Their scratch overlaps the tree's sE / deviate window, which only
+// the LS phase uses; the cluster barriers separate the phases.
+#ifndef DK_RUNSW_XWARPS
+#define DK_RUNSW_XWARPS 0
+#endif
+template <int W, int D>
+__host__ __device__ constexpr int run_sw_threads() { return tree_threads<W, D, 1>() + 32 * DK_RUNSW_XWARPS; }
+
 template <int W, int MAXC, int D = 2>
-__global__ void __launch_bounds__(tree_threads<W, D, 1>(), 1) k_run_sw(const LigDev L, const GridDev g,
+#if DK_RUNSW_XWARPS > 0
+// 2 CTAs of 5 warps per SM need <= 3 warps per SM sub-partition at <= 168 registers (16 K each)
+#define DK_RUNSW_BOUNDS __maxnreg__(168)
+#else
+#define DK_RUNSW_BOUNDS __launch_bounds__(run_sw_threads<W, D>(), 1)
+#endif
+__global__ void DK_RUNSW_BOUNDS k_run_sw(const LigDev L, const GridDev g,
                                                                       const ScratchLayout SL, const SearchDev sp,
                                                                       const PopDev pop, const LsArgs a,
                                                                       unsigned long long *prof) {
     namespace cg = cooperative_groups;
-    constexpr int NGR = ipow3(D) - 1;
+    constexpr int NGA = run_sw_threads<W, D>() / W;          // lane groups of the GA phase
     cg::cluster_group cl = cg::this_cluster();
     const int nq = (int)cl.num_blocks(), q = (int)cl.block_rank();
     const int r = blockIdx.x / nq;
@@ -821,8 +838,8 @@ __global__ void __launch_bounds__(tree_threads<W, D, 1>(), 1) k_run_sw(const Lig
         st.evals = __ldcg(&pop.state[r].evals); st.gen = __ldcg(&pop.state[r].gen);
         if (!run_active(st, sp)) break;                   // uniform over the cluster
         // ---- GA phase ----
-        for (int base = 0; base < P; base += nq * NGR) {
-            const int k = base + q * NGR + gidx;
+        for (int base = 0; base < P; base += nq * NGA) {
+            const int k = base + q * NGA + gidx;
             ga_slot_group<W, MAXC>(Ls, g, S, reinterpret_cast<int *>(gbase + SL.off_extra), sp, pop, G, k < P, st, r,
                                    k < P ? k : 0, sub, nullptr);
         }
@@ -1041,6 +1058,14 @@ static size_t tree_smem(const LigDev &L, const ScratchLayout &SL, int D, int KP)
     return (size_t)staged_bytes(L, false) + (size_t)ngr * SL.bytes + 4 * (2 * ngr + kTriAhead * kMaxGenes);
 }
 
+// k_run_sw: the tree's shared memory, or the GA phase's scratch of all its lane groups
+static size_t run_sw_smem(const LigDev &L, const ScratchLayout &SL, int D) {
+    const int nga = (D == 3 ? run_sw_threads<16, 3>() : run_sw_threads<16, 2>()) / 16;   // W = 16: most groups
+    const size_t ga = (size_t)staged_bytes(L, false) + (size_t)nga * SL.bytes;
+    const size_t tr = tree_smem(L, SL, D, 1);
+    return ga > tr ? ga : tr;
+}
+
 cudaError_t launch_ls(const LigDev &L, const GridDev &g, const SearchDev &sp, const PopDev &pop, const LsArgs &a,
                       int n_total, cudaStream_t s) {
     if (n_total <= 0) return cudaSuccess;
@@ -1138,7 +1163,7 @@ int run_sw_eligible(const LigDev &L, const SearchDev &sp) {
     if (sp.sw_split == 2 || sp.sw_split == 4 || (sp.sw_split == 0 && L.P >= 2000 && pick_group(L.N).W == 32)) return 0;
     const GroupCfg cfg = pick_group(L.N);
     const ScratchLayout SL = scratch_layout(L, false, 4 * sp.pop);
-    const size_t smem = tree_smem(L, SL, sp.sw_depth == 3 ? 3 : 2, 1);
+    const size_t smem = run_sw_smem(L, SL, sp.sw_depth == 3 ? 3 : 2);
     if (smem > (size_t)kSmemMax) return 0;
     if (sp.sw_depth == 0 && !std::getenv("DOCK_RUNSW_ANY")) {   // the auto depth rule of launch_ls, on all runs' chains
         int dev = 0, nsm = 148, per_sm = 0;
@@ -1156,7 +1181,7 @@ int run_sw_eligible(const LigDev &L, const SearchDev &sp) {
         cudaLaunchConfig_t lc = {};
         lc.gridDim = dim3((unsigned)sp.n_ls);
         const bool d3 = sp.sw_depth == 3;
-        lc.blockDim = dim3(d3 ? tree_threads<W, 3>() : tree_threads<W, 2>());
+        lc.blockDim = dim3(d3 ? run_sw_threads<W, 3>() : run_sw_threads<W, 2>());
         lc.dynamicSmemBytes = smem;
         cudaLaunchAttribute at[1];
         at[0].id = cudaLaunchAttributeClusterDimension;
@@ -1175,7 +1200,7 @@ cudaError_t launch_run_sw(const LigDev &L, const GridDev &g, const SearchDev &sp
     const GroupCfg cfg = pick_group(L.N);
     const ScratchLayout SL = scratch_layout(L, false, 4 * sp.pop);
     const int D = sp.sw_depth == 3 ? 3 : 2;   // depth 3 only on request (sw_depth = 3)
-    const size_t smem = tree_smem(L, SL, D, 1);
+    const size_t smem = run_sw_smem(L, SL, D);
     LsArgs a{};
     a.use_state = 1; a.n_per_run = sp.n_ls; a.iters = sp.ls_iters;
     cudaError_t e = cudaSuccess;
@@ -1183,7 +1208,7 @@ cudaError_t launch_run_sw(const LigDev &L, const GridDev &g, const SearchDev &sp
         auto kern = D == 3 ? k_run_sw<W, MAXC, 3> : k_run_sw<W, MAXC, 2>;
         cudaLaunchConfig_t lc = {};
         lc.gridDim = dim3((unsigned)(sp.runs * sp.n_ls));
-        lc.blockDim = dim3(D == 3 ? tree_threads<W, 3>() : tree_threads<W, 2>());
+        lc.blockDim = dim3(D == 3 ? run_sw_threads<W, 3>() : run_sw_threads<W, 2>());
         lc.dynamicSmemBytes = smem;
         lc.stream = s;
         cudaLaunchAttribute at[1];
