@@ -33,6 +33,13 @@ def test_exports_every_declared_symbol(dock):
     assert declared == set(dock.EXPORTED)
 
 
+def test_introspection_null_context(dock):
+    # engine / launch queries on a NULL context: -1, never a crash (include/dock.h)
+    assert dock.lib.dock_last_engine(None) == -1
+    assert dock.lib.dock_run_branches(None) == -1
+    assert dock.lib.dock_launch_count(None) == -1
+
+
 def test_params_default(dock):
     p = dock.params_default()
     assert (p.p_tour, p.p_cross, p.p_mut) == (np.float32(0.6), np.float32(0.8), np.float32(0.02))
