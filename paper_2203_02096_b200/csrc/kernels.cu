@@ -610,7 +610,10 @@ constexpr int tree_threads() { return ((ipow3(D) - 1) * KP * W + 31) / 32 * 32; 
 // groups, ligand already staged (k_ls_sw_tree, and the LS phase of k_run_sw).  Shared
 // memory after the ligand block: the groups' scratch, then x, b, partial energies and the
 // double-buffered deviate shapes (tree_smem).
-constexpr int kTriAhead = 16;   // SW iterations whose deviate shapes are precomputed at a time (>= D)
+#ifndef DK_TRI_AHEAD
+#define DK_TRI_AHEAD 32
+#endif
+constexpr int kTriAhead = DK_TRI_AHEAD;   // SW iterations whose deviate shapes are precomputed at a time (>= D)
 
 template <int W, int MAXC, int D, int KP>
 __device__ __forceinline__ void sw_tree_chain(const LigSm &Ls, const GridDev &g, const ScratchLayout &SL,
