@@ -1,7 +1,9 @@
 #!/usr/bin/env python
 """bench.py — score evaluations/s of the B200 LGA docking hot path (BASELINE.json metric).
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--config 1stp] [--impl ours|reference]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config 7cpa] [--impl ours|reference]
+
+The default config is BASELINE.json configs[3] (7cpa-shaped), the largest single-GPU config.
 
 A step = one complete docking job of the config (all hot-path rows: init, GA generations
 with offspring scoring, local search with scoring(+gradient), sum_evals/termination,
@@ -30,30 +32,32 @@ UNIT = "evals/s"
 
 
 # ---------------------------------------------------------------------------
-# Algorithmic work model: FP32 flops per energy evaluation, FMA = 2.
+# Algorithmic work model: SURVEY.md §8(d) "Op-count model" (FP32 flops, FMA = 2), used
+# verbatim for roofline.achieved:
+#   per pair   21 (energy) / 40 (energy + gradient)
+#   per atom   60 / 100 interpolation + 18 pose (+ 15 back-projection with the gradient)
+#   per torsion 55 / 92;  per gene 12 (ADADELTA update, gradient path only)
+# C3 (N 70, T 15, P 2,000): 48.3 k / 91.1 k flop per evaluation, as §8(d)'s table.
 # ---------------------------------------------------------------------------
-F_ORIENT = 30          # n, q, R(q) from (phi, theta, alpha)
-F_TORSION = 110        # Rodrigues matrix + composite with the parent transform
-F_ATOM_POSE = 18       # one 3x4 transform per atom
-F_ATOM_INTER = 77      # trilinear: corner combine (3 maps), value and gradient
-F_PAIR_E = 33          # D5 energy of one pair
-F_PAIR_EG = 55         # D5 energy + dE/drho2 + force on both atoms (unique pair)
-F_ATOM_BACK = 18       # (r - t) x g, sums
-F_TORSION_BACK = 20    # per-torsion projection (plus 6 per moved atom)
+F_PAIR = (21, 40)
+F_ATOM_INTER = (60, 100)
+F_ATOM_POSE = 18
+F_ATOM_BACK = 15
+F_TORSION = (55, 92)
 F_GENE_ADADELTA = 12
-# NEXT-2 D5-AD4 pair: + r, smoothing, the sigmoidal dielectric and two cutoffs
-F_PAIR_E_AD4 = 52
-F_PAIR_EG_AD4 = 84
+# NEXT-2 D5-AD4 pair: + r, smoothing, the sigmoidal dielectric and two cutoffs;
+# not in §8(d), scaled from D5's pair by the AD4 pair's extra XU + FMA work (5 vs 2 XU ops)
+F_PAIR_AD4 = (33, 62)
 
 SCORING = 0            # --scoring: 0 = D5, 1 = D5-AD4 (dock_params.scoring)
 
 
-def flops_per_eval(N, T, P, moved_total, grad):
-    f = F_ORIENT + T * F_TORSION + N * (F_ATOM_POSE + F_ATOM_INTER)
+def flops_per_eval(N, T, P, grad):
+    """§8(d) op-count model of one evaluation (energy only, or energy + gradient + ADADELTA)."""
+    g = 1 if grad else 0
+    f = P * (F_PAIR_AD4 if SCORING else F_PAIR)[g] + N * (F_ATOM_INTER[g] + F_ATOM_POSE) + T * F_TORSION[g]
     if grad:
-        f += P * (F_PAIR_EG_AD4 if SCORING else F_PAIR_EG) + N * F_ATOM_BACK + T * F_TORSION_BACK + 6 * moved_total + (6 + T) * F_GENE_ADADELTA
-    else:
-        f += P * (F_PAIR_E_AD4 if SCORING else F_PAIR_E)
+        f += N * F_ATOM_BACK + (6 + T) * F_GENE_ADADELTA
     return f
 
 
@@ -256,9 +260,8 @@ def run_ours(args, cfg, lig, grid):
     gens = torch.empty(runs, dtype=torch.int32, device=dev)
     gathered = {}
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
-    moved_total = int(np.asarray(d.torsions()[1]).sum())
-    f_e = flops_per_eval(d.N, d.T, d.P, moved_total, grad=False)
-    f_eg = flops_per_eval(d.N, d.T, d.P, moved_total, grad=True)
+    f_e = flops_per_eval(d.N, d.T, d.P, grad=False)
+    f_eg = flops_per_eval(d.N, d.T, d.P, grad=True)
 
     def step(seed, ctx=None):
         with torch.cuda.stream(stream):
@@ -597,7 +600,7 @@ def run_micro(args, cfg, lig, grid):
     t_in = res["inter"]
     pair_steps = n * iters * d.P
     t_pr = res["intra"]
-    fl = pair_steps * (F_PAIR_EG_AD4 if SCORING else F_PAIR_EG) / t_pr / 1e12
+    fl = pair_steps * (F_PAIR_AD4 if SCORING else F_PAIR)[1] / t_pr / 1e12
     line = {"metric": "microbench", "config": {"workload": workload_desc(cfg), "genotypes": n, "iters": iters},
             "inter": {"kernel": "k_bench_part<kInter> (pose + trilinear E+G)", "ms": 1e3 * t_in,
                       "atom_lookups_per_s": lookups / t_in,
@@ -616,7 +619,7 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="1stp", choices=["tiny", "1stp", "3ce3", "7cpa", "hts", "ps", "pm", "pl"])
+    ap.add_argument("--config", default="7cpa", choices=["tiny", "1stp", "3ce3", "7cpa", "hts", "ps", "pm", "pl"])
     ap.add_argument("--runs", type=int, default=0, help="override runs per GPU (NEXT-1 sweeps)")
     ap.add_argument("--max-evals", type=int, default=0, help="override evals per run (NEXT-1 sweeps)")
     ap.add_argument("--micro", action="store_true", help="isolated inter/intra microbenchmarks (roofline evidence)")

@@ -510,8 +510,26 @@ class Docker:
                                   _ptr(ev, C.c_int64), _ptr(gens, C.c_int32)))
         return dict(best_E=bE, best_genes=bG, best_xyz=bX, evals=ev, generations=gens)
 
+    def _check_dev(self, name, t, dtype, numel):
+        """A device output buffer the kernels write: right dtype, on this context's device,
+        contiguous and large enough (DockError otherwise, before any launch)."""
+        import torch
+        if not isinstance(t, torch.Tensor):
+            raise DockError(DOCK_E_INPUT, f"{name}: expected a torch CUDA tensor")
+        if t.dtype != dtype or not t.is_cuda or t.device.index != self.params.device or not t.is_contiguous() \
+                or t.numel() < numel:
+            raise DockError(DOCK_E_INPUT, f"{name}: need a contiguous {dtype} tensor on cuda:{self.params.device} "
+                                          f"with >= {numel} elements (got {t.dtype}, {t.device}, {t.numel()})")
+
     def run_device(self, pop, runs, max_evals, seed, best_E, best_genes, evals=None, gens=None,
                    run_base=0, ligand_id=0, stream=0):
+        import torch
+        self._check_dev("best_E", best_E, torch.float32, runs)
+        self._check_dev("best_genes", best_genes, torch.float32, runs * self.G)
+        if evals is not None:
+            self._check_dev("evals", evals, torch.int64, runs)
+        if gens is not None:
+            self._check_dev("gens", gens, torch.int32, runs)
         self._chk(lib.dock_run_device(self._ctx, pop, runs, run_base, ligand_id, max_evals, seed,
                                       best_E.data_ptr(), best_genes.data_ptr(),
                                       evals.data_ptr() if evals is not None else None,

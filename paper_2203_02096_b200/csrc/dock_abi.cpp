@@ -91,6 +91,7 @@ dk::PopDev pop_of(const dock_ctx *c) {
 int ensure_buffers(dock_ctx *c, int runs, int pop) {
     if (runs <= c->cap_runs && pop <= c->cap_pop) return DOCK_OK;
     const int R = std::max(runs, c->cap_runs), P = std::max(pop, c->cap_pop);
+    CK(dk::after_last_use(c, c->stream));   // kernels of an earlier asynchronous call may still use them
     CK(cudaStreamSynchronize(c->stream));
     dk::dfree(c->d_genes, c->stream); dk::dfree(c->d_E, c->stream); dk::dfree(c->d_state, c->stream);
     dk::dfree(c->d_perm, c->stream); dk::dfree(c->d_ls_evals, c->stream); dk::dfree(c->d_ls_count, c->stream);
@@ -137,6 +138,14 @@ struct DevBuf {
 namespace dk {
 
 bool prob_ok(float p) { return std::isfinite(p) && p >= 0.f && p <= 1.f; }
+
+cudaError_t after_last_use(dock_ctx *c, cudaStream_t s) {
+    return c->last_use ? cudaStreamWaitEvent(s, c->last_use, 0) : cudaSuccess;
+}
+
+cudaError_t mark_last_use(dock_ctx *c, cudaStream_t s) {
+    return c->last_use ? cudaEventRecord(c->last_use, s) : cudaSuccess;
+}
 
 int validate_params(const dock_params &p, std::string *err) {
     if (!prob_ok(p.p_tour) || !prob_ok(p.p_cross) || !prob_ok(p.p_mut)) { *err = "params: probabilities must be in [0,1]"; return DOCK_E_INPUT; }
@@ -245,6 +254,7 @@ int ctx_create(std::shared_ptr<Receptor> rec, const dock_params &p, dock_ctx **o
     {
         Trace tr("ctx.stream_create");
         if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess) return bail("cudaStreamCreate failed");
+        if (cudaEventCreateWithFlags(&c->last_use, cudaEventDisableTiming) != cudaSuccess) return bail("cudaEventCreate failed");
     }
     {
         // kernel attributes are per device and process: set them once
@@ -289,6 +299,7 @@ int ctx_create(std::shared_ptr<Receptor> rec, const dock_params &p, dock_ctx **o
 
 int ctx_reserve(dock_ctx *c, size_t blob_bytes, int runs, int pop) {
     CK(cudaSetDevice(c->device));
+    CK(after_last_use(c, c->stream));   // the ligand block may still be read by an earlier call
     if (blob_bytes > c->blob_cap) {
         if (c->d_blob) { CK(cudaStreamSynchronize(c->stream)); dfree(c->d_blob, c->stream); }
         c->d_blob = nullptr; c->blob_cap = 0;
@@ -391,6 +402,7 @@ void dock_free(dock_ctx *c) {
     cudaSetDevice(c->device);
     {
         Trace t1("free.sync");
+        if (c->last_use) cudaEventSynchronize(c->last_use);   // kernels of asynchronous calls on other streams
         if (c->stream) cudaStreamSynchronize(c->stream);
     }
     {
@@ -405,6 +417,7 @@ void dock_free(dock_ctx *c) {
         for (cudaEvent_t e : c->events) cudaEventDestroy(e);
         for (cudaEvent_t e : c->branch_events) cudaEventDestroy(e);
         for (cudaStream_t b : c->branch_streams) cudaStreamDestroy(b);
+        if (c->last_use) cudaEventDestroy(c->last_use);
         if (c->stream) cudaStreamDestroy(c->stream);
     }
     cudaGetLastError();
@@ -444,6 +457,7 @@ int dock_run_device(dock_ctx *c, int32_t pop, int32_t runs, int32_t run_base, ui
     CK(cudaSetDevice(c->device));
     if (int rc = ensure_buffers(c, runs, pop)) return rc;
     cudaStream_t s = stream ? (cudaStream_t)stream : c->stream;
+    CK(dk::after_last_use(c, s));
     const dk::SearchDev sp = make_search(c, pop, runs, run_base, ligand_id, max_evals, seed);
     const dk::PopDev pd = pop_of(c);
     int K = c->params.gens_per_graph;
@@ -473,6 +487,7 @@ int dock_run_device(dock_ctx *c, int32_t pop, int32_t runs, int32_t run_base, ui
         CK(dk::launch_init(c->lig, c->grid, sp, pd, s));
         CK(dk::launch_run_sw(c->lig, c->grid, sp, pd, prof ? c->d_prof : nullptr, s));
         CK(dk::launch_best(c->lig, sp, pd, d_best_energy, d_best_genotype, (long long *)d_evals_used, d_generations, s));
+        CK(dk::mark_last_use(c, s));   // this path returns before k_run_sw finishes
         c->launches += 3;
         if (prof) {
             unsigned long long h[2] = {0, 0};
@@ -613,6 +628,7 @@ int dock_run_device(dock_ctx *c, int32_t pop, int32_t runs, int32_t run_base, ui
     cudaGraphDestroy(graph);
     if (rc != DOCK_OK) return rc;
     CK(dk::launch_best(c->lig, sp, pd, d_best_energy, d_best_genotype, (long long *)d_evals_used, d_generations, s));
+    CK(dk::mark_last_use(c, s));
     c->launches += 1;
     return DOCK_OK;
 }
@@ -661,7 +677,9 @@ int dock_eval_device(dock_ctx *c, int32_t n, const float *d_genotypes, float *d_
     if (n < 0) return input_error(c, "n: must be >= 0");
     if (n > 0 && (!d_genotypes || !d_energy)) return input_error(c, "d_genotypes/d_energy: NULL");
     CK(cudaSetDevice(c->device));
+    CK(dk::after_last_use(c, (cudaStream_t)stream));
     CK(dk::launch_eval(c->lig, c->grid, n, d_genotypes, d_energy, d_grad, d_xyz, c->d_dfs2orig, (cudaStream_t)stream));
+    CK(dk::mark_last_use(c, (cudaStream_t)stream));
     c->launches += 1;
     return DOCK_OK;
 }
@@ -672,7 +690,9 @@ int dock_bench_part(dock_ctx *c, int32_t part, int32_t n, int32_t iters, const f
     if (part < 0 || part > 1 || n < 0 || iters < 1) return input_error(c, "part in {0,1}, n >= 0, iters >= 1");
     if (n > 0 && (!d_genotypes || !d_out)) return input_error(c, "d_genotypes/d_out: NULL");
     CK(cudaSetDevice(c->device));
+    CK(dk::after_last_use(c, (cudaStream_t)stream));
     CK(dk::launch_bench_part(c->lig, c->grid, part, n, iters, d_genotypes, d_out, (cudaStream_t)stream));
+    CK(dk::mark_last_use(c, (cudaStream_t)stream));
     c->launches += 1;
     return DOCK_OK;
 }
@@ -691,6 +711,7 @@ int dock_eval(dock_ctx *c, int32_t n, const float *genotypes, float *energy, flo
     CK(dE.alloc(sizeof(float) * n));
     if (grad) CK(dgr.alloc(sizeof(float) * n * G));
     if (xyz) CK(dx.alloc(sizeof(float) * n * N * 3));
+    CK(dk::after_last_use(c, c->stream));
     CK(cudaMemcpyAsync(dg.p, genotypes, sizeof(float) * n * G, cudaMemcpyHostToDevice, c->stream));
     CK(dk::launch_eval(c->lig, c->grid, n, (const float *)dg.p, (float *)dE.p, (float *)dgr.p, (float *)dx.p,
                        c->d_dfs2orig, c->stream));
@@ -715,6 +736,7 @@ int dock_eval_terms(dock_ctx *c, int32_t n, const float *genotypes, float *inter
     CK(dg.alloc(sizeof(float) * n * G));
     CK(dI.alloc(sizeof(float) * n));
     CK(dP.alloc(sizeof(float) * n));
+    CK(dk::after_last_use(c, c->stream));
     CK(cudaMemcpyAsync(dg.p, genotypes, sizeof(float) * n * G, cudaMemcpyHostToDevice, c->stream));
     CK(dk::launch_eval(c->lig, c->grid, n, (const float *)dg.p, (float *)dI.p, nullptr, nullptr, c->d_dfs2orig,
                        c->stream, dk::kPartsInter));
@@ -843,6 +865,7 @@ int dock_ga_step(dock_ctx *c, uint64_t seed, uint32_t ligand_id, int32_t run, in
     dk::RunState st{0, gen - 1, 0};
     DevBuf ddbg(c->stream);
     CK(ddbg.alloc(sizeof(int) * 8 * pop));
+    CK(dk::after_last_use(c, c->stream));
     CK(cudaMemcpyAsync(c->d_genes + (size_t)cur * 1 * pop * G, old_genes, sizeof(float) * pop * G, cudaMemcpyHostToDevice, c->stream));
     CK(cudaMemcpyAsync(c->d_E + (size_t)cur * pop, old_E, sizeof(float) * pop, cudaMemcpyHostToDevice, c->stream));
     CK(cudaMemcpyAsync(c->d_state, &st, sizeof(st), cudaMemcpyHostToDevice, c->stream));
@@ -872,6 +895,7 @@ int dock_ls_step(dock_ctx *c, int32_t method, int32_t n, int32_t iters, uint64_t
     CK(dE.alloc(sizeof(float) * n));
     CK(dev.alloc(sizeof(int) * n));
     CK(dsl.alloc(sizeof(int) * n));
+    CK(dk::after_last_use(c, c->stream));
     CK(cudaMemcpyAsync(dg.p, genes, sizeof(float) * n * G, cudaMemcpyHostToDevice, c->stream));
     CK(cudaMemcpyAsync(dE.p, energy, sizeof(float) * n, cudaMemcpyHostToDevice, c->stream));
     CK(cudaMemcpyAsync(dsl.p, slots, sizeof(int) * n, cudaMemcpyHostToDevice, c->stream));

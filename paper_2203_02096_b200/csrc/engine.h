@@ -98,6 +98,11 @@ struct dock_ctx {
     int last_branches = 1;
     int last_engine = 0;        // dock_last_engine: 0 lockstep, 1 run branches, 2 persistent clusters
     unsigned long long *d_prof = nullptr;       // k_run_sw LS-phase timer (profile)
+    // Recorded after the last kernel of every device-side call (dock_run_device and the
+    // stream-taking hooks may return before their kernels finish).  Every later use of the
+    // context's buffers -- a reallocation, a ligand swap, dock_free, a hook on c->stream,
+    // another dock_run_device on any stream -- is ordered after it (dk::after_last_use).
+    cudaEvent_t last_use = nullptr;
 };
 
 namespace dk {
@@ -113,5 +118,10 @@ int ctx_attach_ligand(dock_ctx *c, Prepared &&p);
 int ctx_reserve(dock_ctx *c, size_t blob_bytes, int runs, int pop);
 
 int validate_params(const dock_params &p, std::string *err);
+
+// Order stream s after the context's last recorded device-side use (cudaStreamWaitEvent),
+// and record a new last use at the current end of s.
+cudaError_t after_last_use(dock_ctx *c, cudaStream_t s);
+cudaError_t mark_last_use(dock_ctx *c, cudaStream_t s);
 
 }  // namespace dk

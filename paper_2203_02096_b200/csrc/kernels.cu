@@ -658,8 +658,10 @@ __device__ __forceinline__ void sw_tree_chain(const LigSm &Ls, const GridDev &g,
     // deviate shapes of kTriAhead iterations at a time (one Philox block per (iteration,
     // gene)), refilled when a round would run past them: the Philox work leaves the
     // per-round critical path
+    // (only the iterations the chain can still reach: min(kTriAhead, iters - sbase); a node
+    // beyond a.iters is never live, so the unfilled tail of the window is never read)
     int sbase = 0;
-    for (int q = threadIdx.x; q < kTriAhead * G; q += blockDim.x) {
+    for (int q = threadIdx.x; q < min(kTriAhead, a.iters) * G; q += blockDim.x) {
         const int k = q / G, j = q - k * G;
         stri[q] = sw_tri(key, t.slot, t.gen, t.run_g, G, k, j);
     }
@@ -670,7 +672,7 @@ __device__ __forceinline__ void sw_tree_chain(const LigSm &Ls, const GridDev &g,
         if (it + D > sbase + kTriAhead) {                     // uniform: refill the deviate window
             __syncthreads();                                  // the previous round's path reads are done
             sbase = it;
-            for (int q = threadIdx.x; q < kTriAhead * G; q += blockDim.x) {
+            for (int q = threadIdx.x; q < min(kTriAhead, a.iters - sbase) * G; q += blockDim.x) {
                 const int k = q / G, j = q - k * G;
                 stri[q] = sw_tri(key, t.slot, t.gen, t.run_g, G, sbase + k, j);
             }
@@ -1168,7 +1170,10 @@ int run_sw_eligible(const LigDev &L, const SearchDev &sp) {
     const ScratchLayout SL = scratch_layout(L, false, 4 * sp.pop);
     const size_t smem = run_sw_smem(L, SL, sp.sw_depth == 3 ? 3 : 2);
     if (smem > (size_t)kSmemMax) return 0;
-    if (sp.sw_depth == 0 && !std::getenv("DOCK_RUNSW_ANY")) {   // the auto depth rule of launch_ls, on all runs' chains
+#ifndef DK_RUNSW_ANY
+#define DK_RUNSW_ANY 0   // experiment build only (scripts/variants.py): lift the one-wave condition
+#endif
+    if (sp.sw_depth == 0 && !DK_RUNSW_ANY) {   // the auto depth rule of launch_ls, on all runs' chains
         int dev = 0, nsm = 148, per_sm = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);

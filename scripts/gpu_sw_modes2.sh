@@ -10,7 +10,7 @@ from gen import config_inputs
 for name, runs in [("ps", 100), ("pm", 100), ("ps", 40), ("1stp", 50)]:
     cfg, lig, grid = config_inputs(name)
     for mode, env in ((2, None), (3, "1")):
-        if env: os.environ["DOCK_RUNSW_ANY"] = env
+        if env: os.environ["DOCK_RUNSW_ANY"] = env  # (round 1; now the -DDK_RUNSW_ANY=1 build variant)
         else: os.environ.pop("DOCK_RUNSW_ANY", None)
         d = dock.Docker.from_inputs(grid, lig, ls_method=1, ls_rate=cfg.ls_rate, ls_max_iters=cfg.ls_iters, run_branches=mode)
         budget = cfg.max_evals if name == "1stp" else 1_000_000
