@@ -213,6 +213,14 @@ int dock_philox(int32_t n, const uint32_t *ctr4, const uint32_t *key2, uint32_t 
 int dock_stream_words(uint64_t seed, uint32_t ligand_id, uint32_t purpose, uint32_t slot,
                       uint32_t gen, uint32_t run, uint32_t m0, int32_t n, uint32_t *out);
 
+/* D8 generation 0 (row a2; "starting population"): the initial
+   populations of runs run_base .. run_base+num_runs-1 exactly as dock_run_ex draws them
+   (k_init: gene j of individual k from INIT word j; translation uniform in the box
+   [origin, origin + (n-1) spacing], angles 2 pi u01) and their energies.  Host outputs
+   genes [num_runs*pop_size*G], energy [num_runs*pop_size].  Synchronous. */
+int dock_init_population(dock_ctx *ctx, int32_t pop_size, int32_t num_runs, int32_t run_base,
+                         uint32_t ligand_id, uint64_t seed, float *genes, float *energy);
+
 /* D8 one GA generation of one run on an injected population (genes [pop*G], E [pop]):
    new_genes [pop*G], new_E [pop] (offspring evaluated, slot 0 = elite copy),
    debug [pop*8] = {A, B, crossover, c1, c2, mutation mask lo, hi, elite (slot 0)},
@@ -227,6 +235,30 @@ int dock_ga_step(dock_ctx *ctx, uint64_t seed, uint32_t ligand_id, int32_t run, 
 int dock_ls_step(dock_ctx *ctx, int32_t method, int32_t n, int32_t iters, uint64_t seed,
                  uint32_t ligand_id, int32_t run, int32_t gen, const int32_t *slots,
                  float *genes, float *energy, int64_t *evals);
+
+/* D9 parity protocol: dock_ls_step's Solis-Wets search with traces,
+   optionally "fed".  fed_energy [n*iters*2] (may be NULL): the energy of candidate c
+   (0 = x+b+d, 1 = x-b-d) of iteration it of individual i is fed_energy[(i*iters + it)*2 + c]
+   instead of the evaluated one, so the accept/reject logic, the bias and rho updates and
+   the evaluation count can be compared with the oracle's D9 on identical energies.
+   trace_outcome [n*iters] receives 0 / 1 (candidate accepted) or 2 (both rejected) per
+   executed iteration and -1 after the search stopped (rho < rho_min); trace_rho [n*iters]
+   the rho of each executed iteration.  Runs the production kernels (k_ls_sw or the
+   speculative k_ls_sw_tree, per params.sw_depth / sw_split). */
+int dock_sw_trace(dock_ctx *ctx, int32_t n, int32_t iters, uint64_t seed, uint32_t ligand_id,
+                  int32_t run, int32_t gen, const int32_t *slots, const float *fed_energy,
+                  float *genes, float *energy, int64_t *evals, int32_t *trace_outcome,
+                  float *trace_rho);
+
+/* D10 parity protocol: dock_ls_step's ADADELTA search (k_ls_adadelta, the production
+   kernel) with traces, optionally "fed".  fed [n*iters*(1+G)] (may be NULL): iteration
+   it of individual i uses energy fed[(i*iters + it)*(1+G)] and gradient the next G values
+   instead of its evaluation, so the D10 update and best tracking can be compared with the
+   oracle's on identical inputs.  trace_x, trace_g [n*iters*G]: the genotype evaluated at
+   every iteration and its gradient; trace_E [n*iters]: its energy (the evaluated or fed
+   values).  genes / energy / evals as dock_ls_step (best tracking, Lamarckian result). */
+int dock_ad_trace(dock_ctx *ctx, int32_t n, int32_t iters, const float *fed, float *genes,
+                  float *energy, int64_t *evals, float *trace_x, float *trace_E, float *trace_g);
 
 /* ---------------- multi-ligand / multi-GPU screen ----------------
    PAPER.md:34-38 [§I]: docking a ligand library is "a load balancing and dataflow

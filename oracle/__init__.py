@@ -115,6 +115,7 @@ def lib():
         L.or_kink_margin.argtypes = [P(CProblem), P(d)]; L.or_kink_margin.restype = d
         L.or_binding_dG.argtypes = [P(CProblem), d]; L.or_binding_dG.restype = d
         L.or_energy.argtypes = [P(CProblem), P(d), P(d), P(d), P(d)]; L.or_energy.restype = d
+        L.or_energy_at.argtypes = [P(CProblem), P(d), P(d), P(d), P(d)]; L.or_energy_at.restype = d
         L.or_margins.argtypes = [P(CProblem), P(d), P(d), P(d)]
         L.or_elite.argtypes = [i, P(d)]; L.or_elite.restype = i
         L.or_ga_slot.argtypes = [P(CParams), u64, u32, u32, u32, u32, i, i, P(d), P(d), P(d), P(i)]
@@ -123,6 +124,11 @@ def lib():
         L.or_solis_wets.argtypes = [P(CProblem), P(d), i, P(CParams), u64, u32, u32, u32, u32,
                                     P(d), P(d), P(i64)]
         L.or_adadelta.argtypes = [P(CProblem), P(d), i, P(CParams), i, P(d), P(d), P(i64)]
+        L.or_solis_wets_traced.argtypes = [P(CProblem), P(d), i, P(CParams), u64, u32, u32, u32, u32,
+                                           P(d), P(d), P(i64), P(d), P(i), P(d), P(d)]
+        L.or_adadelta_traced.argtypes = [P(CProblem), P(d), i, P(CParams), i, P(d), P(d), P(i64), P(d), P(d),
+                                         P(d), P(d)]
+        L.or_init_population.argtypes = [P(CProblem), i, u64, u32, u32, P(d), P(d)]
         L.or_dock_run.argtypes = [P(CProblem), P(CParams), i, i64, u64, u32, u32, P(d), P(d),
                                   P(i64), P(i), P(d)]
         L.or_dock_run.restype = i
@@ -278,6 +284,13 @@ class Problem:
                             _p(xyz, C.c_double), _p(terms, C.c_double))
         return dict(E=e, grad=gg if grad else None, xyz=xyz.reshape(self.N, 3), inter=terms[0], intra=terms[1])
 
+    def energy_at(self, genes, xyz, grad=True):
+        """D6 + D7 at the given world coordinates xyz [N, 3] (e.g. the GPU's own pose)."""
+        x = _f64(genes); r = _f64(xyz).reshape(-1); gg = np.zeros(self.G); terms = np.zeros(2)
+        e = lib().or_energy_at(self.ref(), _p(x, C.c_double), _p(r, C.c_double),
+                               _p(gg, C.c_double) if grad else None, _p(terms, C.c_double))
+        return dict(E=e, grad=gg if grad else None, inter=terms[0], intra=terms[1])
+
     # NEXT-2
     def kink_margin(self, xyz):
         x = _f64(xyz).reshape(-1)
@@ -355,6 +368,40 @@ def solis_wets(prob, pp, seed, ligand_id, run, gen, slot, x, E, bowl=None):
     return x, Ec.value, ev.value
 
 
+def solis_wets_traced(prob, pp, seed, ligand_id, run, gen, slot, x, E, bowl=None, fed=None):
+    """D9 with traces; fed [iters, 2]: the energies of the two candidates of every iteration
+    (fed mode), else evaluated.  Returns x, E, evals, outcome [iters] (-1 = not executed),
+    rho [iters], Etrace [iters, 3] = (E_x before, E(x+b+d), E(x-b-d) or NaN)."""
+    x = _f64(x).copy(); Ec = C.c_double(E); ev = C.c_int64(0)
+    G = x.shape[0]; n = pp.ls_max_iters
+    b = _f64(bowl) if bowl is not None else None
+    ft = _f64(fed).reshape(-1) if fed is not None else None
+    to = np.full(max(n, 1), -1, np.int32); tr = np.zeros(max(n, 1)); tE = np.full((max(n, 1), 3), np.nan)
+    lib().or_solis_wets_traced(prob.ref() if prob is not None else None,
+                               _p(b, C.c_double) if b is not None else None, G, C.byref(pp), seed, ligand_id, run,
+                               gen, slot, _p(x, C.c_double), C.byref(Ec), C.byref(ev),
+                               _p(ft, C.c_double) if ft is not None else None, _p(to, C.c_int), _p(tr, C.c_double),
+                               _p(tE, C.c_double))
+    return x, Ec.value, ev.value, to[:n], tr[:n], tE[:n]
+
+
+def adadelta_traced(prob, pp, iters, x, E, bowl=None, fed=None):
+    """D10 with traces; fed [iters, G+1] = (E, grad) per iteration (fed mode) or None.
+    Returns x (best), E (best), evals, trace_x [iters, G] (point evaluated at each
+    iteration), trace_E [iters], trace_g [iters, G]."""
+    x = _f64(x).copy(); Ec = C.c_double(E); ev = C.c_int64(0)
+    G = x.shape[0]
+    b = _f64(bowl) if bowl is not None else None
+    fd = _f64(fed).reshape(-1) if fed is not None else None
+    tx = np.zeros((max(iters, 1), G)); tE = np.zeros(max(iters, 1)); tg = np.zeros((max(iters, 1), G))
+    lib().or_adadelta_traced(prob.ref() if prob is not None else None,
+                             _p(b, C.c_double) if b is not None else None, G, C.byref(pp), iters,
+                             _p(x, C.c_double), C.byref(Ec), C.byref(ev),
+                             _p(fd, C.c_double) if fd is not None else None, _p(tx, C.c_double),
+                             _p(tE, C.c_double), _p(tg, C.c_double))
+    return x, Ec.value, ev.value, tx[:iters], tE[:iters], tg[:iters]
+
+
 def adadelta(prob, pp, iters, x, E, bowl=None):
     x = _f64(x).copy(); Ec = C.c_double(E); ev = C.c_int64(0)
     G = x.shape[0]
@@ -363,6 +410,14 @@ def adadelta(prob, pp, iters, x, E, bowl=None):
                       _p(b, C.c_double) if b is not None else None, G, C.byref(pp), iters,
                       _p(x, C.c_double), C.byref(Ec), C.byref(ev))
     return x, Ec.value, ev.value
+
+
+def init_population(prob, pop, seed, ligand_id=0, run=0, energies=True):
+    """D8 generation 0 of one run: (genes [pop, G], E [pop] or None)."""
+    g = np.zeros((pop, prob.G)); E = np.zeros(pop) if energies else None
+    lib().or_init_population(prob.ref(), pop, seed, ligand_id, run, _p(g, C.c_double),
+                             _p(E, C.c_double) if energies else None)
+    return g, E
 
 
 def dock_run(prob, pp, pop, max_evals, seed, ligand_id=0, run=0):

@@ -465,12 +465,13 @@ double or_intra(const or_problem *P, const double *xyz, double *grad) {
 /* ========================================================================
  * D6 total energy and D7 genotype gradient (NS).
  * ======================================================================== */
-double or_energy(const or_problem *P, const double *genes, double *ggrad, double *xyz_out, double *terms) {
+/* D6 + D7 of the genotype `genes` whose world coordinates are r (or_pose(genes), or a
+   given pose: or_energy_at).  Everything after D3 is evaluated at r. */
+static double energy_of_pose(const or_problem *P, const double *genes, const double *r, double *ggrad,
+                             double *terms) {
     int N = P->N;
-    double *r = (double *)malloc(sizeof(double) * 3 * N);
     double *gi = (double *)malloc(sizeof(double) * 3 * N);
     double *gp = (double *)malloc(sizeof(double) * 3 * N);
-    or_pose(P, genes, r);
     double Ei = or_inter(P, r, ggrad ? gi : NULL);
     double Ep = or_intra(P, r, ggrad ? gp : NULL);
     if (ggrad) {
@@ -515,10 +516,23 @@ double or_energy(const or_problem *P, const double *genes, double *ggrad, double
             ggrad[6 + k] = dot3(wk, S);
         }
     }
-    if (xyz_out) for (int i = 0; i < 3 * N; ++i) xyz_out[i] = r[i];
     if (terms) { terms[0] = Ei; terms[1] = Ep; }
-    free(r); free(gi); free(gp);
+    free(gi); free(gp);
     return Ei + Ep;                                                     /* D6: E = E_inter + E_intra */
+}
+
+double or_energy(const or_problem *P, const double *genes, double *ggrad, double *xyz_out, double *terms) {
+    int N = P->N;
+    double *r = (double *)malloc(sizeof(double) * 3 * N);
+    or_pose(P, genes, r);                                               /* D3 */
+    double E = energy_of_pose(P, genes, r, ggrad, terms);
+    if (xyz_out) for (int i = 0; i < 3 * N; ++i) xyz_out[i] = r[i];
+    free(r);
+    return E;
+}
+
+double or_energy_at(const or_problem *P, const double *genes, const double *xyz, double *ggrad, double *terms) {
+    return energy_of_pose(P, genes, xyz, ggrad, terms);
 }
 
 void or_margins(const or_problem *P, const double *xyz, double *face_margin, double *clamp_margin) {
@@ -622,51 +636,84 @@ static double objective(const or_problem *P, const double *bowl, int G, const do
     return E;
 }
 
-void or_solis_wets(const or_problem *P, const double *bowl, int G, const or_params *pp,
-                   uint64_t seed, uint32_t ligand_id, uint32_t run, uint32_t gen, uint32_t slot,
-                   double *x, double *E, int64_t *evals) {
+/* One energy call of the D9 / D10 objective: the docking energy of P, the bowl, or (Solis-
+   Wets "fed" mode, parity protocol of SURVEY §8(c)) the table entry Etab[2 it + cand]. */
+static double sw_objective(const or_problem *P, const double *bowl, int G, const double *Etab, int it, int cand,
+                           const double *x) {
+    if (Etab) return Etab[2 * it + cand];
+    return objective(P, bowl, G, x, NULL);
+}
+
+void or_solis_wets_traced(const or_problem *P, const double *bowl, int G, const or_params *pp,
+                          uint64_t seed, uint32_t ligand_id, uint32_t run, uint32_t gen, uint32_t slot,
+                          double *x, double *E, int64_t *evals, const double *Etab,
+                          int *trace_o, double *trace_rho, double *trace_E) {
     double rho = pp->sw_rho, b[OR_MAX_GENES], d[OR_MAX_GENES], c[OR_MAX_GENES];
     int succ = 0, fail = 0;
     double Ex = *E;
     int64_t ne = 0;
     for (int j = 0; j < G; ++j) b[j] = 0.0;
     for (int it = 0; it < pp->ls_max_iters; ++it) {
+        if (trace_o) trace_o[it] = -1;                                   /* not executed */
         if (rho < pp->sw_rho_min) break;                                 /* 1. */
+        if (trace_rho) trace_rho[it] = rho;
         for (int j = 0; j < G; ++j) {                                    /* 2. triangular deviate */
             uint32_t w1 = or_word(seed, ligand_id, PURPOSE_SW, slot, gen, run, (uint32_t)(2 * G * it + 2 * j));
             uint32_t w2 = or_word(seed, ligand_id, PURPOSE_SW, slot, gen, run, (uint32_t)(2 * G * it + 2 * j + 1));
             d[j] = rho * (or_u01(w1) + or_u01(w2) - 1.0);
         }
+        int o;
+        double Ex0 = Ex, E2 = NAN;
         for (int j = 0; j < G; ++j) c[j] = x[j] + b[j] + d[j];          /* 3. x + b + d */
-        double Ec = objective(P, bowl, G, c, NULL); ++ne;
+        double Ec = sw_objective(P, bowl, G, Etab, it, 0, c); ++ne;
+        double E1 = Ec;
         if (Ec < Ex) {
             for (int j = 0; j < G; ++j) { x[j] = c[j]; b[j] = 0.2 * b[j] + 0.4 * d[j]; }
-            Ex = Ec; ++succ; fail = 0;
+            Ex = Ec; ++succ; fail = 0; o = 0;
         } else {
             for (int j = 0; j < G; ++j) c[j] = x[j] - b[j] - d[j];      /* 4. x - b - d */
-            Ec = objective(P, bowl, G, c, NULL); ++ne;
+            Ec = sw_objective(P, bowl, G, Etab, it, 1, c); ++ne;
+            E2 = Ec;
             if (Ec < Ex) {
                 for (int j = 0; j < G; ++j) { x[j] = c[j]; b[j] = b[j] - 0.4 * d[j]; }
-                Ex = Ec; ++succ; fail = 0;
+                Ex = Ec; ++succ; fail = 0; o = 1;
             } else {                                                     /* 5. */
                 for (int j = 0; j < G; ++j) b[j] = 0.5 * b[j];
-                ++fail; succ = 0;
+                ++fail; succ = 0; o = 2;
             }
         }
         if (succ >= pp->sw_cons_succ) { rho *= pp->sw_expand; succ = 0; }   /* 6. */
         if (fail >= pp->sw_cons_fail) { rho *= pp->sw_contract; fail = 0; }
+        if (trace_o) trace_o[it] = o;
+        if (trace_E) { trace_E[3 * it] = Ex0; trace_E[3 * it + 1] = E1; trace_E[3 * it + 2] = E2; }
     }
     *E = Ex;
     *evals = ne;
 }
 
-void or_adadelta(const or_problem *P, const double *bowl, int G, const or_params *pp,
-                 int iters, double *x, double *E, int64_t *evals) {
+void or_solis_wets(const or_problem *P, const double *bowl, int G, const or_params *pp,
+                   uint64_t seed, uint32_t ligand_id, uint32_t run, uint32_t gen, uint32_t slot,
+                   double *x, double *E, int64_t *evals) {
+    or_solis_wets_traced(P, bowl, G, pp, seed, ligand_id, run, gen, slot, x, E, evals, NULL, NULL, NULL, NULL);
+}
+
+void or_adadelta_traced(const or_problem *P, const double *bowl, int G, const or_params *pp,
+                        int iters, double *x, double *E, int64_t *evals, const double *fed,
+                        double *trace_x, double *trace_E, double *trace_g) {
     double best[OR_MAX_GENES], sg[OR_MAX_GENES], sd[OR_MAX_GENES], g[OR_MAX_GENES];
     double Ebest = *E;
     for (int j = 0; j < G; ++j) { best[j] = x[j]; sg[j] = 0.0; sd[j] = 0.0; }
     for (int it = 0; it < iters; ++it) {
-        double Ei = objective(P, bowl, G, x, g);                         /* 1. energy + gradient */
+        if (trace_x) for (int j = 0; j < G; ++j) trace_x[it * G + j] = x[j];
+        double Ei;                                                       /* 1. energy + gradient */
+        if (fed) {                                                       /* fed mode: (E, grad) of iteration it */
+            Ei = fed[it * (G + 1)];
+            for (int j = 0; j < G; ++j) g[j] = fed[it * (G + 1) + 1 + j];
+        } else {
+            Ei = objective(P, bowl, G, x, g);
+        }
+        if (trace_E) trace_E[it] = Ei;
+        if (trace_g) for (int j = 0; j < G; ++j) trace_g[it * G + j] = g[j];
         if (Ei < Ebest) { Ebest = Ei; for (int j = 0; j < G; ++j) best[j] = x[j]; }
         for (int j = 0; j < G; ++j) {                                    /* 2. ADADELTA (Zeiler 2012) */
             sg[j] = pp->ad_rho * sg[j] + (1.0 - pp->ad_rho) * g[j] * g[j];
@@ -680,6 +727,11 @@ void or_adadelta(const or_problem *P, const double *bowl, int G, const or_params
     *evals = iters;
 }
 
+void or_adadelta(const or_problem *P, const double *bowl, int G, const or_params *pp,
+                 int iters, double *x, double *E, int64_t *evals) {
+    or_adadelta_traced(P, bowl, G, pp, iters, x, E, evals, NULL, NULL, NULL, NULL);
+}
+
 /* ========================================================================
  * D8 + D11 — one run ("several full optimizations each with a starting
  * population of 150 individuals"; P:92 sum_evals; S:336 termination).
@@ -688,6 +740,27 @@ int64_t or_sum_evals(int n, const int64_t *counters) {
     int64_t s = 0;
     for (int i = 0; i < n; ++i) s += counters[i];                        /* left to right */
     return s;
+}
+
+/* D8 generation 0 ("starting population"): gene j of individual k from
+   INIT word j of slot k; translation uniform in the box [o, o + (n-1)s], angles 2 pi u01;
+   every individual evaluated once (no local search at g = 0). */
+void or_init_population(const or_problem *P, int pop, uint64_t seed, uint32_t ligand_id, uint32_t run,
+                        double *genes, double *E) {
+    int G = 6 + P->T;
+    const int n[3] = {P->nx, P->ny, P->nz};
+    for (int k = 0; k < pop; ++k) {
+        for (int j = 0; j < G; ++j) {
+            double u = or_u01(or_word(seed, ligand_id, PURPOSE_INIT, (uint32_t)k, 0, run, (uint32_t)j));
+            if (j < 3) {
+                double lo = P->origin[j], hi = P->origin[j] + (double)(n[j] - 1) * P->spacing;
+                genes[k * G + j] = lo + u * (hi - lo);
+            } else {
+                genes[k * G + j] = 2.0 * OR_PI * u;
+            }
+        }
+        if (E) E[k] = or_energy(P, genes + k * G, NULL, NULL, NULL);
+    }
 }
 
 int or_dock_run(const or_problem *P, const or_params *pp, int pop, int64_t max_evals,
@@ -701,21 +774,8 @@ int or_dock_run(const or_problem *P, const or_params *pp, int pop, int64_t max_e
     double *nE = (double *)malloc(sizeof(double) * pop);
     int64_t *cnt = (int64_t *)calloc((size_t)pop, sizeof(int64_t));
     int *perm = (int *)malloc(sizeof(int) * pop);
-    const int n[3] = {P->nx, P->ny, P->nz};
-    /* generation 0: genes from INIT words, translation uniform in the box, angles in [0, 2pi) */
-    for (int k = 0; k < pop; ++k) {
-        for (int j = 0; j < G; ++j) {
-            double u = or_u01(or_word(seed, ligand_id, PURPOSE_INIT, (uint32_t)k, 0, run, (uint32_t)j));
-            if (j < 3) {
-                double lo = P->origin[j], hi = P->origin[j] + (double)(n[j] - 1) * P->spacing;
-                genes[k * G + j] = lo + u * (hi - lo);
-            } else {
-                genes[k * G + j] = 2.0 * OR_PI * u;
-            }
-        }
-        E[k] = or_energy(P, genes + k * G, NULL, NULL, NULL);
-        cnt[k] = 1;
-    }
+    or_init_population(P, pop, seed, ligand_id, run, genes, E);        /* generation 0 */
+    for (int k = 0; k < pop; ++k) cnt[k] = 1;
     int64_t evals = or_sum_evals(pop, cnt);                               /* = pop */
     int g = 0;
     int n_ls = or_n_ls(pp->ls_rate, pop);

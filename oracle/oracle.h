@@ -115,6 +115,14 @@ double or_binding_dG(const or_problem *P, double e_inter);
 /* ---- D6 + D7: total energy and genotype gradient ---- */
 double or_energy(const or_problem *P, const double *genes, double *ggrad /*[G] nullable*/,
                  double *xyz /*[N*3] nullable*/, double *terms /*[2] inter,intra nullable*/);
+/* D6 + D7 evaluated at GIVEN world coordinates xyz [N*3] of the genotype `genes` (the
+   D7 back-projection uses genes' t, phi, theta, alpha and the given r_a).  With
+   xyz = or_pose(genes) this is or_energy.  Parity use (DESIGN.md §3 reading 22b): the
+   GPU's energy and gradient are compared with this function at the GPU's own FP32 pose,
+   so the FP32 rounding of the pose itself (checked separately at |dr| <= 1e-4 Å) does
+   not enter the energy comparison. */
+double or_energy_at(const or_problem *P, const double *genes, const double *xyz, double *ggrad /*[G] nullable*/,
+                    double *terms /*[2] nullable*/);
 /* smallest distance, in grid units, of any atom coordinate to a cell/box face, and
    smallest |rho2 - 1e-4| over pairs (both used to flag boundary poses). */
 void or_margins(const or_problem *P, const double *xyz, double *face_margin, double *clamp_margin);
@@ -135,6 +143,29 @@ void or_solis_wets(const or_problem *P, const double *bowl, int G, const or_para
                    double *x, double *E, int64_t *evals);
 void or_adadelta(const or_problem *P, const double *bowl, int G, const or_params *pp,
                  int iters, double *x, double *E, int64_t *evals);
+
+/* The same D9 / D10 searches with traces (parity protocol):
+   Solis-Wets: Etab [iters*2] nullable -- "fed" mode: the energy of candidate c (0 = x+b+d,
+   1 = x-b-d) of iteration it is Etab[2 it + c] instead of an evaluation, so the D9 state
+   machine can be compared with the GPU's on identical energies; trace_o [iters] outcome
+   per iteration (0 / 1 accepted candidate, 2 both rejected, -1 not executed: rho < rho_min),
+   trace_rho [iters] the rho used, trace_E [iters*3] = {E_x before, E(x+b+d), E(x-b-d) or NaN}.
+   ADADELTA: fed [iters*(G+1)] nullable -- fed mode: iteration it's energy and gradient are
+   (fed[it*(G+1)], fed[it*(G+1)+1 ..]) instead of an evaluation (the D10 update and best
+   tracking on identical inputs); trace_x [iters*G] the point evaluated at iteration it,
+   trace_E [iters] its energy, trace_g [iters*G] its gradient.
+   Every trace pointer may be NULL. */
+void or_solis_wets_traced(const or_problem *P, const double *bowl, int G, const or_params *pp,
+                          uint64_t seed, uint32_t ligand_id, uint32_t run, uint32_t gen, uint32_t slot,
+                          double *x, double *E, int64_t *evals, const double *Etab,
+                          int *trace_o, double *trace_rho, double *trace_E);
+void or_adadelta_traced(const or_problem *P, const double *bowl, int G, const or_params *pp,
+                        int iters, double *x, double *E, int64_t *evals, const double *fed,
+                        double *trace_x, double *trace_E, double *trace_g);
+
+/* ---- D8 generation 0 of one run: genes [pop*G], energies [pop] (nullable) ---- */
+void or_init_population(const or_problem *P, int pop, uint64_t seed, uint32_t ligand_id, uint32_t run,
+                        double *genes, double *E);
 
 /* ---- D8 + D11: one full run ---- */
 int or_dock_run(const or_problem *P, const or_params *pp, int pop, int64_t max_evals,

@@ -112,6 +112,9 @@ def _load():
         "dock_philox": (i32, [i32, P(u32), P(u32), P(u32)]),
         "dock_stream_words": (i32, [u64, u32, u32, u32, u32, u32, u32, i32, P(u32)]),
         "dock_ga_step": (i32, [v, u64, u32, i32, i32, i32, P(f), P(f), P(f), P(f), P(i32), P(i32)]),
+        "dock_init_population": (i32, [v, i32, i32, i32, u32, u64, P(f), P(f)]),
+        "dock_ad_trace": (i32, [v, i32, i32, P(f), P(f), P(f), P(i64), P(f), P(f), P(f)]),
+        "dock_sw_trace": (i32, [v, i32, i32, u64, u32, i32, i32, P(i32), P(f), P(f), P(f), P(i64), P(i32), P(f)]),
         "dock_ls_step": (i32, [v, i32, i32, i32, u64, u32, i32, i32, P(i32), P(f), P(f), P(i64)]),
         "dock_launch_count": (i64, [v]),
         "dock_kernel_stats": (i32, [v, P(C.c_double), P(i64)]),
@@ -139,7 +142,8 @@ EXPORTED = ("dock_params_default", "dock_builtin_type_param", "dock_init", "dock
             "dock_philox", "dock_stream_words", "dock_ga_step", "dock_ls_step", "dock_launch_count",
             "dock_topology", "dock_kernel_stats", "dock_upload_bytes", "dock_screen", "dock_screen_last_error",
             "dock_bench_part", "dock_eval_terms", "dock_cluster", "dock_write_result", "dock_run_branches",
-            "dock_write_screen", "dock_last_engine")
+            "dock_write_screen", "dock_last_engine", "dock_init_population", "dock_sw_trace",
+            "dock_ad_trace")
 
 
 def write_result(res: dict, fmt: str = "json", timings: dict | None = None) -> str:
@@ -535,6 +539,14 @@ class Docker:
                                       evals.data_ptr() if evals is not None else None,
                                       gens.data_ptr() if gens is not None else None, stream or None))
 
+    def init_population(self, pop, runs, seed, run_base=0, ligand_id=0):
+        """Generation 0 as dock_run_ex draws it (row a2): genes [runs, pop, G], E [runs, pop]."""
+        g = np.zeros((runs, pop, self.G), np.float32)
+        E = np.zeros((runs, pop), np.float32)
+        self._chk(lib.dock_init_population(self._ctx, pop, runs, run_base, ligand_id, seed, _ptr(g, C.c_float),
+                                           _ptr(E, C.c_float)))
+        return g, E
+
     def ga_step(self, seed, ligand_id, run, gen, old_genes, old_E):
         og = np.ascontiguousarray(old_genes, dtype=np.float32)
         oE = np.ascontiguousarray(old_E, dtype=np.float32)
@@ -545,6 +557,36 @@ class Docker:
                                    _ptr(oE, C.c_float), _ptr(ng, C.c_float), _ptr(nE, C.c_float),
                                    _ptr(dbg, C.c_int32), _ptr(perm, C.c_int32)))
         return ng, nE, dbg, perm
+
+    def sw_trace(self, genes, energy, iters, seed=0, ligand_id=0, run=0, gen=1, slots=None, fed=None):
+        """Solis-Wets with traces (dock_sw_trace): fed [n, iters, 2] candidate energies or None.
+        Returns genes, E, evals, outcome [n, iters] (-1 = not executed), rho [n, iters]."""
+        g = np.ascontiguousarray(genes, dtype=np.float32).reshape(-1, self.G).copy()
+        E = np.ascontiguousarray(energy, dtype=np.float32).copy()
+        n = g.shape[0]
+        sl = np.ascontiguousarray(slots if slots is not None else np.arange(n), dtype=np.int32)
+        fd = np.ascontiguousarray(fed, dtype=np.float32).reshape(n, iters, 2) if fed is not None else None
+        ev = np.zeros(n, np.int64)
+        to = np.zeros((n, iters), np.int32); tr = np.zeros((n, iters), np.float32)
+        self._chk(lib.dock_sw_trace(self._ctx, n, iters, seed, ligand_id, run, gen, _ptr(sl, C.c_int32),
+                                    _ptr(fd, C.c_float) if fd is not None else None, _ptr(g, C.c_float),
+                                    _ptr(E, C.c_float), _ptr(ev, C.c_int64), _ptr(to, C.c_int32), _ptr(tr, C.c_float)))
+        return g, E, ev, to, tr
+
+    def ad_trace(self, genes, energy, iters, fed=None):
+        """ADADELTA with traces (dock_ad_trace): fed [n, iters, 1+G] (energy, gradient) or None.
+        Returns genes, E, evals, trace_x [n, iters, G], trace_E [n, iters], trace_g [n, iters, G]."""
+        g = np.ascontiguousarray(genes, dtype=np.float32).reshape(-1, self.G).copy()
+        E = np.ascontiguousarray(energy, dtype=np.float32).copy()
+        n = g.shape[0]
+        fd = np.ascontiguousarray(fed, dtype=np.float32).reshape(n, iters, self.G + 1) if fed is not None else None
+        ev = np.zeros(n, np.int64)
+        tx = np.zeros((n, iters, self.G), np.float32); tE = np.zeros((n, iters), np.float32)
+        tg = np.zeros((n, iters, self.G), np.float32)
+        self._chk(lib.dock_ad_trace(self._ctx, n, iters, _ptr(fd, C.c_float) if fd is not None else None,
+                                    _ptr(g, C.c_float), _ptr(E, C.c_float), _ptr(ev, C.c_int64), _ptr(tx, C.c_float),
+                                    _ptr(tE, C.c_float), _ptr(tg, C.c_float)))
+        return g, E, ev, tx, tE, tg
 
     def ls_step(self, method, genes, energy, iters, seed=0, ligand_id=0, run=0, gen=1, slots=None):
         g = np.ascontiguousarray(genes, dtype=np.float32).reshape(-1, self.G).copy()

@@ -32,9 +32,15 @@ def build(force: bool = False, verbose: bool = False, out: str | None = None, de
     obj_dir = os.path.join(ROOT, "build", "obj" if out is None else "obj_" + os.path.basename(out))
     os.makedirs(obj_dir, exist_ok=True)
     procs, objs = [], []
-    # kernels.cu is compiled twice: the D5 scoring function (dk::d5) and, with -DDK_AD4,
-    # the NEXT-2 AutoDock4.1-calibrated variant (dk::ad4); the objects build in parallel.
-    units = [(src, src + ".o", ()) for src in SOURCES] + [("kernels.cu", "kernels_ad4.cu.o", ("DK_AD4",))]
+    # kernels.cu is compiled once per scoring function -- D5 (dk::d5) and, with -DDK_AD4,
+    # the NEXT-2 AutoDock4.1-calibrated variant (dk::ad4) -- and per part (DK_PART 1: eval /
+    # init / GA / misc, 2: ADADELTA, 3: Solis-Wets, 4: the Solis-Wets parity-hook
+    # instantiations; each part instantiates only its own
+    # kernels).  All objects build in parallel.
+    units = [(src, src + ".o", ()) for src in SOURCES if src != "kernels.cu"]
+    for sf, tag in (((), "d5"), (("DK_AD4",), "ad4")):
+        for part in (1, 2, 3, 4):
+            units.append(("kernels.cu", f"kernels_{tag}_p{part}.cu.o", (*sf, f"DK_PART={part}")))
     for src, oname, extra in units:
         obj = os.path.join(obj_dir, oname)
         objs.append(obj)

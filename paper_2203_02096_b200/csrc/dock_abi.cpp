@@ -848,6 +848,24 @@ int dock_stream_words(uint64_t seed, uint32_t ligand_id, uint32_t purpose, uint3
     return DOCK_OK;
 }
 
+int dock_init_population(dock_ctx *c, int32_t pop, int32_t runs, int32_t run_base, uint32_t ligand_id, uint64_t seed,
+                         float *genes, float *energy) {
+    if (!c) return DOCK_E_INPUT;
+    if (int rc = check_run_args(c, pop, runs, run_base, pop)) return rc;
+    if (!genes || !energy) return input_error(c, "genes/energy: NULL");
+    CK(cudaSetDevice(c->device));
+    if (int rc = ensure_buffers(c, runs, pop)) return rc;
+    CK(dk::after_last_use(c, c->stream));
+    const dk::SearchDev sp = make_search(c, pop, runs, run_base, ligand_id, pop, seed);
+    CK(dk::launch_init(c->lig, c->grid, sp, pop_of(c), c->stream));
+    c->launches += 1;
+    const size_t G = (size_t)c->prep.G;   // generation 0 is parity block 0, rows [run][pop][G]
+    CK(cudaMemcpyAsync(genes, c->d_genes, sizeof(float) * runs * pop * G, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaMemcpyAsync(energy, c->d_E, sizeof(float) * runs * pop, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    return DOCK_OK;
+}
+
 int dock_ga_step(dock_ctx *c, uint64_t seed, uint32_t ligand_id, int32_t run, int32_t gen, int32_t pop,
                  const float *old_genes, const float *old_E, float *new_genes, float *new_E, int32_t *debug,
                  int32_t *perm) {
@@ -876,6 +894,98 @@ int dock_ga_step(dock_ctx *c, uint64_t seed, uint32_t ligand_id, int32_t run, in
     if (debug) CK(cudaMemcpyAsync(debug, ddbg.p, sizeof(int) * 8 * pop, cudaMemcpyDeviceToHost, c->stream));
     if (perm) CK(cudaMemcpyAsync(perm, c->d_perm, sizeof(int) * pop, cudaMemcpyDeviceToHost, c->stream));
     CK(cudaStreamSynchronize(c->stream));
+    return DOCK_OK;
+}
+
+int dock_sw_trace(dock_ctx *c, int32_t n, int32_t iters, uint64_t seed, uint32_t ligand_id, int32_t run, int32_t gen,
+                  const int32_t *slots, const float *fed_energy, float *genes, float *energy, int64_t *evals,
+                  int32_t *trace_outcome, float *trace_rho) {
+    if (!c) return DOCK_E_INPUT;
+    if (n < 0 || iters < 0) return input_error(c, "n, iters: must be >= 0");
+    if (n == 0 || iters == 0) return DOCK_OK;
+    if (!slots || !genes || !energy || !trace_outcome || !trace_rho) return input_error(c, "sw_trace buffers: NULL");
+    CK(cudaSetDevice(c->device));
+    const int G = c->prep.G;
+    dk::SearchDev sp = make_search(c, 2, 1, run, ligand_id, LLONG_MAX, seed);
+    sp.ls_method = DOCK_LS_SOLIS_WETS;
+    const size_t nt = (size_t)n * iters;
+    DevBuf dg(c->stream), dE(c->stream), dev(c->stream), dsl(c->stream), dfed(c->stream), dtr(c->stream),
+        drho(c->stream);
+    CK(dg.alloc(sizeof(float) * n * G));
+    CK(dE.alloc(sizeof(float) * n));
+    CK(dev.alloc(sizeof(int) * n));
+    CK(dsl.alloc(sizeof(int) * n));
+    CK(dtr.alloc(sizeof(int) * nt));
+    CK(drho.alloc(sizeof(float) * nt));
+    if (fed_energy) CK(dfed.alloc(sizeof(float) * nt * 2));
+    CK(dk::after_last_use(c, c->stream));
+    CK(cudaMemcpyAsync(dg.p, genes, sizeof(float) * n * G, cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemcpyAsync(dE.p, energy, sizeof(float) * n, cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemcpyAsync(dsl.p, slots, sizeof(int) * n, cudaMemcpyHostToDevice, c->stream));
+    if (fed_energy) CK(cudaMemcpyAsync(dfed.p, fed_energy, sizeof(float) * nt * 2, cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemsetAsync(dtr.p, 0xff, sizeof(int) * nt, c->stream));   // -1: not executed
+    CK(cudaMemsetAsync(drho.p, 0, sizeof(float) * nt, c->stream));
+    dk::LsArgs la{};
+    la.use_state = 0; la.n_per_run = n; la.iters = iters;
+    la.genes = (float *)dg.p; la.E = (float *)dE.p; la.evals = (int *)dev.p; la.rng_slot = (const int *)dsl.p;
+    la.gen = gen; la.run = run;
+    la.sw_fed = (const float *)dfed.p; la.sw_trace = (int *)dtr.p; la.sw_trace_rho = (float *)drho.p;
+    CK(dk::launch_ls(c->lig, c->grid, sp, pop_of(c), la, n, c->stream));
+    c->launches += 1;
+    std::vector<int> ev(n);
+    CK(cudaMemcpyAsync(genes, dg.p, sizeof(float) * n * G, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaMemcpyAsync(energy, dE.p, sizeof(float) * n, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaMemcpyAsync(ev.data(), dev.p, sizeof(int) * n, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaMemcpyAsync(trace_outcome, dtr.p, sizeof(int) * nt, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaMemcpyAsync(trace_rho, drho.p, sizeof(float) * nt, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    if (evals) for (int i = 0; i < n; ++i) evals[i] = ev[i];
+    return DOCK_OK;
+}
+
+int dock_ad_trace(dock_ctx *c, int32_t n, int32_t iters, const float *fed, float *genes, float *energy, int64_t *evals,
+                  float *trace_x, float *trace_E, float *trace_g) {
+    if (!c) return DOCK_E_INPUT;
+    if (n < 0 || iters < 0) return input_error(c, "n, iters: must be >= 0");
+    if (n == 0 || iters == 0) return DOCK_OK;
+    if (!genes || !energy || !trace_x || !trace_E || !trace_g) return input_error(c, "ad_trace buffers: NULL");
+    CK(cudaSetDevice(c->device));
+    const int G = c->prep.G;
+    dk::SearchDev sp = make_search(c, 2, 1, 0, 0, LLONG_MAX, 0);
+    sp.ls_method = DOCK_LS_ADADELTA;
+    const size_t nt = (size_t)n * iters;
+    DevBuf dg(c->stream), dE(c->stream), dev(c->stream), dsl(c->stream), dfed(c->stream), dtx(c->stream),
+        dtE(c->stream), dtg(c->stream);
+    CK(dg.alloc(sizeof(float) * n * G));
+    CK(dE.alloc(sizeof(float) * n));
+    CK(dev.alloc(sizeof(int) * n));
+    CK(dsl.alloc(sizeof(int) * n));
+    CK(dtx.alloc(sizeof(float) * nt * G));
+    CK(dtE.alloc(sizeof(float) * nt));
+    CK(dtg.alloc(sizeof(float) * nt * G));
+    if (fed) CK(dfed.alloc(sizeof(float) * nt * (G + 1)));
+    CK(dk::after_last_use(c, c->stream));
+    CK(cudaMemcpyAsync(dg.p, genes, sizeof(float) * n * G, cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemcpyAsync(dE.p, energy, sizeof(float) * n, cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemsetAsync(dsl.p, 0, sizeof(int) * n, c->stream));
+    if (fed) CK(cudaMemcpyAsync(dfed.p, fed, sizeof(float) * nt * (G + 1), cudaMemcpyHostToDevice, c->stream));
+    dk::LsArgs la{};
+    la.use_state = 0; la.n_per_run = n; la.iters = iters;
+    la.genes = (float *)dg.p; la.E = (float *)dE.p; la.evals = (int *)dev.p; la.rng_slot = (const int *)dsl.p;
+    la.gen = 1; la.run = 0;
+    la.ad_fed = (const float *)dfed.p;
+    la.ad_trace_x = (float *)dtx.p; la.ad_trace_E = (float *)dtE.p; la.ad_trace_g = (float *)dtg.p;
+    CK(dk::launch_ls(c->lig, c->grid, sp, pop_of(c), la, n, c->stream));
+    c->launches += 1;
+    std::vector<int> ev(n);
+    CK(cudaMemcpyAsync(genes, dg.p, sizeof(float) * n * G, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaMemcpyAsync(energy, dE.p, sizeof(float) * n, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaMemcpyAsync(ev.data(), dev.p, sizeof(int) * n, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaMemcpyAsync(trace_x, dtx.p, sizeof(float) * nt * G, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaMemcpyAsync(trace_E, dtE.p, sizeof(float) * nt, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaMemcpyAsync(trace_g, dtg.p, sizeof(float) * nt * G, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    if (evals) for (int i = 0; i < n; ++i) evals[i] = ev[i];
     return DOCK_OK;
 }
 

@@ -26,11 +26,36 @@
 #include "philox.cuh"
 #include "score.cuh"
 
+// This file is compiled once per (scoring function, part) in parallel (_build.py): the
+// kernel templates are defined in every translation unit, but each part instantiates --
+// launches -- only its own:
+//   DK_PART 1  evaluation hooks, init, GA, generation end, best, microbenchmarks, RNG hooks
+//   DK_PART 2  the ADADELTA local search (k_ls_adadelta)
+//   DK_PART 3  the Solis-Wets local searches (k_ls_sw, k_ls_sw_tree, k_run_sw)
+//   DK_PART 4  their parity-hook (TRACE) instantiations (dock_sw_trace)
+// (one monolithic unit took ~5 min per scoring function to compile).
+#ifndef DK_PART
+#error "compile kernels.cu with -DDK_PART=1, 2, 3 or 4 (see _build.py)"
+#endif
+
 namespace dk {
 namespace DK_SF_NS {   // d5, or ad4 when compiled with -DDK_AD4 (score.cuh)
 
+// per-part pieces of launch_ls and setup_kernel_attributes (defined in parts 2 and 3)
+cudaError_t launch_ls_adadelta(const LigDev &L, const GridDev &g, const SearchDev &sp, const PopDev &pop,
+                               const LsArgs &a, int n_total, cudaStream_t s);
+cudaError_t launch_ls_sw(const LigDev &L, const GridDev &g, const SearchDev &sp, const PopDev &pop,
+                         const LsArgs &a, int n_total, cudaStream_t s);
+cudaError_t setup_attributes_adadelta();
+cudaError_t setup_attributes_sw();
+template <bool TR>
+cudaError_t launch_ls_sw_t(const LigDev &L, const GridDev &g, const SearchDev &sp, const PopDev &pop,
+                           const LsArgs &a, int n_total, cudaStream_t s);
+cudaError_t setup_attributes_sw_trace();
+
 static inline __host__ __device__ int a16(int x) { return (x + 15) & ~15; }
 
+#if DK_PART == 1
 ScratchLayout scratch_layout(const LigDev &L, bool grad, int extra) {
     ScratchLayout s;
     const int N = L.N, T = L.T, G = L.G;
@@ -56,6 +81,7 @@ GroupCfg pick_group(int N) {
     c.MAXC = N <= 32 ? 1 : (N <= 64 ? 2 : (N <= 96 ? 3 : (N <= 128 ? 4 : 8)));
     return c;
 }
+#endif
 
 // Bytes of the ligand block a kernel stages: gradient kernels skip the pair list and the
 // pair constants of the energy-only path.
@@ -336,6 +362,7 @@ struct LsTarget {
     int *evals;
     uint32_t slot, gen, run_g;
     int run_l;                    // engine mode: run index in the launch (for the fused gen end); -1: hook
+    int idx;                      // hook mode: index of the individual in the call (fed / trace rows); -1: engine
 };
 
 __device__ __forceinline__ LsTarget ls_target(const SearchDev &sp, const PopDev &pop, const LsArgs &a, int gi,
@@ -343,6 +370,7 @@ __device__ __forceinline__ LsTarget ls_target(const SearchDev &sp, const PopDev 
     LsTarget t;
     t.act = false;
     t.run_l = -1;
+    t.idx = -1;
     if (a.use_state) {
         if (gi >= sp.runs * a.n_per_run) return t;
         const int r = gi / a.n_per_run, s = gi % a.n_per_run;
@@ -363,6 +391,7 @@ __device__ __forceinline__ LsTarget ls_target(const SearchDev &sp, const PopDev 
         t.E = a.E + gi;
         t.evals = a.evals + gi;
         t.slot = (uint32_t)a.rng_slot[gi]; t.gen = (uint32_t)a.gen; t.run_g = (uint32_t)a.run;
+        t.idx = gi;
         t.act = true;
     }
     return t;
@@ -394,7 +423,9 @@ __device__ __forceinline__ void ls_finish(const SearchDev &sp, const PopDev &pop
 #ifndef DK_ADA_MINB
 #define DK_ADA_MINB 2   // min resident CTAs/SM for the ADADELTA kernel (register cap 65536/(256*MINB))
 #endif
-template <int W, int MAXC>
+// TRACE: the parity-hook instantiation (dock_ad_trace: fed inputs and traces, LsArgs::ad_*);
+// the production instantiation carries none of that code (register pressure at the cap).
+template <int W, int MAXC, bool TRACE = false>
 __global__ void __launch_bounds__(256, (MAXC <= 4 ? DK_ADA_MINB : 1)) k_ls_adadelta(const LigDev L, const GridDev g, const ScratchLayout SL,
                                                      const SearchDev sp, const PopDev pop, const LsArgs a) {
     extern __shared__ uint4 smem_u4[];
@@ -424,7 +455,23 @@ __global__ void __launch_bounds__(256, (MAXC <= 4 ? DK_ADA_MINB : 1)) k_ls_adade
     const float rho = sp.ad_rho, eps = sp.ad_eps;
     __syncwarp(mask);
     for (int it = 0; it < a.iters; ++it) {
-        const float E = eval_group<W, MAXC, true>(Ls, g, S, sub, mask);
+        float E = eval_group<W, MAXC, true>(Ls, g, S, sub, mask);
+        if constexpr (TRACE) {            // parity hook only
+            const size_t row = (size_t)t.idx * a.iters + it;
+            if (a.ad_fed && t.act) {
+                E = a.ad_fed[row * (G + 1)];
+                for (int j = sub; j < G; j += W) S.grad[j] = a.ad_fed[row * (G + 1) + 1 + j];
+            }
+            __syncwarp(mask);
+            if (a.ad_trace_x && t.act) {
+#pragma unroll
+                for (int s = 0; s < NSET; ++s) {
+                    const int j = sub + W * s;
+                    if (j < G) { a.ad_trace_x[row * G + j] = x[s]; a.ad_trace_g[row * G + j] = S.grad[j]; }
+                }
+                if (sub == 0) a.ad_trace_E[row] = E;
+            }
+        }
         if (E < Ebest) {
             Ebest = E;
 #pragma unroll
@@ -490,7 +537,8 @@ __device__ __forceinline__ void sw_scalar_step(int o, const SearchDev &sp, float
 // k_ls_sw: Solis-Wets (D9; P:64 citing Solis & Wets 1981).  One warp per individual.
 // W <= 16: the two half-warps score x+b+d and x-b-d concurrently.
 // ---------------------------------------------------------------------------
-template <int W, int MAXC>
+// TRACE: the parity-hook instantiation (dock_sw_trace: fed energies, outcome traces).
+template <int W, int MAXC, bool TRACE = false>
 __global__ void __launch_bounds__(256) k_ls_sw(const LigDev L, const GridDev g, const ScratchLayout SL,
                                                const SearchDev sp, const PopDev pop, const LsArgs a) {
     constexpr int NG = (W <= 16) ? 2 : 1;
@@ -536,10 +584,12 @@ __global__ void __launch_bounds__(256) k_ls_sw(const LigDev L, const GridDev g, 
         }
         __syncwarp();
         float E1, E2 = 0.0f;
+        const float *fed = (TRACE && a.sw_fed) ? a.sw_fed + ((size_t)t.idx * a.iters + it) * 2 : nullptr;   // parity mode
         if (NG == 2) {
             const float e = eval_group<W, MAXC, false>(Ls, g, Sg, sub, gmask);
             E1 = __shfl_sync(0xffffffffu, e, 0);
             E2 = __shfl_sync(0xffffffffu, e, W);
+            if constexpr (TRACE) if (fed) { E1 = fed[0]; E2 = fed[1]; }
         } else {
             // x+b+d, then x-b-d only if the first failed: one evaluation call site (the
             // kernel's instruction footprint matters at one warp per SM)
@@ -555,28 +605,36 @@ __global__ void __launch_bounds__(256) k_ls_sw(const LigDev L, const GridDev g, 
                     }
                     __syncwarp();
                 }
-                const float e = eval_group<W, MAXC, false>(Ls, g, S0, sub, gmask);
+                float e = eval_group<W, MAXC, false>(Ls, g, S0, sub, gmask);
+                if constexpr (TRACE) if (fed) e = fed[trial];
                 if (trial == 0) E1 = e; else E2 = e;
             }
         }
+        const float rho_it = rho;
+        int o;
         ++ne;
         if (E1 < Ex) {
 #pragma unroll
             for (int s = 0; s < NSET; ++s) sw_gene_step(0, d[s], x[s], b[s]);
             Ex = E1;
-            sw_scalar_step(0, sp, rho, succ, fail);
+            o = 0;
         } else {
             ++ne;
             if (E2 < Ex) {
 #pragma unroll
                 for (int s = 0; s < NSET; ++s) sw_gene_step(1, d[s], x[s], b[s]);
                 Ex = E2;
-                sw_scalar_step(1, sp, rho, succ, fail);
+                o = 1;
             } else {
 #pragma unroll
                 for (int s = 0; s < NSET; ++s) sw_gene_step(2, d[s], x[s], b[s]);
-                sw_scalar_step(2, sp, rho, succ, fail);
+                o = 2;
             }
+        }
+        sw_scalar_step(o, sp, rho, succ, fail);
+        if constexpr (TRACE) if (lane == 0) {
+            a.sw_trace[(size_t)t.idx * a.iters + it] = o;
+            a.sw_trace_rho[(size_t)t.idx * a.iters + it] = rho_it;
         }
         __syncwarp();
     }
@@ -615,7 +673,7 @@ constexpr int tree_threads() { return ((ipow3(D) - 1) * KP * W + 31) / 32 * 32; 
 #endif
 constexpr int kTriAhead = DK_TRI_AHEAD;   // SW iterations whose deviate shapes are precomputed at a time (>= D)
 
-template <int W, int MAXC, int D, int KP>
+template <int W, int MAXC, int D, int KP, bool TRACE = false>
 __device__ __forceinline__ void sw_tree_chain(const LigSm &Ls, const GridDev &g, const ScratchLayout &SL,
                                               const SearchDev &sp, const PopDev &pop, const LsArgs &a,
                                               const LsTarget &t, uint8_t *sm, const int staged, const int G) {
@@ -710,7 +768,9 @@ __device__ __forceinline__ void sw_tree_chain(const LigSm &Ls, const GridDev &g,
                 }
             }
             __syncwarp(gmask);
-            const float e = eval_group<W, MAXC, false, kAll, KP>(Ls, g, S, sub, gmask, part);
+            float e = eval_group<W, MAXC, false, kAll, KP>(Ls, g, S, sub, gmask, part);
+            if constexpr (TRACE)                                   // parity mode: the fed energy
+                if (a.sw_fed && live) e = part == 0 ? a.sw_fed[((size_t)t.idx * a.iters + it + lvl) * 2 + cand] : 0.0f;
             if (sub == 0) sEc[gidx] = live ? e : INFINITY;
         }
         __syncthreads();
@@ -739,6 +799,10 @@ __device__ __forceinline__ void sw_tree_chain(const LigSm &Ls, const GridDev &g,
                 else o = 2;
             }
             sw_scalar_step(o, sp, rho, succ, fail);
+            if constexpr (TRACE) if (threadIdx.x == 0) {
+                a.sw_trace[(size_t)t.idx * a.iters + it] = o;
+                a.sw_trace_rho[(size_t)t.idx * a.iters + it] = rl[k];
+            }
             path[k] = o;
             sg = 3 * sg + o;
             ++it;
@@ -766,7 +830,7 @@ __device__ __forceinline__ void sw_tree_chain(const LigSm &Ls, const GridDev &g,
     if (threadIdx.x == 0) { *t.E = Ex; *t.evals = ne; ls_finish(sp, pop, t); }
 }
 
-template <int W, int MAXC, int D, int KP = 1>
+template <int W, int MAXC, int D, int KP = 1, bool TRACE = false>
 __global__ void __launch_bounds__(tree_threads<W, D, KP>(), (W == 16 && D == 3) ? 2 : 1) k_ls_sw_tree(const LigDev L, const GridDev g,
                                                                      const ScratchLayout SL, const SearchDev sp,
                                                                      const PopDev pop, const LsArgs a) {
@@ -778,7 +842,7 @@ __global__ void __launch_bounds__(tree_threads<W, D, KP>(), (W == 16 && D == 3) 
     if (!t.act) return;                                      // uniform: one individual per CTA
     const int staged = staged_bytes(L, false);
     const LigSm Ls = stage_ligand(L, sm, staged);
-    sw_tree_chain<W, MAXC, D, KP>(Ls, g, SL, sp, pop, a, t, sm, staged, G);
+    sw_tree_chain<W, MAXC, D, KP, TRACE>(Ls, g, SL, sp, pop, a, t, sm, staged, G);
 }
 
 // ---------------------------------------------------------------------------
@@ -860,6 +924,7 @@ __global__ void DK_RUNSW_BOUNDS k_run_sw(const LigDev L, const GridDev g,
     }
 }
 
+#if DK_PART == 1   // non-template kernels: defined in one part only
 // ---------------------------------------------------------------------------
 // k_gen_end: sum_evals (Listing 1: per-run reduction over the population's
 // evaluation counters with warp shuffles) and the generation counter.
@@ -909,6 +974,8 @@ __global__ void __launch_bounds__(256) k_best(const int G, const SearchDev sp, c
     }
 }
 
+#endif
+
 // ---------------------------------------------------------------------------
 // k_bench_part: microbenchmark of one part of the evaluation: PARTS =
 // kInter -> pose + grid interpolation (a3+a4, energy + gradient), PARTS = kIntra -> pose
@@ -940,6 +1007,7 @@ __global__ void __launch_bounds__(256, (MAXC <= 4 ? DK_ADA_MINB : 1)) k_bench_pa
     if (sub == 0) E[gi] = acc;
 }
 
+#if DK_PART == 1
 __global__ void k_philox(int n, const uint4 *ctr, const uint2 *key, uint4 *out) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i < n) out[i] = philox4x32_10(ctr[i], key[i]);
@@ -950,6 +1018,7 @@ __global__ void k_stream_words(uint2 key, uint32_t purpose, uint32_t slot, uint3
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i < n) out[i] = stream_word(key, purpose, slot, gen, run, m0 + (uint32_t)i);
 }
+#endif
 
 // ---------------------------------------------------------------------------
 // Launchers
@@ -974,14 +1043,36 @@ static cudaError_t allow_smem(K kernel) {
     return cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemMax);
 }
 
+#if DK_PART == 3 || DK_PART == 4
 // cooperative SW trees exist for 32-lane groups only
-template <int W, int MAXC>
+template <int W, int MAXC, bool TRACE>
 static cudaError_t allow_split() {
     if constexpr (W == 32) {
-        cudaError_t e = allow_smem(k_ls_sw_tree<W, MAXC, 1, 4>);
-        return e == cudaSuccess ? allow_smem(k_ls_sw_tree<W, MAXC, 2, 2>) : e;
+        cudaError_t e = allow_smem(k_ls_sw_tree<W, MAXC, 1, 4, TRACE>);
+        return e == cudaSuccess ? allow_smem(k_ls_sw_tree<W, MAXC, 2, 2, TRACE>) : e;
     }
     return cudaSuccess;
+}
+
+template <int W, int MAXC, bool TRACE>
+static cudaError_t allow_sw() {
+    cudaError_t e = allow_smem(k_ls_sw<W, MAXC, TRACE>);
+    if (e == cudaSuccess) e = allow_smem(k_ls_sw_tree<W, MAXC, 2, 1, TRACE>);
+    if (e == cudaSuccess) e = allow_smem(k_ls_sw_tree<W, MAXC, 3, 1, TRACE>);
+    if (e == cudaSuccess) e = allow_split<W, MAXC, TRACE>();
+    return e;
+}
+
+#endif
+
+static inline int ceil_div(long long a, long long b) { return (int)((a + b - 1) / b); }
+
+#if DK_PART == 1
+cudaError_t launch_ls(const LigDev &L, const GridDev &g, const SearchDev &sp, const PopDev &pop, const LsArgs &a,
+                      int n_total, cudaStream_t s) {
+    if (n_total <= 0) return cudaSuccess;
+    return sp.ls_method == 1 ? launch_ls_sw(L, g, sp, pop, a, n_total, s)
+                             : launch_ls_adadelta(L, g, sp, pop, a, n_total, s);
 }
 
 cudaError_t setup_kernel_attributes() {
@@ -993,24 +1084,54 @@ cudaError_t setup_kernel_attributes() {
     if (e == cudaSuccess) e = allow_smem(k_eval<W, MAXC, false, kIntra>);            \
     if (e == cudaSuccess) e = allow_smem(k_init<W, MAXC>);                           \
     if (e == cudaSuccess) e = allow_smem(k_ga<W, MAXC>);                             \
-    if (e == cudaSuccess) e = allow_smem(k_ls_adadelta<W, MAXC>);                    \
-    if (e == cudaSuccess) e = allow_smem(k_ls_sw<W, MAXC>);                         \
-    if (e == cudaSuccess) e = allow_smem(k_ls_sw_tree<W, MAXC, 2>);                  \
-    if (e == cudaSuccess) e = allow_smem(k_ls_sw_tree<W, MAXC, 3>);                  \
-    if (e == cudaSuccess) e = allow_split<W, MAXC>();                                 \
-    if (e == cudaSuccess) e = allow_smem(k_run_sw<W, MAXC, 2>);                      \
-    if (e == cudaSuccess) e = cudaFuncSetAttribute(k_run_sw<W, MAXC, 2>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1); \
-    if (e == cudaSuccess) e = allow_smem(k_run_sw<W, MAXC, 3>);                      \
-    if (e == cudaSuccess) e = cudaFuncSetAttribute(k_run_sw<W, MAXC, 3>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1); \
     if (e == cudaSuccess) e = allow_smem(k_bench_part<W, MAXC, kInter>);             \
     if (e == cudaSuccess) e = allow_smem(k_bench_part<W, MAXC, kIntra>);
     DK_ATTR(16, 1) DK_ATTR(32, 1) DK_ATTR(32, 2) DK_ATTR(32, 3) DK_ATTR(32, 4) DK_ATTR(32, 8)
 #undef DK_ATTR
+    if (e == cudaSuccess) e = setup_attributes_adadelta();
+    if (e == cudaSuccess) e = setup_attributes_sw();
     return e;
 }
+#endif
 
-static inline int ceil_div(long long a, long long b) { return (int)((a + b - 1) / b); }
+#if DK_PART == 2
+cudaError_t setup_attributes_adadelta() {
+    cudaError_t e = cudaSuccess;
+#define DK_ATTR(W, MAXC)                                                             \
+    if (e == cudaSuccess) e = allow_smem(k_ls_adadelta<W, MAXC>);                    \
+    if (e == cudaSuccess) e = allow_smem(k_ls_adadelta<W, MAXC, true>);
+    DK_ATTR(16, 1) DK_ATTR(32, 1) DK_ATTR(32, 2) DK_ATTR(32, 3) DK_ATTR(32, 4) DK_ATTR(32, 8)
+#undef DK_ATTR
+    return e;
+}
+#endif
 
+#if DK_PART == 3
+cudaError_t setup_attributes_sw() {
+    cudaError_t e = cudaSuccess;
+#define DK_ATTR(W, MAXC)                                                             \
+    if (e == cudaSuccess) e = allow_sw<W, MAXC, false>();                            \
+    if (e == cudaSuccess) e = allow_smem(k_run_sw<W, MAXC, 2>);                      \
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(k_run_sw<W, MAXC, 2>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1); \
+    if (e == cudaSuccess) e = allow_smem(k_run_sw<W, MAXC, 3>);                      \
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(k_run_sw<W, MAXC, 3>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    DK_ATTR(16, 1) DK_ATTR(32, 1) DK_ATTR(32, 2) DK_ATTR(32, 3) DK_ATTR(32, 4) DK_ATTR(32, 8)
+#undef DK_ATTR
+    return e == cudaSuccess ? setup_attributes_sw_trace() : e;
+}
+#endif
+
+#if DK_PART == 4
+cudaError_t setup_attributes_sw_trace() {
+    cudaError_t e = cudaSuccess;
+#define DK_ATTR(W, MAXC) if (e == cudaSuccess) e = allow_sw<W, MAXC, true>();
+    DK_ATTR(16, 1) DK_ATTR(32, 1) DK_ATTR(32, 2) DK_ATTR(32, 3) DK_ATTR(32, 4) DK_ATTR(32, 8)
+#undef DK_ATTR
+    return e;
+}
+#endif
+
+#if DK_PART == 1
 cudaError_t launch_eval(const LigDev &L, const GridDev &g, int n, const float *genes, float *E, float *grad,
                         float *xyz, const int *dfs2orig, cudaStream_t s, int parts) {
     if (n <= 0) return cudaSuccess;
@@ -1056,6 +1177,9 @@ cudaError_t launch_ga(const LigDev &L, const GridDev &g, const SearchDev &sp, co
     return cudaGetLastError();
 }
 
+#endif
+
+#if DK_PART == 3 || DK_PART == 4
 // shared memory of a k_ls_sw_tree<.., D, KP> CTA: ligand block, one scratch per lane
 // group, x and b, the partial energies and the double-buffered deviate shapes
 static size_t tree_smem(const LigDev &L, const ScratchLayout &SL, int D, int KP) {
@@ -1071,11 +1195,15 @@ static size_t run_sw_smem(const LigDev &L, const ScratchLayout &SL, int D) {
     return ga > tr ? ga : tr;
 }
 
-cudaError_t launch_ls(const LigDev &L, const GridDev &g, const SearchDev &sp, const PopDev &pop, const LsArgs &a,
-                      int n_total, cudaStream_t s) {
-    if (n_total <= 0) return cudaSuccess;
+// TR = true: the parity-hook (TRACE) instantiations, compiled in part 4.
+#define DK_TRACE_SEL(...)                                                          \
+    do { __VA_ARGS__; } while (0)
+
+template <bool TR>
+cudaError_t launch_ls_sw_t(const LigDev &L, const GridDev &g, const SearchDev &sp, const PopDev &pop, const LsArgs &a,
+                           int n_total, cudaStream_t s) {
     const GroupCfg cfg = pick_group(L.N);
-    if (sp.ls_method == 1) {
+    {
         const ScratchLayout SL = scratch_layout(L, false, 0);
         // (A full warp per node for W = 16 ligands -- half the pairs per lane -- was measured
         // 0.63x on 1stp: twice the warps per round, same critical path.)
@@ -1121,8 +1249,8 @@ cudaError_t launch_ls(const LigDev &L, const GridDev &g, const SearchDev &sp, co
             switch (tcfg.MAXC) {
 #define DK_SPLIT(M)                                                                                     \
     case M:                                                                                             \
-        if (split == 2) k_ls_sw_tree<32, M, 2, 2><<<n_total, tree_threads<32, 2, 2>(), smem, s>>>(L, g, SL, sp, pop, a); \
-        else k_ls_sw_tree<32, M, 1, 4><<<n_total, tree_threads<32, 1, 4>(), smem, s>>>(L, g, SL, sp, pop, a);           \
+        DK_TRACE_SEL(if (split == 2) k_ls_sw_tree<32, M, 2, 2, TR><<<n_total, tree_threads<32, 2, 2>(), smem, s>>>(L, g, SL, sp, pop, a); \
+                     else k_ls_sw_tree<32, M, 1, 4, TR><<<n_total, tree_threads<32, 1, 4>(), smem, s>>>(L, g, SL, sp, pop, a)); \
         break;
                 DK_SPLIT(1) DK_SPLIT(2) DK_SPLIT(3) DK_SPLIT(4)
                 default: DK_SPLIT(8)
@@ -1133,10 +1261,9 @@ cudaError_t launch_ls(const LigDev &L, const GridDev &g, const SearchDev &sp, co
         if (depth >= 2) {
             const size_t smem = tree_smem(L, SL, depth, 1);
             if (smem > (size_t)kSmemMax) return cudaErrorInvalidConfiguration;
-            DK_DISPATCH(tcfg, {
-                if (depth == 3) k_ls_sw_tree<W, MAXC, 3><<<n_total, tree_threads<W, 3>(), smem, s>>>(L, g, SL, sp, pop, a);
-                else k_ls_sw_tree<W, MAXC, 2><<<n_total, tree_threads<W, 2>(), smem, s>>>(L, g, SL, sp, pop, a);
-            });
+            DK_DISPATCH(tcfg, { DK_TRACE_SEL(
+                if (depth == 3) k_ls_sw_tree<W, MAXC, 3, 1, TR><<<n_total, tree_threads<W, 3>(), smem, s>>>(L, g, SL, sp, pop, a);
+                else k_ls_sw_tree<W, MAXC, 2, 1, TR><<<n_total, tree_threads<W, 2>(), smem, s>>>(L, g, SL, sp, pop, a)); });
             return cudaGetLastError();
         }
         // depth 1: one warp per individual; few individuals -> one warp per CTA so they
@@ -1146,16 +1273,18 @@ cudaError_t launch_ls(const LigDev &L, const GridDev &g, const SearchDev &sp, co
         const size_t smem = (size_t)staged_bytes(L, false) + (size_t)warps * ng * SL.bytes;
         if (smem > (size_t)kSmemMax) return cudaErrorInvalidConfiguration;
         const int blocks = ceil_div(n_total, warps);
-        DK_DISPATCH(cfg, { k_ls_sw<W, MAXC><<<blocks, warps * 32, smem, s>>>(L, g, SL, sp, pop, a); });
-    } else {
-        const ScratchLayout SL = scratch_layout(L, true, 0);
-        const int groups = kThreads / cfg.W;
-        const size_t smem = (size_t)staged_bytes(L, true) + (size_t)groups * SL.bytes;
-        if (smem > (size_t)kSmemMax) return cudaErrorInvalidConfiguration;
-        const int blocks = ceil_div(n_total, groups);
-        DK_DISPATCH(cfg, { k_ls_adadelta<W, MAXC><<<blocks, kThreads, smem, s>>>(L, g, SL, sp, pop, a); });
+        DK_DISPATCH(cfg, { DK_TRACE_SEL(k_ls_sw<W, MAXC, TR><<<blocks, warps * 32, smem, s>>>(L, g, SL, sp, pop, a)); });
     }
     return cudaGetLastError();
+}
+#if DK_PART == 4
+template cudaError_t launch_ls_sw_t<true>(const LigDev &, const GridDev &, const SearchDev &, const PopDev &,
+                                         const LsArgs &, int, cudaStream_t);
+#else
+cudaError_t launch_ls_sw(const LigDev &L, const GridDev &g, const SearchDev &sp, const PopDev &pop, const LsArgs &a,
+                         int n_total, cudaStream_t s) {
+    return a.sw_trace ? launch_ls_sw_t<true>(L, g, sp, pop, a, n_total, s)
+                      : launch_ls_sw_t<false>(L, g, sp, pop, a, n_total, s);
 }
 
 // Persistent cluster engine (k_run_sw): eligible when the run's LS individuals fit one
@@ -1227,7 +1356,28 @@ cudaError_t launch_run_sw(const LigDev &L, const GridDev &g, const SearchDev &sp
     });
     return e != cudaSuccess ? e : cudaGetLastError();
 }
+#endif  // DK_PART == 3 (launch_ls_sw .. launch_run_sw)
+#endif  // DK_PART == 3 || DK_PART == 4
 
+#if DK_PART == 2
+cudaError_t launch_ls_adadelta(const LigDev &L, const GridDev &g, const SearchDev &sp, const PopDev &pop,
+                               const LsArgs &a, int n_total, cudaStream_t s) {
+    const GroupCfg cfg = pick_group(L.N);
+    {
+        const ScratchLayout SL = scratch_layout(L, true, 0);
+        const int groups = kThreads / cfg.W;
+        const size_t smem = (size_t)staged_bytes(L, true) + (size_t)groups * SL.bytes;
+        if (smem > (size_t)kSmemMax) return cudaErrorInvalidConfiguration;
+        const int blocks = ceil_div(n_total, groups);
+        if (a.ad_trace_x) DK_DISPATCH(cfg, { k_ls_adadelta<W, MAXC, true><<<blocks, kThreads, smem, s>>>(L, g, SL, sp, pop, a); });
+        else DK_DISPATCH(cfg, { k_ls_adadelta<W, MAXC><<<blocks, kThreads, smem, s>>>(L, g, SL, sp, pop, a); });
+    }
+    return cudaGetLastError();
+}
+
+#endif
+
+#if DK_PART == 1
 cudaError_t launch_bench_part(const LigDev &L, const GridDev &g, int part, int n, int iters, const float *genes,
                               float *E, cudaStream_t s) {
     if (n <= 0) return cudaSuccess;
@@ -1268,6 +1418,8 @@ cudaError_t launch_stream_words(uint32_t k0, uint32_t k1, uint32_t purpose, uint
     k_stream_words<<<ceil_div(n, 128), 128, 0, s>>>(make_uint2(k0, k1), purpose, slot, gen, run, m0, n, out);
     return cudaGetLastError();
 }
+
+#endif
 
 }  // namespace DK_SF_NS
 }  // namespace dk

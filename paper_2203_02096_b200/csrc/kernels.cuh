@@ -25,6 +25,20 @@ struct LsArgs {
     int gen, run;           // hook mode: generation and global run index
     int wave_total;         // LS individuals in flight on the device for the speculation-depth rule
                             // (per-run launches of concurrent branches: all runs'); 0 = this launch's
+    // Solis-Wets "fed" parity mode (hook mode only; SURVEY §8(c) parity protocol): the energy
+    // of candidate c (0 = x+b+d, 1 = x-b-d) of iteration it of individual i is
+    // sw_fed[(i iters + it) 2 + c] instead of the evaluation's, so the D9 state machine is
+    // compared with the oracle's on identical energies.  sw_trace / sw_trace_rho [n][iters]:
+    // outcome (0, 1, 2) and rho of every executed iteration.  All null in production.
+    const float *sw_fed;
+    int *sw_trace;
+    float *sw_trace_rho;
+    // ADADELTA parity mode (hook mode only): ad_fed [n][iters][1+G] replaces iteration it's
+    // (energy, gradient) of individual i; ad_trace_x / ad_trace_g [n][iters][G] and
+    // ad_trace_E [n][iters] receive the point evaluated at every iteration, its gradient and
+    // its energy (the kernel's own, or the fed ones).  All null in production.
+    const float *ad_fed;
+    float *ad_trace_x, *ad_trace_E, *ad_trace_g;
 };
 
 struct GroupCfg {

@@ -12,7 +12,7 @@ import pytest
 
 import oracle
 from gen import config_inputs, random_genotypes
-from test_gpu_parity import CONFIGS_LS, e_tol, near_reference_genotypes, pose_tols
+from test_gpu_parity import CONFIGS_LS, assert_parity, compare_at_pose, e_tol, near_reference_genotypes
 
 pytestmark = pytest.mark.gpu
 
@@ -54,28 +54,14 @@ def test_ad4_energy_gradient_pose_parity(dock, name, n):
     X = random_genotypes(grid, d.T, n, seed=2000 + n, frac_out=0.05)
     X[:5, 6:] = 0.0                                    # a few folded (clash) poses
     E, Gd, xyz = d.eval(X, grad=True, xyz=True)
-    E0, _, _ = d.eval(X, grad=False, xyz=False)        # energy-only kernel path
+    E0, _, xyz0 = d.eval(X, grad=False, xyz=True)      # energy-only kernel path
     assert np.isfinite(E).all() and np.isfinite(E0).all() and np.isfinite(Gd).all()
-    bad_e = bad_g = bad_x = ex_e = ex_g = 0
-    hi = np.array(grid.n) - 1
-    for i in range(n):
-        ref = P.energy(X[i].astype(np.float64))
-        if np.abs(xyz[i] - ref["xyz"]).max() > 1e-4:
-            bad_x += 1
-        u = (ref["xyz"] - grid.origin.astype(np.float64)) / grid.spacing
-        if np.minimum(np.abs(u), np.abs(u - hi)).min() < 1e-4 or cut_margin(P, ref["xyz"]) < 1e-4:
-            ex_e += 1
-            continue
-        tol, gtol = pose_tols(P, ref)
-        if abs(E[i] - ref["E"]) > tol or abs(E0[i] - ref["E"]) > tol:
-            bad_e += 1
-        fm, cm = P.margins(ref["xyz"])
-        if fm < 1e-4 or cm < 1e-4 or P.kink_margin(ref["xyz"]) < 1e-4:
-            ex_g += 1
-            continue
-        if np.abs(Gd[i] - ref["grad"]).max() > gtol:
-            bad_g += 1
-    assert bad_x == 0 and bad_e == 0 and bad_g == 0, (bad_x, bad_e, bad_g, ex_e, ex_g)
+    cut = lambda r: cut_margin(P, r) < 1e-4             # noqa: E731  (energy jumps at a cutoff)
+    c, fails = compare_at_pose(P, grid, X, E, xyz, Gd=Gd, extra_excl=cut, kink=True)
+    assert_parity(c, fails, name + " AD4 energy+gradient")
+    c0, fails0 = compare_at_pose(P, grid, X, E0, xyz0, extra_excl=cut)
+    assert_parity(c0, fails0, name + " AD4 energy-only")
+    ex_e, ex_g = c["ex_e"], c["ex_g"]
     assert ex_e + ex_g < 0.35 * n     # PL: 5,190 pairs x 4 kinks each -> ~1/4 of poses near one
 
 

@@ -95,3 +95,34 @@ def test_empty_moved_set_zero_torsion_gradient(orc):
     g = P.energy(x)["grad"]
     for t in empty:
         assert g[6 + t] == 0.0
+
+
+def test_energy_at_given_pose(orc):
+    """or_energy_at (DESIGN.md §3 reading 22b): at the oracle's own pose it is or_energy
+    bit for bit; at any other pose its energy is or_inter + or_intra of that pose (both
+    pinned by test_oracle_inter/intra) and its translation gradient is the sum of their
+    per-atom gradients (D7: dE/dt = sum_a g_a); the rotational and torsional components
+    are invariant under a common translation of pose and t (D7 uses r_a - t, r_a - r_ak)."""
+    cfg, lig, grid = config_inputs("1stp")
+    P = oracle.Problem(grid, lig)
+    X = random_genotypes(grid, P.T, 20, seed=19, frac_out=0.0, shrink=0.3).astype(np.float64)
+    rng = np.random.default_rng(3)
+    for x in X:
+        own = P.energy(x)
+        at = P.energy_at(x, own["xyz"])
+        assert at["E"] == own["E"] and np.array_equal(at["grad"], own["grad"])
+        r = own["xyz"] + rng.normal(0, 0.05, own["xyz"].shape)       # a perturbed pose
+        at = P.energy_at(x, r)
+        ei, gi = P.inter(r)
+        ep, gp = P.intra(r)
+        assert abs(at["E"] - (ei + ep)) <= 1e-12 * max(1.0, abs(ei + ep))
+        assert np.allclose(at["grad"][:3], (gi + gp).sum(0), rtol=1e-12, atol=1e-9)
+        # common shift of the pose and t: rotational/torsional projections only see
+        # differences (the energy itself changes: the grid is fixed)
+        sh = np.array([0.3, -0.2, 0.1])
+        xs = x.copy(); xs[:3] += sh
+        a2 = P.energy_at(xs, r + sh)
+        g_exp_t = (P.inter(r + sh)[1] + P.intra(r + sh)[1])
+        Gam = np.cross(r + sh - xs[:3], g_exp_t).sum(0)
+        assert abs(a2["grad"][5] - Gam @ np.array([np.sin(x[4]) * np.cos(x[3]), np.sin(x[4]) * np.sin(x[3]),
+                                                   np.cos(x[4])])) <= 1e-9 * max(1.0, np.abs(Gam).max())
