@@ -62,6 +62,11 @@ typedef struct {
     float origin[3];
     int32_t n_types;             /* 1..16 */
     const float *maps;           /* host, (n_types+2)*nx*ny*nz, finite */
+    const char (*type_names)[4]; /* [n_types] NUL-terminated map type names ("C", "OA", ...; S:38-41,
+                                    S:83), or NULL.  Required when dock_init's type_params is NULL: the
+                                    per-type parameters then come from the built-in table by name
+                                    (dock_builtin_type_param); a name with no entry is DOCK_E_INPUT.
+                                    Names must be unique. */
 } dock_grids;
 
 /* Per-type ligand parameters, one per grid type map, in map order (D5; "hydrogen
@@ -71,16 +76,35 @@ typedef struct {
     int32_t role;
 } dock_type_param;
 
-/* Ligand (atoms + rotatable bonds).  Torsions and the intra-
-   molecular pair list are derived by D1. */
+/* Ligand (atoms + rotatable bonds).
+   Topology, two modes (reading D1):
+   * derived (n_tors = n_pairs = -1): torsions and the intramolecular pair list follow from
+     the bond graph and the rotatable flags by D1.1-D1.6 (torsion order by depth, a, b;
+     pairs lexicographic);
+   * verbatim (n_tors >= 0 and n_pairs >= 0; SPEC S:30-36, S:91-93 TORSION / PAIR records):
+     the caller's torsions and pairs are used as given, in the given order, after the D1.7
+     validation: indices in range; an axis of two distinct atoms; a moved set without its
+     axis atoms and without duplicates; moved sets pairwise nested or disjoint; a
+     set nested in another comes after it (parents first); a later torsion never moves an
+     earlier torsion's axis atoms; an earlier torsion whose moved set contains a later
+     one's carries that later axis too (it lies in its moved set or on its axis); no self
+     or duplicate pairs.  Bonds are optional there and `rotatable` must be NULL or all 0.
+   A zero-initialised topology (n_tors = n_pairs = 0) is the verbatim rigid ligand without
+   pairs; set both to -1 to derive. */
 typedef struct {
     int32_t n_atoms;             /* 1..256 */
     const int32_t *type;         /* [n_atoms] index into the grid's type maps */
     const float *charge;         /* [n_atoms] */
     const float *xyz;            /* [n_atoms*3] reference coordinates */
     int32_t n_bonds;
-    const int32_t *bonds;        /* [n_bonds*2] atom pairs; graph must be connected */
+    const int32_t *bonds;        /* [n_bonds*2] atom pairs; graph must be connected (derived mode) */
     const uint8_t *rotatable;    /* [n_bonds] 1 = rotatable (must be a bridge); <= 32 */
+    int32_t n_tors;              /* -1: derive (D1); 0..32: verbatim torsions */
+    const int32_t *tors_axis;    /* [n_tors*2] (a_k, b_k): rotation axis a_k -> b_k, right-handed */
+    const int32_t *tors_moved_off; /* [n_tors+1] CSR offsets into tors_moved */
+    const int32_t *tors_moved;   /* moved(k) = tors_moved[off[k] .. off[k+1]) */
+    int32_t n_pairs;             /* -1: derive (D1); >= 0: verbatim intramolecular pairs */
+    const int32_t *pairs;        /* [n_pairs*2] */
 } dock_ligand;
 
 /* Search parameters (D8-D10). */
@@ -132,7 +156,8 @@ int dock_params_default(dock_params *p);
 int dock_builtin_type_param(const char *name, dock_type_param *out);
 
 /* Preprocess the ligand (D1: torsion tree, DFS renumbering, pair list), pack the grid
-   into the device layout and upload both.  Validation errors -> DOCK_E_INPUT. */
+   into the device layout and upload both.  type_params [grids->n_types] in map order, or
+   NULL: the built-in table by grids->type_names.  Validation errors -> DOCK_E_INPUT. */
 int dock_init(const dock_grids *grids, const dock_type_param *type_params,
               const dock_ligand *ligand, const dock_params *params, dock_ctx **out);
 void dock_free(dock_ctx *ctx);

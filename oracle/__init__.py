@@ -105,6 +105,8 @@ def lib():
         L.or_topology.argtypes = [i, i, P(i), P(C.c_ubyte), P(i), P(i), P(i), P(C.c_ubyte), P(i),
                                   P(i), P(i), i, P(i)]
         L.or_topology.restype = i
+        L.or_topology_verbatim.argtypes = [i, i, P(i), P(i), P(i), i, P(i), P(i), P(i), P(C.c_ubyte), P(i)]
+        L.or_topology_verbatim.restype = i
         L.or_pose.argtypes = [P(CProblem), P(d), P(d)]
         L.or_inter_atom.argtypes = [P(CProblem), i, P(d), P(d)]; L.or_inter_atom.restype = d
         L.or_inter.argtypes = [P(CProblem), P(d), P(d)]; L.or_inter.restype = d
@@ -190,6 +192,29 @@ def topology(n_atoms, bonds, rotatable):
     return dict(T=t, tor_a=ta[:t].copy(), tor_b=tb[:t].copy(), depth=dep[:t].copy(),
                 moved=moved[: t * n_atoms].reshape(t, n_atoms).copy(),
                 pairs=pairs[: 2 * Pn.value].reshape(-1, 2).copy(), frag=frag[:n_atoms].copy())
+
+
+def topology_verbatim(n_atoms, axis, moved, pairs):
+    """D1.7: validate verbatim torsions (axis [T, 2], moved: T index lists) and pairs [P, 2];
+    returns the topology dict (as topology(); depth / frag not defined) or raises ValueError."""
+    ax = np.ascontiguousarray(axis, dtype=np.int32).reshape(-1)
+    T = ax.shape[0] // 2
+    off = np.ascontiguousarray(np.concatenate([[0], np.cumsum([len(m) for m in moved])]), dtype=np.int32)
+    mv = np.ascontiguousarray(np.concatenate([np.asarray(m, np.int64) for m in moved]) if T else np.zeros(1),
+                              dtype=np.int32)
+    pr = np.ascontiguousarray(pairs, dtype=np.int32).reshape(-1)
+    if pr.size == 0:
+        pr = np.zeros(2, np.int32)
+    P = np.asarray(pairs).reshape(-1, 2).shape[0]
+    ta = np.zeros(max(T, 1), np.int32); tb = np.zeros(max(T, 1), np.int32)
+    mo = np.zeros(max(T, 1) * n_atoms, np.uint8); po = np.zeros(max(2 * P, 2), np.int32)
+    rc = lib().or_topology_verbatim(n_atoms, T, _p(ax if T else np.zeros(2, np.int32), C.c_int), _p(off, C.c_int),
+                                    _p(mv, C.c_int), P, _p(pr, C.c_int), _p(ta, C.c_int), _p(tb, C.c_int),
+                                    _p(mo, C.c_ubyte), _p(po, C.c_int))
+    if rc != 0:
+        raise ValueError("oracle topology_verbatim: invalid torsions / pairs")
+    return dict(T=T, tor_a=ta[:T].copy(), tor_b=tb[:T].copy(), moved=mo[: T * n_atoms].reshape(T, n_atoms).copy(),
+                pairs=po[: 2 * P].reshape(-1, 2).copy())
 
 
 # ---------------------------------------------------------------------------

@@ -187,6 +187,60 @@ done:
     return rc;
 }
 
+/* D1.7 — verbatim torsions and pairs ("moved excludes axis_a and axis_b",
+   S:91-93 TORSION / PAIR records), checked by brute force over all torsion pairs k < j:
+   (a) indices in range, a_k != b_k, moved(k) without duplicates and without a_k, b_k;
+   (b) moved(k) and moved(j) nested or disjoint;
+   (c) a nested set comes after the set containing it (parents first);
+   (d) {a_k, b_k} is not moved by a later torsion j;
+   (e) if moved(j) lies inside a non-disjoint moved(k), the axis atoms of j are carried by k
+       (in moved(k) or on k's axis), so the world axis of j turns with k (D7's w_j);
+   (f) pairs: in range, i != j, no duplicate unordered pair; returned with i < j, list order.
+   Returns 0 (ok) or 1 (input error). */
+int or_topology_verbatim(int N, int T, const int *axis, const int *moved_off, const int *moved_idx, int P,
+                         const int *pairs_in, int *tor_a, int *tor_b, unsigned char *moved, int *pairs_out) {
+    if (N < 1 || N > OR_MAX_ATOMS || T < 0 || T > OR_MAX_TORS || P < 0) return 1;
+    for (int k = 0; k < T * N; ++k) moved[k] = 0;
+    for (int k = 0; k < T; ++k) {                                           /* (a) */
+        int a = axis[2 * k], b = axis[2 * k + 1];
+        if (a < 0 || a >= N || b < 0 || b >= N || a == b) return 1;
+        if (moved_off[k + 1] < moved_off[k]) return 1;
+        for (int q = moved_off[k]; q < moved_off[k + 1]; ++q) {
+            int m = moved_idx[q];
+            if (m < 0 || m >= N || m == a || m == b || moved[k * N + m]) return 1;
+            moved[k * N + m] = 1;
+        }
+        tor_a[k] = a; tor_b[k] = b;
+    }
+    for (int k = 0; k < T; ++k)
+        for (int j = k + 1; j < T; ++j) {
+            int both = 0, only_k = 0, only_j = 0;
+            for (int m = 0; m < N; ++m) {
+                both += moved[k * N + m] && moved[j * N + m];
+                only_k += moved[k * N + m] && !moved[j * N + m];
+                only_j += !moved[k * N + m] && moved[j * N + m];
+            }
+            if (both && only_k && only_j) return 1;                            /* (b) */
+            if (both && !only_k && only_j) return 1;                           /* (c) k inside j */
+            if (moved[j * N + tor_a[k]] || moved[j * N + tor_b[k]]) return 1; /* (d) */
+            if (both && !only_j) {                                             /* (e) j inside k */
+                for (int e = 0; e < 2; ++e) {
+                    int x = e ? tor_b[j] : tor_a[j];
+                    if (!moved[k * N + x] && x != tor_a[k] && x != tor_b[k]) return 1;
+                }
+            }
+        }
+    for (int q = 0; q < P; ++q) {                                              /* (f) */
+        int i = pairs_in[2 * q], j = pairs_in[2 * q + 1];
+        if (i < 0 || i >= N || j < 0 || j >= N || i == j) return 1;
+        if (i > j) { int t = i; i = j; j = t; }
+        for (int r = 0; r < q; ++r)
+            if (pairs_out[2 * r] == i && pairs_out[2 * r + 1] == j) return 1;
+        pairs_out[2 * q] = i; pairs_out[2 * q + 1] = j;
+    }
+    return 0;
+}
+
 /* ========================================================================
  * D3 — genotype -> pose (NS "orientation quaternion").
  * ======================================================================== */

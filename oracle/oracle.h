@@ -94,6 +94,11 @@ int or_topology(int N, int n_bonds, const int *bonds, const unsigned char *rotat
                 int *depth /*[32]*/, int *P_out, int *pairs /*[cap*2]*/, int cap,
                 int *frag /*[N] nullable*/);
 
+/* ---- D1.7: verbatim torsions (axis [T*2], CSR moved sets) and pairs [P*2], validated.
+   Outputs tor_a/tor_b [T], moved [T*N], pairs_out [P*2] (i < j, list order).  0 ok, 1 error. ---- */
+int or_topology_verbatim(int N, int T, const int *axis, const int *moved_off, const int *moved_idx, int P,
+                         const int *pairs_in, int *tor_a, int *tor_b, unsigned char *moved, int *pairs_out);
+
 /* ---- D3: genotype -> pose ---- */
 void or_pose(const or_problem *P, const double *genes, double *xyz);
 

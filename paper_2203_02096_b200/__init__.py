@@ -31,7 +31,8 @@ class DockError(RuntimeError):
 
 class Grids(C.Structure):
     _fields_ = [("nx", C.c_int32), ("ny", C.c_int32), ("nz", C.c_int32), ("spacing", C.c_float),
-                ("origin", C.c_float * 3), ("n_types", C.c_int32), ("maps", C.POINTER(C.c_float))]
+                ("origin", C.c_float * 3), ("n_types", C.c_int32), ("maps", C.POINTER(C.c_float)),
+                ("type_names", C.POINTER(C.c_char * 4))]
 
 
 class TypeParam(C.Structure):
@@ -41,7 +42,53 @@ class TypeParam(C.Structure):
 class Ligand(C.Structure):
     _fields_ = [("n_atoms", C.c_int32), ("type", C.POINTER(C.c_int32)), ("charge", C.POINTER(C.c_float)),
                 ("xyz", C.POINTER(C.c_float)), ("n_bonds", C.c_int32), ("bonds", C.POINTER(C.c_int32)),
-                ("rotatable", C.POINTER(C.c_uint8))]
+                ("rotatable", C.POINTER(C.c_uint8)), ("n_tors", C.c_int32), ("tors_axis", C.POINTER(C.c_int32)),
+                ("tors_moved_off", C.POINTER(C.c_int32)), ("tors_moved", C.POINTER(C.c_int32)),
+                ("n_pairs", C.c_int32), ("pairs", C.POINTER(C.c_int32))]
+
+
+def _ligand_struct(types, charges, xyz, bonds, rotatable, tors=None, pairs=None):
+    """A dock_ligand over numpy copies (returned alongside, to keep them alive).
+    tors = (axis [T, 2], moved: T index lists) and pairs [P, 2]: verbatim topology (D1.7,
+    SPEC TORSION / PAIR records); None: derived by D1 (n_tors = n_pairs = -1)."""
+    t = np.ascontiguousarray(types, dtype=np.int32)
+    q = np.ascontiguousarray(charges, dtype=np.float32)
+    x = np.ascontiguousarray(xyz, dtype=np.float32).reshape(-1)
+    b = np.ascontiguousarray(bonds if bonds is not None else np.zeros((0, 2)), dtype=np.int32).reshape(-1)
+    r = np.ascontiguousarray(rotatable if rotatable is not None else np.zeros(b.shape[0] // 2), dtype=np.uint8)
+    lg = Ligand()
+    lg.n_atoms = t.shape[0]; lg.type = _ptr(t, C.c_int32); lg.charge = _ptr(q, C.c_float)
+    lg.xyz = _ptr(x, C.c_float); lg.n_bonds = b.shape[0] // 2
+    lg.bonds = _ptr(b, C.c_int32) if lg.n_bonds else None
+    lg.rotatable = _ptr(r, C.c_uint8) if lg.n_bonds else None
+    keep = [t, q, x, b, r]
+    lg.n_tors = lg.n_pairs = -1
+    if tors is not None or pairs is not None:
+        axis, moved = tors if tors is not None else (np.zeros((0, 2)), [])
+        ax = np.ascontiguousarray(axis, dtype=np.int32).reshape(-1)
+        off = np.ascontiguousarray(np.concatenate([[0], np.cumsum([len(m) for m in moved])]), dtype=np.int32)
+        mv = np.ascontiguousarray(np.concatenate([np.asarray(m, np.int64) for m in moved]) if len(moved) else
+                                  np.zeros(0), dtype=np.int32)
+        pr = np.ascontiguousarray(pairs if pairs is not None else np.zeros((0, 2)), dtype=np.int32).reshape(-1)
+        keep += [ax, off, mv, pr]
+        lg.n_tors = ax.shape[0] // 2
+        lg.tors_axis = _ptr(ax, C.c_int32); lg.tors_moved_off = _ptr(off, C.c_int32); lg.tors_moved = _ptr(mv, C.c_int32)
+        lg.n_pairs = pr.shape[0] // 2
+        lg.pairs = _ptr(pr, C.c_int32)
+    return lg, keep
+
+
+def _names_array(type_names):
+    """grids.type_names: [n_types] char[4] (NUL-terminated names), or None."""
+    if type_names is None:
+        return None
+    arr = ((C.c_char * 4) * len(type_names))()
+    for i, nm in enumerate(type_names):
+        b = nm.encode() if isinstance(nm, str) else bytes(nm)
+        if not 0 < len(b) < 4:
+            raise DockError(DOCK_E_INPUT, f"type_names[{i}]: 1..3 characters")
+        arr[i].value = b
+    return arr
 
 
 class Params(C.Structure):
@@ -211,30 +258,22 @@ def write_screen(out: dict, fmt: str = "json", ids=None, n_genes=None) -> str:
     return buf.value.decode()
 
 
-def topology(types, charges, xyz, bonds, rotatable, type_params, roles):
-    """D1 on the host (no device needed): (axis [T,2], moved [T,N], pairs [P,2])."""
-    t = np.ascontiguousarray(types, dtype=np.int32)
-    q = np.ascontiguousarray(charges, dtype=np.float32)
-    x = np.ascontiguousarray(xyz, dtype=np.float32).reshape(-1)
-    b = np.ascontiguousarray(bonds, dtype=np.int32).reshape(-1)
-    r = np.ascontiguousarray(rotatable, dtype=np.uint8)
+def topology(types, charges, xyz, bonds, rotatable, type_params, roles, tors=None, pairs=None):
+    """D1 on the host (no device needed): (axis [T,2], moved [T,N], pairs [P,2]).  tors /
+    pairs: verbatim topology to validate (D1.7), as in Docker."""
     tp = np.asarray(type_params, dtype=np.float32).reshape(-1, 4)
     tarr = (TypeParam * tp.shape[0])()
     for k in range(tp.shape[0]):
         tarr[k] = TypeParam(*(float(v) for v in tp[k]), int(roles[k]))
-    lg = Ligand()
-    lg.n_atoms = t.shape[0]; lg.type = _ptr(t, C.c_int32); lg.charge = _ptr(q, C.c_float)
-    lg.xyz = _ptr(x, C.c_float); lg.n_bonds = b.shape[0] // 2
-    lg.bonds = _ptr(b, C.c_int32) if lg.n_bonds else None
-    lg.rotatable = _ptr(r, C.c_uint8) if lg.n_bonds else None
-    N = t.shape[0]
+    lg, keep = _ligand_struct(types, charges, xyz, bonds, rotatable, tors, pairs)
+    N = lg.n_atoms
     cap = max(1, N * (N - 1) // 2)
     T = C.c_int32(0); Pn = C.c_int32(0)
-    axis = np.zeros(64, np.int32); moved = np.zeros(32 * N, np.uint8); pairs = np.zeros(2 * cap, np.int32)
+    axis = np.zeros(64, np.int32); moved = np.zeros(32 * N, np.uint8); pairs_out = np.zeros(2 * cap, np.int32)
     _check(lib.dock_topology(C.byref(lg), tarr, tp.shape[0], C.byref(T), _ptr(axis, C.c_int32),
-                             _ptr(moved, C.c_uint8), C.byref(Pn), _ptr(pairs, C.c_int32), cap))
+                             _ptr(moved, C.c_uint8), C.byref(Pn), _ptr(pairs_out, C.c_int32), cap))
     return (axis[: 2 * T.value].reshape(-1, 2), moved[: T.value * N].reshape(T.value, N),
-            pairs[: 2 * Pn.value].reshape(-1, 2))
+            pairs_out[: 2 * Pn.value].reshape(-1, 2))
 
 
 def _ptr(a, ct):
@@ -313,17 +352,10 @@ def screen(grid, ligands, pop, runs, max_evals, seed, ligand_ids=None, devices=N
     keep = []
     larr = (Ligand * max(n, 1))()
     for i, lig in enumerate(ligands):
-        t = np.ascontiguousarray(lig.types, dtype=np.int32)
-        q = np.ascontiguousarray(lig.charges, dtype=np.float32)
-        x = np.ascontiguousarray(lig.xyz, dtype=np.float32).reshape(-1)
-        b = np.ascontiguousarray(lig.bonds, dtype=np.int32).reshape(-1)
-        r = np.ascontiguousarray(lig.rotatable, dtype=np.uint8)
-        keep.append((t, q, x, b, r))
-        L = larr[i]
-        L.n_atoms = t.shape[0]; L.type = _ptr(t, C.c_int32); L.charge = _ptr(q, C.c_float)
-        L.xyz = _ptr(x, C.c_float); L.n_bonds = b.shape[0] // 2
-        L.bonds = _ptr(b, C.c_int32) if L.n_bonds else None
-        L.rotatable = _ptr(r, C.c_uint8) if L.n_bonds else None
+        lg, kp = _ligand_struct(lig.types, lig.charges, lig.xyz, lig.bonds, lig.rotatable,
+                                getattr(lig, "tors", None), getattr(lig, "pairs", None))
+        keep.append(kp)
+        larr[i] = lg
     ids = None if ligand_ids is None else np.ascontiguousarray(ligand_ids, dtype=np.uint32)
     if params is None:
         params = params_default(**overrides)
@@ -356,34 +388,32 @@ class Docker:
     """One (device, receptor grid, ligand) docking context (dock_init ... dock_free)."""
 
     def __init__(self, maps, n, spacing, origin, type_params, roles, types, charges, xyz, bonds,
-                 rotatable, params: Params | None = None, **overrides):
+                 rotatable, params: Params | None = None, tors=None, pairs=None, type_names=None, **overrides):
+        """type_params None: the built-in table by type_names (dock_init with NULL type_params);
+        tors = (axis [T, 2], moved index lists) and / or pairs [P, 2]: verbatim topology."""
         maps = np.ascontiguousarray(maps, dtype=np.float32).reshape(-1)
         n = tuple(int(v) for v in n)
-        tp = np.asarray(type_params, dtype=np.float32).reshape(-1, 4)
-        roles = np.asarray(roles, dtype=np.int32).reshape(-1)
         g = Grids()
         g.nx, g.ny, g.nz = n
         g.spacing = float(spacing)
         for d in range(3):
             g.origin[d] = float(origin[d])
-        g.n_types = tp.shape[0]
         g.maps = _ptr(maps, C.c_float)
-        tarr = (TypeParam * tp.shape[0])()
-        for t in range(tp.shape[0]):
-            tarr[t] = TypeParam(*(float(x) for x in tp[t]), int(roles[t]))
-        self._types = np.ascontiguousarray(types, dtype=np.int32)
-        self._charges = np.ascontiguousarray(charges, dtype=np.float32)
-        self._xyz = np.ascontiguousarray(xyz, dtype=np.float32).reshape(-1)
-        self._bonds = np.ascontiguousarray(bonds, dtype=np.int32).reshape(-1)
-        self._rot = np.ascontiguousarray(rotatable, dtype=np.uint8)
-        lg = Ligand()
-        lg.n_atoms = self._types.shape[0]
-        lg.type = _ptr(self._types, C.c_int32)
-        lg.charge = _ptr(self._charges, C.c_float)
-        lg.xyz = _ptr(self._xyz, C.c_float)
-        lg.n_bonds = self._bonds.shape[0] // 2
-        lg.bonds = _ptr(self._bonds, C.c_int32) if lg.n_bonds else None
-        lg.rotatable = _ptr(self._rot, C.c_uint8) if lg.n_bonds else None
+        self._names = _names_array(type_names)
+        g.type_names = C.cast(self._names, C.POINTER(C.c_char * 4)) if self._names is not None else None
+        if type_params is None:
+            if type_names is None:
+                raise DockError(DOCK_E_INPUT, "type_params None needs type_names (the built-in table)")
+            g.n_types = len(type_names)
+            tarr = None
+        else:
+            tp = np.asarray(type_params, dtype=np.float32).reshape(-1, 4)
+            roles = np.asarray(roles, dtype=np.int32).reshape(-1)
+            g.n_types = tp.shape[0]
+            tarr = (TypeParam * tp.shape[0])()
+            for t in range(tp.shape[0]):
+                tarr[t] = TypeParam(*(float(x) for x in tp[t]), int(roles[t]))
+        lg, self._keep = _ligand_struct(types, charges, xyz, bonds, rotatable, tors, pairs)
         if params is None:
             params = params_default(**overrides)
         else:

@@ -368,10 +368,12 @@ int dock_init(const dock_grids *grids, const dock_type_param *type_params, const
         Trace tr("init.pack_grid");
         if (dk::pack_grid(grids, &packed, &err) != DOCK_OK) { g_init_error = err; return DOCK_E_INPUT; }
     }
+    std::vector<dock_type_param> tparams;
+    if (dk::resolve_type_params(grids, type_params, &tparams, &err) != DOCK_OK) { g_init_error = err; return DOCK_E_INPUT; }
     dk::Prepared prep;
     {
         Trace tr("init.prepare_ligand");
-        if (dk::prepare_ligand(ligand, type_params, grids->n_types, dk::scoring_of(p), &prep, &err) != DOCK_OK) { g_init_error = err; return DOCK_E_INPUT; }
+        if (dk::prepare_ligand(ligand, tparams.data(), grids->n_types, dk::scoring_of(p), &prep, &err) != DOCK_OK) { g_init_error = err; return DOCK_E_INPUT; }
     }
     int ndev = 0;
     if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev < 1) {

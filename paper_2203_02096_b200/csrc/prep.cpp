@@ -37,28 +37,21 @@ Scoring scoring_of(const dock_params &p) {
     return s;
 }
 
-int prepare_ligand(const dock_ligand *l, const dock_type_param *tp, int n_types, const Scoring &sf, Prepared *out,
-                   std::string *err) {
+struct Tor { int a, b, depth; };
+
+// D1 outputs shared by both topology modes (DFS numbering: every moved set is one range).
+struct Topo {
+    std::vector<Tor> tors;                     // torsion order of the genotype
+    std::vector<int> order, pos;               // dfs position -> caller atom, and back
+    std::vector<int> lo, hi, parent;           // per torsion: moved range [lo, hi), parent torsion
+    std::vector<int> deep;                     // per dfs position: innermost torsion (-1: root)
+    std::vector<int> pairs;                    // [P*2] caller atom indices, i < j
+};
+
+// Derived mode (D1.1-D1.6): union-find, Tarjan bridges, BFS orientation, DFS preorder.
+int derive_topology(const dock_ligand *l, Topo &tp, std::string *err) {
     auto fail = [&](const std::string &m) { *err = m; return (int)DOCK_E_INPUT; };
-    if (!l) return fail("ligand: NULL");
     const int N = l->n_atoms;
-    if (N < 1 || N > kMaxAtoms) return fail("ligand.n_atoms: must be in 1..256");
-    if (!l->type || !l->charge || !l->xyz) return fail("ligand.type/charge/xyz: NULL");
-    if (l->n_bonds < 0 || (l->n_bonds > 0 && !l->bonds)) return fail("ligand.bonds: NULL or negative count");
-    if (!tp || n_types < 1) return fail("type_params: NULL");
-    for (int t = 0; t < n_types; ++t) {
-        const dock_type_param &q = tp[t];
-        if (!std::isfinite(q.R) || !std::isfinite(q.eps) || !std::isfinite(q.S) || !std::isfinite(q.V) ||
-            q.R < 0.f || q.eps < 0.f || q.role < 0 || q.role > 2)
-            return fail("type_params[" + std::to_string(t) + "]: non-finite, negative or bad role");
-    }
-    for (int a = 0; a < N; ++a) {
-        if (l->type[a] < 0 || l->type[a] >= n_types)
-            return fail("ligand.type[" + std::to_string(a) + "]: no grid map for this type");
-        if (!std::isfinite(l->charge[a])) return fail("ligand.charge[" + std::to_string(a) + "]: non-finite");
-        for (int d = 0; d < 3; ++d)
-            if (!std::isfinite(l->xyz[3 * a + d])) return fail("ligand.xyz[" + std::to_string(a) + "]: non-finite");
-    }
     // ---- bond graph ----
     const int B = l->n_bonds;
     std::vector<std::vector<std::pair<int, int>>> adj(N);   // (neighbour, edge id)
@@ -134,7 +127,6 @@ int prepare_ligand(const dock_ligand *l, const dock_type_param *tp, int n_types,
                 if (bpar[w] == -2) { bpar[w] = u; rotdepth[w] = rotdepth[u] + (is_rot(e) ? 1 : 0); q.push_back(w); }
         }
     }
-    struct Tor { int a, b, depth; };
     std::vector<Tor> tors;
     for (int e = 0; e < B; ++e) {
         if (!is_rot(e)) continue;
@@ -198,6 +190,163 @@ int prepare_ligand(const dock_ligand *l, const dock_type_param *tp, int n_types,
                 if (mark[j] != i && frag[i] != frag[j]) { pairs.push_back(i); pairs.push_back(j); }
         }
     }
+    tp.tors = std::move(tors);
+    tp.order = std::move(order); tp.pos = std::move(pos);
+    tp.lo = std::move(lo); tp.hi = std::move(hi); tp.parent = std::move(parent);
+    tp.deep = std::move(deep); tp.pairs = std::move(pairs);
+    return DOCK_OK;
+}
+
+// Verbatim mode (D1.7): the caller's torsions and pairs, validated.
+// The moved sets form a laminar family; a DFS over it (children in torsion order) gives
+// every moved set one contiguous range, and parent(k) = the nearest earlier torsion whose
+// moved set contains moved(k).
+int verbatim_topology(const dock_ligand *l, Topo &tp, std::string *err) {
+    auto fail = [&](const std::string &m) { *err = m; return (int)DOCK_E_INPUT; };
+    const int N = l->n_atoms, T = l->n_tors;
+    if (T > kMaxTors) return fail("ligand.n_tors: at most 32 torsions");
+    if (l->n_pairs < 0) return fail("ligand.n_pairs: must be >= 0 with verbatim torsions (or both -1)");
+    if (l->rotatable)
+        for (int e = 0; e < l->n_bonds; ++e)
+            if (l->rotatable[e])
+                return fail("ligand.rotatable[" + std::to_string(e) +
+                            "]: must be 0 with verbatim torsions (set n_tors = n_pairs = -1 to derive)");
+    if (T > 0 && (!l->tors_axis || !l->tors_moved_off)) return fail("ligand.tors_axis/tors_moved_off: NULL");
+    std::vector<std::vector<uint8_t>> in(T, std::vector<uint8_t>(N, 0));
+    std::vector<int> size(T, 0);
+    for (int k = 0; k < T; ++k) {
+        const std::string tag = "ligand.torsion[" + std::to_string(k) + "]";
+        const int a = l->tors_axis[2 * k], b = l->tors_axis[2 * k + 1];
+        if (a < 0 || b < 0 || a >= N || b >= N) return fail(tag + ": axis atom out of range");
+        if (a == b) return fail(tag + ": axis atoms equal");
+        const int o0 = l->tors_moved_off[k], o1 = l->tors_moved_off[k + 1];
+        if (o0 < 0 || o1 < o0 || (o1 > o0 && !l->tors_moved)) return fail(tag + ": bad tors_moved_off / NULL tors_moved");
+        for (int q = o0; q < o1; ++q) {
+            const int m = l->tors_moved[q];
+            if (m < 0 || m >= N) return fail(tag + ": moved atom out of range");
+            if (m == a || m == b) return fail(tag + ": moved set contains an axis atom (S:32)");
+            if (in[k][m]) return fail(tag + ": duplicate moved atom " + std::to_string(m));
+            in[k][m] = 1;
+            ++size[k];
+        }
+    }
+    // laminar family, outer sets first, axis consistency (DESIGN.md §3 reading D1.7)
+    auto subset = [&](int x, int y) {   // moved(x) within moved(y)
+        for (int m = 0; m < N; ++m) if (in[x][m] && !in[y][m]) return false;
+        return true;
+    };
+    for (int k = 0; k < T; ++k)
+        for (int j = k + 1; j < T; ++j) {
+            const std::string tag = "ligand.torsion[" + std::to_string(j) + "] vs [" + std::to_string(k) + "]";
+            bool meet = false;
+            for (int m = 0; m < N && !meet; ++m) meet = in[k][m] && in[j][m];
+            const bool j_in_k = subset(j, k), k_in_j = subset(k, j);
+            if (meet && !j_in_k && !k_in_j) return fail(tag + ": moved sets neither nested nor disjoint");
+            if (meet && k_in_j && !j_in_k) return fail(tag + ": a nested moved set must come after its parent");
+            const int ak = l->tors_axis[2 * k], bk = l->tors_axis[2 * k + 1];
+            if (in[j][ak] || in[j][bk]) return fail(tag + ": a later torsion moves an earlier torsion's axis");
+            if (meet && j_in_k) {
+                const int aj = l->tors_axis[2 * j], bj = l->tors_axis[2 * j + 1];
+                auto carried = [&](int x) { return in[k][x] || x == ak || x == bk; };
+                if (!carried(aj) || !carried(bj))
+                    return fail(tag + ": the axis of a nested torsion must move with its parent");
+            }
+        }
+    tp.tors.resize(T);
+    tp.parent.assign(T, -1);
+    for (int k = 0; k < T; ++k) {
+        for (int j = k - 1; j >= 0; --j)      // nearest earlier superset (equal sets chain by index)
+            if (size[j] > 0 && subset(k, j) && size[k] > 0 && (tp.parent[k] < 0 || size[j] < size[tp.parent[k]]))
+                tp.parent[k] = j;
+        tp.tors[k].a = l->tors_axis[2 * k];
+        tp.tors[k].b = l->tors_axis[2 * k + 1];
+        tp.tors[k].depth = tp.parent[k] < 0 ? 1 : tp.tors[tp.parent[k]].depth + 1;
+    }
+    // DFS layout: root atoms (in no moved set), then each top-level torsion's subtree: its own
+    // atoms (in no child's set), then its children in torsion order
+    std::vector<std::vector<int>> kids(T);
+    std::vector<int> tops;
+    for (int k = 0; k < T; ++k) (tp.parent[k] < 0 ? tops : kids[tp.parent[k]]).push_back(k);
+    tp.order.clear();
+    tp.lo.assign(T, 0); tp.hi.assign(T, 0);
+    std::vector<uint8_t> placed(N, 0);
+    auto in_any = [&](const std::vector<int> &ks, int m) { for (int k : ks) if (in[k][m]) return true; return false; };
+    for (int m = 0; m < N; ++m)
+        if (!in_any(tops, m)) { tp.order.push_back(m); placed[m] = 1; }
+    std::vector<std::pair<int, int>> st;     // (torsion, 0 = enter / 1 = leave)
+    for (int i = (int)tops.size() - 1; i >= 0; --i) st.push_back({tops[i], 0});
+    while (!st.empty()) {
+        const auto [k, phase] = st.back();
+        st.pop_back();
+        if (phase == 1) { tp.hi[k] = (int)tp.order.size(); continue; }
+        tp.lo[k] = (int)tp.order.size();
+        for (int m = 0; m < N; ++m)
+            if (in[k][m] && !placed[m] && !in_any(kids[k], m)) { tp.order.push_back(m); placed[m] = 1; }
+        st.push_back({k, 1});
+        for (int i = (int)kids[k].size() - 1; i >= 0; --i) st.push_back({kids[k][i], 0});
+    }
+    if ((int)tp.order.size() != N) return fail("internal: verbatim DFS layout");
+    tp.pos.assign(N, -1);
+    for (int p = 0; p < N; ++p) tp.pos[tp.order[p]] = p;
+    for (int k = 0; k < T; ++k) {
+        if (tp.hi[k] - tp.lo[k] != size[k]) return fail("internal: moved set not contiguous");
+        for (int p = tp.lo[k]; p < tp.hi[k]; ++p)
+            if (!in[k][tp.order[p]]) return fail("internal: moved set not contiguous");
+    }
+    tp.deep.assign(N, -1);
+    for (int p = 0; p < N; ++p)                 // innermost = the latest torsion containing it
+        for (int k = 0; k < T; ++k)
+            if (in[k][tp.order[p]]) tp.deep[p] = k;
+    // pairs: as given, each normalised to i < j
+    if (l->n_pairs > 0 && !l->pairs) return fail("ligand.pairs: NULL");
+    std::vector<uint8_t> seen((size_t)N * N, 0);
+    tp.pairs.clear();
+    for (int q = 0; q < l->n_pairs; ++q) {
+        int i = l->pairs[2 * q], j = l->pairs[2 * q + 1];
+        const std::string tag = "ligand.pairs[" + std::to_string(q) + "]";
+        if (i < 0 || j < 0 || i >= N || j >= N) return fail(tag + ": atom index out of range");
+        if (i == j) return fail(tag + ": self pair");
+        if (i > j) std::swap(i, j);
+        if (seen[(size_t)i * N + j]) return fail(tag + ": duplicate pair");
+        seen[(size_t)i * N + j] = 1;
+        tp.pairs.push_back(i); tp.pairs.push_back(j);
+    }
+    return DOCK_OK;
+}
+
+int prepare_ligand(const dock_ligand *l, const dock_type_param *tp, int n_types, const Scoring &sf, Prepared *out,
+                   std::string *err) {
+    auto fail = [&](const std::string &m) { *err = m; return (int)DOCK_E_INPUT; };
+    if (!l) return fail("ligand: NULL");
+    const int N = l->n_atoms;
+    if (N < 1 || N > kMaxAtoms) return fail("ligand.n_atoms: must be in 1..256");
+    if (!l->type || !l->charge || !l->xyz) return fail("ligand.type/charge/xyz: NULL");
+    if (l->n_bonds < 0 || (l->n_bonds > 0 && !l->bonds)) return fail("ligand.bonds: NULL or negative count");
+    if (!tp || n_types < 1) return fail("type_params: NULL");
+    for (int t = 0; t < n_types; ++t) {
+        const dock_type_param &q = tp[t];
+        if (!std::isfinite(q.R) || !std::isfinite(q.eps) || !std::isfinite(q.S) || !std::isfinite(q.V) ||
+            q.R < 0.f || q.eps < 0.f || q.role < 0 || q.role > 2)
+            return fail("type_params[" + std::to_string(t) + "]: non-finite, negative or bad role");
+    }
+    for (int a = 0; a < N; ++a) {
+        if (l->type[a] < 0 || l->type[a] >= n_types)
+            return fail("ligand.type[" + std::to_string(a) + "]: no grid map for this type");
+        if (!std::isfinite(l->charge[a])) return fail("ligand.charge[" + std::to_string(a) + "]: non-finite");
+        for (int d = 0; d < 3; ++d)
+            if (!std::isfinite(l->xyz[3 * a + d])) return fail("ligand.xyz[" + std::to_string(a) + "]: non-finite");
+    }
+    Topo topo;
+    if (l->n_tors >= 0 || l->n_pairs >= 0) {
+        if (l->n_tors < 0) return fail("ligand.n_tors: must be >= 0 with verbatim pairs (or both -1)");
+        if (int rc = verbatim_topology(l, topo, err)) return rc;
+    } else {
+        if (int rc = derive_topology(l, topo, err)) return rc;
+    }
+    const std::vector<Tor> &tors = topo.tors;
+    const int T = (int)tors.size();
+    const std::vector<int> &order = topo.order, &pos = topo.pos, &lo = topo.lo, &hi = topo.hi,
+                           &parent = topo.parent, &deep = topo.deep, &pairs = topo.pairs;
     const int P = (int)pairs.size() / 2;
     if (P > 65535) return fail("ligand: more than 65535 intramolecular pairs");
 
@@ -464,6 +613,34 @@ int prepare_ligand(const dock_ligand *l, const dock_type_param *tp, int n_types,
                               (float)((double)ti.S * tj.V + (double)tj.S * ti.V),
                               (float)(332.06363 / 4.0 * (double)l->charge[i] * (double)l->charge[j]));
     }
+    return DOCK_OK;
+}
+
+int resolve_type_params(const dock_grids *g, const dock_type_param *tp, std::vector<dock_type_param> *out,
+                        std::string *err) {
+    auto fail = [&](const std::string &m) { *err = m; return (int)DOCK_E_INPUT; };
+    if (!g) return fail("grids: NULL");
+    if (g->n_types < 1 || g->n_types > 16) return fail("grids.n_types: must be in 1..16");
+    std::vector<std::string> names;
+    if (g->type_names) {
+        for (int t = 0; t < g->n_types; ++t) {
+            const char *nm = g->type_names[t];
+            const size_t len = strnlen(nm, 4);
+            if (len == 0 || len == 4) return fail("grids.type_names[" + std::to_string(t) + "]: empty or not NUL-terminated");
+            for (const auto &o : names)
+                if (o == std::string(nm, len)) return fail("grids.type_names[" + std::to_string(t) + "]: duplicate '" + o + "'");
+            names.emplace_back(nm, len);
+        }
+    }
+    out->assign(g->n_types, dock_type_param{});
+    if (tp) {
+        std::copy(tp, tp + g->n_types, out->begin());
+        return DOCK_OK;
+    }
+    if (!g->type_names) return fail("type_params: NULL needs grids.type_names (the built-in table is by name)");
+    for (int t = 0; t < g->n_types; ++t)
+        if (dock_builtin_type_param(names[t].c_str(), &(*out)[t]) != DOCK_OK)
+            return fail("grids.type_names[" + std::to_string(t) + "]: no built-in parameters for '" + names[t] + "'");
     return DOCK_OK;
 }
 

@@ -34,6 +34,12 @@ Scoring scoring_of(const dock_params &p);
 int prepare_ligand(const dock_ligand *l, const dock_type_param *tp, int n_types, const Scoring &sf, Prepared *out,
                    std::string *err);
 
+// The per-type parameters of a grid (DESIGN.md §3 D5): `tp` if given, else the built-in
+// table by grids->type_names (dock_builtin_type_param).  Also validates type_names when
+// present (NUL-terminated within 4 chars, non-empty, unique).  DOCK_OK or DOCK_E_INPUT.
+int resolve_type_params(const dock_grids *g, const dock_type_param *tp, std::vector<dock_type_param> *out,
+                        std::string *err);
+
 // Grid validation and packing into one float4 {M_type, M_E, M_D, 0} per (type, node).
 int pack_grid(const dock_grids *g, std::vector<float4> *packed, std::string *err);
 

@@ -58,7 +58,12 @@ extern "C" int dock_screen(const dock_grids *grids, const dock_type_param *type_
     auto fail_input = [](const std::string &m) { g_screen_error = m; return (int)DOCK_E_INPUT; };
     if (n_ligands < 0) return fail_input("n_ligands: must be >= 0");
     if (n_ligands > 0 && (!ligands || !best_energy || !best_genotype)) return fail_input("ligands/best_energy/best_genotype: NULL");
-    if (!type_params) return fail_input("type_params: NULL");
+    std::vector<dock_type_param> tparams;
+    {
+        std::string terr;
+        if (dk::resolve_type_params(grids, type_params, &tparams, &terr) != DOCK_OK) return fail_input(terr);
+    }
+    type_params = tparams.data();   // per-type parameters by value, or the built-in table by name
     if (pop < 2 || pop > 4096) return fail_input("pop_size: must be in 2..4096");
     if (runs < 1) return fail_input("num_runs: must be >= 1");
     if (max_evals < pop) return fail_input("max_evals: must be >= pop_size");

@@ -145,3 +145,25 @@ def test_no_cpu_fallback_without_gpu(dock):
     with pytest.raises(dock.DockError) as e:
         dock.Docker.from_inputs(grid, lig)
     assert e.value.code == dock.DOCK_E_INTERNAL
+
+
+def test_builtin_types_need_names_and_known_names(dock):
+    """dock_init with NULL type_params (SURVEY §8(b)): the built-in table by grids.type_names;
+    missing / unknown / duplicate names are input errors, raised before any device use."""
+    from gen import config_inputs
+    cfg, lig, grid = config_inputs("tiny")
+    with pytest.raises(dock.DockError):
+        dock.Docker(grid.maps, grid.n, grid.spacing, grid.origin, None, None, lig.types, lig.charges, lig.xyz,
+                    lig.bonds, lig.rotatable)
+    bad = list(grid.type_names)
+    bad[0] = "Zz"
+    with pytest.raises(dock.DockError) as e:
+        dock.Docker(grid.maps, grid.n, grid.spacing, grid.origin, None, None, lig.types, lig.charges, lig.xyz,
+                    lig.bonds, lig.rotatable, type_names=bad)
+    assert e.value.code == dock.DOCK_E_INPUT
+    dup = list(grid.type_names)
+    dup[1] = dup[0]
+    tp, roles = grid.type_params()
+    with pytest.raises(dock.DockError):
+        dock.Docker(grid.maps, grid.n, grid.spacing, grid.origin, tp, roles, lig.types, lig.charges, lig.xyz,
+                    lig.bonds, lig.rotatable, type_names=dup)

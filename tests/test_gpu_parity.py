@@ -681,3 +681,34 @@ def test_screen_solis_wets_cluster_engine(dock):
         assert d.run_branches == 4
         assert out["best_E"][i] == np.nanmin(r["best_E"]) and out["evals"][i] == r["evals"].sum()
         d.close()
+
+
+# ---------------------------------------------------------------------------
+# SURVEY §8(b) boundary: a SPEC-format ligand (verbatim torsions + pairs, D1.7; S:30-36,
+# S:91-93) and NULL type_params (the built-in table by the grid's type names).
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("name", ["1stp", "3ce3", "7cpa"])
+def test_spec_style_ligand_verbatim_topology_builtin_types(dock, name):
+    from test_verbatim_topology import spec_style
+    cfg, lig, grid = config_inputs(name)
+    ref = oracle.topology(len(lig.types), lig.bonds, lig.rotatable)
+    axis, moved, pr = spec_style(lig, ref, drop=(1,))
+    topo = oracle.topology_verbatim(len(lig.types), axis, moved, pr)
+    P = oracle.Problem(grid, lig, topo=topo)
+    d = dock.Docker(grid.maps, grid.n, grid.spacing, grid.origin, None, None, lig.types, lig.charges, lig.xyz,
+                    None, None, tors=(axis, moved), pairs=pr, type_names=grid.type_names)
+    assert d.T == P.T == ref["T"] - 1 and d.P == P.P
+    ax, mv = d.torsions()
+    assert np.array_equal(ax, axis) and np.array_equal(mv, topo["moved"])
+    assert np.array_equal(d.pairs(), topo["pairs"])                  # caller order, i < j
+    X = random_genotypes(grid, d.T, 300, seed=77, frac_out=0.05)
+    E, Gd, xyz = d.eval(X, grad=True, xyz=True)
+    c, fails = compare_at_pose(P, grid, X, E, xyz, Gd=Gd)
+    assert_parity(c, fails, f"{name} verbatim topology, built-in types")
+    E0, _, xyz0 = d.eval(X, grad=False, xyz=True)
+    c0, fails0 = compare_at_pose(P, grid, X, E0, xyz0)
+    assert_parity(c0, fails0, f"{name} verbatim topology, energy-only")
+    r = d.run(cfg.pop, 2, 20_000, 42, xyz=True)
+    c1, fails1 = compare_at_pose(P, grid, r["best_genes"], r["best_E"], r["best_xyz"])
+    assert_parity(c1, fails1, f"{name} verbatim topology, run")
+    d.close()
