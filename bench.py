@@ -205,6 +205,36 @@ def oracle_sample(cfg, lig, grid, budget, threads, seed=42):
     return sum(out), dt
 
 
+def cpu_model():
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+def cpu_baseline(cfg, lig, grid, repeats=3):
+    """The oracle as it stands on the host (SURVEY.md §8(d) "CPU oracle baseline"): per core
+    (one run on one thread) and per box (one run per hardware thread, `repeats` times: median
+    and spread), on a bounded sample of the same workload."""
+    threads = os.cpu_count() or 1
+    budget = cpu_budget(cfg)
+    e1, t1 = oracle_sample(cfg, lig, grid, budget, 1)
+    box = []
+    for r in range(repeats):
+        e, t = oracle_sample(cfg, lig, grid, budget, threads, seed=42 + r)
+        box.append(e / t)
+    med = statistics.median(box)
+    return {"value": med, "unit": UNIT, "cores": threads, "kind": "oracle",
+            "per_core": e1 / t1, "box_runs": box, "box_spread": (max(box) - min(box)) / med,
+            "cpu_model": cpu_model(),
+            "sample": f"{threads} runs x {budget} evals of the same workload, one per hardware thread, median of "
+                      f"{repeats}; per_core: one run of {budget} evals on one thread",
+            "note": "double-precision C oracle, gcc -O2, no fast-math: a reported baseline, not the target"}
+
+
 def cpu_budget(cfg):
     # ~2-4 s of one core per run (oracle rates: 1stp 1.6e5, 3ce3 3e4, 7cpa 1e4 evals/s/core)
     return {"tiny": 2000, "1stp": 400_000, "3ce3": 90_000, "7cpa": 30_000}.get(cfg.name, 50_000)
@@ -251,8 +281,15 @@ def run_ours(args, cfg, lig, grid):
                                        ls_max_iters=cfg.ls_iters, profile=prof, device=gpu, sw_depth=args.sw_depth,
                                        scoring=SCORING, sw_split=args.sw_split)
     d = make(1)          # profiled context (CUDA events around the LS launches)
-    runs = cfg.runs
-    run_base = rank * runs
+    # the config's R runs are split contiguously over the ranks, rank k docks
+    # global runs [kR/G, (k+1)R/G) (strong scaling; the Philox counter carries the global run
+    # index, so the results equal the 1-GPU run's).  --weak: every rank docks R runs of its own.
+    total_runs = cfg.runs * world if args.weak else cfg.runs
+    run_base = rank * cfg.runs if args.weak else rank * total_runs // world
+    runs = cfg.runs if args.weak else (rank + 1) * total_runs // world - run_base
+    rmax = -(-total_runs // world)                  # gather rows per rank (padded)
+    if runs < 1:
+        raise SystemExit(f"rank {rank}: no runs ({total_runs} runs over {world} ranks); use fewer GPUs or --runs")
     stream = torch.cuda.Stream(device=dev)
     bE = torch.empty(runs, dtype=torch.float32, device=dev)
     bG = torch.empty(runs, d.G, dtype=torch.float32, device=dev)
@@ -267,9 +304,12 @@ def run_ours(args, cfg, lig, grid):
         with torch.cuda.stream(stream):
             (ctx or d).run_device(cfg.pop, runs, cfg.max_evals, seed, bE, bG, ev, gens, run_base=run_base,
                                   stream=stream.cuda_stream)
-            if world > 1:   # NS: NCCL only for the final gather of best poses
-                gathered["E"] = all_gather_cat(bE, cdev)
-                gathered["G"] = all_gather_cat(bG, cdev)
+            if world > 1:   # NS: NCCL only for the final gather of best poses (rows padded to rmax)
+                pE = torch.full((rmax,), float("nan"), dtype=torch.float32, device=dev)
+                pG = torch.zeros(rmax, d.G, dtype=torch.float32, device=dev)
+                pE[:runs] = bE; pG[:runs] = bG
+                gathered["E"] = all_gather_cat(pE, cdev)
+                gathered["G"] = all_gather_cat(pG, cdev)
 
     for w in range(args.warmup):
         step(42)
@@ -391,27 +431,42 @@ def run_ours(args, cfg, lig, grid):
         e2e_evals = int(reduce_scalar(e2e_evals, torch.int64, dist.ReduceOp.SUM, cdev))
     e2e_value = e2e_evals / e2e_t
 
+    # digest of every run's best energy and genotype (all ranks' runs, global run order): equal
+    # at any rank count (the R split) -- tests/test_gpu_multirank.py compares 1 and 2 ranks
+    import hashlib
+    if world > 1:
+        gE = gathered["E"].cpu().numpy().reshape(world, rmax)
+        gG = gathered["G"].cpu().numpy().reshape(world, rmax, d.G)
+        cnt = [(k + 1) * total_runs // world - k * total_runs // world for k in range(world)] if not args.weak \
+            else [runs] * world
+        allE = np.concatenate([gE[k, :cnt[k]] for k in range(world)])
+        allG = np.concatenate([gG[k, :cnt[k]] for k in range(world)])
+    else:
+        allE, allG = bE.cpu().numpy(), bG.cpu().numpy()
+    result_digest = hashlib.sha256(allE.astype(np.float32).tobytes() + allG.astype(np.float32).tobytes()).hexdigest()[:16]
+
     line = None
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
-                "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+                "scaling": "weak" if args.weak else "strong", "vs_baseline": None, "dtype": "f32",
                 "data": "synthetic (gen/synth.py, seeded ligand + pseudo-receptor maps)",
-                "config": {"workload": workload_desc(cfg), "runs_per_gpu": runs, "global_runs": runs * world,
+                "config": {"workload": workload_desc(cfg), "runs_per_gpu": runs if args.weak else rmax,
+                           "global_runs": total_runs,
                            "l2": "flushed between steps (256 MiB write); grid pinned by an L2 access window",
-                           "parallelism": f"dp{world} (independent runs per GPU)"},
-                "ligands_per_hour": 3600.0 * world / (ms_per_step / 1e3),
+                           "parallelism": (f"dp{world} (every rank its own {cfg.runs} runs, global run ids)" if args.weak
+                                           else f"dp{world} (rank k docks runs [kR/G, (k+1)R/G) of R = {total_runs})")},
+                "ligands_per_hour": 3600.0 * (world if args.weak else 1) / (ms_per_step / 1e3),
+                "result_digest": result_digest,
                 "gpu_launches": launches,
                 "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                         "note": "dock_init (host grid+ligand upload) + dock_run_ex (host outputs) + dock_free, wall clock"},
                 "roofline": roofline,
                 "clocks": clk}
+        if world == 1 and not args.no_parts:
+            line["roofline_parts"] = parts_roofline(d, cfg, grid, dev)
         if world == 1 and not args.no_cpu:
-            threads = os.cpu_count() or 1
-            budget = cpu_budget(cfg)
-            ce, ct = oracle_sample(cfg, lig, grid, budget, threads)
-            line["cpu_baseline"] = {"value": ce / ct, "unit": UNIT, "cores": threads, "kind": "oracle",
-                                    "sample": f"{threads} runs x {budget} evals of the same workload, one per thread"}
+            line["cpu_baseline"] = cpu_baseline(cfg, lig, grid)
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()
@@ -556,60 +611,61 @@ def run_hts(args, cfg, grid):
 
 
 # ---------------------------------------------------------------------------
-# --micro: the two isolated parts of an evaluation for roofline evidence
+# The two isolated parts of an evaluation (SURVEY.md §8(d) "isolating the two kernels for
+# ncu"): k_bench_part inter (pose + trilinear E+G) and intra (pose + pair tiles E+forces) on
+# the config's population, each against its own roofline: the interpolation against the
+# measured L2 gather ceiling (k_l2_gather: random 16-byte __ldg over a resident buffer the
+# size of the grid), the pair tiles against the FP32 peak.
 # ---------------------------------------------------------------------------
-def run_micro(args, cfg, lig, grid):
+def parts_roofline(d, cfg, grid, dev, reps=3, iters=5):
     import numpy as np
     import torch
     import paper_2203_02096_b200 as dock
     from gen import random_genotypes
-
-    dev = torch.device("cuda", 0)
-    d = dock.Docker.from_inputs(grid, lig, ls_method=0, scoring=SCORING)
     n = cfg.runs * cfg.pop
     X = torch.from_numpy(random_genotypes(grid, d.T, n, seed=5, frac_out=0.0, shrink=0.2)).to(dev)
     out = torch.empty(n, dtype=torch.float32, device=dev)
     st = torch.cuda.Stream(device=dev)
-    iters = args.micro_iters
     res = {}
     for part, name in ((0, "inter"), (1, "intra")):
         with torch.cuda.stream(st):
-            for _ in range(2):
-                d.bench_part(part, X, out, iters, stream=st.cuda_stream)
+            d.bench_part(part, X, out, iters, stream=st.cuda_stream)
             e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
             e0.record(st)
-            for _ in range(args.steps):
+            for _ in range(reps):
                 d.bench_part(part, X, out, iters, stream=st.cuda_stream)
             e1.record(st)
         torch.cuda.synchronize()
-        res[name] = e0.elapsed_time(e1) / args.steps / 1e3
-    # L2 streaming-read reference: a 48 MiB resident buffer summed repeatedly (torch)
-    buf = torch.ones(12 * 1024 * 1024, dtype=torch.float32, device=dev)
-    for _ in range(3):
-        buf.sum()
-    e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
-    e0.record()
-    for _ in range(50):
-        buf.sum()
-    e1.record()
-    torch.cuda.synchronize()
-    l2_gbs = 50 * buf.numel() * 4 / (e0.elapsed_time(e1) / 1e3) / 1e9
+        res[name] = e0.elapsed_time(e1) / reps / 1e3
+    grid_mib = max(16, int(np.ceil(grid.maps.nbytes * 4 / 3 / 2 ** 20)))   # the packed float4 grid
+    l2_gbs, _ = dock.bench_l2_gather(dev.index, grid_mib, 8, 64)
     peaks = measured_peaks()
     sm_mhz = float(peaks.get("sm_max_mhz", 1965.0))
     lookups = n * iters * d.N
-    t_in = res["inter"]
-    pair_steps = n * iters * d.P
-    t_pr = res["intra"]
-    fl = pair_steps * (F_PAIR_AD4 if SCORING else F_PAIR)[1] / t_pr / 1e12
-    line = {"metric": "microbench", "config": {"workload": workload_desc(cfg), "genotypes": n, "iters": iters},
-            "inter": {"kernel": "k_bench_part<kInter> (pose + trilinear E+G)", "ms": 1e3 * t_in,
-                      "atom_lookups_per_s": lookups / t_in,
-                      "algorithmic_GBps_96B": 96 * lookups / t_in / 1e9,
-                      "moved_GBps_128B": 128 * lookups / t_in / 1e9,
-                      "hbm_peak_GBps": peaks.get("hbm_gbs"), "l2_stream_read_ref_GBps": l2_gbs},
-            "intra": {"kernel": "k_bench_part<kIntra> (pose + pair tiles E+forces)", "ms": 1e3 * t_pr,
-                      "pairs_per_s": pair_steps / t_pr, "tflops_model": fl,
-                      "fp32_peak_tflops": fp32_peak_tflops(sm_mhz), "frac": fl / fp32_peak_tflops(sm_mhz)}}
+    alg = 96 * lookups / res["inter"] / 1e9
+    pairs = n * iters * d.P
+    fl = pairs * (F_PAIR_AD4 if SCORING else F_PAIR)[1] / res["intra"] / 1e12
+    pk = fp32_peak_tflops(sm_mhz)
+    return {"inter": {"kernel": "k_bench_part<kInter> (pose + trilinear E+G; 8 float4 corner __ldg per atom)",
+                      "ms": 1e3 * res["inter"], "atom_lookups_per_s": lookups / res["inter"],
+                      "algorithmic_GBps_96B": alg, "moved_GBps_128B": 128 * lookups / res["inter"] / 1e9,
+                      "l2_gather_ceiling_GBps": l2_gbs, "l2_gather_buffer_MiB": grid_mib,
+                      "frac_of_l2_gather": 128 * lookups / res["inter"] / 1e9 / l2_gbs,
+                      "hbm_peak_GBps": peaks.get("hbm_gbs"),
+                      "note": "fraction = moved bytes (128 B: 8 float4 corners) / the measured random-gather ceiling"},
+            "intra": {"kernel": "k_bench_part<kIntra> (pose + pair tiles E+forces)", "ms": 1e3 * res["intra"],
+                      "pairs_per_s": pairs / res["intra"], "tflops_8d_model": fl, "fp32_peak_tflops": pk,
+                      "frac": fl / pk, "flop_per_pair": (F_PAIR_AD4 if SCORING else F_PAIR)[1]}}
+
+
+def run_micro(args, cfg, lig, grid):
+    import torch
+    import paper_2203_02096_b200 as dock
+    dev = torch.device("cuda", 0)
+    d = dock.Docker.from_inputs(grid, lig, ls_method=0, scoring=SCORING)
+    line = {"metric": "microbench", "config": {"workload": workload_desc(cfg), "genotypes": cfg.runs * cfg.pop,
+                                               "iters": args.micro_iters}}
+    line.update(parts_roofline(d, cfg, grid, dev, reps=args.steps, iters=args.micro_iters))
     print(json.dumps(line), flush=True)
     d.close()
 
@@ -630,6 +686,8 @@ def main():
     ap.add_argument("--slots", type=int, default=4, help="hts: ligands in flight per GPU")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--no-parts", action="store_true", help="skip the inter / intra / L2-gather roofline parts")
+    ap.add_argument("--weak", action="store_true", help="N > 1: every rank docks the config's runs (default: split them)")
     ap.add_argument("--scoring", default="d5", choices=["d5", "ad4"],
                     help="intramolecular scoring: D5 (default) or the NEXT-2 AD4.1-calibrated variant")
     args = ap.parse_args()

@@ -219,6 +219,14 @@ int dock_eval_terms(dock_ctx *ctx, int32_t n, const float *genotypes, float *int
 int dock_bench_part(dock_ctx *ctx, int32_t part, int32_t n, int32_t iters, const float *d_genotypes,
                     float *d_out, void *stream);
 
+/* The L2 gather ceiling of the interpolation (SURVEY.md §8(d) "random 16 B gathers over a
+   resident 16-64 MiB buffer"): k_l2_gather on `device` over a buffer of `mib` MiB, 148 x
+   `blocks_per_sm` CTAs of 256 threads, each thread `iters` rounds of 8 independent random
+   16-byte __ldg loads.  After one warm-up launch (the buffer is then L2-resident), the
+   timed launch (CUDA events) gives *gbps = 16 B x loads / time and *ms.  Synchronous. */
+int dock_bench_l2_gather(int32_t device, int32_t mib, int32_t blocks_per_sm, int32_t iters, double *gbps,
+                         double *ms);
+
 /* D1 on the host, without a device (runs the same preprocessing as dock_init):
    *n_tors, axis [T*2] (a on the root side), moved [T*n_atoms], *n_pairs, pairs [P*2]
    (lexicographic, caller indices).  pair_cap = capacity of `pairs` in pairs; returns

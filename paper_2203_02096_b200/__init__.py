@@ -160,6 +160,7 @@ def _load():
         "dock_stream_words": (i32, [u64, u32, u32, u32, u32, u32, u32, i32, P(u32)]),
         "dock_ga_step": (i32, [v, u64, u32, i32, i32, i32, P(f), P(f), P(f), P(f), P(i32), P(i32)]),
         "dock_init_population": (i32, [v, i32, i32, i32, u32, u64, P(f), P(f)]),
+        "dock_bench_l2_gather": (i32, [i32, i32, i32, i32, P(C.c_double), P(C.c_double)]),
         "dock_ad_trace": (i32, [v, i32, i32, P(f), P(f), P(f), P(i64), P(f), P(f), P(f)]),
         "dock_sw_trace": (i32, [v, i32, i32, u64, u32, i32, i32, P(i32), P(f), P(f), P(f), P(i64), P(i32), P(f)]),
         "dock_ls_step": (i32, [v, i32, i32, i32, u64, u32, i32, i32, P(i32), P(f), P(f), P(i64)]),
@@ -190,7 +191,7 @@ EXPORTED = ("dock_params_default", "dock_builtin_type_param", "dock_init", "dock
             "dock_topology", "dock_kernel_stats", "dock_upload_bytes", "dock_screen", "dock_screen_last_error",
             "dock_bench_part", "dock_eval_terms", "dock_cluster", "dock_write_result", "dock_run_branches",
             "dock_write_screen", "dock_last_engine", "dock_init_population", "dock_sw_trace",
-            "dock_ad_trace")
+            "dock_ad_trace", "dock_bench_l2_gather")
 
 
 def write_result(res: dict, fmt: str = "json", timings: dict | None = None) -> str:
@@ -300,6 +301,13 @@ def builtin_type_param(name: str) -> TypeParam:
     t = TypeParam()
     _check(lib.dock_builtin_type_param(name.encode(), C.byref(t)))
     return t
+
+
+def bench_l2_gather(device=0, mib=48, blocks_per_sm=8, iters=64):
+    """L2 gather ceiling (dock_bench_l2_gather): (GB/s of random 16-byte loads, ms)."""
+    g = C.c_double(0); t = C.c_double(0)
+    _check(lib.dock_bench_l2_gather(device, mib, blocks_per_sm, iters, C.byref(g), C.byref(t)))
+    return g.value, t.value
 
 
 def philox(ctr, key):

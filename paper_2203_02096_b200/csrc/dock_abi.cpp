@@ -788,6 +788,39 @@ int dock_cluster(dock_ctx *c, int32_t n, const float *xyz, const float *energy, 
     return DOCK_OK;
 }
 
+int dock_bench_l2_gather(int32_t device, int32_t mib, int32_t blocks_per_sm, int32_t iters, double *gbps, double *ms) {
+    if (mib < 1 || mib > 4096 || blocks_per_sm < 1 || iters < 1 || !gbps) {
+        g_init_error = "bench_l2_gather: mib 1..4096, blocks_per_sm >= 1, iters >= 1, gbps non-NULL";
+        return DOCK_E_INPUT;
+    }
+    dock_ctx tmp;
+    dock_ctx *c = &tmp;
+    c->device = device;
+    CK(cudaSetDevice(device));
+    int nsm = 148;
+    CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device));
+    const size_t n = (size_t)mib * (1u << 20) / 16;
+    DevBuf buf(c->stream), out(c->stream);
+    CK(buf.alloc(n * 16));
+    CK(out.alloc((size_t)nsm * blocks_per_sm * 256 * 4));
+    CK(cudaMemsetAsync(buf.p, 0, n * 16, c->stream));
+    const int blocks = nsm * blocks_per_sm;
+    cudaEvent_t e0, e1;
+    CK(cudaEventCreate(&e0));
+    CK(cudaEventCreate(&e1));
+    CK(dk::launch_l2_gather((const float4 *)buf.p, (uint32_t)n, blocks, iters, (float *)out.p, c->stream));   // warm-up
+    CK(cudaEventRecord(e0, c->stream));
+    CK(dk::launch_l2_gather((const float4 *)buf.p, (uint32_t)n, blocks, iters, (float *)out.p, c->stream));
+    CK(cudaEventRecord(e1, c->stream));
+    CK(cudaEventSynchronize(e1));
+    float t = 0.f;
+    CK(cudaEventElapsedTime(&t, e0, e1));
+    cudaEventDestroy(e0); cudaEventDestroy(e1);
+    *gbps = 16.0 * 8.0 * (double)blocks * 256 * iters / (t * 1e-3) / 1e9;
+    if (ms) *ms = t;
+    return DOCK_OK;
+}
+
 int dock_topology(const dock_ligand *ligand, const dock_type_param *type_params, int32_t n_types, int32_t *n_tors,
                   int32_t *axis, uint8_t *moved, int32_t *n_pairs, int32_t *pairs, int32_t pair_cap) {
     dk::Prepared p;

@@ -1013,6 +1013,28 @@ __global__ void k_philox(int n, const uint4 *ctr, const uint2 *key, uint4 *out) 
     if (i < n) out[i] = philox4x32_10(ctr[i], key[i]);
 }
 
+// k_l2_gather: the L2 gather ceiling of the interpolation kernel: every
+// thread issues `iters` rounds of 8 independent random 16-byte loads (__ldg, the corner-
+// fetch instruction of inter_atom) over a device-resident buffer of n float4 that fits L2.
+// Index: a multiplicative hash of (thread, round, corner).  The checksum keeps the loads live.
+__global__ void __launch_bounds__(256) k_l2_gather(const float4 *__restrict__ buf, uint32_t n, int iters,
+                                                   float *out) {
+    const uint32_t tid = blockIdx.x * blockDim.x + threadIdx.x;
+    float acc = 0.f;
+    uint32_t h = tid * 0x9E3779B9u + 0x7F4A7C15u;
+    for (int it = 0; it < iters; ++it) {
+        float4 v[8];
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+            h = h * 1664525u + 1013904223u;
+            v[c] = __ldg(buf + (uint32_t)(((uint64_t)h * n) >> 32));
+        }
+#pragma unroll
+        for (int c = 0; c < 8; ++c) acc += v[c].x + v[c].y + v[c].z + v[c].w;
+    }
+    if (acc == 1234.5f) out[tid] = acc;
+}
+
 __global__ void k_stream_words(uint2 key, uint32_t purpose, uint32_t slot, uint32_t gen, uint32_t run,
                                uint32_t m0, int n, uint32_t *out) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -1409,6 +1431,11 @@ cudaError_t launch_philox(int n, const uint32_t *ctr, const uint32_t *key, uint3
     if (n <= 0) return cudaSuccess;
     k_philox<<<ceil_div(n, 128), 128, 0, s>>>(n, reinterpret_cast<const uint4 *>(ctr),
                                               reinterpret_cast<const uint2 *>(key), reinterpret_cast<uint4 *>(out));
+    return cudaGetLastError();
+}
+
+cudaError_t launch_l2_gather(const float4 *buf, uint32_t n, int blocks, int iters, float *out, cudaStream_t s) {
+    k_l2_gather<<<blocks, 256, 0, s>>>(buf, n, iters, out);
     return cudaGetLastError();
 }
 

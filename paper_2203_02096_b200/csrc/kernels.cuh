@@ -69,6 +69,7 @@ struct GroupCfg {
     cudaError_t launch_best(const LigDev &L, const SearchDev &sp, const PopDev &pop, float *bestE,           \
                             float *bestG, long long *evals, int *gens, cudaStream_t s);                      \
     cudaError_t launch_philox(int n, const uint32_t *ctr, const uint32_t *key, uint32_t *out, cudaStream_t s); \
+    cudaError_t launch_l2_gather(const float4 *buf, uint32_t n, int blocks, int iters, float *out, cudaStream_t s); \
     cudaError_t launch_stream_words(uint32_t k0, uint32_t k1, uint32_t purpose, uint32_t slot, uint32_t gen, \
                                     uint32_t run, uint32_t m0, int n, uint32_t *out, cudaStream_t s);
 namespace d5 { DK_LAUNCHER_DECLS }
@@ -128,6 +129,9 @@ inline cudaError_t launch_best(const LigDev &L, const SearchDev &sp, const PopDe
 }
 inline cudaError_t launch_philox(int n, const uint32_t *ctr, const uint32_t *key, uint32_t *out, cudaStream_t s) {
     return d5::launch_philox(n, ctr, key, out, s);
+}
+inline cudaError_t launch_l2_gather(const float4 *buf, uint32_t n, int blocks, int iters, float *out, cudaStream_t s) {
+    return d5::launch_l2_gather(buf, n, blocks, iters, out, s);
 }
 inline cudaError_t launch_stream_words(uint32_t k0, uint32_t k1, uint32_t purpose, uint32_t slot, uint32_t gen,
                                        uint32_t run, uint32_t m0, int n, uint32_t *out, cudaStream_t s) {

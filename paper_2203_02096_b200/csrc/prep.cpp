@@ -420,7 +420,8 @@ int prepare_ligand(const dock_ligand *l, const dock_type_param *tp, int n_types,
         const int Bt_ = Bf + L.tail_rot;
         const int steps = Bt_ * (Wg / 2) + (Bt_ * (Bt_ - 1) / 2) * Wg;
         int extra = 0;
-        if (tail > 0 && !L.tail_rot) extra = L.tail_seg ? (Bf * tpw + seg_rounds) * Wg : tail * (Bf + 1) * Wg;
+        if (tail > 0 && !L.tail_rot)
+            extra = L.tail_seg ? (Bf * tpw + seg_rounds) * Wg : tail * (Bf + 1) * Wg;
         return steps * Wg + extra;
     };
     L.n_slots = slot_count();
@@ -432,7 +433,12 @@ int prepare_ligand(const dock_ligand *l, const dock_type_param *tp, int n_types,
     }
     const int Bt = Bf + L.tail_rot;
     L.off_slot4 = off; off += L.slot_mode ? 16 * L.n_slots : 0;
-    L.off_slotq = off; off += L.slot_mode ? a16(4 * L.n_slots) : 0;
+#if defined(DK_FOLD) && !DK_FOLD
+    const bool sep_q = true;                   // A/B build: the unfolded {r_eq^2, A, B, SV} + qq tables
+#else
+    const bool sep_q = ad4;                    // D5 folds qq into slot4
+#endif
+    L.off_slotq = off; off += (L.slot_mode && sep_q) ? a16(4 * L.n_slots) : 0;
     L.grad_bytes = off;              // the gradient kernels stage only up to here
     // Energy-only kernels stage the pair list + per-pair constants (20 B per pair) when it
     // fits comfortably in shared memory; beyond that (P > ~4,900, e.g. N >= ~110) they use
@@ -519,7 +525,7 @@ int prepare_ligand(const dock_ligand *l, const dock_type_param *tp, int n_types,
             // a non-pair slot contributes exactly 0 (A = B = SV = qq = 0); under D5-AD4 its
             // r_eq operand is 1 Å so the smoothed distance stays >= 0.26 Å (x^2 finite, 0 * x^12 = 0)
             s4[slot] = make_float4(ad4 ? 1.f : 0.f, 0.f, 0.f, 0.f);
-            sq[slot] = 0.f;
+            if (sep_q) sq[slot] = 0.f;
             if (!on || da >= N || db >= N || !is_pair[(size_t)da * N + db]) return;
             const int ia = order[da], ib = order[db];
             const dock_type_param &ta = tp[l->type[ia]], &tb = tp[l->type[ib]];
@@ -533,10 +539,20 @@ int prepare_ligand(const dock_ligand *l, const dock_type_param *tp, int n_types,
                 sq[slot] = (float)(sf.w_el * 332.06363 * (double)l->charge[ia] * (double)l->charge[ib]);
                 return;
             }
+#if defined(DK_FOLD) && !DK_FOLD
             s4[slot] = make_float4((float)(req * req), (float)((hb ? 5.0 : 1.0) * eps),
                                    hb ? -(float)(6.0 * eps) : (float)(2.0 * eps),
                                    (float)((double)ta.S * tb.V + (double)tb.S * ta.V));
             sq[slot] = (float)(332.06363 / 4.0 * (double)l->charge[ia] * (double)l->charge[ib]);
+            return;
+#endif
+            // D5, folded (score.cuh pair_eg_folded): {A r_eq^12, +-|B| r_eq^n (n = 10: negative),
+            // S_aV_b + S_bV_a, 332.06363/4 q_a q_b}, in double then rounded once
+            const double req2 = req * req, r6 = req2 * req2 * req2, r12 = r6 * r6;
+            s4[slot] = make_float4((float)((hb ? 5.0 : 1.0) * eps * r12),
+                                   hb ? -(float)(6.0 * eps * r6 * req2 * req2) : (float)(2.0 * eps * r6),
+                                   (float)((double)ta.S * tb.V + (double)tb.S * ta.V),
+                                   (float)(332.06363 / 4.0 * (double)l->charge[ia] * (double)l->charge[ib]));
         };
         int slot = 0;
         for (int I = 0; I < Bt; ++I)
@@ -577,7 +593,7 @@ int prepare_ligand(const dock_ligand *l, const dock_type_param *tp, int n_types,
                 bool any = false;
                 for (int ln = 0; ln < Wg; ++ln) {
                     const float4 v = s4c[st * Wg + ln];
-                    if (v.y != 0.f || v.z != 0.f || v.w != 0.f || sq[st * Wg + ln] != 0.f) { any = true; ++real; }
+                    if (v.x != 0.f || v.y != 0.f || v.z != 0.f || v.w != 0.f || (sep_q && sq[st * Wg + ln] != 0.f)) { any = true; ++real; }
                 }
                 if (!any) ++empty;
             }

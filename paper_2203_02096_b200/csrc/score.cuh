@@ -473,7 +473,11 @@ __device__ __forceinline__ void intra_tiles(const LigSm &L, const Scratch &S, in
     }
 }
 
-// One pair inside the slot-table tiles: constants c = {r_eq^2, A, B, SV} and qq from the
+#ifndef DK_FOLD
+#define DK_FOLD 1   // D5 slot constants folded (A r_eq^12, B r_eq^n, SV, qq); 0: {r_eq^2, A, B, SV} + qq (A/B)
+#endif
+#if defined(DK_AD4) || !DK_FOLD
+// One pair inside the slot-table tiles: constants c = {r_eq, A, B, SV} and qq from the
 // slot (all zero for a non-pair, so no membership test), force as in tile_pair.
 __device__ __forceinline__ void slot_pair(float rxi, float ryi, float rzi, float4 rj, float4 c, float qq, float &e,
                                           float &gxi, float &gyi, float &gzi, float &fx, float &fy, float &fz) {
@@ -484,6 +488,38 @@ __device__ __forceinline__ void slot_pair(float rxi, float ryi, float rzi, float
     gxi = fmaf(dE, dx, gxi); gyi = fmaf(dE, dy, gyi); gzi = fmaf(dE, dz, gzi);
     fx = fmaf(-dE, dx, fx); fy = fmaf(-dE, dy, fy); fz = fmaf(-dE, dz, fz);
 }
+#define DK_SLOT(q) L.slot4[q], L.slotq[q]
+#else
+// D5 pair from folded slot constants c = {A' = A r_eq^12, B' = +-|B| r_eq^n, SV, qq} (prep.cpp;
+// sign of B': the 12-10 H-bond form): with inv = 1/rho^2, E_vdw = A' inv^6 - |B'| inv^{n/2},
+// rho^2 dE_vdw/drho^2 = -6 A' inv^6 + (n/2) |B'| inv^{n/2} -- one multiply and one 4-byte
+// shared-memory read fewer per slot than {r_eq^2, A, B, SV} + qq.  Zero for a non-pair.
+__device__ __forceinline__ float pair_eg_folded(float rho2, float4 c, float &dE) {
+    const bool clamped = rho2 < 1e-4f;
+    rho2 = fmaxf(rho2, 1e-4f);                           // 0.01 Å clamp
+    const float inv = rcp_approx(rho2);
+    const float i2 = inv * inv, i3 = i2 * inv, i6 = i3 * i3;
+    const bool ten = __float_as_int(c.y) < 0;
+    const float xn = ten ? i3 * i2 : i3;
+    const float tA = c.x * i6, tB = fabsf(c.y) * xn;
+    const float dvr = fmaf(-6.0f, tA, (ten ? 5.0f : 3.0f) * tB);
+    const float Eel = c.w * inv;
+    const float Eds = c.z * ex2_approx(rho2 * kExpScale);
+    const float d = fmaf(dvr - Eel, inv, -Eds * kInvTwoSigma2);
+    dE = clamped ? 0.0f : d;
+    return (tA - tB) + Eel + Eds;
+}
+__device__ __forceinline__ void slot_pair(float rxi, float ryi, float rzi, float4 rj, float4 c, float &e,
+                                          float &gxi, float &gyi, float &gzi, float &fx, float &fy, float &fz) {
+    const float dx = rxi - rj.x, dy = ryi - rj.y, dz = rzi - rj.z;
+    const float rho2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
+    float dE;
+    e += pair_eg_folded(rho2, c, dE);
+    gxi = fmaf(dE, dx, gxi); gyi = fmaf(dE, dy, gyi); gzi = fmaf(dE, dz, gzi);
+    fx = fmaf(-dE, dx, fx); fy = fmaf(-dE, dy, fy); fz = fmaf(-dE, dz, fz);
+}
+#define DK_SLOT(q) L.slot4[q]
+#endif
 
 // intra_tiles with precomputed pair-slot constants (L.slot_mode, prep.cpp): the same
 // rotation / broadcast schedule and force bookkeeping, one 16-byte + one 4-byte
@@ -509,14 +545,12 @@ __device__ __forceinline__ void intra_tiles_slots(const LigSm &L, const Scratch 
             if (J >= Bt) break;
             const float4 *rrow = S.r + J * 2 * W + sub;         // partner of step s: rrow[s]
             const int s0 = (I == J) ? 1 : 0, s1 = (I == J) ? W / 2 : W - 1;
-            const float4 *crow = L.slot4 + slot0 + sub - s0 * W;   // constants of step s: crow[s * W]
-            const float *qrow = L.slotq + slot0 + sub - s0 * W;
+            const int cbase = slot0 + sub - s0 * W;             // constants of step s: slot cbase + s * W
             slot0 += (s1 - s0 + 1) * W;
             float fx = 0.f, fy = 0.f, fz = 0.f;
 #pragma unroll kTileUnroll
             for (int s = s0; s <= s1; ++s) {
-                slot_pair(rx[I], ry[I], rz[I], rrow[s], crow[s * W], qrow[s * W], e, hx[I], hy[I], hz[I], fx, fy,
-                          fz);
+                slot_pair(rx[I], ry[I], rz[I], rrow[s], DK_SLOT(cbase + s * W), e, hx[I], hy[I], hz[I], fx, fy, fz);
                 if (s < s1) {
                     const int src = (sub + 1) & (W - 1);
                     fx = __shfl_sync(mask, fx, src, W);
@@ -550,7 +584,7 @@ __device__ __forceinline__ void intra_tiles_slots(const LigSm &L, const Scratch 
             for (int I = 0; I < MAXC; ++I) {
                 if (I >= Bf) break;
                 const int q = slot0 + (st * Bf + I) * W + sub;
-                slot_pair(rx[I], ry[I], rz[I], rj, L.slot4[q], L.slotq[q], e, hx[I], hy[I], hz[I], fx, fy, fz);
+                slot_pair(rx[I], ry[I], rz[I], rj, DK_SLOT(q), e, hx[I], hy[I], hz[I], fx, fy, fz);
             }
             const int src = (sl + 1) & (tp - 1);               // after the last step: back to the owner
             fx = __shfl_sync(mask, fx, src, tp);
@@ -563,7 +597,7 @@ __device__ __forceinline__ void intra_tiles_slots(const LigSm &L, const Scratch 
             const int st = 1 + g + r * nseg;
             const int q = slot0 + r * W + sub;
             float px = 0.f, py = 0.f, pz = 0.f;
-            slot_pair(ro.x, ro.y, ro.z, trow[(sl + st) & (tp - 1)], L.slot4[q], L.slotq[q], e, fx, fy, fz, px, py,
+            slot_pair(ro.x, ro.y, ro.z, trow[(sl + st) & (tp - 1)], DK_SLOT(q), e, fx, fy, fz, px, py,
                       pz);
             const int src = (sl - st) & (tp - 1);              // lane m receives the force on m from m - st
             fx += __shfl_sync(mask, px, src, tp);
@@ -587,7 +621,7 @@ __device__ __forceinline__ void intra_tiles_slots(const LigSm &L, const Scratch 
 #pragma unroll
             for (int I = 0; I < MAXC; ++I) {
                 if (I > Bf) break;
-                slot_pair(rx[I], ry[I], rz[I], rj, L.slot4[sk + I * W], L.slotq[sk + I * W], e, hx[I], hy[I], hz[I],
+                slot_pair(rx[I], ry[I], rz[I], rj, DK_SLOT(sk + I * W), e, hx[I], hy[I], hz[I],
                           fx, fy, fz);
             }
             fx = gsum<W>(fx, mask); fy = gsum<W>(fy, mask); fz = gsum<W>(fz, mask);

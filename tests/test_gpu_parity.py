@@ -712,3 +712,58 @@ def test_spec_style_ligand_verbatim_topology_builtin_types(dock, name):
     c1, fails1 = compare_at_pose(P, grid, r["best_genes"], r["best_E"], r["best_xyz"])
     assert_parity(c1, fails1, f"{name} verbatim topology, run")
     d.close()
+
+
+# ---------------------------------------------------------------------------
+# SURVEY §8(c) "Unpinned (i)": full multi-generation runs are chaotic after the first
+# near-tie, so GPU and oracle runs are compared statistically on CFG0 for both LS methods:
+# the median best energies agree within 0.1 kcal/mol, or both sides reach the planted
+# minimum of a planted grid (next test).  DESIGN.md §3 reading 23a: the best energies of
+# CFG0 runs spread with sigma ~1.3 (ADADELTA) / 1.7 (SW) kcal/mol, so with SURVEY's 32 seeds
+# the median difference of two identical distributions has a standard error of ~0.4: the
+# comparison uses R = 8192 runs (global run ids, one RNG stream each), which puts 0.1
+# kcal/mol at ~3 standard errors, and a two-sample Kolmogorov-Smirnov test (p > 1e-3).
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("method,rate", [(0, 1.0), (1, 0.25)])
+def test_run_level_statistics_cfg0(dock, method, rate):
+    import os
+    from concurrent.futures import ThreadPoolExecutor
+    from scipy.stats import ks_2samp
+    cfg, lig, grid, d, P = setup(dock, "tiny", ls_method=method, ls_rate=rate, ls_max_iters=30)
+    R = 8192
+    r = d.run(cfg.pop, R, cfg.max_evals, 42, xyz=False)
+    pp = oracle.params(ls_method=method, ls_rate=rate, ls_max_iters=30)
+    with ThreadPoolExecutor(os.cpu_count() or 4) as ex:   # ctypes releases the GIL
+        ore = np.array(list(ex.map(lambda i: oracle.dock_run(P, pp, cfg.pop, cfg.max_evals, 42, run=i)["best_E"],
+                                   range(R))))
+    gm, om = float(np.median(r["best_E"])), float(np.median(ore))
+    same = int(np.sum(np.abs(r["best_E"] - ore) <= np.maximum(1e-3, 1e-4 * np.abs(ore))))
+    p = ks_2samp(r["best_E"].astype(np.float64), ore).pvalue
+    print(f"CFG0 LS {method}: median best GPU {gm:.4f} oracle {om:.4f} over {R} runs; KS p = {p:.3g}; "
+          f"{same}/{R} runs end at the same energy")
+    assert abs(gm - om) <= 0.1, (gm, om)
+    assert p > 1e-3, p
+
+
+@pytest.mark.parametrize("method", [0, 1])
+def test_run_level_planted_minimum_both(dock, method):
+    """The planted-minimum variant: GPU and oracle each find the unique minimum node
+    within one spacing in >= 9/10 runs."""
+    class L:
+        pass
+    lig = L()
+    lig.types = np.zeros(1, np.int32); lig.charges = np.zeros(1, np.float32)
+    lig.xyz = np.zeros((1, 3), np.float32)
+    lig.bonds = np.zeros((0, 2), np.int32); lig.rotatable = np.zeros(0, np.uint8)
+    node = (9, 3, 12)
+    g = planted_grid(16, 0.75, node)
+    kw = dict(ls_method=method, ls_rate=0.25 if method else 1.0, ls_max_iters=30)
+    d = dock.Docker.from_inputs(g, lig, **kw)
+    r = d.run(16, 10, 2000, 7)
+    P = oracle.Problem(g, lig)
+    pp = oracle.params(**kw)
+    xs = g.origin + np.array(node) * g.spacing
+    og = np.stack([oracle.dock_run(P, pp, 16, 2000, 7, run=i)["best_genes"][:3] for i in range(10)])
+    assert (np.linalg.norm(r["best_genes"][:, :3] - xs, axis=1) <= g.spacing).sum() >= 9
+    assert (np.linalg.norm(og - xs, axis=1) <= g.spacing).sum() >= 9
+    d.close()
