@@ -412,16 +412,28 @@ int prepare_ligand(const dock_ligand *l, const dock_type_param *tp, int n_types,
         const int c_bc = tail * ((Bf + 1) * 40 + 3 * 5);
         int lg = 0;
         while ((1 << lg) < tpw) ++lg;
-        bool use_seg = c_seg < c_rot && c_seg < c_bc;
-        if (const char *f = std::getenv("DOCK_TAIL")) use_seg = std::strcmp(f, "seg") == 0;   // A/B experiments
-        if (use_seg) { L.tail_seg = tpw | (lg << 8) | (seg_rounds << 16); L.tail_rot = 0; }
+        // hyb (slot mode only, needs full chunks): the full chunks x tail part by broadcast
+        // (t*Bf evaluations + 3 sums per tail atom), the tail x tail part by the segment rounds
+        const int c_hyb = tail * (Bf * 40 + 3 * 5) + seg_rounds * 46 + 6 * seg_lg();
+        bool use_seg = c_seg < c_rot && c_seg < c_bc && c_seg <= c_hyb;
+        bool use_hyb = !use_seg && Bf > 0 && c_hyb < c_rot && c_hyb < c_bc;
+        if (const char *f = std::getenv("DOCK_TAIL")) {   // A/B experiments and the schedule tests
+            if (std::strcmp(f, "seg") == 0) { use_seg = true; use_hyb = false; }
+            else if (std::strcmp(f, "hyb") == 0) { use_seg = false; use_hyb = Bf > 0; }
+            else if (std::strcmp(f, "bcast1") == 0 || std::strcmp(f, "bcast") == 0) { use_seg = false; use_hyb = false; }
+        }
+        if (use_seg || use_hyb) {
+            L.tail_seg = tpw | (lg << 8) | (seg_rounds << 16) | (use_hyb ? 1 << 24 : 0);
+            L.tail_rot = 0;
+        }
     }
+    const bool hyb = (L.tail_seg >> 24) & 1;
     auto slot_count = [&]() {
         const int Bt_ = Bf + L.tail_rot;
         const int steps = Bt_ * (Wg / 2) + (Bt_ * (Bt_ - 1) / 2) * Wg;
         int extra = 0;
         if (tail > 0 && !L.tail_rot)
-            extra = L.tail_seg ? (Bf * tpw + seg_rounds) * Wg : tail * (Bf + 1) * Wg;
+            extra = L.tail_seg ? ((hyb ? tail * Bf : Bf * tpw) + seg_rounds) * Wg : tail * (Bf + 1) * Wg;
         return steps * Wg + extra;
     };
     L.n_slots = slot_count();
@@ -564,7 +576,13 @@ int prepare_ligand(const dock_ligand *l, const dock_type_param *tp, int n_types,
                         fill(slot, I * Wg + ln, J * Wg + ((ln + st) & (Wg - 1)), once);
                     }
             }
-        if (tail > 0 && L.tail_seg) {
+        if (tail > 0 && L.tail_seg && hyb) {
+            // hyb, own chunks x tail by broadcast: tail atom k, chunk I, lane ln -> atom I*Wg + ln
+            for (int k = 0; k < tail; ++k)
+                for (int I = 0; I < Bf; ++I)
+                    for (int ln = 0; ln < Wg; ++ln, ++slot)
+                        fill(slot, I * Wg + ln, Bf * Wg + k, true);
+        } else if (tail > 0 && L.tail_seg) {
             // own chunks x tail: step s, chunk I, lane ln -> tail position ((ln mod tpw) + s) mod tpw
             for (int st = 0; st < tpw; ++st)
                 for (int I = 0; I < Bf; ++I)
@@ -572,6 +590,8 @@ int prepare_ligand(const dock_ligand *l, const dock_type_param *tp, int n_types,
                         const int k = ((ln & (tpw - 1)) + st) & (tpw - 1);
                         fill(slot, I * Wg + ln, Bf * Wg + k, k < tail);
                     }
+        }
+        if (tail > 0 && L.tail_seg) {
             // tail x tail: round r, segment g = ln / tpw takes step 1 + g + r * (Wg / tpw)
             for (int r = 0; r < seg_rounds; ++r)
                 for (int ln = 0; ln < Wg; ++ln, ++slot) {

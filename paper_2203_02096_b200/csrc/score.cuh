@@ -46,6 +46,9 @@ constexpr float kDielLB2 = kDielLB * (78.4f + 8.5525f);           // lambda B^2
 #define DK_WALK_DEPTH 4
 #endif
 constexpr int kWalkDepth = DK_WALK_DEPTH;
+#ifndef DK_TILE_STREAMS
+#define DK_TILE_STREAMS 1   // 2: two partner-accumulator streams per tile (A/B: scripts/variants.py)
+#endif
 #ifndef DK_TILE_UNROLL
 #define DK_TILE_UNROLL 4   // steps unrolled in the pair-slot tile loop (A/B: scripts/variants.py)
 #endif
@@ -547,6 +550,29 @@ __device__ __forceinline__ void intra_tiles_slots(const LigSm &L, const Scratch 
             const int s0 = (I == J) ? 1 : 0, s1 = (I == J) ? W / 2 : W - 1;
             const int cbase = slot0 + sub - s0 * W;             // constants of step s: slot cbase + s * W
             slot0 += (s1 - s0 + 1) * W;
+#if DK_TILE_STREAMS == 2
+            // two independent partner-accumulator streams per tile (steps s0.. and s0+h..):
+            // their shuffle chains overlap, so a lane has two pairs in flight per step
+            const int h = (s1 - s0 + 1) / 2;
+            float ax = 0.f, ay = 0.f, az = 0.f, bx = 0.f, by = 0.f, bz = 0.f;
+#pragma unroll kTileUnroll
+            for (int u = 0; u < h; ++u) {
+                const int sa = s0 + u, sb = s0 + h + u;
+                slot_pair(rx[I], ry[I], rz[I], rrow[sa], DK_SLOT(cbase + sa * W), e, hx[I], hy[I], hz[I], ax, ay, az);
+                slot_pair(rx[I], ry[I], rz[I], rrow[sb], DK_SLOT(cbase + sb * W), e, hx[I], hy[I], hz[I], bx, by, bz);
+                if (u < h - 1) {
+                    const int src = (sub + 1) & (W - 1);
+                    ax = __shfl_sync(mask, ax, src, W); ay = __shfl_sync(mask, ay, src, W);
+                    az = __shfl_sync(mask, az, src, W);
+                    bx = __shfl_sync(mask, bx, src, W); by = __shfl_sync(mask, by, src, W);
+                    bz = __shfl_sync(mask, bz, src, W);
+                }
+            }
+            const int backa = (sub - (s0 + h - 1)) & (W - 1), backb = (sub - s1) & (W - 1);
+            hx[J] += __shfl_sync(mask, ax, backa, W) + __shfl_sync(mask, bx, backb, W);
+            hy[J] += __shfl_sync(mask, ay, backa, W) + __shfl_sync(mask, by, backb, W);
+            hz[J] += __shfl_sync(mask, az, backa, W) + __shfl_sync(mask, bz, backb, W);
+#else
             float fx = 0.f, fy = 0.f, fz = 0.f;
 #pragma unroll kTileUnroll
             for (int s = s0; s <= s1; ++s) {
@@ -563,6 +589,7 @@ __device__ __forceinline__ void intra_tiles_slots(const LigSm &L, const Scratch 
             fy = __shfl_sync(mask, fy, back, W);
             fz = __shfl_sync(mask, fz, back, W);
             hx[J] += fx; hy[J] += fy; hz[J] += fz;
+#endif
         }
     }
     if (t > 0 && L.tail_seg > 0) {
@@ -574,24 +601,42 @@ __device__ __forceinline__ void intra_tiles_slots(const LigSm &L, const Scratch 
         // beyond tp/2); the partner force goes back by one segment shuffle.  A butterfly over
         // the segments then sums each tail atom's force.  Fixed order: deterministic.
         // tail_seg packs tp | log2(tp) << 8 | rounds << 16 (no integer divisions here)
-        const int tp = L.tail_seg & 0xff, lg = (L.tail_seg >> 8) & 0xff, rounds = L.tail_seg >> 16;
+        // bit 24 (hyb): the full chunks x tail part by broadcast instead (every lane meets tail
+        // atom k at once, one butterfly per force component), then the segment rounds
+        const int tp = L.tail_seg & 0xff, lg = (L.tail_seg >> 8) & 0xff, rounds = (L.tail_seg >> 16) & 0xff;
         const int sl = sub & (tp - 1), nseg = W >> lg, g = sub >> lg;
         const float4 *trow = S.r + Bf * 2 * W;                  // tail chunk (positions 0..tp-1)
         float fx = 0.f, fy = 0.f, fz = 0.f;
-        for (int st = 0; st < tp; ++st) {
-            const float4 rj = trow[(sl + st) & (tp - 1)];
+        if ((L.tail_seg >> 24) & 1) {
+            for (int k = 0; k < t; ++k) {
+                const float4 rj = trow[k];                      // uniform: shared-memory broadcast
+                float px = 0.f, py = 0.f, pz = 0.f;
 #pragma unroll
-            for (int I = 0; I < MAXC; ++I) {
-                if (I >= Bf) break;
-                const int q = slot0 + (st * Bf + I) * W + sub;
-                slot_pair(rx[I], ry[I], rz[I], rj, DK_SLOT(q), e, hx[I], hy[I], hz[I], fx, fy, fz);
+                for (int I = 0; I < MAXC; ++I) {
+                    if (I >= Bf) break;
+                    slot_pair(rx[I], ry[I], rz[I], rj, DK_SLOT(slot0 + (k * Bf + I) * W + sub), e, hx[I], hy[I], hz[I],
+                              px, py, pz);
+                }
+                px = gsum<W>(px, mask); py = gsum<W>(py, mask); pz = gsum<W>(pz, mask);
+                if (sub == k) { fx += px; fy += py; fz += pz; }   // segment 0 holds the tail owners
             }
-            const int src = (sl + 1) & (tp - 1);               // after the last step: back to the owner
-            fx = __shfl_sync(mask, fx, src, tp);
-            fy = __shfl_sync(mask, fy, src, tp);
-            fz = __shfl_sync(mask, fz, src, tp);
+            slot0 += t * Bf * W;
+        } else {
+            for (int st = 0; st < tp; ++st) {
+                const float4 rj = trow[(sl + st) & (tp - 1)];
+#pragma unroll
+                for (int I = 0; I < MAXC; ++I) {
+                    if (I >= Bf) break;
+                    const int q = slot0 + (st * Bf + I) * W + sub;
+                    slot_pair(rx[I], ry[I], rz[I], rj, DK_SLOT(q), e, hx[I], hy[I], hz[I], fx, fy, fz);
+                }
+                const int src = (sl + 1) & (tp - 1);           // after the last step: back to the owner
+                fx = __shfl_sync(mask, fx, src, tp);
+                fy = __shfl_sync(mask, fy, src, tp);
+                fz = __shfl_sync(mask, fz, src, tp);
+            }
+            slot0 += tp * Bf * W;
         }
-        slot0 += tp * Bf * W;
         const float4 ro = trow[sl];
         for (int r = 0; r < rounds; ++r) {
             const int st = 1 + g + r * nseg;

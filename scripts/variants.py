@@ -1,5 +1,5 @@
 """Build experimental libdock variants (extra -D defines) under build/variants/ for A/B
-timing on the GPU box:  DOCK_LIB=build/variants/libdock_<tag>.so python bench.py ..."""
+timing on the GPU box:  DOCK_LIB=build/ab/libdock_<tag>.so python bench.py ..."""
 import os
 import sys
 
@@ -12,5 +12,5 @@ spec.loader.exec_module(b)
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 for arg in sys.argv[1:]:                      # tag=DEF1,DEF2
     tag, _, defs = arg.partition("=")
-    out = os.path.join(ROOT, "build", "variants", f"libdock_{tag}.so")
+    out = os.path.join(ROOT, "build", "ab", f"libdock_{tag}.so")   # build/ab travels with gpurun (build/variants does not)
     print(b.build(force=True, out=out, defines=[d for d in defs.split(",") if d]))

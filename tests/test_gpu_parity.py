@@ -595,7 +595,7 @@ def test_sw_cooperative_split(dock, split, depth):
 # choice between the other two (bcast).
 # ---------------------------------------------------------------------------
 @pytest.mark.parametrize("n_atoms", [9, 13, 24, 33, 36, 40, 41, 47, 50, 57, 63, 65, 70, 72, 80])
-@pytest.mark.parametrize("mode", ["seg", "bcast"])
+@pytest.mark.parametrize("mode", ["seg", "bcast", "hyb", "bcast1"])
 def test_tail_schedules_parity(dock, n_atoms, mode, monkeypatch):
     from gen import make_ligand
     from gen.synth import TYPE_NAMES, make_grid
