@@ -462,7 +462,10 @@ def run_ours(args, cfg, lig, grid):
                 "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                         "note": "dock_init (host grid+ligand upload) + dock_run_ex (host outputs) + dock_free, wall clock"},
                 "roofline": roofline,
-                "clocks": clk}
+                "clocks": clk,
+                "step_ms": {"median": statistics.median(times), "min": min(times), "max": max(times),
+                            "spread": (max(times) - min(times)) / statistics.median(times),
+                            "note": "this rank's timed steps (the paper reports means of 10 replicas, P:153)"}}
         if world == 1 and not args.no_parts:
             line["roofline_parts"] = parts_roofline(d, cfg, grid, dev)
         if world == 1 and not args.no_cpu:

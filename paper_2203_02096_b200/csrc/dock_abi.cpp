@@ -85,6 +85,7 @@ dk::PopDev pop_of(const dock_ctx *c) {
     dk::PopDev d;
     d.genes = c->d_genes; d.E = c->d_E; d.state = c->d_state; d.perm = c->d_perm; d.ls_evals = c->d_ls_evals;
     d.ls_count = c->d_ls_count;
+    d.spec_done = c->d_spec_done; d.spec_ctr = c->d_spec_ctr; d.spec_words = (c->cap_pop + 31) / 32;
     return d;
 }
 
@@ -95,8 +96,9 @@ int ensure_buffers(dock_ctx *c, int runs, int pop) {
     CK(cudaStreamSynchronize(c->stream));
     dk::dfree(c->d_genes, c->stream); dk::dfree(c->d_E, c->stream); dk::dfree(c->d_state, c->stream);
     dk::dfree(c->d_perm, c->stream); dk::dfree(c->d_ls_evals, c->stream); dk::dfree(c->d_ls_count, c->stream);
+    dk::dfree(c->d_spec_done, c->stream); dk::dfree(c->d_spec_ctr, c->stream);
     c->d_genes = nullptr; c->d_E = nullptr; c->d_state = nullptr; c->d_perm = nullptr; c->d_ls_evals = nullptr;
-    c->d_ls_count = nullptr;
+    c->d_ls_count = nullptr; c->d_spec_done = nullptr; c->d_spec_ctr = nullptr;
     c->cap_runs = c->cap_pop = 0;
     // rows are strided by the ligand's G, but sized for the largest G so a context can be
     // reused for any ligand (dock_screen slots)
@@ -109,6 +111,9 @@ int ensure_buffers(dock_ctx *c, int runs, int pop) {
     CK(dk::dmalloc((void **)&c->d_ls_evals, (size_t)R * P * sizeof(int), s));
     CK(dk::dmalloc((void **)&c->d_ls_count, (size_t)R * sizeof(int), s));
     CK(cudaMemsetAsync(c->d_ls_count, 0, (size_t)R * sizeof(int), s));
+    const size_t spw = (size_t)(P + 31) / 32;
+    CK(dk::dmalloc((void **)&c->d_spec_done, (size_t)R * 2 * spw * sizeof(unsigned), s));
+    CK(dk::dmalloc((void **)&c->d_spec_ctr, (size_t)R * 2 * sizeof(int), s));
     CK(cudaStreamSynchronize(s));   // usable from any stream (dock_run_device's) from here on
     if (!c->h_state.reserve(R)) { c->err = "pinned host allocation failed"; return DOCK_E_INTERNAL; }
     c->cap_runs = R; c->cap_pop = P;
@@ -486,6 +491,8 @@ int dock_run_device(dock_ctx *c, int32_t pop, int32_t runs, int32_t run_base, ui
         for (int i = 0; i < 3; ++i) { c->prof_ms[i] = 0; c->prof_n[i] = 0; }
         if (prof && !c->d_prof) CK(dk::dmalloc((void **)&c->d_prof, 2 * sizeof(unsigned long long), s));
         if (prof) CK(cudaMemsetAsync(c->d_prof, 0, 2 * sizeof(unsigned long long), s));
+        CK(cudaMemsetAsync(c->d_spec_done, 0, sizeof(unsigned) * (size_t)runs * 2 * pd.spec_words, s));
+        CK(cudaMemsetAsync(c->d_spec_ctr, 0, sizeof(int) * (size_t)runs * 2, s));
         CK(dk::launch_init(c->lig, c->grid, sp, pd, s));
         CK(dk::launch_run_sw(c->lig, c->grid, sp, pd, prof ? c->d_prof : nullptr, s));
         CK(dk::launch_best(c->lig, sp, pd, d_best_energy, d_best_genotype, (long long *)d_evals_used, d_generations, s));
@@ -568,6 +575,7 @@ int dock_run_device(dock_ctx *c, int32_t pop, int32_t runs, int32_t run_base, ui
             pr.genes = pd.genes + (size_t)r * P * G; pr.E = pd.E + (size_t)r * P; pr.state = pd.state + r;
             pr.perm = pd.perm + (size_t)r * P; pr.ls_evals = pd.ls_evals + (size_t)r * P;
             pr.ls_count = pd.ls_count + r;
+            pr.spec_done = pd.spec_done + (size_t)r * 2 * pd.spec_words; pr.spec_ctr = pd.spec_ctr + 2 * r;
             for (int k = 0; k < K && ce == cudaSuccess; ++k) {
                 ce = dk::launch_ga(c->lig, c->grid, spr, pr, nullptr, b);
                 if (ce == cudaSuccess && prof && r == 0) ce = cudaEventRecordWithFlags(ev[2 * k], b, cudaEventRecordExternal);

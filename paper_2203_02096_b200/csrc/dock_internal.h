@@ -106,6 +106,11 @@ struct PopDev {
     int *perm;                    // [runs][pop] LS pick order
     int *ls_evals;                // [runs][pop] per-LS evaluation counts
     int *ls_count;                // [runs] LS individuals finished this generation (fused gen end)
+    // k_run_sw speculative GA: per run and generation parity, the bitmap of
+    // offspring slots already scored during the previous LS phase, and its claim counter
+    unsigned *spec_done;          // [runs][2][spec_words], spec_words = ceil(pop / 32)
+    int *spec_ctr;                // [runs][2]
+    int spec_words;
 };
 
 }  // namespace dk

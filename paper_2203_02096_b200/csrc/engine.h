@@ -87,6 +87,8 @@ struct dock_ctx {
     float *d_genes = nullptr, *d_E = nullptr;
     dk::RunState *d_state = nullptr;
     int *d_perm = nullptr, *d_ls_evals = nullptr, *d_ls_count = nullptr;
+    unsigned *d_spec_done = nullptr;            // k_run_sw speculative GA bitmaps [runs][2][ceil(pop/32)]
+    int *d_spec_ctr = nullptr;                  // [runs][2]
     dk::PinnedBuf<dk::RunState> h_state;   // termination poll target
     std::string err;
     long long launches = 0;

@@ -874,6 +874,9 @@ __device__ __forceinline__ unsigned long long global_ns() {
 #ifndef DK_RUNSW_XWARPS
 #define DK_RUNSW_XWARPS 0
 #endif
+#ifndef DK_RUNSW_SPEC
+#define DK_RUNSW_SPEC 0   // 1: speculative GA slots in the LS phase (A/B: 1stp 0.99x, PS 0.96x -- DESIGN.md §15)
+#endif
 template <int W, int D>
 __host__ __device__ constexpr int run_sw_threads() { return tree_threads<W, D, 1>() + 32 * DK_RUNSW_XWARPS; }
 
@@ -902,22 +905,118 @@ __global__ void DK_RUNSW_BOUNDS k_run_sw(const LigDev L, const GridDev g,
     uint8_t *gbase = sm + staged + gidx * SL.bytes;
     const Scratch S = scratch_at(gbase, SL);
     const bool timer = prof != nullptr && r == 0 && q == 0 && threadIdx.x == 0;
+    // Speculative GA: an offspring slot of the next generation whose four
+    // tournament candidates all lie outside this generation's LS sample depends only on data
+    // that is final once the GA phase ends (genes / energies of the non-sampled individuals,
+    // counter-based words).  CTAs whose Solis-Wets chain has finished score such slots while
+    // the run's longer chains still run (they wait at the LS barrier anyway), mark them in the
+    // per-parity bitmap, and the next GA phase deals only the rest.  Each slot's arithmetic is
+    // that of ga_slot_group whoever computes it, so results are bit-identical.  Scratch: the
+    // tree's energy / deviate region (free outside the chain), list capacity kSpecCap slots.
+    int *slist = reinterpret_cast<int *>(sm + staged + NGA * SL.bytes);
+    constexpr int kSpecCap = 2 * 8 + kTriAhead * kMaxGenes;   // ints of tree_smem's tail (NGA >= 8)
+    const bool spec = DK_RUNSW_SPEC && P < kSpecCap && pop.spec_done != nullptr;
+    const int SWd = pop.spec_words;
+    const uint2 key = make_uint2(sp.key0, sp.key1);
+    const uint32_t run_g = (uint32_t)(sp.run_base + r);
     for (;;) {
         RunState st;
         st.evals = __ldcg(&pop.state[r].evals); st.gen = __ldcg(&pop.state[r].gen);
         if (!run_active(st, sp)) break;                   // uniform over the cluster
         // ---- GA phase ----
-        for (int base = 0; base < P; base += nq * NGA) {
-            const int k = base + q * NGA + gidx;
-            ga_slot_group<W, MAXC>(Ls, g, S, reinterpret_cast<int *>(gbase + SL.off_extra), sp, pop, G, k < P, st, r,
-                                   k < P ? k : 0, sub, nullptr);
+        const int par = (st.gen + 1) & 1;                 // parity of the generation being created
+        if (spec) {
+            // the slots still to score: slot 0 (elite + LS pick) and those not marked done
+            const unsigned *done = pop.spec_done + ((size_t)r * 2 + par) * SWd;
+            if (threadIdx.x < 32) {
+                int n = 0;
+                for (int w = 0; w < SWd; ++w) {
+                    const int k = w * 32 + (int)threadIdx.x;
+                    const bool todo = k < P && (k == 0 || !((__ldcg(done + w) >> threadIdx.x) & 1u));
+                    const unsigned bal = __ballot_sync(0xffffffffu, todo);
+                    if (todo) slist[n + __popc(bal & ((1u << threadIdx.x) - 1u))] = k;
+                    n += __popc(bal);
+                }
+                if (threadIdx.x == 0) slist[kSpecCap - 1] = n;
+            }
+            __syncthreads();
+            const int nrem = slist[kSpecCap - 1];
+            for (int base = 0; base < nrem; base += nq * NGA) {
+                const int i = base + q * NGA + gidx;
+                ga_slot_group<W, MAXC>(Ls, g, S, reinterpret_cast<int *>(gbase + SL.off_extra), sp, pop, G, i < nrem, st,
+                                       r, i < nrem ? slist[i] : 0, sub, nullptr);
+            }
+            if (q == 0 && threadIdx.x == 0) pop.spec_ctr[2 * r + par] = 0;   // this parity's claims are consumed
+        } else {
+            for (int base = 0; base < P; base += nq * NGA) {
+                const int k = base + q * NGA + gidx;
+                ga_slot_group<W, MAXC>(Ls, g, S, reinterpret_cast<int *>(gbase + SL.off_extra), sp, pop, G, k < P, st,
+                                       r, k < P ? k : 0, sub, nullptr);
+            }
         }
         __threadfence();
         cl.sync();
         const unsigned long long t0 = timer ? global_ns() : 0ull;
         // ---- LS phase ----
+        if (spec && q == 0)                               // this parity's bitmap is consumed (read above)
+            for (int w = threadIdx.x; w < SWd; w += blockDim.x) pop.spec_done[((size_t)r * 2 + par) * SWd + w] = 0u;
         const LsTarget t = ls_target(sp, pop, a, r * nq + q, G);
         sw_tree_chain<W, MAXC, D, 1>(Ls, g, SL, sp, pop, a, t, sm, staged, G);
+        if (spec) {
+            // next generation g2 = st.gen + 2 (parity par ^ 1): the slots whose candidates avoid
+            // this generation's LS sample (pop.perm[r][0, n_ls), written in the GA phase)
+            const uint32_t g2 = (uint32_t)st.gen + 2u;
+            const int *ls = pop.perm + (size_t)r * P;
+            __syncthreads();                              // the chain's reads of the tree region are done
+            if (threadIdx.x < 32) {
+                int n = 0;
+                for (int k0 = 1; k0 < P; k0 += 32) {
+                    const int k = k0 + (int)threadIdx.x;
+                    bool ok = k < P;
+                    if (ok) {
+                        const uint4 b0 = stream_block(key, kGA, (uint32_t)k, g2, run_g, 0u);
+                        const uint4 b1 = stream_block(key, kGA, (uint32_t)k, g2, run_g, 1u);
+                        const uint32_t wv[4] = {b0.x, b0.y, b0.w, b1.x};       // words 0, 1 (A) and 3, 4 (B)
+#pragma unroll
+                        for (int h = 0; h < 2; ++h) {
+                            const int ci = (int)below(wv[2 * h], (uint32_t)P);
+                            int cj = (int)below(wv[2 * h + 1], (uint32_t)(P - 1));
+                            if (cj >= ci) cj += 1;
+                            for (int s2 = 0; s2 < sp.n_ls; ++s2) {
+                                const int m = __ldcg(ls + s2);
+                                if (m == ci || m == cj) ok = false;
+                            }
+                        }
+                    }
+                    const unsigned bal = __ballot_sync(0xffffffffu, ok);
+                    if (ok) slist[n + __popc(bal & ((1u << threadIdx.x) - 1u))] = k;
+                    n += __popc(bal);
+                }
+                if (threadIdx.x == 0) slist[kSpecCap - 1] = n;
+            }
+            __syncthreads();
+            const int nspec = slist[kSpecCap - 1];
+            RunState st2 = st;
+            st2.gen = st.gen + 1;                         // the generation g2 is created from
+            int *ctr = pop.spec_ctr + 2 * r + (par ^ 1);
+            unsigned *done2 = pop.spec_done + ((size_t)r * 2 + (par ^ 1)) * SWd;
+            const int lane = threadIdx.x & 31, wgrp = lane / W;   // lane group within the warp
+            for (;;) {
+                int c = 0;
+                if (lane == 0) c = atomicAdd(ctr, 32 / W);       // one slot per lane group of the warp
+                c = __shfl_sync(0xffffffffu, c, 0);
+                if (c >= nspec) break;                            // uniform per warp
+                const int i = c + wgrp;
+                const bool act = i < nspec;
+                const int k = act ? slist[i] : 0;
+                ga_slot_group<W, MAXC>(Ls, g, S, reinterpret_cast<int *>(gbase + SL.off_extra), sp, pop, G, act, st2,
+                                       r, k, sub, nullptr);
+                if (act && sub == 0) {
+                    __threadfence();
+                    atomicOr(done2 + (k >> 5), 1u << (k & 31));
+                }
+            }
+        }
         __threadfence();
         cl.sync();
         if (timer) { prof[0] += global_ns() - t0; prof[1] += 1ull; }
