@@ -279,7 +279,7 @@ def run_ours(args, cfg, lig, grid):
     def make(prof):
         return dock.Docker.from_inputs(grid, lig, ls_method=cfg.ls_method, ls_rate=cfg.ls_rate,
                                        ls_max_iters=cfg.ls_iters, profile=prof, device=gpu, sw_depth=args.sw_depth,
-                                       scoring=SCORING, sw_split=args.sw_split)
+                                       scoring=SCORING, sw_split=args.sw_split, run_branches=args.run_branches)
     d = make(1)          # profiled context (CUDA events around the LS launches)
     # the config's R runs are split contiguously over the ranks, rank k docks
     # global runs [kR/G, (k+1)R/G) (strong scaling; the Philox counter carries the global run
@@ -300,11 +300,13 @@ def run_ours(args, cfg, lig, grid):
     f_e = flops_per_eval(d.N, d.T, d.P, grad=False)
     f_eg = flops_per_eval(d.N, d.T, d.P, grad=True)
 
-    def step(seed, ctx=None):
+    def step(seed, ctx=None, gather=True):
+        # gather=False: this rank's extra (unprofiled-context warm-up / profiled) steps, which
+        # other ranks may not run (engines can differ per rank), so no collective in them
         with torch.cuda.stream(stream):
             (ctx or d).run_device(cfg.pop, runs, cfg.max_evals, seed, bE, bG, ev, gens, run_base=run_base,
                                   stream=stream.cuda_stream)
-            if world > 1:   # NS: NCCL only for the final gather of best poses (rows padded to rmax)
+            if world > 1 and gather:   # NS: NCCL only for the final gather of best poses (rows padded to rmax)
                 pE = torch.full((rmax,), float("nan"), dtype=torch.float32, device=dev)
                 pG = torch.zeros(rmax, d.G, dtype=torch.float32, device=dev)
                 pE[:runs] = bE; pG[:runs] = bG
@@ -323,7 +325,7 @@ def run_ours(args, cfg, lig, grid):
     if branches > 1:
         dt = make(0)
         for w in range(args.warmup):
-            step(42, dt)
+            step(42, dt, gather=False)
         torch.cuda.synchronize()
     clocks = ClockSampler(gpu)
     clocks.start()
@@ -353,7 +355,7 @@ def run_ours(args, cfg, lig, grid):
         # launches run concurrently with them
         e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        step(42)
+        step(42, gather=False)
         e1.record(stream)
         torch.cuda.synchronize()
         ms, n = d.kernel_stats()
@@ -547,7 +549,8 @@ def run_hts(args, cfg, grid):
     costs = sched.ligand_cost([len(l.types) for l in ligs], n_pairs)
     mine = sched.lpt_partition(costs, world)[rank]
     my_ligs = [ligs[i] for i in mine]
-    kw = dict(ls_method=cfg.ls_method, ls_rate=cfg.ls_rate, ls_max_iters=cfg.ls_iters, scoring=SCORING)
+    kw = dict(ls_method=cfg.ls_method, ls_rate=cfg.ls_rate, ls_max_iters=cfg.ls_iters, scoring=SCORING,
+              run_branches=args.run_branches)
     for _ in range(args.warmup):   # warm-up on a slice: context, kernels, graphs
         dock.screen(grid, my_ligs[:8], cfg.pop, cfg.runs, cfg.max_evals // 10, 7, ligand_ids=mine[:8],
                     devices=[local], slots_per_device=args.slots, **kw)
@@ -685,6 +688,7 @@ def main():
     ap.add_argument("--micro-iters", type=int, default=20)
     ap.add_argument("--sw-depth", type=int, default=0, help="Solis-Wets speculation depth (0 = auto)")
     ap.add_argument("--sw-split", type=int, default=0, help="Solis-Wets warps per evaluation (0 = auto)")
+    ap.add_argument("--run-branches", type=int, default=0, help="dock_params.run_branches (0 = auto, 1 lockstep, 2 branches, 3 clusters)")
     ap.add_argument("--n-ligs", type=int, default=256, help="hts: ligands per step (sample of configs[4])")
     ap.add_argument("--slots", type=int, default=4, help="hts: ligands in flight per GPU")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])

@@ -506,7 +506,15 @@ int dock_run_device(dock_ctx *c, int32_t pop, int32_t runs, int32_t run_base, ui
         }
         return DOCK_OK;
     }
-    const bool branched = runs > 1 && do_ls && (mode >= 2 || (mode == 0 && sp.ls_method == DOCK_LS_SOLIS_WETS));
+    // ADADELTA chains all last ls_max_iters iterations, so lockstep is best while one
+    // generation's LS launch spans many waves; with few runs per GPU (the R split over 4-8
+    // GPUs) the last partial wave idles most SMs and independent run branches fill it.
+    // Measured on one B200, 7cpa: 13 runs 1.12e8 lockstep / 1.27e8 branches,
+    // 25 runs 1.22e8 / 1.26e8, 50 runs 1.31e8 / 1.25e8, 100 runs 1.34e8 / 1.26e8.
+    const bool ada_few = sp.ls_method == DOCK_LS_ADADELTA && do_ls &&
+                         (long long)runs * sp.n_ls < 4LL * dk::adadelta_resident_groups(c->lig);
+    const bool branched = runs > 1 && do_ls &&
+                          (mode >= 2 || (mode == 0 && (sp.ls_method == DOCK_LS_SOLIS_WETS || ada_few)));
     const int NB = branched ? runs : 1;
     c->last_branches = NB;
     c->last_engine = branched ? 1 : 0;

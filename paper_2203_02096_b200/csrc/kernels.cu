@@ -1481,6 +1481,21 @@ cudaError_t launch_run_sw(const LigDev &L, const GridDev &g, const SearchDev &sp
 #endif  // DK_PART == 3 || DK_PART == 4
 
 #if DK_PART == 2
+// Lane groups of k_ls_adadelta resident on the whole device (occupancy x SMs x groups per
+// CTA): the engine's auto rule compares one generation's LS individuals with it.
+int adadelta_resident_groups(const LigDev &L) {
+    const GroupCfg cfg = pick_group(L.N);
+    const ScratchLayout SL = scratch_layout(L, true, 0);
+    const int groups = kThreads / cfg.W;
+    const size_t smem = (size_t)staged_bytes(L, true) + (size_t)groups * SL.bytes;
+    int dev = 0, nsm = 148, per_sm = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    DK_DISPATCH(cfg, { cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_ls_adadelta<W, MAXC>, kThreads, smem); });
+    cudaGetLastError();
+    return per_sm * nsm * groups;
+}
+
 cudaError_t launch_ls_adadelta(const LigDev &L, const GridDev &g, const SearchDev &sp, const PopDev &pop,
                                const LsArgs &a, int n_total, cudaStream_t s) {
     const GroupCfg cfg = pick_group(L.N);

@@ -61,6 +61,7 @@ struct GroupCfg {
     cudaError_t launch_ls(const LigDev &L, const GridDev &g, const SearchDev &sp, const PopDev &pop,         \
                           const LsArgs &a, int n_total, cudaStream_t s);                                     \
     int run_sw_eligible(const LigDev &L, const SearchDev &sp);                                               \
+    int adadelta_resident_groups(const LigDev &L);                                                           \
     cudaError_t launch_run_sw(const LigDev &L, const GridDev &g, const SearchDev &sp, const PopDev &pop,     \
                               unsigned long long *prof, cudaStream_t s);                                     \
     cudaError_t launch_bench_part(const LigDev &L, const GridDev &g, int part, int n, int iters,             \
@@ -112,6 +113,9 @@ inline cudaError_t launch_bench_part(const LigDev &L, const GridDev &g, int part
                                      const float *genes, float *E, cudaStream_t s) {
     return L.sf == kScoreAD4 ? ad4::launch_bench_part(L, g, part, n, iters, genes, E, s)
                              : d5::launch_bench_part(L, g, part, n, iters, genes, E, s);
+}
+inline int adadelta_resident_groups(const LigDev &L) {
+    return L.sf == kScoreAD4 ? ad4::adadelta_resident_groups(L) : d5::adadelta_resident_groups(L);
 }
 inline int run_sw_eligible(const LigDev &L, const SearchDev &sp) {
     return L.sf == kScoreAD4 ? ad4::run_sw_eligible(L, sp) : d5::run_sw_eligible(L, sp);
