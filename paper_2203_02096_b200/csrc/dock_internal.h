@@ -25,7 +25,9 @@ struct LigDev {
     int blob_bytes;               // multiple of 16
     int grad_bytes;               // prefix needed by the gradient kernels (no pair list / pair constants)
     // byte offsets inside the blob (all 16-byte aligned)
-    int off_lvl;      // int[kMaxTors+1] copy of lvl_start (read from shared memory)
+    int off_tlane;    // int[32] torsion-gradient lane blocks (score.cuh a6): per lane k | lane in
+                      //   block << 8 | log2(block size) << 16, k = 255 for an unused lane
+    int tlane_top;    // largest block size / 2: the block butterfly's first level (0: none)
     int off_p;        // float4[N]  body coordinates p = X - c (x,y,z), charge q in .w
     int off_par;      // float4[N]  R/2, sqrt(eps), S, V
     int off_meta;     // int[N]     type | role << 8 | (deep + 1) << 16

@@ -96,7 +96,8 @@ __device__ __forceinline__ LigSm stage_ligand(const LigDev &L, uint8_t *sm, int 
     __syncthreads();
     LigSm v;
     v.N = L.N; v.T = L.T; v.G = L.G; v.P = L.P; v.NW = L.NW; v.n_levels = L.n_levels;
-    v.lvl = reinterpret_cast<const int *>(sm + L.off_lvl);
+    v.tlane = reinterpret_cast<const int *>(sm + L.off_tlane);
+    v.tlane_top = L.tlane_top;
     v.p = reinterpret_cast<const float4 *>(sm + L.off_p);
     v.par = reinterpret_cast<const float4 *>(sm + L.off_par);
     v.meta = reinterpret_cast<const int *>(sm + L.off_meta);

@@ -378,7 +378,7 @@ int prepare_ligand(const dock_ligand *l, const dock_type_param *tp, int n_types,
     auto S_of = [&](int a) { const double S = tp[l->type[a]].S; return ad4 ? S + sf.qasp * std::fabs((double)l->charge[a]) : S; };
     auto V_of = [&](int a) { const double V = tp[l->type[a]].V; return ad4 ? sf.w_ds * V : V; };
     int off = 0;
-    L.off_lvl = off; off += a16(4 * (kMaxTors + 1));
+    L.off_tlane = off; off += 4 * 32;
     L.off_p = off; off += 16 * N;
     L.off_par = off; off += 16 * N;
     L.off_meta = off; off += a16(4 * N);
@@ -467,12 +467,43 @@ int prepare_ligand(const dock_ligand *l, const dock_type_param *tp, int n_types,
     int n_levels = 0;
     for (int k = 0; k < T; ++k) n_levels = std::max(n_levels, tors[k].depth);
     L.n_levels = n_levels;
-    int *lvl = reinterpret_cast<int *>(bl + L.off_lvl);
     for (int d = 0; d <= kMaxTors; ++d) {
         int s = 0;
         while (s < T && tors[s].depth <= d) ++s;   // first torsion with depth > d
-        lvl[d] = s;
         L.lvl_start[d] = s;
+    }
+    // torsion-gradient lane blocks (score.cuh a6): every torsion gets a power-of-two block of
+    // lanes; starting from one lane each, the block of the torsion with the longest walk
+    // ceil(len / size) is doubled while the blocks fit the Wg lanes.  Blocks are placed
+    // largest first, so each is aligned to its size (the butterfly stays inside it).
+    {
+        std::vector<int> bsz(T, 1);
+        int used = T;
+        for (;;) {
+            int kmax = -1, wmax = 0;
+            for (int k = 0; k < T; ++k) {
+                const int w = (hi[k] - lo[k] + bsz[k] - 1) / bsz[k];
+                if (w > wmax) { wmax = w; kmax = k; }
+            }
+            if (kmax < 0 || wmax <= 1 || used + bsz[kmax] > Wg || 2 * bsz[kmax] > Wg) break;
+            used += bsz[kmax];
+            bsz[kmax] *= 2;
+        }
+        std::vector<int> byb(T);
+        std::iota(byb.begin(), byb.end(), 0);
+        std::stable_sort(byb.begin(), byb.end(), [&](int x, int y) { return bsz[x] > bsz[y]; });
+        int *tl = reinterpret_cast<int *>(bl + L.off_tlane);
+        for (int q = 0; q < 32; ++q) tl[q] = 255;
+        int pos0 = 0, top = 1;
+        for (int k : byb) {
+            int lg = 0;
+            while ((1 << lg) < bsz[k]) ++lg;
+            for (int i = 0; i < bsz[k]; ++i) tl[pos0 + i] = k | (i << 8) | (lg << 16);
+            pos0 += bsz[k];
+            top = std::max(top, bsz[k]);
+        }
+        if (pos0 > Wg) return fail("internal: torsion lane blocks");
+        L.tlane_top = top / 2;
     }
     // body frame: c = centroid of the reference coordinates, computed in double (D1.8)
     double c[3] = {0, 0, 0};

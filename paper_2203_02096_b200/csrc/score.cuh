@@ -57,7 +57,8 @@ constexpr int kTileUnroll = DK_TILE_UNROLL;   // torsion trees up to this depth:
 // Shared-memory view of the staged ligand block.
 struct LigSm {
     int N, T, G, P, NW, n_levels;
-    const int *lvl;               // [kMaxTors+1]
+    const int *tlane;             // [32] torsion block per lane: k | lane << 8 | log2(size) << 16 (k 255: none)
+    int tlane_top;                // largest block size / 2 (butterfly levels), 0 if every block is 1 lane
     const float4 *p;              // body coords + charge
     const float4 *par;            // R/2, sqrt eps, S, V
     const int *meta;              // type | role<<8 | (deep+1)<<16
@@ -947,13 +948,14 @@ __device__ float eval_group(const LigSm &L, const GridDev &grid, const Scratch &
         Gx = gsum<W>(Gx, mask); Gy = gsum<W>(Gy, mask); Gz = gsum<W>(Gz, mask);
         __syncwarp(mask);
         // torsions: dE/dtau_k = w_k . sum_{a in moved(k)} (r_a - r_{a_k}) x g_a.  The moved
-        // set is one DFS range [lo, hi); LPT = largest power of two <= W / T lanes share a
-        // torsion (strided over the range, then a butterfly inside the segment), so idle
-        // lanes shorten the longest range walk (T <= W always holds, see a3).
+        // set is one DFS range [lo, hi).  Each torsion gets an aligned block of lpt lanes, a
+        // power of two sized to its range length by the host (prep.cpp, L.tlane: buddy
+        // allocation that minimises the longest walk), strided over the range, then a
+        // butterfly inside the block (levels up to the largest block only, L.tlane_lv).
         {
             const int T = L.T;
-            const int lpt = T * 16 <= W ? 16 : (T * 8 <= W ? 8 : (T * 4 <= W ? 4 : (T * 2 <= W ? 2 : 1)));
-            const int k = sub / lpt, sl = sub - k * lpt;
+            const int tl = L.tlane[sub];                    // k | lane in block << 8 | log2(lpt) << 16
+            const int lpt = 1 << (tl >> 16), k = tl & 0xff, sl = (tl >> 8) & 0xff;
             const bool own = k < T;
             float cx = 0.f, cy = 0.f, cz = 0.f, hx = 0.f, hy = 0.f, hz = 0.f;
             int4 tm = make_int4(0, 0, 0, 0);
@@ -966,10 +968,11 @@ __device__ float eval_group(const LigSm &L, const GridDev &grid, const Scratch &
                     hx += g4.x; hy += g4.y; hz += g4.z;
                 }
             }
-            for (int m = lpt >> 1; m >= 1; m >>= 1) {     // fixed-order segment butterfly
-                cx += __shfl_xor_sync(mask, cx, m, W); cy += __shfl_xor_sync(mask, cy, m, W);
-                cz += __shfl_xor_sync(mask, cz, m, W); hx += __shfl_xor_sync(mask, hx, m, W);
-                hy += __shfl_xor_sync(mask, hy, m, W); hz += __shfl_xor_sync(mask, hz, m, W);
+            for (int m = L.tlane_top; m >= 1; m >>= 1) {   // fixed-order block butterfly (uniform levels)
+                const float ox = __shfl_xor_sync(mask, cx, m, W), oy = __shfl_xor_sync(mask, cy, m, W);
+                const float oz = __shfl_xor_sync(mask, cz, m, W), ogx = __shfl_xor_sync(mask, hx, m, W);
+                const float ogy = __shfl_xor_sync(mask, hy, m, W), ogz = __shfl_xor_sync(mask, hz, m, W);
+                if (m < lpt) { cx += ox; cy += oy; cz += oz; hx += ogx; hy += ogy; hz += ogz; }
             }
             if (own && sl == 0) {
                 const float4 ra = S.r[ridx<W>(tm.y)], rb = S.r[ridx<W>(tm.z)];
