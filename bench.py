@@ -267,6 +267,54 @@ def run_reference(args, cfg, lig, grid):
 
 
 # ---------------------------------------------------------------------------
+def other_configs(gpu, steps=3):
+    """The other BASELINE.json configs in the same run (C1-C3 at 1 GPU, and
+    the HTS sample), each device-timed like the headline: one warm-up job, then `steps` jobs
+    with CUDA events around dock_run_device (HTS: wall clock around dock_screen)."""
+    import torch
+    import paper_2203_02096_b200 as dock
+    from gen import config_inputs, hts_ligands
+    out = {}
+    dev = torch.device("cuda", gpu)
+    for name in ("1stp", "3ce3"):
+        c, lg, gr = config_inputs(name)
+        d = dock.Docker.from_inputs(gr, lg, ls_method=c.ls_method, ls_rate=c.ls_rate, ls_max_iters=c.ls_iters,
+                                    device=gpu)
+        st = torch.cuda.Stream(device=dev)
+        bE = torch.empty(c.runs, dtype=torch.float32, device=dev)
+        bG = torch.empty(c.runs, d.G, dtype=torch.float32, device=dev)
+        ev = torch.empty(c.runs, dtype=torch.int64, device=dev)
+        gens = torch.empty(c.runs, dtype=torch.int32, device=dev)
+        ms, evals = [], 0
+        for s in range(steps + 1):
+            torch.cuda.synchronize()
+            e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(st)
+            d.run_device(c.pop, c.runs, c.max_evals, 42, bE, bG, ev, gens, stream=st.cuda_stream)
+            e1.record(st)
+            torch.cuda.synchronize()
+            if s > 0:
+                ms.append(e0.elapsed_time(e1)); evals += int(ev.sum().item())
+        out[f"configs[{1 if name == '1stp' else 2}] {name}"] = {
+            "value": evals / (sum(ms) / 1e3), "unit": UNIT, "ms_per_step": statistics.median(ms),
+            "engine": d.engine, "workload": workload_desc(c), "steps": steps}
+        d.close()
+    c, _, gr = config_inputs("hts")
+    ligs = hts_ligands(256)
+    kw = dict(ls_method=c.ls_method, ls_rate=c.ls_rate, ls_max_iters=c.ls_iters)
+    dock.screen(gr, ligs[:8], c.pop, c.runs, c.max_evals // 10, 7, devices=[gpu], **kw)
+    t = []
+    for s in range(2):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        dock.screen(gr, ligs, c.pop, c.runs, c.max_evals, 42, devices=[gpu], **kw)
+        t.append(time.perf_counter() - t0)
+    out["configs[4] hts"] = {"value": 3600.0 * len(ligs) * len(t) / sum(t), "unit": "ligands/h",
+                             "workload": f"256-ligand sample of configs[4] (N ~ U{{10..70}}), pop {c.pop}, "
+                                         f"{c.runs} runs x {c.max_evals} evals, dock_screen wall clock", "steps": 2}
+    return out
+
+
 def run_ours(args, cfg, lig, grid):
     import numpy as np
     import torch
@@ -472,6 +520,8 @@ def run_ours(args, cfg, lig, grid):
             line["roofline_parts"] = parts_roofline(d, cfg, grid, dev)
         if world == 1 and not args.no_cpu:
             line["cpu_baseline"] = cpu_baseline(cfg, lig, grid)
+        if world == 1 and not args.no_also and args.config == "7cpa":
+            line["also"] = other_configs(gpu)
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()
@@ -694,6 +744,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-parts", action="store_true", help="skip the inter / intra / L2-gather roofline parts")
+    ap.add_argument("--no-also", action="store_true", help="skip the other configs (1stp, 3ce3, HTS sample) of the 7cpa line")
     ap.add_argument("--weak", action="store_true", help="N > 1: every rank docks the config's runs (default: split them)")
     ap.add_argument("--scoring", default="d5", choices=["d5", "ad4"],
                     help="intramolecular scoring: D5 (default) or the NEXT-2 AD4.1-calibrated variant")

@@ -46,6 +46,10 @@ constexpr float kDielLB2 = kDielLB * (78.4f + 8.5525f);           // lambda B^2
 #define DK_WALK_DEPTH 4
 #endif
 constexpr int kWalkDepth = DK_WALK_DEPTH;
+#ifndef DK_HYB_UNROLL
+#define DK_HYB_UNROLL 1     // tail atoms per iteration of the hybrid tail's broadcast loop (A/B)
+#endif
+constexpr int kHybUnroll = DK_HYB_UNROLL;
 #ifndef DK_TILE_STREAMS
 #define DK_TILE_STREAMS 1   // 2: two partner-accumulator streams per tile (A/B: scripts/variants.py)
 #endif
@@ -609,6 +613,7 @@ __device__ __forceinline__ void intra_tiles_slots(const LigSm &L, const Scratch 
         const float4 *trow = S.r + Bf * 2 * W;                  // tail chunk (positions 0..tp-1)
         float fx = 0.f, fy = 0.f, fz = 0.f;
         if ((L.tail_seg >> 24) & 1) {
+#pragma unroll kHybUnroll
             for (int k = 0; k < t; ++k) {
                 const float4 rj = trow[k];                      // uniform: shared-memory broadcast
                 float px = 0.f, py = 0.f, pz = 0.f;
