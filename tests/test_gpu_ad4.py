@@ -94,35 +94,25 @@ def test_ad4_energy_terms_and_binding_estimate(dock, name):
 
 @pytest.mark.parametrize("name,iters", [("tiny", 5), ("3ce3", 3), ("7cpa", 2)])
 def test_ad4_adadelta_steps(dock, name, iters):
+    """AD4 ADADELTA: every iteration of the GPU's trajectory at NS tolerance against the
+    oracle's D5-AD4 at the GPU's pose (kinks / cutoffs excluded and counted)."""
+    from test_gpu_ls_protocol import ad_trajectory_check
     cfg, lig, grid, d, P = setup(dock, name)
     X = near_reference_genotypes(grid, lig, d.T, 64, seed=31)
     g, E, ev = d.ls_step(0, X, np.full(64, 1e30, np.float32), iters)
     assert (ev == iters).all()
-    pp = oracle.params()
-    ok = 0
-    for i in range(64):
-        x, Eo, _ = oracle.adadelta(P, pp, iters, X[i], 1e30)
-        if abs(E[i] - Eo) <= e_tol(Eo) and np.abs(g[i] - x).max() <= 1e-3 * max(1.0, np.abs(x).max()):
-            ok += 1
-    assert ok >= 56, ok          # the rest: cell-face / kink crossings, near-ties in best tracking
+    ad_trajectory_check(d, P, grid, X, iters, f"AD4 {name}", kink=True,
+                        extra_excl=lambda r: cut_margin(P, r) < 1e-4)
 
 
 @pytest.mark.parametrize("name", ["1stp", "pm"])
 def test_ad4_solis_wets_steps(dock, name):
+    from test_gpu_ls_protocol import sw_free_run_check
     cfg, lig, grid, d, P = setup(dock, name, ls_method=1)
     n = 48
     X = random_genotypes(grid, d.T, n, seed=41, frac_out=0.0, shrink=0.2)
     E0 = np.array([P.energy(x, grad=False)["E"] for x in X], np.float32)
-    slots = np.arange(n, dtype=np.int32) * 3
-    g, E, ev = d.ls_step(1, X, E0, 20, seed=9, run=2, gen=4, slots=slots)
-    pp = oracle.params(ls_max_iters=20)
-    ok = 0
-    for i in range(n):
-        x, Eo, evo = oracle.solis_wets(P, pp, 9, 0, 2, 4, int(slots[i]), X[i], float(E0[i]))
-        assert E[i] <= E0[i]
-        if ev[i] == evo and abs(E[i] - Eo) <= e_tol(Eo):
-            ok += 1
-    assert ok >= 0.9 * n, ok
+    sw_free_run_check(d, P, grid, X, E0, 20, 9, 2, 4, np.arange(n, dtype=np.int32) * 3, f"AD4 {name}")
 
 
 @pytest.mark.parametrize("name,runs,budget", [("1stp", 8, 40_000), ("7cpa", 3, 60_000)])

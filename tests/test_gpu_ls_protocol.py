@@ -110,6 +110,63 @@ def _first_diff(a, b):
     return int(k[0]) if k.size else -1
 
 
+def sw_free_run_check(d, P, grid, X, E0, iters, seed, run, gen, slots, label):
+    """The GPU's Solis-Wets outcome trace (dock_sw_trace, free running) against the oracle's
+    (or_solis_wets_traced): identical trajectories agree in evaluations and energy; every
+    divergence starts at a near-tie (an evaluated candidate within twice the energy tolerance
+    of E_x) or at the box face.  Returns (identical, diverged)."""
+    g, E, ev, to, tr = d.sw_trace(X, E0, iters, seed=seed, run=run, gen=gen, slots=slots)
+    _, _, gxyz = d.eval(g, grad=False, xyz=True)
+    pp = oracle.params(ls_max_iters=iters)
+    same = diverged = 0
+    unexplained = []
+    for i in range(X.shape[0]):
+        assert E[i] <= E0[i]                                  # never worsens (S:303)
+        x, Eo, evo, oto, otr, otE = oracle.solis_wets_traced(P, pp, seed, 0, run, gen, int(slots[i]), X[i],
+                                                             float(E0[i]))
+        k = _first_diff(to[i], oto)
+        if k < 0:
+            same += 1
+            assert ev[i] == evo, (label, i, ev[i], evo)
+            # identical decisions: the genes agree within the FP32 rounding of the iterates, and
+            # the GPU's final energy is at NS tolerance against the oracle at the GPU's final
+            # pose (reading 22b; the oracle's own energy at its own genes differs from that only
+            # by its sensitivity to the genes' FP32 drift)
+            assert np.abs(g[i] - x).max() <= 1e-4 * max(1.0, np.abs(x).max()), (label, i)
+            at = P.energy_at(g[i].astype(np.float64), gxyz[i].astype(np.float64), grad=False)["E"]
+            assert abs(E[i] - at) <= e_tol(at), (label, i, E[i], at)
+            continue
+        diverged += 1
+        Ex, E1, E2 = otE[k]
+        near = abs(E1 - Ex) <= 2 * e_tol(Ex) or (not math.isnan(E2) and abs(E2 - Ex) <= 2 * e_tol(Ex))
+        if not near:
+            xo, _, _, _, _, _ = oracle.solis_wets_traced(P, oracle.params(ls_max_iters=k), seed, 0, run, gen,
+                                                        int(slots[i]), X[i], float(E0[i]))
+            near = box_margin(grid, P.pose(xo)) < 5e-3 or E1 > 5e4 or (not math.isnan(E2) and E2 > 5e4)
+        if not near:
+            unexplained.append((i, k, Ex, E1, E2, int(to[i][k]), int(oto[k])))
+    print(f"SW free run {label}: {same} identical, {diverged} diverged, unexplained {unexplained}")
+    assert not unexplained, unexplained
+    return same, diverged
+
+
+def ad_trajectory_check(d, P, grid, X, K, label, kink=False, extra_excl=None):
+    """Every iteration of the GPU's own ADADELTA trajectory (dock_ad_trace) at NS tolerance
+    against the oracle at the GPU's pose of that point (energy and gradient)."""
+    from test_gpu_parity import assert_parity, compare_at_pose
+    n = X.shape[0]
+    g, E, ev, tx, tE, tg = d.ad_trace(X, np.full(n, 1e30, np.float32), K)
+    assert (ev == K).all()                                    # exactly max_iters evaluations (D10)
+    flat = tx.reshape(-1, d.G)
+    _, _, xyz = d.eval(flat, grad=False, xyz=True)
+    c, fails = compare_at_pose(P, grid, flat, tE.reshape(-1), xyz, Gd=tg.reshape(-1, d.G), kink=kink,
+                               extra_excl=extra_excl)
+    assert_parity(c, fails, f"{label} ADADELTA trajectory ({n} x {K} iterations)")
+    # best tracking: the returned energy is the minimum of the traced ones (lowest iteration on ties)
+    assert np.array_equal(E, tE.min(axis=1))
+    return c
+
+
 @pytest.mark.parametrize("name,depth", [("1stp", 0), ("1stp", 1), ("3ce3", 0), ("pm", 0)])
 def test_sw_free_run_divergence_only_at_near_ties(dock, name, depth):
     cfg, lig, grid = config_inputs(name)
@@ -118,33 +175,8 @@ def test_sw_free_run_divergence_only_at_near_ties(dock, name, depth):
     n, iters = 48, 80
     X = random_genotypes(grid, d.T, n, seed=41, frac_out=0.0, shrink=0.2)
     E0 = np.array([P.energy(x, grad=False)["E"] for x in X], np.float32)
-    slots = np.arange(n, dtype=np.int32) * 3
-    seed, run, gen = 9, 2, 4
-    g, E, ev, to, tr = d.sw_trace(X, E0, iters, seed=seed, run=run, gen=gen, slots=slots)
-    pp = oracle.params(ls_max_iters=iters)
-    same = diverged = 0
-    unexplained = []
-    for i in range(n):
-        assert E[i] <= E0[i]                                  # never worsens
-        x, Eo, evo, oto, otr, otE = oracle.solis_wets_traced(P, pp, seed, 0, run, gen, int(slots[i]), X[i],
-                                                             float(E0[i]))
-        k = _first_diff(to[i], oto)
-        if k < 0:
-            same += 1
-            assert ev[i] == evo and abs(E[i] - Eo) <= e_tol(Eo), (i, E[i], Eo)
-            continue
-        diverged += 1
-        Ex, E1, E2 = otE[k]
-        near = abs(E1 - Ex) <= 2 * e_tol(Ex) or (not math.isnan(E2) and abs(E2 - Ex) <= 2 * e_tol(Ex))
-        if not near:
-            # a candidate at the box face (D4.5 jump): recompute the oracle's candidates of it k
-            xo, _, _, _, _, _ = oracle.solis_wets_traced(P, oracle.params(ls_max_iters=k), seed, 0, run, gen,
-                                                        int(slots[i]), X[i], float(E0[i]))
-            near = box_margin(grid, P.pose(xo)) < 5e-3 or E1 > 5e4 or (not math.isnan(E2) and E2 > 5e4)
-        if not near:
-            unexplained.append((i, k, Ex, E1, E2, int(to[i][k]), int(oto[k])))
-    print(f"SW free run {name} depth {depth}: {same} identical, {diverged} diverged, unexplained {unexplained}")
-    assert not unexplained, unexplained
+    same, _ = sw_free_run_check(d, P, grid, X, E0, iters, 9, 2, 4, np.arange(n, dtype=np.int32) * 3,
+                                f"{name} depth {depth}")
     assert same >= n // 2, same
     d.close()
 
