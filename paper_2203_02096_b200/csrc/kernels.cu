@@ -66,7 +66,8 @@ ScratchLayout scratch_layout(const LigDev &L, bool grad, int extra) {
     s.off_r = o; o += a16(dup ? 16 * 2 * L.Wg * L.NC : 16 * N);
     s.off_W = o; o += a16(48 * (T > 0 ? T : 1));
     s.off_tp = o; o += a16(4 * (T > 0 ? T : 1));
-    s.off_ts = o; if (grad) o += a16(32 * N);
+    // ts: back-projection rows (2N float4); also the packed tiles' pose rows (144 float4)
+    s.off_ts = o; if (grad) o += a16(32 * N > 16 * 144 || !L.packed ? 32 * N : 16 * 144);
     s.off_genes = o; o += a16(4 * G);
     s.off_grad = o; if (grad) o += a16(4 * G);
     s.off_extra = o; o += a16(extra);
@@ -114,6 +115,10 @@ __device__ __forceinline__ LigSm stage_ligand(const LigDev &L, uint8_t *sm, int 
     v.slot_mode = L.slot_mode;
     v.slot4 = reinterpret_cast<const float4 *>(sm + L.off_slot4);
     v.slotq = reinterpret_cast<const float *>(sm + L.off_slotq);
+    v.nhb = L.nhb;
+    v.packed = L.packed;
+    v.hbc = reinterpret_cast<const float4 *>(sm + L.off_hbc);
+    v.hbadj = reinterpret_cast<const int *>(sm + L.off_hbadj);
     v.energy_tiles = L.energy_tiles;
     v.wA_v = L.wA_v; v.wB_v = L.wB_v; v.wA_h = L.wA_h; v.wB_h = L.wB_h; v.qscale = L.qscale;
     return v;

@@ -438,6 +438,30 @@ int prepare_ligand(const dock_ligand *l, const dock_type_param *tp, int n_types,
     };
     L.n_slots = slot_count();
     L.slot_mode = (20 * L.n_slots <= 64 * 1024) ? 1 : 0;      // beyond: per-atom params + bits
+    // D5 lean slots (DK_LEAN): the H-bond pairs' 12-10 vdW terms go to a side list whose
+    // per-pair forces are staged in the per-group gradient scratch (2N float4), so a ligand
+    // with more than 2N H-bond pairs uses the per-atom-parameter tiles instead.
+    std::vector<int> hbl;   // dfs positions i < j, in pair-list order
+    for (size_t q = 0; q + 1 < pairs.size(); q += 2) {
+        const int ri = tp[l->type[pairs[q]]].role, rj = tp[l->type[pairs[q + 1]]].role;
+        if ((ri == 1 && rj == 2) || (ri == 2 && rj == 1)) {
+            const int di = pos[pairs[q]], dj = pos[pairs[q + 1]];
+            hbl.push_back(std::min(di, dj)); hbl.push_back(std::max(di, dj));
+        }
+    }
+    const int nhb = (int)hbl.size() / 2;
+#if defined(DK_LEAN) && DK_LEAN
+#if !defined(DK_FOLD) || DK_FOLD
+    L.lean = ad4 ? 0 : 1;
+#endif
+#endif
+    if (L.lean && L.slot_mode && nhb > 2 * N) L.slot_mode = 0;
+    if (!L.slot_mode) L.lean = 0;
+    // packed FP32x2 tiles (score.cuh tiles_packed): two full 32-atom chunks, no tail or the
+    // hybrid tail (its broadcast part packs chunks 0 and 1)
+#if !defined(DK_PACKED) || DK_PACKED
+    L.packed = (L.lean && Wg == 32 && Bf == 2 && !L.tail_rot && (tail == 0 || ((L.tail_seg >> 24) & 1))) ? 1 : 0;
+#endif
     if (!L.slot_mode && L.tail_seg) {                          // seg needs the slot tables
         L.tail_seg = 0;
         L.tail_rot = (tail > 0 && (Wg / 2 + Bf * Wg) * 40 < tail * ((Bf + 1) * 40 + 3 * 5)) ? 1 : 0;
@@ -451,7 +475,10 @@ int prepare_ligand(const dock_ligand *l, const dock_type_param *tp, int n_types,
     const bool sep_q = ad4;                    // D5 folds qq into slot4
 #endif
     L.off_slotq = off; off += (L.slot_mode && sep_q) ? a16(4 * L.n_slots) : 0;
-    L.grad_bytes = off;              // the gradient kernels stage only up to here
+    L.nhb = L.lean ? nhb : 0;
+    L.off_hbc = off; off += 16 * L.nhb;
+    L.off_hbadj = off; off += L.lean ? a16(4 * (N + 1 + 2 * L.nhb)) : 0;
+    L.grad_bytes = off;             // the gradient kernels stage only up to here
     // Energy-only kernels stage the pair list + per-pair constants (20 B per pair) when it
     // fits comfortably in shared memory; beyond that (P > ~4,900, e.g. N >= ~110) they use
     // the pair tiles like the gradient kernels, and the list is not stored at all.
@@ -589,16 +616,61 @@ int prepare_ligand(const dock_ligand *l, const dock_type_param *tp, int n_types,
             sq[slot] = (float)(332.06363 / 4.0 * (double)l->charge[ia] * (double)l->charge[ib]);
             return;
 #endif
+            const double req2 = req * req, r6 = req2 * req2 * req2, r12 = r6 * r6;
+            if (L.lean) {
+                // D5, lean (score.cuh slot_pair, DK_LEAN): {-eps r_eq^12, 2 eps r_eq^6,
+                // -(S_aV_b + S_bV_a) / (3 * 2 sigma^2), -(332.06363/4) q_a q_b / 3}; the H-bond
+                // pair's 12-10 vdW lives in the side list (zero vdW constants here)
+                const double sv = (double)ta.S * tb.V + (double)tb.S * ta.V;
+                const double qq = 332.06363 / 4.0 * (double)l->charge[ia] * (double)l->charge[ib];
+                s4[slot] = make_float4(hb ? 0.f : -(float)(eps * r12), hb ? 0.f : (float)(2.0 * eps * r6),
+                                       (float)(-sv / (3.0 * 2.0 * 3.6 * 3.6)), (float)(-qq / 3.0));
+                return;
+            }
             // D5, folded (score.cuh pair_eg_folded): {A r_eq^12, +-|B| r_eq^n (n = 10: negative),
             // S_aV_b + S_bV_a, 332.06363/4 q_a q_b}, in double then rounded once
-            const double req2 = req * req, r6 = req2 * req2 * req2, r12 = r6 * r6;
             s4[slot] = make_float4((float)((hb ? 5.0 : 1.0) * eps * r12),
                                    hb ? -(float)(6.0 * eps * r6 * req2 * req2) : (float)(2.0 * eps * r6),
                                    (float)((double)ta.S * tb.V + (double)tb.S * ta.V),
                                    (float)(332.06363 / 4.0 * (double)l->charge[ia] * (double)l->charge[ib]));
         };
         int slot = 0;
-        for (int I = 0; I < Bt; ++I)
+        if (L.packed) {
+            // packed order (score.cuh tiles_packed): per packed step two rows of Wg float4,
+            // {c_a.x, c_b.x, c_a.y, c_b.y} and {c_a.z, c_b.z, c_a.w, c_b.w}, from the lean
+            // constants c_a, c_b of its two slots (computed by fill into a scratch slot)
+            auto emit2 = [&](int da, int db, bool on_a, int ea, int eb, bool on_b) {
+                fill(slot, da, db, on_a);
+                const float4 a = s4[slot];
+                fill(slot, ea, eb, on_b);
+                const float4 b = s4[slot];
+                return std::make_pair(make_float4(a.x, b.x, a.y, b.y), make_float4(a.z, b.z, a.w, b.w));
+            };
+            auto put = [&](const std::vector<std::pair<float4, float4>> &row) {
+                for (int ln = 0; ln < Wg; ++ln) s4[slot + ln] = row[ln].first;
+                for (int ln = 0; ln < Wg; ++ln) s4[slot + Wg + ln] = row[ln].second;
+                slot += 2 * Wg;
+            };
+            std::vector<std::pair<float4, float4>> row(Wg);
+            for (int st = 1; st <= Wg / 2; ++st) {          // (a) tiles (0,0) and (1,1), step st
+                for (int ln = 0; ln < Wg; ++ln) {
+                    const bool once = !(st == Wg / 2 && ln >= Wg / 2);
+                    const int p = (ln + st) & (Wg - 1);
+                    row[ln] = emit2(ln, p, once, Wg + ln, Wg + p, once);
+                }
+                put(row);
+            }
+            for (int u = 0; u < Wg / 2; ++u) {              // (b) tile (0,1), steps u and u + 16
+                for (int ln = 0; ln < Wg; ++ln)
+                    row[ln] = emit2(ln, Wg + ((ln + u) & (Wg - 1)), true, ln, Wg + ((ln + u + Wg / 2) & (Wg - 1)), true);
+                put(row);
+            }
+            for (int k = 0; k < tail; ++k) {                // (c) tail atom k vs chunks 0 and 1
+                for (int ln = 0; ln < Wg; ++ln) row[ln] = emit2(ln, 2 * Wg + k, true, Wg + ln, 2 * Wg + k, true);
+                put(row);
+            }
+        }
+        for (int I = 0; I < Bt && !L.packed; ++I)
             for (int J = I; J < Bt; ++J) {
                 const int s0 = (I == J) ? 1 : 0, s1 = (I == J) ? Wg / 2 : Wg - 1;
                 for (int st = s0; st <= s1; ++st)
@@ -607,7 +679,9 @@ int prepare_ligand(const dock_ligand *l, const dock_type_param *tp, int n_types,
                         fill(slot, I * Wg + ln, J * Wg + ((ln + st) & (Wg - 1)), once);
                     }
             }
-        if (tail > 0 && L.tail_seg && hyb) {
+        if (L.packed) {
+            // (the hybrid tail's broadcast part is in the packed rows above)
+        } else if (tail > 0 && L.tail_seg && hyb) {
             // hyb, own chunks x tail by broadcast: tail atom k, chunk I, lane ln -> atom I*Wg + ln
             for (int k = 0; k < tail; ++k)
                 for (int I = 0; I < Bf; ++I)
@@ -637,6 +711,32 @@ int prepare_ligand(const dock_ligand *l, const dock_type_param *tp, int n_types,
                     for (int ln = 0; ln < Wg; ++ln, ++slot)
                         fill(slot, I * Wg + ln, Bf * Wg + k, I < Bf || ln < k);
         if (slot != L.n_slots) return fail("internal: pair-slot count mismatch");
+        if (L.lean) {
+            // H-bond side list: {5 eps r_eq^12, 6 eps r_eq^10, i | j << 16} and, per atom, the
+            // pairs it belongs to (fixed order: ascending pair index)
+            float4 *hc = reinterpret_cast<float4 *>(bl + L.off_hbc);
+            int *adj = reinterpret_cast<int *>(bl + L.off_hbadj);
+            std::vector<std::vector<int>> inc(N);
+            for (int h = 0; h < L.nhb; ++h) {
+                const int di = hbl[2 * h], dj = hbl[2 * h + 1];
+                const dock_type_param &ta = tp[l->type[order[di]]], &tb = tp[l->type[order[dj]]];
+                const double req = 0.5 * ((double)ta.R + (double)tb.R);
+                const double eps = std::sqrt((double)ta.eps * (double)tb.eps);
+                const double req2 = req * req, r10 = req2 * req2 * req2 * req2 * req2;
+                const uint32_t ij = (uint32_t)di | ((uint32_t)dj << 16);
+                float fij;
+                std::memcpy(&fij, &ij, 4);
+                hc[h] = make_float4((float)(5.0 * eps * r10 * req2), (float)(6.0 * eps * r10), fij, 0.f);
+                inc[di].push_back(2 * h);
+                inc[dj].push_back(2 * h + 1);
+            }
+            int e = N + 1;
+            for (int a = 0; a < N; ++a) {
+                adj[a] = e;
+                for (int v : inc[a]) adj[e++] = v;
+            }
+            adj[N] = e;
+        }
         if (std::getenv("DOCK_SLOT_STATS")) {   // diagnostics: steps (W slots) holding no pair at all
             const float4 *s4c = reinterpret_cast<const float4 *>(bl + L.off_slot4);
             int empty = 0, steps = L.n_slots / Wg, real = 0;

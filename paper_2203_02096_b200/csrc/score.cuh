@@ -76,6 +76,10 @@ struct LigSm {
     const float *slotq;           // pair-slot 332.06363/4 q_i q_j (slot_mode)
     int NC, tail_rot, slot_mode, tail_seg;
     int energy_tiles;             // energy-only evaluation through the pair tiles (no pair list)
+    int nhb;                      // lean D5: H-bond side list (LigDev::off_hbc / off_hbadj)
+    int packed;                   // lean D5, W = 32, two full chunks: packed FP32x2 tiles (LigDev::packed)
+    const float4 *hbc;
+    const int *hbadj;
     float wA_v, wB_v, wA_h, wB_h, qscale;   // D5-AD4 constants (LigDev; unused by D5)
 };
 
@@ -484,15 +488,235 @@ __device__ __forceinline__ void intra_tiles(const LigSm &L, const Scratch &S, in
 #ifndef DK_FOLD
 #define DK_FOLD 1   // D5 slot constants folded (A r_eq^12, B r_eq^n, SV, qq); 0: {r_eq^2, A, B, SV} + qq (A/B)
 #endif
+#ifndef DK_LEAN
+#define DK_LEAN 0   // 1: D5 lean slots + packed FP32x2 tiles (experiment: slower on B200)
+#endif
+#if !defined(DK_AD4) && DK_FOLD && DK_LEAN
+#define DK_LEAN_ON 1
+#endif
+
+#ifdef DK_LEAN_ON
+// Lean D5 slot arithmetic (prep.cpp, LigDev::lean).  Slot constants c = {-A', B', -(k/3) SV,
+// -qq/3} with A' = eps r_eq^12, B' = 2 eps r_eq^6 (the 12-6 form; zero for an H-bond pair,
+// whose 12-10 term is hb_side's), k = 1/2sigma^2, qq = 332.06363/4 q_i q_j.  With
+// inv = 1/rho^2 and i3 = inv^3:
+//   u = B' - A' i3, E_vdw = A' i6 - B' i3 = -i3 u;  v = B' - 2 A' i3, rho^2 dE_vdw/drho^2 = 3 i3 v;
+//   t = i3 v - qq inv / 3 = (rho^2 dE_vdw/drho^2 - E_el) / 3;  d = t inv - k E_ds / 3 = (dE/drho^2) / 3.
+// The energy goes to three sums scaled as above (EAcc: -E_vdw, -E_el/3, -k E_ds/3), unscaled
+// once per evaluation; the forces carry dE/drho^2 / 3, so the per-atom factor is 6, not 2.
+// 24 FP32 operations per slot instead of 29, and no per-slot H-bond selects.
+struct EAcc { float v = 0.0f, el = 0.0f, ds = 0.0f; };
+constexpr float kDsUnscale = -3.0f * 2.0f * 3.6f * 3.6f;   // -3/k
+__device__ __forceinline__ float eacc_total(const EAcc &a) { return fmaf(-3.0f, a.el, fmaf(kDsUnscale, a.ds, -a.v)); }
+constexpr float kForceScale = 6.0f;
+__device__ __forceinline__ void slot_pair(float rxi, float ryi, float rzi, float4 rj, float4 c, EAcc &e,
+                                          float &gxi, float &gyi, float &gzi, float &fx, float &fy, float &fz) {
+    const float dx = rxi - rj.x, dy = ryi - rj.y, dz = rzi - rj.z;
+    const float rho2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
+    const bool clamped = rho2 < 1e-4f;
+    const float r2 = fmaxf(rho2, 1e-4f);                 // 0.01 Å clamp
+    const float inv = rcp_approx(r2), i2 = inv * inv, i3 = i2 * inv;
+    const float u = fmaf(c.x, i3, c.y);
+    const float v = fmaf(c.x, i3, u);
+    e.v = fmaf(i3, u, e.v);
+    const float el = c.w * inv;
+    e.el += el;
+    const float t = fmaf(i3, v, el);
+    const float ed = c.z * ex2_approx(r2 * kExpScale);
+    e.ds += ed;
+    const float d = fmaf(t, inv, ed);
+    const float dE = clamped ? 0.0f : d;                 // zero force inside the clamp
+    gxi = fmaf(dE, dx, gxi); gyi = fmaf(dE, dy, gyi); gzi = fmaf(dE, dz, gzi);
+    fx = fmaf(-dE, dx, fx); fy = fmaf(-dE, dy, fy); fz = fmaf(-dE, dz, fz);
+}
+#define DK_SLOT(q) L.slot4[q]
+
+// The H-bond pairs' 12-10 vdW terms (lean slots): lane p takes pairs p, p + W, ...; its
+// force d (r_i - r_j) (d = (dE/drho^2) / 3, as in the tiles) is staged in the group's
+// gradient scratch, then every atom adds its pairs' forces in ascending pair order (+ as i,
+// - as j).  Fixed order: deterministic.  E = A'' i6 - B'' i5 (A'' = 5 eps r_eq^12,
+// B'' = 6 eps r_eq^10), rho^2 dE/drho^2 = -6 A'' i6 + 5 B'' i5.
+template <int W, int MAXC>
+__device__ __forceinline__ void hb_side(const LigSm &L, const Scratch &S, int sub, unsigned mask, float (&hx)[MAXC],
+                                        float (&hy)[MAXC], float (&hz)[MAXC], EAcc &e) {
+    for (int p = sub; p < L.nhb; p += W) {
+        const float4 c = L.hbc[p];
+        const uint32_t ij = __float_as_uint(c.z);
+        const float4 ri = S.r[ridx<W>((int)(ij & 0xffffu))], rj = S.r[ridx<W>((int)(ij >> 16))];
+        const float dx = ri.x - rj.x, dy = ri.y - rj.y, dz = ri.z - rj.z;
+        const float rho2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
+        const bool clamped = rho2 < 1e-4f;
+        const float r2 = fmaxf(rho2, 1e-4f);
+        const float inv = rcp_approx(r2), i2 = inv * inv, i3 = i2 * inv, i5 = i3 * i2, i6 = i3 * i3;
+        const float tA = c.x * i6, tB = c.y * i5;
+        e.v += tB - tA;
+        const float d = clamped ? 0.0f : fmaf(-6.0f, tA, 5.0f * tB) * inv * (1.0f / 3.0f);
+        S.ts[p] = make_float4(d * dx, d * dy, d * dz, 0.0f);
+    }
+    __syncwarp(mask);
+#pragma unroll
+    for (int c = 0; c < MAXC; ++c) {
+        const int a = sub + W * c;
+        if (a < L.N) {
+            const int k1 = L.hbadj[a + 1];
+            for (int k = L.hbadj[a]; k < k1; ++k) {
+                const int ent = L.hbadj[k];
+                const float4 f = S.ts[ent >> 1];
+                if (ent & 1) { hx[c] -= f.x; hy[c] -= f.y; hz[c] -= f.z; }
+                else { hx[c] += f.x; hy[c] += f.y; hz[c] += f.z; }
+            }
+        }
+    }
+    __syncwarp(mask);   // the back-projection reuses the scratch
+}
+
+// ---- Packed FP32x2 lean slots (sm_100 fma/mul/add/sub.rn.f32x2: one instruction, two
+// independent IEEE FP32 operations) for the two-full-chunk shape (W = 32, Bf = 2: 64 <= N
+// <= 96 with a hybrid tail; LigDev::packed, prep.cpp).  Every lane evaluates TWO slots per
+// instruction stream, so the 24 FP32 operations of a lean slot cost 12 issue slots:
+//   (a) diagonal pair: tiles (0,0) and (1,1) together, step s = 1..16 (own atoms sub and
+//       32 + sub, partners (sub + s) of chunk 0 and of chunk 1);
+//   (b) split tile (0,1): steps u and u + 16 together, u = 0..15 (own atom sub twice);
+//   (c) hybrid tail: tail atom k against chunks 0 and 1 together.
+// The partner poses of (a) and (b) are re-laid out per evaluation as {x_a, x_b, y_a, y_b}
+// + {z_a, z_b} rows (one LDS.128 + one LDS.64 per packed step), in the group's gradient
+// scratch (dead until the back-projection).  The slot constants of packed step q are two
+// float4 rows [q][0..W) = {-A'_a, -A'_b, B'_a, B'_b} and [q][W..2W) = {SV_a, SV_b, Q_a, Q_b}
+// (the lean constants of slots a and b).  Same arithmetic per slot as slot_pair, so the
+// results equal the scalar lean path's up to the order of the partial sums.
+typedef unsigned long long f2_t;
+__device__ __forceinline__ f2_t f2_pk(float a, float b) {
+    f2_t r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+    return r;
+}
+__device__ __forceinline__ float f2_lo(f2_t v) {
+    float a, b;
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(v));
+    return a;
+}
+__device__ __forceinline__ float f2_hi(f2_t v) {
+    float a, b;
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(v));
+    return b;
+}
+__device__ __forceinline__ f2_t add2(f2_t a, f2_t b) { f2_t d; asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b)); return d; }
+__device__ __forceinline__ f2_t sub2(f2_t a, f2_t b) { f2_t d; asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b)); return d; }
+__device__ __forceinline__ f2_t mul2(f2_t a, f2_t b) { f2_t d; asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b)); return d; }
+__device__ __forceinline__ f2_t fma2(f2_t a, f2_t b, f2_t c) {
+    f2_t d;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+    return d;
+}
+__device__ __forceinline__ f2_t f2_shfl(f2_t v, int src, unsigned mask) {
+    return f2_pk(__shfl_sync(mask, f2_lo(v), src), __shfl_sync(mask, f2_hi(v), src));
+}
+struct EAcc2 { f2_t v = 0ull, el = 0ull, ds = 0ull; };   // bit pattern 0 = (+0.0f, +0.0f)
+
+__device__ __forceinline__ void slot_pair2(f2_t ox, f2_t oy, f2_t oz, f2_t px, f2_t py, f2_t pz, float4 ca, float4 cb,
+                                           EAcc2 &e, f2_t &gx, f2_t &gy, f2_t &gz, f2_t &fx, f2_t &fy, f2_t &fz) {
+    const f2_t dx = sub2(ox, px), dy = sub2(oy, py), dz = sub2(oz, pz);
+    const f2_t rho2 = fma2(dx, dx, fma2(dy, dy, mul2(dz, dz)));
+    const float q0 = f2_lo(rho2), q1 = f2_hi(rho2);
+    const float r0 = fmaxf(q0, 1e-4f), r1 = fmaxf(q1, 1e-4f);   // 0.01 Å clamp
+    const f2_t inv = f2_pk(rcp_approx(r0), rcp_approx(r1));
+    const f2_t i2 = mul2(inv, inv), i3 = mul2(i2, inv);
+    const f2_t u = fma2(f2_pk(ca.x, ca.y), i3, f2_pk(ca.z, ca.w));
+    const f2_t v = fma2(f2_pk(ca.x, ca.y), i3, u);
+    e.v = fma2(i3, u, e.v);
+    const f2_t el = mul2(f2_pk(cb.z, cb.w), inv);
+    e.el = add2(e.el, el);
+    const f2_t t = fma2(i3, v, el);
+    const f2_t ea = mul2(f2_pk(r0, r1), f2_pk(kExpScale, kExpScale));
+    const f2_t ed = mul2(f2_pk(cb.x, cb.y), f2_pk(ex2_approx(f2_lo(ea)), ex2_approx(f2_hi(ea))));
+    e.ds = add2(e.ds, ed);
+    const f2_t d = fma2(t, inv, ed);
+    const f2_t dE = f2_pk(q0 < 1e-4f ? 0.0f : f2_lo(d), q1 < 1e-4f ? 0.0f : f2_hi(d));   // zero force in the clamp
+    gx = fma2(dE, dx, gx); gy = fma2(dE, dy, gy); gz = fma2(dE, dz, gz);
+    fx = fma2(dE, dx, fx); fy = fma2(dE, dy, fy); fz = fma2(dE, dz, fz);   // partner: subtracted on return
+}
+
+#ifndef DK_PACK_UNROLL
+#define DK_PACK_UNROLL 2   // packed steps unrolled (A/B: scripts/variants.py)
+#endif
+constexpr int kPackUnroll = DK_PACK_UNROLL;
+
+// (a) + (b): the full-chunk tiles of the Bf = 2 shape.  Own-atom forces go to hx[0..1] etc.
+template <int W, int MAXC>
+__device__ __forceinline__ void tiles_packed(const LigSm &L, const Scratch &S, int sub, unsigned mask,
+                                             const float (&rx)[MAXC], const float (&ry)[MAXC], const float (&rz)[MAXC],
+                                             float (&hx)[MAXC], float (&hy)[MAXC], float (&hz)[MAXC], EAcc2 &e2) {
+    static_assert(W == 32 && MAXC >= 2, "packed tiles: two full 32-atom chunks");
+    float4 *pdxy = S.ts, *psxy = S.ts + 48;                         // [48] rows each
+    float2 *pdz = reinterpret_cast<float2 *>(S.ts + 96), *psz = pdz + 48;
+    {
+        const float x16 = __shfl_xor_sync(mask, rx[1], 16), y16 = __shfl_xor_sync(mask, ry[1], 16),
+                    z16 = __shfl_xor_sync(mask, rz[1], 16);
+        const float4 d4 = make_float4(rx[0], rx[1], ry[0], ry[1]), s4 = make_float4(rx[1], x16, ry[1], y16);
+        const float2 d2 = make_float2(rz[0], rz[1]), s2 = make_float2(rz[1], z16);
+        pdxy[sub] = d4; pdz[sub] = d2; psxy[sub] = s4; psz[sub] = s2;
+        if (sub < 16) { pdxy[sub + 32] = d4; pdz[sub + 32] = d2; psxy[sub + 32] = s4; psz[sub + 32] = s2; }
+    }
+    __syncwarp(mask);
+    const int src = sub + 1;                                        // shfl.idx takes the lane mod 32
+    const float4 *cst = L.slot4 + sub;
+    // own-atom pairs re-read from the rows (64-bit register pairs from the loads; the scalar
+    // pose registers are dead here, eval_group reloads them after the tiles)
+    const float4 o4 = pdxy[sub];
+    const float2 o2 = pdz[sub];
+    // (a) diagonal pair, packed steps q = 0..15 (tile step s = q + 1)
+    {
+        const f2_t ox = f2_pk(o4.x, o4.y), oy = f2_pk(o4.z, o4.w), oz = f2_pk(o2.x, o2.y);
+        f2_t gx = 0ull, gy = 0ull, gz = 0ull, fx = 0ull, fy = 0ull, fz = 0ull;
+#pragma unroll kPackUnroll
+        for (int q = 0; q < 16; ++q) {
+            const float4 xy = pdxy[sub + q + 1];
+            const float2 zz = pdz[sub + q + 1];
+            slot_pair2(ox, oy, oz, f2_pk(xy.x, xy.y), f2_pk(xy.z, xy.w), f2_pk(zz.x, zz.y), cst[q * 2 * W],
+                       cst[q * 2 * W + W], e2, gx, gy, gz, fx, fy, fz);
+            fx = f2_shfl(fx, src, mask); fy = f2_shfl(fy, src, mask); fz = f2_shfl(fz, src, mask);
+        }
+        const int back = (sub - 17) & (W - 1);
+        fx = f2_shfl(fx, back, mask); fy = f2_shfl(fy, back, mask); fz = f2_shfl(fz, back, mask);
+        const f2_t hx01 = sub2(gx, fx), hy01 = sub2(gy, fy), hz01 = sub2(gz, fz);
+        hx[0] += f2_lo(hx01); hx[1] += f2_hi(hx01);
+        hy[0] += f2_lo(hy01); hy[1] += f2_hi(hy01);
+        hz[0] += f2_lo(hz01); hz[1] += f2_hi(hz01);
+    }
+    // (b) split tile (0,1), packed steps q = 16..31 (tile steps u and u + 16, u = q - 16)
+    {
+        const f2_t ox = f2_pk(o4.x, o4.x), oy = f2_pk(o4.z, o4.z), oz = f2_pk(o2.x, o2.x);
+        f2_t gx = 0ull, gy = 0ull, gz = 0ull, fx = 0ull, fy = 0ull, fz = 0ull;
+#pragma unroll kPackUnroll
+        for (int u = 0; u < 16; ++u) {
+            const float4 xy = psxy[sub + u];
+            const float2 zz = psz[sub + u];
+            slot_pair2(ox, oy, oz, f2_pk(xy.x, xy.y), f2_pk(xy.z, xy.w), f2_pk(zz.x, zz.y), cst[(16 + u) * 2 * W],
+                       cst[(16 + u) * 2 * W + W], e2, gx, gy, gz, fx, fy, fz);
+            fx = f2_shfl(fx, src, mask); fy = f2_shfl(fy, src, mask); fz = f2_shfl(fz, src, mask);
+        }
+        // stream a (steps u) ends 16 lanes past its owner, stream b (steps u + 16) at its owner
+        const int back = sub ^ 16;
+        hx[1] -= __shfl_sync(mask, f2_lo(fx), back) + f2_hi(fx);
+        hy[1] -= __shfl_sync(mask, f2_lo(fy), back) + f2_hi(fy);
+        hz[1] -= __shfl_sync(mask, f2_lo(fz), back) + f2_hi(fz);
+        hx[0] += f2_lo(gx) + f2_hi(gx); hy[0] += f2_lo(gy) + f2_hi(gy); hz[0] += f2_lo(gz) + f2_hi(gz);
+    }
+    __syncwarp(mask);   // the scratch rows are reused (H-bond side list, back-projection)
+}
+#else
+struct EAcc { float e = 0.0f; };
+__device__ __forceinline__ float eacc_total(const EAcc &a) { return a.e; }
+constexpr float kForceScale = 2.0f;
 #if defined(DK_AD4) || !DK_FOLD
 // One pair inside the slot-table tiles: constants c = {r_eq, A, B, SV} and qq from the
 // slot (all zero for a non-pair, so no membership test), force as in tile_pair.
-__device__ __forceinline__ void slot_pair(float rxi, float ryi, float rzi, float4 rj, float4 c, float qq, float &e,
+__device__ __forceinline__ void slot_pair(float rxi, float ryi, float rzi, float4 rj, float4 c, float qq, EAcc &e,
                                           float &gxi, float &gyi, float &gzi, float &fx, float &fy, float &fz) {
     const float dx = rxi - rj.x, dy = ryi - rj.y, dz = rzi - rj.z;
     const float rho2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
     float dE;
-    e += pair_eg_ab(rho2, c.x, c.y, c.z, c.w, qq, dE);
+    e.e += pair_eg_ab(rho2, c.x, c.y, c.z, c.w, qq, dE);
     gxi = fmaf(dE, dx, gxi); gyi = fmaf(dE, dy, gyi); gzi = fmaf(dE, dz, gzi);
     fx = fmaf(-dE, dx, fx); fy = fmaf(-dE, dy, fy); fz = fmaf(-dE, dz, fz);
 }
@@ -517,16 +741,17 @@ __device__ __forceinline__ float pair_eg_folded(float rho2, float4 c, float &dE)
     dE = clamped ? 0.0f : d;
     return (tA - tB) + Eel + Eds;
 }
-__device__ __forceinline__ void slot_pair(float rxi, float ryi, float rzi, float4 rj, float4 c, float &e,
+__device__ __forceinline__ void slot_pair(float rxi, float ryi, float rzi, float4 rj, float4 c, EAcc &e,
                                           float &gxi, float &gyi, float &gzi, float &fx, float &fy, float &fz) {
     const float dx = rxi - rj.x, dy = ryi - rj.y, dz = rzi - rj.z;
     const float rho2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
     float dE;
-    e += pair_eg_folded(rho2, c, dE);
+    e.e += pair_eg_folded(rho2, c, dE);
     gxi = fmaf(dE, dx, gxi); gyi = fmaf(dE, dy, gyi); gzi = fmaf(dE, dz, gzi);
     fx = fmaf(-dE, dx, fx); fy = fmaf(-dE, dy, fy); fz = fmaf(-dE, dz, fz);
 }
 #define DK_SLOT(q) L.slot4[q]
+#endif
 #endif
 
 // intra_tiles with precomputed pair-slot constants (L.slot_mode, prep.cpp): the same
@@ -536,7 +761,8 @@ template <int W, int MAXC>
 __device__ __forceinline__ void intra_tiles_slots(const LigSm &L, const Scratch &S, int sub, unsigned mask,
                                                   const float (&rx)[MAXC], const float (&ry)[MAXC],
                                                   const float (&rz)[MAXC], float (&gx)[MAXC], float (&gy)[MAXC],
-                                                  float (&gz)[MAXC], float &e) {
+                                                  float (&gz)[MAXC], float &e_out) {
+    EAcc e;
     const int N = L.N;
     const int Bf = N / W, t = N - Bf * W;
     const bool tail_rot = L.tail_rot != 0;
@@ -545,9 +771,33 @@ __device__ __forceinline__ void intra_tiles_slots(const LigSm &L, const Scratch 
 #pragma unroll
     for (int c = 0; c < MAXC; ++c) hx[c] = hy[c] = hz[c] = 0.0f;
     int slot0 = 0;                        // first slot of the current tile
+#ifdef DK_LEAN_ON
+    EAcc2 e2;
+    bool packed = false;
+    if constexpr (W == 32 && (MAXC == 2 || MAXC == 3)) packed = L.packed != 0;
+    if (packed) {
+        if constexpr (W == 32 && (MAXC == 2 || MAXC == 3)) {
+            // the intermolecular gradients wait in the (unused here) duplicate pose half, so
+            // the packed tiles have their registers
+#pragma unroll
+            for (int c = 0; c < MAXC; ++c)
+                if (sub + W * c < N) S.r[ridx<W>(sub + W * c) + W] = make_float4(gx[c], gy[c], gz[c], 0.0f);
+            tiles_packed<W, MAXC>(L, S, sub, mask, rx, ry, rz, hx, hy, hz, e2);
+#pragma unroll
+            for (int c = 0; c < MAXC; ++c)
+                if (sub + W * c < N) {
+                    const float4 g4 = S.r[ridx<W>(sub + W * c) + W];
+                    gx[c] = g4.x; gy[c] = g4.y; gz[c] = g4.z;
+                }
+        }
+        slot0 = 64 * W;                   // 32 packed steps x 2W rows = the 64 scalar tile steps
+    }
+#else
+    constexpr bool packed = false;
+#endif
 #pragma unroll
     for (int I = 0; I < MAXC; ++I) {
-        if (I >= Bt) break;
+        if (I >= Bt || packed) break;
 #pragma unroll
         for (int J = I; J < MAXC; ++J) {
             if (J >= Bt) break;
@@ -579,17 +829,17 @@ __device__ __forceinline__ void intra_tiles_slots(const LigSm &L, const Scratch 
             hz[J] += __shfl_sync(mask, az, backa, W) + __shfl_sync(mask, bz, backb, W);
 #else
             float fx = 0.f, fy = 0.f, fz = 0.f;
+            // the partner accumulator moves one lane after EVERY step (the last shift is
+            // folded into the return offset): no per-step guard in the unrolled loop
 #pragma unroll kTileUnroll
             for (int s = s0; s <= s1; ++s) {
                 slot_pair(rx[I], ry[I], rz[I], rrow[s], DK_SLOT(cbase + s * W), e, hx[I], hy[I], hz[I], fx, fy, fz);
-                if (s < s1) {
-                    const int src = (sub + 1) & (W - 1);
-                    fx = __shfl_sync(mask, fx, src, W);
-                    fy = __shfl_sync(mask, fy, src, W);
-                    fz = __shfl_sync(mask, fz, src, W);
-                }
+                const int src = (sub + 1) & (W - 1);
+                fx = __shfl_sync(mask, fx, src, W);
+                fy = __shfl_sync(mask, fy, src, W);
+                fz = __shfl_sync(mask, fz, src, W);
             }
-            const int back = (sub - s1) & (W - 1);
+            const int back = (sub - s1 - 1) & (W - 1);
             fx = __shfl_sync(mask, fx, back, W);
             fy = __shfl_sync(mask, fy, back, W);
             fz = __shfl_sync(mask, fz, back, W);
@@ -613,6 +863,30 @@ __device__ __forceinline__ void intra_tiles_slots(const LigSm &L, const Scratch 
         const float4 *trow = S.r + Bf * 2 * W;                  // tail chunk (positions 0..tp-1)
         float fx = 0.f, fy = 0.f, fz = 0.f;
         if ((L.tail_seg >> 24) & 1) {
+#ifdef DK_LEAN_ON
+          if (packed) {
+            if constexpr (W == 32 && (MAXC == 2 || MAXC == 3)) {
+                // (c) tail atom k against chunks 0 and 1 together (packed step k)
+                const float4 o4 = S.ts[sub];                    // tiles_packed's rows: {x0, x1, y0, y1}
+                const float2 o2 = reinterpret_cast<const float2 *>(S.ts + 96)[sub];
+                const f2_t ox = f2_pk(o4.x, o4.y), oy = f2_pk(o4.z, o4.w), oz = f2_pk(o2.x, o2.y);
+                f2_t gx2 = 0ull, gy2 = 0ull, gz2 = 0ull;
+                for (int k = 0; k < t; ++k) {
+                    const float4 rj = trow[k];                  // uniform: shared-memory broadcast
+                    f2_t px2 = 0ull, py2 = 0ull, pz2 = 0ull;
+                    slot_pair2(ox, oy, oz, f2_pk(rj.x, rj.x), f2_pk(rj.y, rj.y), f2_pk(rj.z, rj.z),
+                               L.slot4[slot0 + k * 2 * W + sub], L.slot4[slot0 + k * 2 * W + W + sub], e2, gx2, gy2,
+                               gz2, px2, py2, pz2);
+                    float px = -(f2_lo(px2) + f2_hi(px2)), py = -(f2_lo(py2) + f2_hi(py2)), pz = -(f2_lo(pz2) + f2_hi(pz2));
+                    px = gsum<W>(px, mask); py = gsum<W>(py, mask); pz = gsum<W>(pz, mask);
+                    if (sub == k) { fx += px; fy += py; fz += pz; }
+                }
+                hx[0] += f2_lo(gx2); hx[1] += f2_hi(gx2);
+                hy[0] += f2_lo(gy2); hy[1] += f2_hi(gy2);
+                hz[0] += f2_lo(gz2); hz[1] += f2_hi(gz2);
+            }
+          } else
+#endif
 #pragma unroll kHybUnroll
             for (int k = 0; k < t; ++k) {
                 const float4 rj = trow[k];                      // uniform: shared-memory broadcast
@@ -681,9 +955,17 @@ __device__ __forceinline__ void intra_tiles_slots(const LigSm &L, const Scratch 
                 if (c == Bf && sub == k) { hx[c] += fx; hy[c] += fy; hz[c] += fz; }
         }
     }
+#ifdef DK_LEAN_ON
+    if (L.nhb > 0) hb_side<W, MAXC>(L, S, sub, mask, hx, hy, hz, e);
+#endif
+#ifdef DK_LEAN_ON
+    e.v += f2_lo(e2.v) + f2_hi(e2.v); e.el += f2_lo(e2.el) + f2_hi(e2.el); e.ds += f2_lo(e2.ds) + f2_hi(e2.ds);
+#endif
+    e_out += eacc_total(e);
 #pragma unroll
     for (int c = 0; c < MAXC; ++c) {
-        gx[c] = fmaf(2.0f, hx[c], gx[c]); gy[c] = fmaf(2.0f, hy[c], gy[c]); gz[c] = fmaf(2.0f, hz[c], gz[c]);
+        gx[c] = fmaf(kForceScale, hx[c], gx[c]); gy[c] = fmaf(kForceScale, hy[c], gy[c]);
+        gz[c] = fmaf(kForceScale, hz[c], gz[c]);
     }
 }
 
@@ -926,6 +1208,18 @@ __device__ float eval_group(const LigSm &L, const GridDev &grid, const Scratch &
     } else {
         if (L.slot_mode) intra_tiles_slots<W, MAXC>(L, S, sub, mask, rx, ry, rz, gx, gy, gz, e_part);
         else intra_tiles<W, MAXC>(L, S, sub, mask, rx, ry, rz, gx, gy, gz, e_part);
+#ifdef DK_LEAN_ON
+        // the pose again from the group's rows (the same values): the tiles need not keep
+        // the scalar pose registers alive (the packed tiles work on 64-bit register pairs)
+#pragma unroll
+        for (int c = 0; c < MAXC; ++c) {
+            const int a = sub + W * c;
+            if (a < L.N) {
+                const float4 rv = S.r[ridx<W>(a)];
+                rx[c] = rv.x; ry[c] = rv.y; rz[c] = rv.z;
+            }
+        }
+#endif
         if constexpr (PARTS == kIntra) {
             const float E = gsum<W>(e_part, mask);
 #pragma unroll
