@@ -404,6 +404,12 @@ int dock_run_branches(const dock_ctx *ctx);
    0 before the first run; -1 for a NULL context. */
 int dock_last_engine(const dock_ctx *ctx);
 
+/* Gradient pair-tile schedule prep.cpp chose for this ligand:
+   bit 0 slot tables, bit 1 tail as a padded rotated chunk, bit 2 segmented tail,
+   bit 3 hybrid tail, bit 4 packed FP32x2 tiles; bits 8..15 the H-bond pairs of the packed
+   side list.  -1 for a NULL context.  Host-side only (no device work). */
+int dock_tile_schedule(const dock_ctx *ctx);
+
 /* Bytes dock_init copied host -> device (packed grid + ligand block + atom map). */
 int64_t dock_upload_bytes(const dock_ctx *ctx);
 

@@ -169,6 +169,7 @@ def _load():
         "dock_upload_bytes": (i64, [v]),
         "dock_run_branches": (i32, [v]),
         "dock_last_engine": (i32, [v]),
+        "dock_tile_schedule": (i32, [v]),
         "dock_screen": (i32, [P(Grids), P(TypeParam), P(Ligand), i32, P(u32), P(Params), P(ScreenOpts), i32, i32,
                               i64, u64, P(f), P(i32), P(f), P(i64), P(i32), P(i32), P(ScreenStats)]),
         "dock_screen_last_error": (C.c_char_p, []),
@@ -191,7 +192,7 @@ EXPORTED = ("dock_params_default", "dock_builtin_type_param", "dock_init", "dock
             "dock_topology", "dock_kernel_stats", "dock_upload_bytes", "dock_screen", "dock_screen_last_error",
             "dock_bench_part", "dock_eval_terms", "dock_cluster", "dock_write_result", "dock_run_branches",
             "dock_write_screen", "dock_last_engine", "dock_init_population", "dock_sw_trace",
-            "dock_ad_trace", "dock_bench_l2_gather")
+            "dock_ad_trace", "dock_bench_l2_gather", "dock_tile_schedule")
 
 
 def write_result(res: dict, fmt: str = "json", timings: dict | None = None) -> str:
@@ -472,6 +473,13 @@ class Docker:
     def engine(self) -> str:
         """Generation engine of the last run (dock_last_engine): lockstep, branches or clusters."""
         return self.ENGINES[int(lib.dock_last_engine(self._ctx))]
+
+    @property
+    def tile_schedule(self) -> dict:
+        """Gradient pair-tile schedule of this ligand (dock_tile_schedule)."""
+        v = int(lib.dock_tile_schedule(self._ctx))
+        return {"slots": bool(v & 1), "tail": ("rot" if v & 2 else "seg" if v & 4 else "hyb" if v & 8 else "bcast"),
+                "packed": bool(v & 16), "hb_side_pairs": (v >> 8) & 0xff}
 
     @property
     def upload_bytes(self) -> int:

@@ -441,6 +441,12 @@ int64_t dock_launch_count(const dock_ctx *c) { return c ? c->launches : -1; }
 
 int dock_run_branches(const dock_ctx *c) { return c ? c->last_branches : -1; }
 int dock_last_engine(const dock_ctx *c) { return c ? c->last_engine : -1; }
+int dock_tile_schedule(const dock_ctx *c) {
+    if (!c) return -1;
+    const dk::LigDev &L = c->prep.layout;
+    return (L.slot_mode ? 1 : 0) | (L.tail_rot ? 2 : 0) | (L.tail_seg && !((L.tail_seg >> 24) & 1) ? 4 : 0) |
+           ((L.tail_seg >> 24) & 1 ? 8 : 0) | (L.packed ? 16 : 0) | ((L.nhb & 0xff) << 8);
+}
 
 int64_t dock_upload_bytes(const dock_ctx *c) {
     return c ? (int64_t)(c->rec->bytes + c->prep.blob.size() + sizeof(int) * c->prep.N) : -1;

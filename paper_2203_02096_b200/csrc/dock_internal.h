@@ -58,18 +58,20 @@ struct LigDev {
     int off_slot4;    // float4[n_slots]
     int off_slotq;    // float[n_slots]
     int n_slots;
-    // D5 "lean" slot constants (DK_LEAN builds): every slot holds the 12-6
-    // form {-A r_eq^12, 2 eps r_eq^6, -(k/3)(S_iV_j + S_jV_i), -(332.06363/4) q_i q_j / 3}
-    // (k = 1/2sigma^2); an H-bond pair's slot keeps its desolvation and electrostatics with
-    // zero vdW constants, and its 12-10 vdW term is evaluated once per pair from the side
-    // list below and delivered to both atoms in a fixed order (per-atom incidence lists).
-    int lean;
-    int nhb;          // H-bond pairs (lean side list)
+    // Packed FP32x2 tiles (D5, Wg = 32, two full chunks and a hybrid tail: 65 <= N <= 96;
+    // score.cuh tiles_packed).  The slot table then starts with the packed rows:
+    // per packed step q two rows [q][0..Wg) {-A'_a, -A'_b, B'_a, B'_b}, [q][Wg..2Wg)
+    // {SV'_a, SV'_b, Q_a, Q_b} of the lean constants of its two slots (A' = eps r_eq^12,
+    // B' = 2 eps r_eq^6, SV' = -(S_iV_j + S_jV_i) / (3 * 2 sigma^2), Q = -(332.06363/4) q_i q_j / 3;
+    // an H-bond pair's row keeps zero vdW constants and its 12-10 vdW term goes to the side
+    // list below); the tail x tail rounds that follow keep the folded constants.
+    int packed;
+    int nhb;          // H-bond pairs of the packed rows
     int off_hbc;      // float4[nhb] {5 eps r_eq^12, 6 eps r_eq^10, bits(i | j << 16), 0} (dfs)
-    int off_hbadj;    // int[N + 1] incidence starts, then int[2 nhb] entries pair << 1 | (atom is j)
-    int packed;       // lean, Wg = 32, two full chunks (64 <= N), no tail or a hybrid tail: packed
-                      //   FP32x2 tiles (score.cuh tiles_packed) and this slot order: per packed step
-                      //   q two rows [q][0..Wg) {-A'_a, -A'_b, B'_a, B'_b}, [q][Wg..2Wg) {SV_a, SV_b, Q_a, Q_b}
+    int nhbr;         // rounds of the per-atom sums (score.cuh hb_side)
+    int off_hbseg;    // int[nhbr][32] atom contributions, sorted by atom, never split across
+                      //   rounds: pair | neg << 8 | first lane << 9 | last << 14 | valid << 15 |
+                      //   atom << 16; then int[NC] per-chunk lane masks of atoms with H-bond pairs
     int off_ppar;     // float4[NC][2*Wg] partner params {R/2, sqrt(eps), S, V}, duplicated chunks;
                       //   R/2 negated for acceptors and sqrt(eps) negated for donors (role
                       //   in the sign bits; magnitudes via free |.| operand modifiers)

@@ -66,7 +66,8 @@ ScratchLayout scratch_layout(const LigDev &L, bool grad, int extra) {
     s.off_r = o; o += a16(dup ? 16 * 2 * L.Wg * L.NC : 16 * N);
     s.off_W = o; o += a16(48 * (T > 0 ? T : 1));
     s.off_tp = o; o += a16(4 * (T > 0 ? T : 1));
-    // ts: back-projection rows (2N float4); also the packed tiles' pose rows (144 float4)
+    // ts: back-projection rows (2N float4); packed tiles: also their pose rows (144 float4)
+    // and the H-bond pair forces + per-atom totals (nhb + N <= 2N float4, prep.cpp)
     s.off_ts = o; if (grad) o += a16(32 * N > 16 * 144 || !L.packed ? 32 * N : 16 * 144);
     s.off_genes = o; o += a16(4 * G);
     s.off_grad = o; if (grad) o += a16(4 * G);
@@ -116,9 +117,9 @@ __device__ __forceinline__ LigSm stage_ligand(const LigDev &L, uint8_t *sm, int 
     v.slot4 = reinterpret_cast<const float4 *>(sm + L.off_slot4);
     v.slotq = reinterpret_cast<const float *>(sm + L.off_slotq);
     v.nhb = L.nhb;
-    v.packed = L.packed;
+    v.nhbr = L.nhbr;
+    v.hbseg = reinterpret_cast<const int *>(sm + L.off_hbseg);
     v.hbc = reinterpret_cast<const float4 *>(sm + L.off_hbc);
-    v.hbadj = reinterpret_cast<const int *>(sm + L.off_hbadj);
     v.energy_tiles = L.energy_tiles;
     v.wA_v = L.wA_v; v.wB_v = L.wB_v; v.wA_h = L.wA_h; v.wB_h = L.wB_h; v.qscale = L.qscale;
     return v;
@@ -144,7 +145,7 @@ __device__ __forceinline__ float nan_inf(float v) { return isnan(v) ? INFINITY :
 // ---------------------------------------------------------------------------
 // k_eval: batched energy (+ gradient, + pose) of given genotypes.
 // ---------------------------------------------------------------------------
-template <int W, int MAXC, bool GRAD, int PARTS = kAll>
+template <int W, int MAXC, bool GRAD, int PARTS = kAll, bool PK = false>
 __global__ void __launch_bounds__(256) k_eval(const LigDev L, const GridDev g, const ScratchLayout SL,
                                               int n, const float *__restrict__ genes, float *E,
                                               float *grad, float *xyz, const int *__restrict__ dfs2orig) {
@@ -159,7 +160,7 @@ __global__ void __launch_bounds__(256) k_eval(const LigDev L, const GridDev g, c
     const int G = L.G;
     for (int j = sub; j < G; j += W) S.genes[j] = genes[(size_t)gi * G + j];
     __syncwarp(mask);
-    const float e = eval_group<W, MAXC, GRAD, PARTS>(Ls, g, S, sub, mask);
+    const float e = eval_group<W, MAXC, GRAD, PARTS, 1, PK>(Ls, g, S, sub, mask);
     if (sub == 0) E[gi] = e;
     if (GRAD && grad)
         for (int j = sub; j < G; j += W) grad[(size_t)gi * G + j] = S.grad[j];
@@ -431,7 +432,7 @@ __device__ __forceinline__ void ls_finish(const SearchDev &sp, const PopDev &pop
 #endif
 // TRACE: the parity-hook instantiation (dock_ad_trace: fed inputs and traces, LsArgs::ad_*);
 // the production instantiation carries none of that code (register pressure at the cap).
-template <int W, int MAXC, bool TRACE = false>
+template <int W, int MAXC, bool TRACE = false, bool PK = false>
 __global__ void __launch_bounds__(256, (MAXC <= 4 ? DK_ADA_MINB : 1)) k_ls_adadelta(const LigDev L, const GridDev g, const ScratchLayout SL,
                                                      const SearchDev sp, const PopDev pop, const LsArgs a) {
     extern __shared__ uint4 smem_u4[];
@@ -461,7 +462,7 @@ __global__ void __launch_bounds__(256, (MAXC <= 4 ? DK_ADA_MINB : 1)) k_ls_adade
     const float rho = sp.ad_rho, eps = sp.ad_eps;
     __syncwarp(mask);
     for (int it = 0; it < a.iters; ++it) {
-        float E = eval_group<W, MAXC, true>(Ls, g, S, sub, mask);
+        float E = eval_group<W, MAXC, true, kAll, 1, PK>(Ls, g, S, sub, mask);
         if constexpr (TRACE) {            // parity hook only
             const size_t row = (size_t)t.idx * a.iters + it;
             if (a.ad_fed && t.act) {
@@ -1087,7 +1088,7 @@ __global__ void __launch_bounds__(256) k_best(const int G, const SearchDev sp, c
 // + pair tiles (a3+a5, energy + forces).  Each group evaluates its genotype `iters`
 // times, nudging the translation by 1e-3 Å per iteration (ADADELTA-like locality).
 // ---------------------------------------------------------------------------
-template <int W, int MAXC, int PARTS>
+template <int W, int MAXC, int PARTS, bool PK = false>
 __global__ void __launch_bounds__(256, (MAXC <= 4 ? DK_ADA_MINB : 1)) k_bench_part(const LigDev L, const GridDev g,
                                                                                   const ScratchLayout SL, int n, int iters,
                                                                                   const float *__restrict__ genes, float *E) {
@@ -1105,7 +1106,7 @@ __global__ void __launch_bounds__(256, (MAXC <= 4 ? DK_ADA_MINB : 1)) k_bench_pa
     __syncwarp(mask);
     float acc = 0.0f;
     for (int it = 0; it < iters; ++it) {
-        acc += eval_group<W, MAXC, true, PARTS>(Ls, g, S, sub, mask);
+        acc += eval_group<W, MAXC, true, PARTS, 1, PK>(Ls, g, S, sub, mask);
         if (sub == 0) S.genes[0] += 1e-3f;
         __syncwarp(mask);
     }
@@ -1162,6 +1163,21 @@ __global__ void k_stream_words(uint2 key, uint32_t purpose, uint32_t slot, uint3
         }                                                                    \
     } while (0)
 
+// The packed FP32x2 gradient tiles (score.cuh, LigDev::packed: D5, W = 32, 65 <= N <= 96)
+// are a compile-time variant (PK) of the gradient kernels: DK_IF_PACKED(L, cfg, body) runs
+// body with W = 32, MAXC = 3, PK = true for a packed ligand, else falls through to the
+// statement that follows it.
+#ifdef DK_PACK_ON
+#define DK_IF_PACKED(L, cfg, ...)                                                              \
+    if ((L).packed && (cfg).W == 32 && (cfg).MAXC == 3) {                                      \
+        constexpr int W = 32, MAXC = 3;                                                        \
+        constexpr bool PK = true;                                                              \
+        __VA_ARGS__;                                                                           \
+    } else
+#else
+#define DK_IF_PACKED(L, cfg, ...)
+#endif
+
 static constexpr int kThreads = 256;
 static constexpr int kSmemMax = 227 * 1024;
 
@@ -1215,6 +1231,10 @@ cudaError_t setup_kernel_attributes() {
     if (e == cudaSuccess) e = allow_smem(k_bench_part<W, MAXC, kIntra>);
     DK_ATTR(16, 1) DK_ATTR(32, 1) DK_ATTR(32, 2) DK_ATTR(32, 3) DK_ATTR(32, 4) DK_ATTR(32, 8)
 #undef DK_ATTR
+#ifdef DK_PACK_ON
+    if (e == cudaSuccess) e = allow_smem(k_eval<32, 3, true, kAll, true>);
+    if (e == cudaSuccess) e = allow_smem(k_bench_part<32, 3, kIntra, true>);
+#endif
     if (e == cudaSuccess) e = setup_attributes_adadelta();
     if (e == cudaSuccess) e = setup_attributes_sw();
     return e;
@@ -1229,6 +1249,10 @@ cudaError_t setup_attributes_adadelta() {
     if (e == cudaSuccess) e = allow_smem(k_ls_adadelta<W, MAXC, true>);
     DK_ATTR(16, 1) DK_ATTR(32, 1) DK_ATTR(32, 2) DK_ATTR(32, 3) DK_ATTR(32, 4) DK_ATTR(32, 8)
 #undef DK_ATTR
+#ifdef DK_PACK_ON
+    if (e == cudaSuccess) e = allow_smem(k_ls_adadelta<32, 3, false, true>);
+    if (e == cudaSuccess) e = allow_smem(k_ls_adadelta<32, 3, true, true>);
+#endif
     return e;
 }
 #endif
@@ -1275,7 +1299,10 @@ cudaError_t launch_eval(const LigDev &L, const GridDev &g, int n, const float *g
             k_eval<W, MAXC, false, kInter><<<blocks, kThreads, smem, s>>>(L, g, SL, n, genes, E, nullptr, xyz, dfs2orig);
         else if (parts == kIntra && !want_grad)
             k_eval<W, MAXC, false, kIntra><<<blocks, kThreads, smem, s>>>(L, g, SL, n, genes, E, nullptr, xyz, dfs2orig);
-        else if (want_grad) k_eval<W, MAXC, true><<<blocks, kThreads, smem, s>>>(L, g, SL, n, genes, E, grad, xyz, dfs2orig);
+        else if (want_grad) {
+            DK_IF_PACKED(L, cfg, { k_eval<W, MAXC, true, kAll, PK><<<blocks, kThreads, smem, s>>>(L, g, SL, n, genes, E, grad, xyz, dfs2orig); })
+            k_eval<W, MAXC, true><<<blocks, kThreads, smem, s>>>(L, g, SL, n, genes, E, grad, xyz, dfs2orig);
+        }
         else k_eval<W, MAXC, false><<<blocks, kThreads, smem, s>>>(L, g, SL, n, genes, E, grad, xyz, dfs2orig);
     });
     return cudaGetLastError();
@@ -1497,6 +1524,7 @@ int adadelta_resident_groups(const LigDev &L) {
     int dev = 0, nsm = 148, per_sm = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    DK_IF_PACKED(L, cfg, { cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_ls_adadelta<W, MAXC, false, PK>, kThreads, smem); })
     DK_DISPATCH(cfg, { cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_ls_adadelta<W, MAXC>, kThreads, smem); });
     cudaGetLastError();
     return per_sm * nsm * groups;
@@ -1511,8 +1539,13 @@ cudaError_t launch_ls_adadelta(const LigDev &L, const GridDev &g, const SearchDe
         const size_t smem = (size_t)staged_bytes(L, true) + (size_t)groups * SL.bytes;
         if (smem > (size_t)kSmemMax) return cudaErrorInvalidConfiguration;
         const int blocks = ceil_div(n_total, groups);
-        if (a.ad_trace_x) DK_DISPATCH(cfg, { k_ls_adadelta<W, MAXC, true><<<blocks, kThreads, smem, s>>>(L, g, SL, sp, pop, a); });
-        else DK_DISPATCH(cfg, { k_ls_adadelta<W, MAXC><<<blocks, kThreads, smem, s>>>(L, g, SL, sp, pop, a); });
+        if (a.ad_trace_x) {
+            DK_IF_PACKED(L, cfg, { k_ls_adadelta<W, MAXC, true, PK><<<blocks, kThreads, smem, s>>>(L, g, SL, sp, pop, a); })
+            DK_DISPATCH(cfg, { k_ls_adadelta<W, MAXC, true><<<blocks, kThreads, smem, s>>>(L, g, SL, sp, pop, a); });
+        } else {
+            DK_IF_PACKED(L, cfg, { k_ls_adadelta<W, MAXC, false, PK><<<blocks, kThreads, smem, s>>>(L, g, SL, sp, pop, a); })
+            DK_DISPATCH(cfg, { k_ls_adadelta<W, MAXC><<<blocks, kThreads, smem, s>>>(L, g, SL, sp, pop, a); });
+        }
     }
     return cudaGetLastError();
 }
@@ -1529,6 +1562,10 @@ cudaError_t launch_bench_part(const LigDev &L, const GridDev &g, int part, int n
     const size_t smem = (size_t)staged_bytes(L, true) + (size_t)groups * SL.bytes;
     if (smem > (size_t)kSmemMax) return cudaErrorInvalidConfiguration;
     const int blocks = ceil_div(n, groups);
+    DK_IF_PACKED(L, cfg, {
+        if (part == 0) k_bench_part<W, MAXC, kInter><<<blocks, kThreads, smem, s>>>(L, g, SL, n, iters, genes, E);
+        else k_bench_part<W, MAXC, kIntra, PK><<<blocks, kThreads, smem, s>>>(L, g, SL, n, iters, genes, E);
+    })
     DK_DISPATCH(cfg, {
         if (part == 0) k_bench_part<W, MAXC, kInter><<<blocks, kThreads, smem, s>>>(L, g, SL, n, iters, genes, E);
         else k_bench_part<W, MAXC, kIntra><<<blocks, kThreads, smem, s>>>(L, g, SL, n, iters, genes, E);

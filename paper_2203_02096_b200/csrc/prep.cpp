@@ -438,29 +438,27 @@ int prepare_ligand(const dock_ligand *l, const dock_type_param *tp, int n_types,
     };
     L.n_slots = slot_count();
     L.slot_mode = (20 * L.n_slots <= 64 * 1024) ? 1 : 0;      // beyond: per-atom params + bits
-    // D5 lean slots (DK_LEAN): the H-bond pairs' 12-10 vdW terms go to a side list whose
-    // per-pair forces are staged in the per-group gradient scratch (2N float4), so a ligand
-    // with more than 2N H-bond pairs uses the per-atom-parameter tiles instead.
+    // Packed FP32x2 tiles (score.cuh tiles_packed, D5 only): W = 32, two full chunks and a
+    // hybrid tail (65 <= N <= 96).  The H-bond pairs of the packed rows (all but tail x tail)
+    // go to a side list (their 12-10 vdW terms) whose forces and per-atom totals are staged in
+    // the per-group gradient scratch (2N float4): nhb + N <= 2N, and an atom's contributions
+    // must fit one 32-lane round of the per-atom sums.
     std::vector<int> hbl;   // dfs positions i < j, in pair-list order
     for (size_t q = 0; q + 1 < pairs.size(); q += 2) {
         const int ri = tp[l->type[pairs[q]]].role, rj = tp[l->type[pairs[q + 1]]].role;
         if ((ri == 1 && rj == 2) || (ri == 2 && rj == 1)) {
             const int di = pos[pairs[q]], dj = pos[pairs[q + 1]];
+            if (std::min(di, dj) >= 2 * Wg) continue;     // tail x tail: folded rounds
             hbl.push_back(std::min(di, dj)); hbl.push_back(std::max(di, dj));
         }
     }
     const int nhb = (int)hbl.size() / 2;
-#if defined(DK_LEAN) && DK_LEAN
-#if !defined(DK_FOLD) || DK_FOLD
-    L.lean = ad4 ? 0 : 1;
-#endif
-#endif
-    if (L.lean && L.slot_mode && nhb > 2 * N) L.slot_mode = 0;
-    if (!L.slot_mode) L.lean = 0;
-    // packed FP32x2 tiles (score.cuh tiles_packed): two full 32-atom chunks, no tail or the
-    // hybrid tail (its broadcast part packs chunks 0 and 1)
-#if !defined(DK_PACKED) || DK_PACKED
-    L.packed = (L.lean && Wg == 32 && Bf == 2 && !L.tail_rot && (tail == 0 || ((L.tail_seg >> 24) & 1))) ? 1 : 0;
+    std::vector<int> hdeg(N, 0);
+    for (int v : hbl) hdeg[v]++;
+    const int hmax = N > 0 ? *std::max_element(hdeg.begin(), hdeg.end()) : 0;
+#if (!defined(DK_PACKED) || DK_PACKED) && (!defined(DK_FOLD) || DK_FOLD)
+    L.packed = (!ad4 && L.slot_mode && Wg == 32 && Bf == 2 && tail > 0 && !L.tail_rot && ((L.tail_seg >> 24) & 1) &&
+                nhb <= N && hmax <= 32) ? 1 : 0;
 #endif
     if (!L.slot_mode && L.tail_seg) {                          // seg needs the slot tables
         L.tail_seg = 0;
@@ -475,9 +473,25 @@ int prepare_ligand(const dock_ligand *l, const dock_type_param *tp, int n_types,
     const bool sep_q = ad4;                    // D5 folds qq into slot4
 #endif
     L.off_slotq = off; off += (L.slot_mode && sep_q) ? a16(4 * L.n_slots) : 0;
-    L.nhb = L.lean ? nhb : 0;
+    // H-bond contribution rounds: atoms in dfs order, each atom's 2..32 contributions kept in one round
+    std::vector<int> hseg;          // [rounds][32] entries (score.cuh hb_side)
+    if (L.packed) {
+        std::vector<std::vector<int>> inc(N);
+        for (int h = 0; h < nhb; ++h) { inc[hbl[2 * h]].push_back(h); inc[hbl[2 * h + 1]].push_back(h | 0x100); }
+        int lane = 32;
+        for (int a = 0; a < N; ++a) {
+            const int d = (int)inc[a].size();
+            if (d == 0) continue;
+            if (lane + d > 32) { hseg.insert(hseg.end(), 32, 0); lane = 0; }
+            const int base = (int)hseg.size() - 32, first = lane;
+            for (int k = 0; k < d; ++k, ++lane)
+                hseg[base + lane] = inc[a][k] | (first << 9) | ((k == d - 1) ? 1 << 14 : 0) | (1 << 15) | (a << 16);
+        }
+    }
+    L.nhb = L.packed ? nhb : 0;
+    L.nhbr = (int)hseg.size() / 32;
     L.off_hbc = off; off += 16 * L.nhb;
-    L.off_hbadj = off; off += L.lean ? a16(4 * (N + 1 + 2 * L.nhb)) : 0;
+    L.off_hbseg = off; off += L.packed ? a16(4 * ((int)hseg.size() + L.NC)) : 0;
     L.grad_bytes = off;             // the gradient kernels stage only up to here
     // Energy-only kernels stage the pair list + per-pair constants (20 B per pair) when it
     // fits comfortably in shared memory; beyond that (P > ~4,900, e.g. N >= ~110) they use
@@ -591,7 +605,7 @@ int prepare_ligand(const dock_ligand *l, const dock_type_param *tp, int n_types,
         }
         float4 *s4 = reinterpret_cast<float4 *>(bl + L.off_slot4);
         float *sq = reinterpret_cast<float *>(bl + L.off_slotq);
-        auto fill = [&](int slot, int da, int db, bool on) {
+        auto fill = [&](int slot, int da, int db, bool on, bool lean = false) {
             // a non-pair slot contributes exactly 0 (A = B = SV = qq = 0); under D5-AD4 its
             // r_eq operand is 1 Å so the smoothed distance stays >= 0.26 Å (x^2 finite, 0 * x^12 = 0)
             s4[slot] = make_float4(ad4 ? 1.f : 0.f, 0.f, 0.f, 0.f);
@@ -617,8 +631,8 @@ int prepare_ligand(const dock_ligand *l, const dock_type_param *tp, int n_types,
             return;
 #endif
             const double req2 = req * req, r6 = req2 * req2 * req2, r12 = r6 * r6;
-            if (L.lean) {
-                // D5, lean (score.cuh slot_pair, DK_LEAN): {-eps r_eq^12, 2 eps r_eq^6,
+            if (lean) {
+                // D5, lean (the packed rows, score.cuh slot_pair2): {-eps r_eq^12, 2 eps r_eq^6,
                 // -(S_aV_b + S_bV_a) / (3 * 2 sigma^2), -(332.06363/4) q_a q_b / 3}; the H-bond
                 // pair's 12-10 vdW lives in the side list (zero vdW constants here)
                 const double sv = (double)ta.S * tb.V + (double)tb.S * ta.V;
@@ -640,9 +654,9 @@ int prepare_ligand(const dock_ligand *l, const dock_type_param *tp, int n_types,
             // {c_a.x, c_b.x, c_a.y, c_b.y} and {c_a.z, c_b.z, c_a.w, c_b.w}, from the lean
             // constants c_a, c_b of its two slots (computed by fill into a scratch slot)
             auto emit2 = [&](int da, int db, bool on_a, int ea, int eb, bool on_b) {
-                fill(slot, da, db, on_a);
+                fill(slot, da, db, on_a, true);
                 const float4 a = s4[slot];
-                fill(slot, ea, eb, on_b);
+                fill(slot, ea, eb, on_b, true);
                 const float4 b = s4[slot];
                 return std::make_pair(make_float4(a.x, b.x, a.y, b.y), make_float4(a.z, b.z, a.w, b.w));
             };
@@ -711,12 +725,11 @@ int prepare_ligand(const dock_ligand *l, const dock_type_param *tp, int n_types,
                     for (int ln = 0; ln < Wg; ++ln, ++slot)
                         fill(slot, I * Wg + ln, Bf * Wg + k, I < Bf || ln < k);
         if (slot != L.n_slots) return fail("internal: pair-slot count mismatch");
-        if (L.lean) {
-            // H-bond side list: {5 eps r_eq^12, 6 eps r_eq^10, i | j << 16} and, per atom, the
-            // pairs it belongs to (fixed order: ascending pair index)
+        if (L.packed) {
+            // H-bond side list {5 eps r_eq^12, 6 eps r_eq^10, i | j << 16}, the contribution
+            // rounds and the per-chunk lane masks of atoms with contributions
             float4 *hc = reinterpret_cast<float4 *>(bl + L.off_hbc);
-            int *adj = reinterpret_cast<int *>(bl + L.off_hbadj);
-            std::vector<std::vector<int>> inc(N);
+            int *hs = reinterpret_cast<int *>(bl + L.off_hbseg);
             for (int h = 0; h < L.nhb; ++h) {
                 const int di = hbl[2 * h], dj = hbl[2 * h + 1];
                 const dock_type_param &ta = tp[l->type[order[di]]], &tb = tp[l->type[order[dj]]];
@@ -727,15 +740,16 @@ int prepare_ligand(const dock_ligand *l, const dock_type_param *tp, int n_types,
                 float fij;
                 std::memcpy(&fij, &ij, 4);
                 hc[h] = make_float4((float)(5.0 * eps * r10 * req2), (float)(6.0 * eps * r10), fij, 0.f);
-                inc[di].push_back(2 * h);
-                inc[dj].push_back(2 * h + 1);
             }
-            int e = N + 1;
-            for (int a = 0; a < N; ++a) {
-                adj[a] = e;
-                for (int v : inc[a]) adj[e++] = v;
+            for (size_t k = 0; k < hseg.size(); ++k) hs[k] = hseg[k];
+            for (int c = 0; c < L.NC; ++c) {
+                uint32_t m = 0;
+                for (int ln = 0; ln < Wg; ++ln) {
+                    const int a = c * Wg + ln;
+                    if (a < N && hdeg[a] > 0) m |= 1u << ln;
+                }
+                hs[hseg.size() + c] = (int)m;
             }
-            adj[N] = e;
         }
         if (std::getenv("DOCK_SLOT_STATS")) {   // diagnostics: steps (W slots) holding no pair at all
             const float4 *s4c = reinterpret_cast<const float4 *>(bl + L.off_slot4);

@@ -76,10 +76,10 @@ struct LigSm {
     const float *slotq;           // pair-slot 332.06363/4 q_i q_j (slot_mode)
     int NC, tail_rot, slot_mode, tail_seg;
     int energy_tiles;             // energy-only evaluation through the pair tiles (no pair list)
-    int nhb;                      // lean D5: H-bond side list (LigDev::off_hbc / off_hbadj)
-    int packed;                   // lean D5, W = 32, two full chunks: packed FP32x2 tiles (LigDev::packed)
+    int nhb;                      // packed: H-bond side list (LigDev::off_hbc / off_hbseg)
     const float4 *hbc;
-    const int *hbadj;
+    int nhbr;                     // packed: H-bond contribution rounds (LigDev::nhbr)
+    const int *hbseg;             // packed: [nhbr][32] contribution entries, then int[NC] chunk masks
     float wA_v, wB_v, wA_h, wB_h, qscale;   // D5-AD4 constants (LigDev; unused by D5)
 };
 
@@ -488,87 +488,66 @@ __device__ __forceinline__ void intra_tiles(const LigSm &L, const Scratch &S, in
 #ifndef DK_FOLD
 #define DK_FOLD 1   // D5 slot constants folded (A r_eq^12, B r_eq^n, SV, qq); 0: {r_eq^2, A, B, SV} + qq (A/B)
 #endif
-#ifndef DK_LEAN
-#define DK_LEAN 0   // 1: D5 lean slots + packed FP32x2 tiles (experiment: slower on B200)
-#endif
-#if !defined(DK_AD4) && DK_FOLD && DK_LEAN
-#define DK_LEAN_ON 1
-#endif
 
-#ifdef DK_LEAN_ON
-// Lean D5 slot arithmetic (prep.cpp, LigDev::lean).  Slot constants c = {-A', B', -(k/3) SV,
-// -qq/3} with A' = eps r_eq^12, B' = 2 eps r_eq^6 (the 12-6 form; zero for an H-bond pair,
-// whose 12-10 term is hb_side's), k = 1/2sigma^2, qq = 332.06363/4 q_i q_j.  With
-// inv = 1/rho^2 and i3 = inv^3:
-//   u = B' - A' i3, E_vdw = A' i6 - B' i3 = -i3 u;  v = B' - 2 A' i3, rho^2 dE_vdw/drho^2 = 3 i3 v;
-//   t = i3 v - qq inv / 3 = (rho^2 dE_vdw/drho^2 - E_el) / 3;  d = t inv - k E_ds / 3 = (dE/drho^2) / 3.
-// The energy goes to three sums scaled as above (EAcc: -E_vdw, -E_el/3, -k E_ds/3), unscaled
-// once per evaluation; the forces carry dE/drho^2 / 3, so the per-atom factor is 6, not 2.
-// 24 FP32 operations per slot instead of 29, and no per-slot H-bond selects.
-struct EAcc { float v = 0.0f, el = 0.0f, ds = 0.0f; };
-constexpr float kDsUnscale = -3.0f * 2.0f * 3.6f * 3.6f;   // -3/k
-__device__ __forceinline__ float eacc_total(const EAcc &a) { return fmaf(-3.0f, a.el, fmaf(kDsUnscale, a.ds, -a.v)); }
-constexpr float kForceScale = 6.0f;
+struct EAcc { float e = 0.0f; };
+__device__ __forceinline__ float eacc_total(const EAcc &a) { return a.e; }
+#if defined(DK_AD4) || !DK_FOLD
+// One pair inside the slot-table tiles: constants c = {r_eq, A, B, SV} and qq from the
+// slot (all zero for a non-pair, so no membership test), force as in tile_pair.
+__device__ __forceinline__ void slot_pair(float rxi, float ryi, float rzi, float4 rj, float4 c, float qq, EAcc &e,
+                                          float &gxi, float &gyi, float &gzi, float &fx, float &fy, float &fz) {
+    const float dx = rxi - rj.x, dy = ryi - rj.y, dz = rzi - rj.z;
+    const float rho2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
+    float dE;
+    e.e += pair_eg_ab(rho2, c.x, c.y, c.z, c.w, qq, dE);
+    gxi = fmaf(dE, dx, gxi); gyi = fmaf(dE, dy, gyi); gzi = fmaf(dE, dz, gzi);
+    fx = fmaf(-dE, dx, fx); fy = fmaf(-dE, dy, fy); fz = fmaf(-dE, dz, fz);
+}
+#define DK_SLOT(q) L.slot4[q], L.slotq[q]
+#else
+// D5 pair from folded slot constants c = {A' = A r_eq^12, B' = +-|B| r_eq^n, SV, qq} (prep.cpp;
+// sign of B': the 12-10 H-bond form): with inv = 1/rho^2, E_vdw = A' inv^6 - |B'| inv^{n/2},
+// rho^2 dE_vdw/drho^2 = -6 A' inv^6 + (n/2) |B'| inv^{n/2} -- one multiply and one 4-byte
+// shared-memory read fewer per slot than {r_eq^2, A, B, SV} + qq.  Zero for a non-pair.
+__device__ __forceinline__ float pair_eg_folded(float rho2, float4 c, float &dE) {
+    const bool clamped = rho2 < 1e-4f;
+    rho2 = fmaxf(rho2, 1e-4f);                           // 0.01 Å clamp (S:197)
+    const float inv = rcp_approx(rho2);
+    const float i2 = inv * inv, i3 = i2 * inv, i6 = i3 * i3;
+    const bool ten = __float_as_int(c.y) < 0;
+    const float xn = ten ? i3 * i2 : i3;
+    const float tA = c.x * i6, tB = fabsf(c.y) * xn;
+    const float dvr = fmaf(-6.0f, tA, (ten ? 5.0f : 3.0f) * tB);
+    const float Eel = c.w * inv;
+    const float Eds = c.z * ex2_approx(rho2 * kExpScale);
+    const float d = fmaf(dvr - Eel, inv, -Eds * kInvTwoSigma2);
+    dE = clamped ? 0.0f : d;
+    return (tA - tB) + Eel + Eds;
+}
 __device__ __forceinline__ void slot_pair(float rxi, float ryi, float rzi, float4 rj, float4 c, EAcc &e,
                                           float &gxi, float &gyi, float &gzi, float &fx, float &fy, float &fz) {
     const float dx = rxi - rj.x, dy = ryi - rj.y, dz = rzi - rj.z;
     const float rho2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
-    const bool clamped = rho2 < 1e-4f;
-    const float r2 = fmaxf(rho2, 1e-4f);                 // 0.01 Å clamp
-    const float inv = rcp_approx(r2), i2 = inv * inv, i3 = i2 * inv;
-    const float u = fmaf(c.x, i3, c.y);
-    const float v = fmaf(c.x, i3, u);
-    e.v = fmaf(i3, u, e.v);
-    const float el = c.w * inv;
-    e.el += el;
-    const float t = fmaf(i3, v, el);
-    const float ed = c.z * ex2_approx(r2 * kExpScale);
-    e.ds += ed;
-    const float d = fmaf(t, inv, ed);
-    const float dE = clamped ? 0.0f : d;                 // zero force inside the clamp
+    float dE;
+    e.e += pair_eg_folded(rho2, c, dE);
     gxi = fmaf(dE, dx, gxi); gyi = fmaf(dE, dy, gyi); gzi = fmaf(dE, dz, gzi);
     fx = fmaf(-dE, dx, fx); fy = fmaf(-dE, dy, fy); fz = fmaf(-dE, dz, fz);
 }
 #define DK_SLOT(q) L.slot4[q]
+#endif
 
-// The H-bond pairs' 12-10 vdW terms (lean slots): lane p takes pairs p, p + W, ...; its
-// force d (r_i - r_j) (d = (dE/drho^2) / 3, as in the tiles) is staged in the group's
-// gradient scratch, then every atom adds its pairs' forces in ascending pair order (+ as i,
-// - as j).  Fixed order: deterministic.  E = A'' i6 - B'' i5 (A'' = 5 eps r_eq^12,
-// B'' = 6 eps r_eq^10), rho^2 dE/drho^2 = -6 A'' i6 + 5 B'' i5.
-template <int W, int MAXC>
-__device__ __forceinline__ void hb_side(const LigSm &L, const Scratch &S, int sub, unsigned mask, float (&hx)[MAXC],
-                                        float (&hy)[MAXC], float (&hz)[MAXC], EAcc &e) {
-    for (int p = sub; p < L.nhb; p += W) {
-        const float4 c = L.hbc[p];
-        const uint32_t ij = __float_as_uint(c.z);
-        const float4 ri = S.r[ridx<W>((int)(ij & 0xffffu))], rj = S.r[ridx<W>((int)(ij >> 16))];
-        const float dx = ri.x - rj.x, dy = ri.y - rj.y, dz = ri.z - rj.z;
-        const float rho2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
-        const bool clamped = rho2 < 1e-4f;
-        const float r2 = fmaxf(rho2, 1e-4f);
-        const float inv = rcp_approx(r2), i2 = inv * inv, i3 = i2 * inv, i5 = i3 * i2, i6 = i3 * i3;
-        const float tA = c.x * i6, tB = c.y * i5;
-        e.v += tB - tA;
-        const float d = clamped ? 0.0f : fmaf(-6.0f, tA, 5.0f * tB) * inv * (1.0f / 3.0f);
-        S.ts[p] = make_float4(d * dx, d * dy, d * dz, 0.0f);
-    }
-    __syncwarp(mask);
-#pragma unroll
-    for (int c = 0; c < MAXC; ++c) {
-        const int a = sub + W * c;
-        if (a < L.N) {
-            const int k1 = L.hbadj[a + 1];
-            for (int k = L.hbadj[a]; k < k1; ++k) {
-                const int ent = L.hbadj[k];
-                const float4 f = S.ts[ent >> 1];
-                if (ent & 1) { hx[c] -= f.x; hy[c] -= f.y; hz[c] -= f.z; }
-                else { hx[c] += f.x; hy[c] += f.y; hz[c] += f.z; }
-            }
-        }
-    }
-    __syncwarp(mask);   // the back-projection reuses the scratch
-}
+#if !defined(DK_AD4) && DK_FOLD
+#define DK_PACK_ON 1   // packed FP32x2 tiles (D5, LigDev::packed)
+// Lean D5 constants of the packed rows (prep.cpp): c = {-A', B', -(k/3) SV, -qq/3} with
+// A' = eps r_eq^12, B' = 2 eps r_eq^6 (the 12-6 form; zero for an H-bond pair, whose 12-10 vdW
+// term is hb_side's), k = 1/2sigma^2, qq = 332.06363/4 q_i q_j.  With inv = 1/rho^2, i3 = inv^3:
+//   u = B' - A' i3, E_vdw = A' i6 - B' i3 = -i3 u;  v = B' - 2 A' i3, rho^2 dE_vdw/drho^2 = 3 i3 v;
+//   t = i3 v - qq inv / 3 = (rho^2 dE_vdw/drho^2 - E_el) / 3;  d = t inv - k E_ds / 3 = (dE/drho^2) / 3.
+// The energy goes to three sums scaled as above (EAcc2: -E_vdw, -E_el/3, -k E_ds/3), unscaled
+// once per evaluation (lean_total); the forces carry (dE/drho^2) / 3 and are multiplied by 3
+// once per tile when they join the folded path's per-atom sums.  24 FP32 operations per
+// slot (12 packed instructions) instead of 29, no per-slot H-bond selects.
+constexpr float kDsUnscale = -3.0f * 2.0f * 3.6f * 3.6f;   // -3/k
 
 // ---- Packed FP32x2 lean slots (sm_100 fma/mul/add/sub.rn.f32x2: one instruction, two
 // independent IEEE FP32 operations) for the two-full-chunk shape (W = 32, Bf = 2: 64 <= N
@@ -679,9 +658,9 @@ __device__ __forceinline__ void tiles_packed(const LigSm &L, const Scratch &S, i
         const int back = (sub - 17) & (W - 1);
         fx = f2_shfl(fx, back, mask); fy = f2_shfl(fy, back, mask); fz = f2_shfl(fz, back, mask);
         const f2_t hx01 = sub2(gx, fx), hy01 = sub2(gy, fy), hz01 = sub2(gz, fz);
-        hx[0] += f2_lo(hx01); hx[1] += f2_hi(hx01);
-        hy[0] += f2_lo(hy01); hy[1] += f2_hi(hy01);
-        hz[0] += f2_lo(hz01); hz[1] += f2_hi(hz01);
+        hx[0] = fmaf(3.0f, f2_lo(hx01), hx[0]); hx[1] = fmaf(3.0f, f2_hi(hx01), hx[1]);   // x 3: folded units
+        hy[0] = fmaf(3.0f, f2_lo(hy01), hy[0]); hy[1] = fmaf(3.0f, f2_hi(hy01), hy[1]);
+        hz[0] = fmaf(3.0f, f2_lo(hz01), hz[0]); hz[1] = fmaf(3.0f, f2_hi(hz01), hz[1]);
     }
     // (b) split tile (0,1), packed steps q = 16..31 (tile steps u and u + 16, u = q - 16)
     {
@@ -697,67 +676,78 @@ __device__ __forceinline__ void tiles_packed(const LigSm &L, const Scratch &S, i
         }
         // stream a (steps u) ends 16 lanes past its owner, stream b (steps u + 16) at its owner
         const int back = sub ^ 16;
-        hx[1] -= __shfl_sync(mask, f2_lo(fx), back) + f2_hi(fx);
-        hy[1] -= __shfl_sync(mask, f2_lo(fy), back) + f2_hi(fy);
-        hz[1] -= __shfl_sync(mask, f2_lo(fz), back) + f2_hi(fz);
-        hx[0] += f2_lo(gx) + f2_hi(gx); hy[0] += f2_lo(gy) + f2_hi(gy); hz[0] += f2_lo(gz) + f2_hi(gz);
+        hx[1] = fmaf(-3.0f, __shfl_sync(mask, f2_lo(fx), back) + f2_hi(fx), hx[1]);
+        hy[1] = fmaf(-3.0f, __shfl_sync(mask, f2_lo(fy), back) + f2_hi(fy), hy[1]);
+        hz[1] = fmaf(-3.0f, __shfl_sync(mask, f2_lo(fz), back) + f2_hi(fz), hz[1]);
+        hx[0] = fmaf(3.0f, f2_lo(gx) + f2_hi(gx), hx[0]); hy[0] = fmaf(3.0f, f2_lo(gy) + f2_hi(gy), hy[0]);
+        hz[0] = fmaf(3.0f, f2_lo(gz) + f2_hi(gz), hz[0]);
     }
     __syncwarp(mask);   // the scratch rows are reused (H-bond side list, back-projection)
 }
-#else
-struct EAcc { float e = 0.0f; };
-__device__ __forceinline__ float eacc_total(const EAcc &a) { return a.e; }
-constexpr float kForceScale = 2.0f;
-#if defined(DK_AD4) || !DK_FOLD
-// One pair inside the slot-table tiles: constants c = {r_eq, A, B, SV} and qq from the
-// slot (all zero for a non-pair, so no membership test), force as in tile_pair.
-__device__ __forceinline__ void slot_pair(float rxi, float ryi, float rzi, float4 rj, float4 c, float qq, EAcc &e,
-                                          float &gxi, float &gyi, float &gzi, float &fx, float &fy, float &fz) {
-    const float dx = rxi - rj.x, dy = ryi - rj.y, dz = rzi - rj.z;
-    const float rho2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
-    float dE;
-    e.e += pair_eg_ab(rho2, c.x, c.y, c.z, c.w, qq, dE);
-    gxi = fmaf(dE, dx, gxi); gyi = fmaf(dE, dy, gyi); gzi = fmaf(dE, dz, gzi);
-    fx = fmaf(-dE, dx, fx); fy = fmaf(-dE, dy, fy); fz = fmaf(-dE, dz, fz);
+
+__device__ __forceinline__ float lean_total(const EAcc2 &a) {
+    const float v = f2_lo(a.v) + f2_hi(a.v), el = f2_lo(a.el) + f2_hi(a.el), ds = f2_lo(a.ds) + f2_hi(a.ds);
+    return fmaf(-3.0f, el, fmaf(kDsUnscale, ds, -v));
 }
-#define DK_SLOT(q) L.slot4[q], L.slotq[q]
-#else
-// D5 pair from folded slot constants c = {A' = A r_eq^12, B' = +-|B| r_eq^n, SV, qq} (prep.cpp;
-// sign of B': the 12-10 H-bond form): with inv = 1/rho^2, E_vdw = A' inv^6 - |B'| inv^{n/2},
-// rho^2 dE_vdw/drho^2 = -6 A' inv^6 + (n/2) |B'| inv^{n/2} -- one multiply and one 4-byte
-// shared-memory read fewer per slot than {r_eq^2, A, B, SV} + qq.  Zero for a non-pair.
-__device__ __forceinline__ float pair_eg_folded(float rho2, float4 c, float &dE) {
-    const bool clamped = rho2 < 1e-4f;
-    rho2 = fmaxf(rho2, 1e-4f);                           // 0.01 Å clamp (S:197)
-    const float inv = rcp_approx(rho2);
-    const float i2 = inv * inv, i3 = i2 * inv, i6 = i3 * i3;
-    const bool ten = __float_as_int(c.y) < 0;
-    const float xn = ten ? i3 * i2 : i3;
-    const float tA = c.x * i6, tB = fabsf(c.y) * xn;
-    const float dvr = fmaf(-6.0f, tA, (ten ? 5.0f : 3.0f) * tB);
-    const float Eel = c.w * inv;
-    const float Eds = c.z * ex2_approx(rho2 * kExpScale);
-    const float d = fmaf(dvr - Eel, inv, -Eds * kInvTwoSigma2);
-    dE = clamped ? 0.0f : d;
-    return (tA - tB) + Eel + Eds;
+
+// The H-bond pairs of the packed rows (their 12-10 vdW terms; prep.cpp, LigDev::nhb): lane p
+// takes pairs p, p + W, ... and stages its force d (r_i - r_j), d = dE/drho^2, in the group's
+// gradient scratch.  The 2 nhb atom contributions (+ as i, - as j), sorted by atom and packed
+// into rounds of W lanes without splitting an atom (L.hbseg), are then summed per atom by a
+// segmented Hillis-Steele scan (shfl.up; each lane knows its segment's first lane), the
+// segment's last lane stores the atom's total, and the owner lanes add it.  Fixed order:
+// deterministic.  E = A'' i6 - B'' i5 (A'' = 5 eps r_eq^12, B'' = 6 eps r_eq^10),
+// rho^2 dE/drho^2 = -6 A'' i6 + 5 B'' i5.
+// hbseg entry: pair | neg << 8 | first lane << 9 | last << 14 | valid << 15 | atom << 16.
+template <int W, int MAXC>
+__device__ __forceinline__ void hb_side(const LigSm &L, const Scratch &S, int sub, unsigned mask, float (&hx)[MAXC],
+                                        float (&hy)[MAXC], float (&hz)[MAXC], EAcc &e) {
+    if (L.nhb == 0) return;
+    for (int p = sub; p < L.nhb; p += W) {
+        const float4 c = L.hbc[p];
+        const uint32_t ij = __float_as_uint(c.z);
+        const float4 ri = S.r[ridx<W>((int)(ij & 0xffffu))], rj = S.r[ridx<W>((int)(ij >> 16))];
+        const float dx = ri.x - rj.x, dy = ri.y - rj.y, dz = ri.z - rj.z;
+        const float rho2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
+        const bool clamped = rho2 < 1e-4f;
+        const float r2 = fmaxf(rho2, 1e-4f);               // 0.01 Å clamp
+        const float inv = rcp_approx(r2), i2 = inv * inv, i3 = i2 * inv, i5 = i3 * i2, i6 = i3 * i3;
+        const float tA = c.x * i6, tB = c.y * i5;
+        e.e += tA - tB;
+        const float d = clamped ? 0.0f : fmaf(-6.0f, tA, 5.0f * tB) * inv;
+        S.ts[p] = make_float4(d * dx, d * dy, d * dz, 0.0f);
+    }
+    __syncwarp(mask);
+    float4 *tot = S.ts + L.nhb;                            // per-atom totals [N]
+    for (int r = 0; r < L.nhbr; ++r) {
+        const int ent = L.hbseg[r * W + sub];
+        float4 f = S.ts[ent & 0xff];
+        const float sg = (ent >> 15) & 1 ? ((ent >> 8) & 1 ? -1.0f : 1.0f) : 0.0f;
+        float fx = sg * f.x, fy = sg * f.y, fz = sg * f.z;
+        const int first = (ent >> 9) & 31;
+#pragma unroll
+        for (int d = 1; d < W; d <<= 1) {
+            const float ox = __shfl_up_sync(mask, fx, d), oy = __shfl_up_sync(mask, fy, d), oz = __shfl_up_sync(mask, fz, d);
+            if (sub - d >= first) { fx += ox; fy += oy; fz += oz; }
+        }
+        if ((ent >> 14) & 1) tot[ent >> 16] = make_float4(fx, fy, fz, 0.0f);
+    }
+    __syncwarp(mask);
+    const int *cmask = L.hbseg + L.nhbr * W;
+#pragma unroll
+    for (int c = 0; c < MAXC; ++c)
+        if ((cmask[c] >> sub) & 1) {
+            const float4 f = tot[sub + W * c];
+            hx[c] += f.x; hy[c] += f.y; hz[c] += f.z;
+        }
+    __syncwarp(mask);   // the back-projection reuses the scratch
 }
-__device__ __forceinline__ void slot_pair(float rxi, float ryi, float rzi, float4 rj, float4 c, EAcc &e,
-                                          float &gxi, float &gyi, float &gzi, float &fx, float &fy, float &fz) {
-    const float dx = rxi - rj.x, dy = ryi - rj.y, dz = rzi - rj.z;
-    const float rho2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
-    float dE;
-    e.e += pair_eg_folded(rho2, c, dE);
-    gxi = fmaf(dE, dx, gxi); gyi = fmaf(dE, dy, gyi); gzi = fmaf(dE, dz, gzi);
-    fx = fmaf(-dE, dx, fx); fy = fmaf(-dE, dy, fy); fz = fmaf(-dE, dz, fz);
-}
-#define DK_SLOT(q) L.slot4[q]
-#endif
 #endif
 
 // intra_tiles with precomputed pair-slot constants (L.slot_mode, prep.cpp): the same
 // rotation / broadcast schedule and force bookkeeping, one 16-byte + one 4-byte
 // conflict-free shared-memory read per slot instead of partner params and pair bits.
-template <int W, int MAXC>
+template <int W, int MAXC, bool PK = false>
 __device__ __forceinline__ void intra_tiles_slots(const LigSm &L, const Scratch &S, int sub, unsigned mask,
                                                   const float (&rx)[MAXC], const float (&ry)[MAXC],
                                                   const float (&rz)[MAXC], float (&gx)[MAXC], float (&gy)[MAXC],
@@ -771,29 +761,27 @@ __device__ __forceinline__ void intra_tiles_slots(const LigSm &L, const Scratch 
 #pragma unroll
     for (int c = 0; c < MAXC; ++c) hx[c] = hy[c] = hz[c] = 0.0f;
     int slot0 = 0;                        // first slot of the current tile
-#ifdef DK_LEAN_ON
+    constexpr bool packed = PK;
+#ifdef DK_PACK_ON
     EAcc2 e2;
-    bool packed = false;
-    if constexpr (W == 32 && (MAXC == 2 || MAXC == 3)) packed = L.packed != 0;
-    if (packed) {
-        if constexpr (W == 32 && (MAXC == 2 || MAXC == 3)) {
-            // the intermolecular gradients wait in the (unused here) duplicate pose half, so
-            // the packed tiles have their registers
+    if constexpr (PK) {
+        static_assert(W == 32 && MAXC == 3, "packed tiles: W = 32, two full chunks and a tail");
+        // the intermolecular gradients wait in the (unused here) duplicate pose half, so
+        // the packed tiles have their registers
 #pragma unroll
-            for (int c = 0; c < MAXC; ++c)
-                if (sub + W * c < N) S.r[ridx<W>(sub + W * c) + W] = make_float4(gx[c], gy[c], gz[c], 0.0f);
-            tiles_packed<W, MAXC>(L, S, sub, mask, rx, ry, rz, hx, hy, hz, e2);
+        for (int c = 0; c < MAXC; ++c)
+            if (sub + W * c < N) S.r[ridx<W>(sub + W * c) + W] = make_float4(gx[c], gy[c], gz[c], 0.0f);
+        tiles_packed<W, MAXC>(L, S, sub, mask, rx, ry, rz, hx, hy, hz, e2);
 #pragma unroll
-            for (int c = 0; c < MAXC; ++c)
-                if (sub + W * c < N) {
-                    const float4 g4 = S.r[ridx<W>(sub + W * c) + W];
-                    gx[c] = g4.x; gy[c] = g4.y; gz[c] = g4.z;
-                }
-        }
+        for (int c = 0; c < MAXC; ++c)
+            if (sub + W * c < N) {
+                const float4 g4 = S.r[ridx<W>(sub + W * c) + W];
+                gx[c] = g4.x; gy[c] = g4.y; gz[c] = g4.z;
+            }
         slot0 = 64 * W;                   // 32 packed steps x 2W rows = the 64 scalar tile steps
     }
 #else
-    constexpr bool packed = false;
+    static_assert(!PK, "packed tiles need the folded D5 build");
 #endif
 #pragma unroll
     for (int I = 0; I < MAXC; ++I) {
@@ -863,9 +851,9 @@ __device__ __forceinline__ void intra_tiles_slots(const LigSm &L, const Scratch 
         const float4 *trow = S.r + Bf * 2 * W;                  // tail chunk (positions 0..tp-1)
         float fx = 0.f, fy = 0.f, fz = 0.f;
         if ((L.tail_seg >> 24) & 1) {
-#ifdef DK_LEAN_ON
+#ifdef DK_PACK_ON
           if (packed) {
-            if constexpr (W == 32 && (MAXC == 2 || MAXC == 3)) {
+            if constexpr (PK) {
                 // (c) tail atom k against chunks 0 and 1 together (packed step k)
                 const float4 o4 = S.ts[sub];                    // tiles_packed's rows: {x0, x1, y0, y1}
                 const float2 o2 = reinterpret_cast<const float2 *>(S.ts + 96)[sub];
@@ -877,13 +865,15 @@ __device__ __forceinline__ void intra_tiles_slots(const LigSm &L, const Scratch 
                     slot_pair2(ox, oy, oz, f2_pk(rj.x, rj.x), f2_pk(rj.y, rj.y), f2_pk(rj.z, rj.z),
                                L.slot4[slot0 + k * 2 * W + sub], L.slot4[slot0 + k * 2 * W + W + sub], e2, gx2, gy2,
                                gz2, px2, py2, pz2);
-                    float px = -(f2_lo(px2) + f2_hi(px2)), py = -(f2_lo(py2) + f2_hi(py2)), pz = -(f2_lo(pz2) + f2_hi(pz2));
+                    // lean forces carry (dE/drho^2) / 3: x 3 here, into the folded units
+                    float px = -3.0f * (f2_lo(px2) + f2_hi(px2)), py = -3.0f * (f2_lo(py2) + f2_hi(py2)),
+                          pz = -3.0f * (f2_lo(pz2) + f2_hi(pz2));
                     px = gsum<W>(px, mask); py = gsum<W>(py, mask); pz = gsum<W>(pz, mask);
                     if (sub == k) { fx += px; fy += py; fz += pz; }
                 }
-                hx[0] += f2_lo(gx2); hx[1] += f2_hi(gx2);
-                hy[0] += f2_lo(gy2); hy[1] += f2_hi(gy2);
-                hz[0] += f2_lo(gz2); hz[1] += f2_hi(gz2);
+                hx[0] = fmaf(3.0f, f2_lo(gx2), hx[0]); hx[1] = fmaf(3.0f, f2_hi(gx2), hx[1]);
+                hy[0] = fmaf(3.0f, f2_lo(gy2), hy[0]); hy[1] = fmaf(3.0f, f2_hi(gy2), hy[1]);
+                hz[0] = fmaf(3.0f, f2_lo(gz2), hz[0]); hz[1] = fmaf(3.0f, f2_hi(gz2), hz[1]);
             }
           } else
 #endif
@@ -955,17 +945,16 @@ __device__ __forceinline__ void intra_tiles_slots(const LigSm &L, const Scratch 
                 if (c == Bf && sub == k) { hx[c] += fx; hy[c] += fy; hz[c] += fz; }
         }
     }
-#ifdef DK_LEAN_ON
-    if (L.nhb > 0) hb_side<W, MAXC>(L, S, sub, mask, hx, hy, hz, e);
-#endif
-#ifdef DK_LEAN_ON
-    e.v += f2_lo(e2.v) + f2_hi(e2.v); e.el += f2_lo(e2.el) + f2_hi(e2.el); e.ds += f2_lo(e2.ds) + f2_hi(e2.ds);
+#ifdef DK_PACK_ON
+    if constexpr (PK) hb_side<W, MAXC>(L, S, sub, mask, hx, hy, hz, e);
 #endif
     e_out += eacc_total(e);
+#ifdef DK_PACK_ON
+    if constexpr (PK) e_out += lean_total(e2);
+#endif
 #pragma unroll
     for (int c = 0; c < MAXC; ++c) {
-        gx[c] = fmaf(kForceScale, hx[c], gx[c]); gy[c] = fmaf(kForceScale, hy[c], gy[c]);
-        gz[c] = fmaf(kForceScale, hz[c], gz[c]);
+        gx[c] = fmaf(2.0f, hx[c], gx[c]); gy[c] = fmaf(2.0f, hy[c], gy[c]); gz[c] = fmaf(2.0f, hz[c], gz[c]);
     }
 }
 
@@ -1038,7 +1027,7 @@ constexpr int kInter = 1, kIntra = 2, kAll = 3;
 // KP > 1 (energy-only path): cooperative evaluation by KP lane groups; this group
 // computes part `part` of the grid and pair sums and returns its PARTIAL energy (the
 // caller adds the KP partials in a fixed order).  The pose is computed by every part.
-template <int W, int MAXC, bool GRAD, int PARTS = kAll, int KP = 1>
+template <int W, int MAXC, bool GRAD, int PARTS = kAll, int KP = 1, bool PK = false>
 __device__ float eval_group(const LigSm &L, const GridDev &grid, const Scratch &S, int sub, unsigned mask,
                             int part = 0) {
     static_assert(KP == 1 || !GRAD, "cooperative evaluation is energy-only");
@@ -1206,11 +1195,11 @@ __device__ float eval_group(const LigSm &L, const GridDev &grid, const Scratch &
         }
         return gsum<W>(e_part, mask);
     } else {
-        if (L.slot_mode) intra_tiles_slots<W, MAXC>(L, S, sub, mask, rx, ry, rz, gx, gy, gz, e_part);
+        if (PK || L.slot_mode) intra_tiles_slots<W, MAXC, PK>(L, S, sub, mask, rx, ry, rz, gx, gy, gz, e_part);
         else intra_tiles<W, MAXC>(L, S, sub, mask, rx, ry, rz, gx, gy, gz, e_part);
-#ifdef DK_LEAN_ON
-        // the pose again from the group's rows (the same values): the tiles need not keep
-        // the scalar pose registers alive (the packed tiles work on 64-bit register pairs)
+        if constexpr (PK) {
+        // the pose again from the group's rows (the same values): the packed tiles need not
+        // keep the scalar pose registers alive (they work on 64-bit register pairs)
 #pragma unroll
         for (int c = 0; c < MAXC; ++c) {
             const int a = sub + W * c;
@@ -1219,7 +1208,7 @@ __device__ float eval_group(const LigSm &L, const GridDev &grid, const Scratch &
                 rx[c] = rv.x; ry[c] = rv.y; rz[c] = rv.z;
             }
         }
-#endif
+        }
         if constexpr (PARTS == kIntra) {
             const float E = gsum<W>(e_part, mask);
 #pragma unroll

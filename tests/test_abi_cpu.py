@@ -36,6 +36,7 @@ def test_exports_every_declared_symbol(dock):
 def test_introspection_null_context(dock):
     # engine / launch queries on a NULL context: -1, never a crash (include/dock.h)
     assert dock.lib.dock_last_engine(None) == -1
+    assert dock.lib.dock_tile_schedule(None) == -1
     assert dock.lib.dock_run_branches(None) == -1
     assert dock.lib.dock_launch_count(None) == -1
 

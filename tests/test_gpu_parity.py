@@ -603,6 +603,54 @@ def test_tail_schedules_parity(dock, n_atoms, mode, monkeypatch):
 
 
 # ---------------------------------------------------------------------------
+# Packed FP32x2 tiles (LigDev::packed): W = 32, two full chunks and a hybrid
+# tail (65 <= N <= ~82, the slot-table limit).  The packed rows carry the lean 12-6 constants, the H-bond pairs'
+# 12-10 vdW terms go through the side list and its segmented per-atom sums (one atom with up
+# to 32 contributions, several atoms per round, several rounds).  Energy and gradient at the
+# GPU's pose against the oracle; the schedule must really be the packed one.
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("n_atoms,donors,acceptors", [(65, 0, 0), (70, 3, 12), (72, 6, 8), (77, 1, 30),
+                                                      (79, 2, 20), (80, 4, 9)])
+def test_packed_tiles_parity(dock, n_atoms, donors, acceptors, monkeypatch):
+    from gen import make_ligand
+    from gen.synth import TYPE_NAMES, make_grid
+    monkeypatch.setenv("DOCK_TAIL", "hyb")
+    lig = make_ligand(n_atoms, min(15, n_atoms // 5), seed=300 + n_atoms, type_names=list(TYPE_NAMES))
+    # re-type atoms spread over the chunks as H-bond donors / acceptors (input data only)
+    names = list(TYPE_NAMES)
+    t = lig.types.copy()
+    t[t == names.index("HD")] = names.index("H")
+    t[t == names.index("OA")] = names.index("O")
+    t[t == names.index("NA")] = names.index("N")
+    order = np.random.default_rng(n_atoms).permutation(n_atoms)
+    t[order[:donors]] = names.index("HD")
+    t[order[donors:donors + acceptors]] = names.index("OA")
+    lig.types = t.astype(np.int32)
+    lig.atom_names = [names[k] for k in lig.types]
+    grid = make_grid(40, 0.5, names, seed=3)
+    d = dock.Docker.from_inputs(grid, lig)
+    P = oracle.Problem(grid, lig)
+    sch = d.tile_schedule
+    assert sch["packed"] and sch["tail"] == "hyb", sch
+    if donors and acceptors:
+        assert sch["hb_side_pairs"] > 0, sch
+    X = near_reference_genotypes(grid, lig, d.T, 64, seed=n_atoms)
+    X[:4, 6:] = 0.0                                          # folded chains: close contacts
+    E, Gd, xyz = d.eval(X, grad=True, xyz=True)
+    assert np.isfinite(E).all() and np.isfinite(Gd).all()
+    c, fails = compare_at_pose(P, grid, X, E, xyz, Gd=Gd)
+    assert_parity(c, fails, f"packed N={n_atoms} hb={sch['hb_side_pairs']}")
+    d.close()
+
+
+def test_packed_schedule_on_7cpa(dock):
+    """The headline config (configs[3], 70 atoms) runs the packed tiles."""
+    cfg, lig, grid, d, P = setup(dock, "7cpa")
+    sch = d.tile_schedule
+    assert sch["packed"] and sch["hb_side_pairs"] > 0, sch
+
+
+# ---------------------------------------------------------------------------
 # Run branches (dock_params.run_branches, DESIGN.md §14): every run stepping through its
 # generations as its own graph branch gives exactly the lockstep results.
 # ---------------------------------------------------------------------------
