@@ -619,6 +619,9 @@ __device__ __forceinline__ void slot_pair2(f2_t ox, f2_t oy, f2_t oz, f2_t px, f
 #define DK_PACK_UNROLL 2   // packed steps unrolled (A/B: scripts/variants.py)
 #endif
 constexpr int kPackUnroll = DK_PACK_UNROLL;
+#ifndef DK_HYB_PAIR
+#define DK_HYB_PAIR 1   // packed hybrid tail: two tail atoms per transposed butterfly (A/B: 0)
+#endif
 
 // (a) + (b): the full-chunk tiles of the Bf = 2 shape.  Own-atom forces go to hx[0..1] etc.
 template <int W, int MAXC>
@@ -703,6 +706,7 @@ template <int W, int MAXC>
 __device__ __forceinline__ void hb_side(const LigSm &L, const Scratch &S, int sub, unsigned mask, float (&hx)[MAXC],
                                         float (&hy)[MAXC], float (&hz)[MAXC], EAcc &e) {
     if (L.nhb == 0) return;
+    __syncwarp(mask);   // the packed tail's reads of the scratch rows precede these writes
     for (int p = sub; p < L.nhb; p += W) {
         const float4 c = L.hbc[p];
         const uint32_t ij = __float_as_uint(c.z);
@@ -859,6 +863,41 @@ __device__ __forceinline__ void intra_tiles_slots(const LigSm &L, const Scratch 
                 const float2 o2 = reinterpret_cast<const float2 *>(S.ts + 96)[sub];
                 const f2_t ox = f2_pk(o4.x, o4.y), oy = f2_pk(o4.z, o4.w), oz = f2_pk(o2.x, o2.y);
                 f2_t gx2 = 0ull, gy2 = 0ull, gz2 = 0ull;
+#if DK_HYB_PAIR
+                // two tail atoms per iteration: two independent packed evaluations, then one
+                // transposed butterfly -- level 16 leaves atom k's partial sums in the low
+                // half-warp and atom k + 1's in the high one, levels 8..1 finish both at once,
+                // and one exchange hands each owner its atom's total (18 shuffles per two atoms
+                // instead of 30, and one dependent chain instead of two)
+                const bool up = sub >= 16;
+                for (int k = 0; k < t; k += 2) {
+                    const bool two = k + 1 < t;                 // uniform
+                    const float4 ra = trow[k], rb = trow[two ? k + 1 : k];
+                    f2_t ax2 = 0ull, ay2 = 0ull, az2 = 0ull, bx2 = 0ull, by2 = 0ull, bz2 = 0ull;
+                    slot_pair2(ox, oy, oz, f2_pk(ra.x, ra.x), f2_pk(ra.y, ra.y), f2_pk(ra.z, ra.z),
+                               L.slot4[slot0 + k * 2 * W + sub], L.slot4[slot0 + k * 2 * W + W + sub], e2, gx2, gy2,
+                               gz2, ax2, ay2, az2);
+                    if (two)
+                        slot_pair2(ox, oy, oz, f2_pk(rb.x, rb.x), f2_pk(rb.y, rb.y), f2_pk(rb.z, rb.z),
+                                   L.slot4[slot0 + (k + 1) * 2 * W + sub], L.slot4[slot0 + (k + 1) * 2 * W + W + sub], e2,
+                                   gx2, gy2, gz2, bx2, by2, bz2);
+                    const float ax = f2_lo(ax2) + f2_hi(ax2), ay = f2_lo(ay2) + f2_hi(ay2), az = f2_lo(az2) + f2_hi(az2);
+                    const float bx = f2_lo(bx2) + f2_hi(bx2), by = f2_lo(by2) + f2_hi(by2), bz = f2_lo(bz2) + f2_hi(bz2);
+                    float kx = up ? bx : ax, ky = up ? by : ay, kz = up ? bz : az;
+                    kx += __shfl_xor_sync(mask, up ? ax : bx, 16);
+                    ky += __shfl_xor_sync(mask, up ? ay : by, 16);
+                    kz += __shfl_xor_sync(mask, up ? az : bz, 16);
+#pragma unroll
+                    for (int m = 8; m >= 1; m >>= 1) {
+                        kx += __shfl_xor_sync(mask, kx, m); ky += __shfl_xor_sync(mask, ky, m); kz += __shfl_xor_sync(mask, kz, m);
+                    }
+                    const float qx = __shfl_xor_sync(mask, kx, 16), qy = __shfl_xor_sync(mask, ky, 16),
+                                qz = __shfl_xor_sync(mask, kz, 16);
+                    // lean forces carry (dE/drho^2) / 3 and the partner sums +dE d: x (-3)
+                    if (sub == k) { fx = fmaf(-3.0f, up ? qx : kx, fx); fy = fmaf(-3.0f, up ? qy : ky, fy); fz = fmaf(-3.0f, up ? qz : kz, fz); }
+                    if (two && sub == k + 1) { fx = fmaf(-3.0f, up ? kx : qx, fx); fy = fmaf(-3.0f, up ? ky : qy, fy); fz = fmaf(-3.0f, up ? kz : qz, fz); }
+                }
+#else
                 for (int k = 0; k < t; ++k) {
                     const float4 rj = trow[k];                  // uniform: shared-memory broadcast
                     f2_t px2 = 0ull, py2 = 0ull, pz2 = 0ull;
@@ -871,6 +910,7 @@ __device__ __forceinline__ void intra_tiles_slots(const LigSm &L, const Scratch 
                     px = gsum<W>(px, mask); py = gsum<W>(py, mask); pz = gsum<W>(pz, mask);
                     if (sub == k) { fx += px; fy += py; fz += pz; }
                 }
+#endif
                 hx[0] = fmaf(3.0f, f2_lo(gx2), hx[0]); hx[1] = fmaf(3.0f, f2_hi(gx2), hx[1]);
                 hy[0] = fmaf(3.0f, f2_lo(gy2), hy[0]); hy[1] = fmaf(3.0f, f2_hi(gy2), hy[1]);
                 hz[0] = fmaf(3.0f, f2_lo(gz2), hz[0]); hz[1] = fmaf(3.0f, f2_hi(gz2), hz[1]);
