@@ -449,7 +449,8 @@ __global__ void __launch_bounds__(256, (MAXC <= 4 ? DK_ADA_MINB : 1)) k_ls_adade
     if (!__any_sync(0xffffffffu, t.act)) return;
     const Scratch S = scratch_at(sm + staged_bytes(L, true) + gl * SL.bytes, SL);
     constexpr unsigned mask = 0xffffffffu;
-    constexpr int NSET = (kMaxGenes + W - 1) / W;
+    // genes per lane: the packed variant is only chosen for G <= 32 (prep.cpp), one per lane
+    constexpr int NSET = PK ? 1 : (kMaxGenes + W - 1) / W;
     float x[NSET], sg[NSET], sd[NSET], bx[NSET];
 #pragma unroll
     for (int s = 0; s < NSET; ++s) {

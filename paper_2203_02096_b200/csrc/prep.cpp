@@ -458,7 +458,7 @@ int prepare_ligand(const dock_ligand *l, const dock_type_param *tp, int n_types,
     const int hmax = N > 0 ? *std::max_element(hdeg.begin(), hdeg.end()) : 0;
 #if (!defined(DK_PACKED) || DK_PACKED) && (!defined(DK_FOLD) || DK_FOLD)
     L.packed = (!ad4 && L.slot_mode && Wg == 32 && Bf == 2 && tail > 0 && !L.tail_rot && ((L.tail_seg >> 24) & 1) &&
-                nhb <= N && hmax <= 32) ? 1 : 0;
+                nhb <= N && hmax <= 32 && 6 + T <= 32) ? 1 : 0;   // G <= 32: one gene per lane (k_ls_adadelta PK)
 #endif
     if (!L.slot_mode && L.tail_seg) {                          // seg needs the slot tables
         L.tail_seg = 0;

@@ -50,6 +50,12 @@ constexpr int kWalkDepth = DK_WALK_DEPTH;
 #define DK_HYB_UNROLL 1     // tail atoms per iteration of the hybrid tail's broadcast loop (A/B)
 #endif
 constexpr int kHybUnroll = DK_HYB_UNROLL;
+#ifndef DK_WALK_UNROLL
+#define DK_WALK_UNROLL 0    // torsion range walk of the back-projection: iterations unrolled; 0 =
+#endif                      // 2 for MAXC >= 3 (long ranges: 7cpa +1 %), else 1 (3ce3: 2 is -1 %)
+#ifndef DK_BP_T
+#define DK_BP_T 1           // back-projection sums by one transposed reduction (W = 32; A/B: 0)
+#endif
 #ifndef DK_TILE_STREAMS
 #define DK_TILE_STREAMS 1   // 2: two partner-accumulator streams per tile (A/B: scripts/variants.py)
 #endif
@@ -561,14 +567,15 @@ constexpr float kDsUnscale = -3.0f * 2.0f * 3.6f * 3.6f;   // -3/k
 // + {z_a, z_b} rows (one LDS.128 + one LDS.64 per packed step), in the group's gradient
 // scratch (dead until the back-projection).  The slot constants of packed step q are two
 // float4 rows [q][0..W) = {-A'_a, -A'_b, B'_a, B'_b} and [q][W..2W) = {SV_a, SV_b, Q_a, Q_b}
-// (the lean constants of slots a and b).  Same arithmetic per slot as slot_pair, so the
-// results equal the scalar lean path's up to the order of the partial sums.
+// (the lean constants of slots a and b).  The same D5 terms as the folded slot_pair in
+// another algebraic form (held to the oracle at NS tolerance: test_packed_tiles_parity).
 typedef unsigned long long f2_t;
 __device__ __forceinline__ f2_t f2_pk(float a, float b) {
     f2_t r;
     asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
     return r;
 }
+#pragma nv_diag_suppress 550   // the unused half of an unpacking mov.b64 (register halves, no instruction)
 __device__ __forceinline__ float f2_lo(f2_t v) {
     float a, b;
     asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(v));
@@ -579,6 +586,7 @@ __device__ __forceinline__ float f2_hi(f2_t v) {
     asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(v));
     return b;
 }
+#pragma nv_diag_default 550
 __device__ __forceinline__ f2_t add2(f2_t a, f2_t b) { f2_t d; asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b)); return d; }
 __device__ __forceinline__ f2_t sub2(f2_t a, f2_t b) { f2_t d; asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b)); return d; }
 __device__ __forceinline__ f2_t mul2(f2_t a, f2_t b) { f2_t d; asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b)); return d; }
@@ -1272,8 +1280,33 @@ __device__ float eval_group(const LigSm &L, const GridDev &grid, const Scratch &
                 S.ts[2 * a + 1] = make_float4(gx[c], gy[c], gz[c], 0.f);
             }
         }
-        sgx = gsum<W>(sgx, mask); sgy = gsum<W>(sgy, mask); sgz = gsum<W>(sgz, mask);
-        Gx = gsum<W>(Gx, mask); Gy = gsum<W>(Gy, mask); Gz = gsum<W>(Gz, mask);
+#if DK_BP_T
+        if constexpr (W == 32) {
+            // the six sums by one transposed reduction (12 shuffles instead of 30): level 16
+            // leaves sum(g) in the low half-warp and sum((r - t) x g) in the high one, level 8
+            // keeps two components in the lanes with bit 3 clear and the third in the others,
+            // level 4 splits the two; levels 2, 1 finish.  Totals: sgx at lane 0, sgy at 4,
+            // sgz at 8, Gx at 16, Gy at 20, Gz at 24; lanes 0..5 (below) fetch what they use.
+            const bool b4 = (sub & 16) != 0, b3 = (sub & 8) != 0, b2 = (sub & 4) != 0;
+            float k0 = b4 ? Gx : sgx, k1 = b4 ? Gy : sgy, k2 = b4 ? Gz : sgz;
+            k0 += __shfl_xor_sync(mask, b4 ? sgx : Gx, 16);
+            k1 += __shfl_xor_sync(mask, b4 ? sgy : Gy, 16);
+            k2 += __shfl_xor_sync(mask, b4 ? sgz : Gz, 16);
+            const float rA = __shfl_xor_sync(mask, b3 ? k0 : k2, 8), rB = __shfl_xor_sync(mask, k1, 8);
+            if (b3) { k2 += rA; } else { k0 += rA; k1 += rB; }
+            float v = b3 ? k2 : (b2 ? k1 : k0);
+            v += __shfl_xor_sync(mask, b3 ? k2 : (b2 ? k0 : k1), 4);
+            v += __shfl_xor_sync(mask, v, 2);
+            v += __shfl_xor_sync(mask, v, 1);
+            const float own = __shfl_sync(mask, v, sub == 1 ? 4 : (sub == 2 ? 8 : 0));
+            Gx = __shfl_sync(mask, v, 16); Gy = __shfl_sync(mask, v, 20); Gz = __shfl_sync(mask, v, 24);
+            sgx = sgy = sgz = own;                      // lane 0: sgx, lane 1: sgy, lane 2: sgz
+        } else
+#endif
+        {
+            sgx = gsum<W>(sgx, mask); sgy = gsum<W>(sgy, mask); sgz = gsum<W>(sgz, mask);
+            Gx = gsum<W>(Gx, mask); Gy = gsum<W>(Gy, mask); Gz = gsum<W>(Gz, mask);
+        }
         __syncwarp(mask);
         // torsions: dE/dtau_k = w_k . sum_{a in moved(k)} (r_a - r_{a_k}) x g_a.  The moved
         // set is one DFS range [lo, hi).  Each torsion gets an aligned block of lpt lanes, a
@@ -1290,6 +1323,8 @@ __device__ float eval_group(const LigSm &L, const GridDev &grid, const Scratch &
             if (own) {
                 tm = L.tmeta[k];
                 const int lo = tm.w & 0xffff, hi = tm.w >> 16;
+                constexpr int kWalkUnroll = DK_WALK_UNROLL ? DK_WALK_UNROLL : (MAXC >= 3 ? 2 : 1);
+#pragma unroll kWalkUnroll
                 for (int a = lo + sl; a < hi; a += lpt) {
                     const float4 c4 = S.ts[2 * a], g4 = S.ts[2 * a + 1];
                     cx += c4.x; cy += c4.y; cz += c4.z;
