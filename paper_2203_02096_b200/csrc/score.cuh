@@ -713,8 +713,8 @@ __device__ __forceinline__ float lean_total(const EAcc2 &a) {
 template <int W, int MAXC>
 __device__ __forceinline__ void hb_side(const LigSm &L, const Scratch &S, int sub, unsigned mask, float (&hx)[MAXC],
                                         float (&hy)[MAXC], float (&hz)[MAXC], EAcc &e) {
+    __syncwarp(mask);   // the packed tail's reads of the scratch rows precede any later writes
     if (L.nhb == 0) return;
-    __syncwarp(mask);   // the packed tail's reads of the scratch rows precede these writes
     for (int p = sub; p < L.nhb; p += W) {
         const float4 c = L.hbc[p];
         const uint32_t ij = __float_as_uint(c.z);
