@@ -1164,14 +1164,19 @@ __global__ void k_stream_words(uint2 key, uint32_t purpose, uint32_t slot, uint3
         }                                                                    \
     } while (0)
 
-// The packed FP32x2 gradient tiles (score.cuh, LigDev::packed: D5, W = 32, 65 <= N <= 96)
-// are a compile-time variant (PK) of the gradient kernels: DK_IF_PACKED(L, cfg, body) runs
-// body with W = 32, MAXC = 3, PK = true for a packed ligand, else falls through to the
+// The packed FP32x2 gradient tiles (score.cuh, LigDev::packed: D5, W = 32, two chunks:
+// 49 <= N <= 64 with the second one padded, 65 <= N <= ~82 with a hybrid tail) are a
+// compile-time variant (PK) of the gradient kernels: DK_IF_PACKED(L, cfg, body) runs body
+// with W = 32, MAXC = 2 or 3, PK = true for a packed ligand, else falls through to the
 // statement that follows it.
 #ifdef DK_PACK_ON
 #define DK_IF_PACKED(L, cfg, ...)                                                              \
     if ((L).packed && (cfg).W == 32 && (cfg).MAXC == 3) {                                      \
         constexpr int W = 32, MAXC = 3;                                                        \
+        constexpr bool PK = true;                                                              \
+        __VA_ARGS__;                                                                           \
+    } else if ((L).packed && (cfg).W == 32 && (cfg).MAXC == 2) {                               \
+        constexpr int W = 32, MAXC = 2;                                                        \
         constexpr bool PK = true;                                                              \
         __VA_ARGS__;                                                                           \
     } else
@@ -1235,6 +1240,8 @@ cudaError_t setup_kernel_attributes() {
 #ifdef DK_PACK_ON
     if (e == cudaSuccess) e = allow_smem(k_eval<32, 3, true, kAll, true>);
     if (e == cudaSuccess) e = allow_smem(k_bench_part<32, 3, kIntra, true>);
+    if (e == cudaSuccess) e = allow_smem(k_eval<32, 2, true, kAll, true>);
+    if (e == cudaSuccess) e = allow_smem(k_bench_part<32, 2, kIntra, true>);
 #endif
     if (e == cudaSuccess) e = setup_attributes_adadelta();
     if (e == cudaSuccess) e = setup_attributes_sw();
@@ -1253,6 +1260,8 @@ cudaError_t setup_attributes_adadelta() {
 #ifdef DK_PACK_ON
     if (e == cudaSuccess) e = allow_smem(k_ls_adadelta<32, 3, false, true>);
     if (e == cudaSuccess) e = allow_smem(k_ls_adadelta<32, 3, true, true>);
+    if (e == cudaSuccess) e = allow_smem(k_ls_adadelta<32, 2, false, true>);
+    if (e == cudaSuccess) e = allow_smem(k_ls_adadelta<32, 2, true, true>);
 #endif
     return e;
 }

@@ -401,6 +401,11 @@ int prepare_ligand(const dock_ligand *l, const dock_type_param *tp, int n_types,
     //     steps 1..tp/2 shared round-robin by the segments, and a butterfly over segments.
     L.tail_seg = 0;
     L.tail_rot = (tail > 0 && (Wg / 2 + Bf * Wg) * 40 < tail * ((Bf + 1) * 40 + 3 * 5)) ? 1 : 0;
+    // 49 <= N <= 63 (no segment form for a tail of 17..31): the tail as a padded rotated
+    // chunk, so the packed FP32x2 tiles (two chunks, the second padded) can take the ligand
+#if (!defined(DK_PACKED) || DK_PACKED) && (!defined(DK_FOLD) || DK_FOLD)
+    if (!ad4 && Wg == 32 && Bf == 1 && tail > Wg / 2) L.tail_rot = 1;
+#endif
     int tpw = 1;   // segment width
     while (tpw < tail) tpw <<= 1;
     const int seg_rounds = (tpw / 2 + (Wg / tpw) - 1) / (Wg / tpw);
@@ -448,7 +453,7 @@ int prepare_ligand(const dock_ligand *l, const dock_type_param *tp, int n_types,
         const int ri = tp[l->type[pairs[q]]].role, rj = tp[l->type[pairs[q + 1]]].role;
         if ((ri == 1 && rj == 2) || (ri == 2 && rj == 1)) {
             const int di = pos[pairs[q]], dj = pos[pairs[q + 1]];
-            if (std::min(di, dj) >= 2 * Wg) continue;     // tail x tail: folded rounds
+            if (!L.tail_rot && std::min(di, dj) >= Bf * Wg) continue;   // tail x tail: folded rounds
             hbl.push_back(std::min(di, dj)); hbl.push_back(std::max(di, dj));
         }
     }
@@ -457,7 +462,11 @@ int prepare_ligand(const dock_ligand *l, const dock_type_param *tp, int n_types,
     for (int v : hbl) hdeg[v]++;
     const int hmax = N > 0 ? *std::max_element(hdeg.begin(), hdeg.end()) : 0;
 #if (!defined(DK_PACKED) || DK_PACKED) && (!defined(DK_FOLD) || DK_FOLD)
-    L.packed = (!ad4 && L.slot_mode && Wg == 32 && Bf == 2 && tail > 0 && !L.tail_rot && ((L.tail_seg >> 24) & 1) &&
+    // two full chunks and a hybrid tail (65 <= N <= ~82), or two chunks with no tail or the
+    // second one a padded rotated chunk (49 <= N <= 64; padded slots hold zero constants)
+    const bool two_hyb = Bf == 2 && tail > 0 && !L.tail_rot && ((L.tail_seg >> 24) & 1);
+    const bool two_rot = (Bf == 2 && tail == 0) || (Bf == 1 && L.tail_rot);
+    L.packed = (!ad4 && L.slot_mode && Wg == 32 && (two_hyb || two_rot) &&
                 nhb <= N && hmax <= 32 && 6 + T <= 32) ? 1 : 0;   // G <= 32: one gene per lane (k_ls_adadelta PK)
 #endif
     if (!L.slot_mode && L.tail_seg) {                          // seg needs the slot tables
@@ -679,7 +688,7 @@ int prepare_ligand(const dock_ligand *l, const dock_type_param *tp, int n_types,
                     row[ln] = emit2(ln, Wg + ((ln + u) & (Wg - 1)), true, ln, Wg + ((ln + u + Wg / 2) & (Wg - 1)), true);
                 put(row);
             }
-            for (int k = 0; k < tail; ++k) {                // (c) tail atom k vs chunks 0 and 1
+            for (int k = 0; k < tail && !L.tail_rot; ++k) { // (c) tail atom k vs chunks 0 and 1 (hybrid tail)
                 for (int ln = 0; ln < Wg; ++ln) row[ln] = emit2(ln, 2 * Wg + k, true, Wg + ln, 2 * Wg + k, true);
                 put(row);
             }

@@ -636,7 +636,7 @@ template <int W, int MAXC>
 __device__ __forceinline__ void tiles_packed(const LigSm &L, const Scratch &S, int sub, unsigned mask,
                                              const float (&rx)[MAXC], const float (&ry)[MAXC], const float (&rz)[MAXC],
                                              float (&hx)[MAXC], float (&hy)[MAXC], float (&hz)[MAXC], EAcc2 &e2) {
-    static_assert(W == 32 && MAXC >= 2, "packed tiles: two full 32-atom chunks");
+    static_assert(W == 32 && MAXC >= 2, "packed tiles: two 32-atom chunks (the second may be padded)");
     float4 *pdxy = S.ts, *psxy = S.ts + 48;                         // [48] rows each
     float2 *pdz = reinterpret_cast<float2 *>(S.ts + 96), *psz = pdz + 48;
     {
@@ -777,7 +777,7 @@ __device__ __forceinline__ void intra_tiles_slots(const LigSm &L, const Scratch 
 #ifdef DK_PACK_ON
     EAcc2 e2;
     if constexpr (PK) {
-        static_assert(W == 32 && MAXC == 3, "packed tiles: W = 32, two full chunks and a tail");
+        static_assert(W == 32 && (MAXC == 2 || MAXC == 3), "packed tiles: W = 32, two chunks");
         // the intermolecular gradients wait in the (unused here) duplicate pose half, so
         // the packed tiles have their registers
 #pragma unroll

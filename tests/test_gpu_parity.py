@@ -603,13 +603,15 @@ def test_tail_schedules_parity(dock, n_atoms, mode, monkeypatch):
 
 
 # ---------------------------------------------------------------------------
-# Packed FP32x2 tiles (LigDev::packed): W = 32, two full chunks and a hybrid
-# tail (65 <= N <= ~82, the slot-table limit).  The packed rows carry the lean 12-6 constants, the H-bond pairs'
+# Packed FP32x2 tiles (LigDev::packed): W = 32, two chunks -- the second one
+# padded and rotated (49 <= N <= 64), or two full chunks and a hybrid tail (65 <= N <= ~82,
+# the slot-table limit).  The packed rows carry the lean 12-6 constants, the H-bond pairs'
 # 12-10 vdW terms go through the side list and its segmented per-atom sums (one atom with up
 # to 32 contributions, several atoms per round, several rounds).  Energy and gradient at the
 # GPU's pose against the oracle; the schedule must really be the packed one.
 # ---------------------------------------------------------------------------
-@pytest.mark.parametrize("n_atoms,donors,acceptors", [(65, 0, 0), (70, 3, 12), (72, 6, 8), (77, 1, 30),
+@pytest.mark.parametrize("n_atoms,donors,acceptors", [(49, 2, 6), (52, 1, 20), (57, 0, 0), (63, 4, 8), (64, 3, 9),
+                                                      (65, 0, 0), (70, 3, 12), (72, 6, 8), (77, 1, 30),
                                                       (79, 2, 20), (80, 4, 9)])
 def test_packed_tiles_parity(dock, n_atoms, donors, acceptors, monkeypatch):
     from gen import make_ligand
@@ -631,7 +633,9 @@ def test_packed_tiles_parity(dock, n_atoms, donors, acceptors, monkeypatch):
     d = dock.Docker.from_inputs(grid, lig)
     P = oracle.Problem(grid, lig)
     sch = d.tile_schedule
-    assert sch["packed"] and sch["tail"] == "hyb", sch
+    # 49..63: the second chunk padded and rotated; 64: no tail; 65..: the hybrid tail
+    want = "rot" if n_atoms < 64 else ("bcast" if n_atoms == 64 else "hyb")
+    assert sch["packed"] and sch["tail"] == want, sch
     if donors and acceptors:
         assert sch["hb_side_pairs"] > 0, sch
     X = near_reference_genotypes(grid, lig, d.T, 64, seed=n_atoms)
