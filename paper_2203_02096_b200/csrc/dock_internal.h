@@ -69,6 +69,8 @@ struct LigDev {
     int nhb;          // H-bond pairs of the packed rows
     int off_hbc;      // float4[nhb] {5 eps r_eq^12, 6 eps r_eq^10, bits(i | j << 16), 0} (dfs)
     int nhbr;         // rounds of the per-atom sums (score.cuh hb_side)
+    int hbspan;       // the largest atom's contribution count rounded up to a power of two:
+                      //   the segmented scan's levels 1, 2, .. < hbspan
     int off_hbseg;    // int[nhbr][32] atom contributions, sorted by atom, never split across
                       //   rounds: pair | neg << 8 | first lane << 9 | last << 14 | valid << 15 |
                       //   atom << 16; then int[NC] per-chunk lane masks of atoms with H-bond pairs

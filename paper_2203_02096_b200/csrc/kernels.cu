@@ -118,6 +118,7 @@ __device__ __forceinline__ LigSm stage_ligand(const LigDev &L, uint8_t *sm, int 
     v.slotq = reinterpret_cast<const float *>(sm + L.off_slotq);
     v.nhb = L.nhb;
     v.nhbr = L.nhbr;
+    v.hbspan = L.hbspan;
     v.hbseg = reinterpret_cast<const int *>(sm + L.off_hbseg);
     v.hbc = reinterpret_cast<const float4 *>(sm + L.off_hbc);
     v.energy_tiles = L.energy_tiles;

@@ -499,6 +499,8 @@ int prepare_ligand(const dock_ligand *l, const dock_type_param *tp, int n_types,
     }
     L.nhb = L.packed ? nhb : 0;
     L.nhbr = (int)hseg.size() / 32;
+    L.hbspan = 1;
+    while (L.packed && L.hbspan < hmax) L.hbspan <<= 1;
     L.off_hbc = off; off += 16 * L.nhb;
     L.off_hbseg = off; off += L.packed ? a16(4 * ((int)hseg.size() + L.NC)) : 0;
     L.grad_bytes = off;             // the gradient kernels stage only up to here

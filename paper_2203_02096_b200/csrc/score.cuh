@@ -85,6 +85,7 @@ struct LigSm {
     int nhb;                      // packed: H-bond side list (LigDev::off_hbc / off_hbseg)
     const float4 *hbc;
     int nhbr;                     // packed: H-bond contribution rounds (LigDev::nhbr)
+    int hbspan;                   // packed: longest per-atom contribution run, rounded up to 2^k
     const int *hbseg;             // packed: [nhbr][32] contribution entries, then int[NC] chunk masks
     float wA_v, wB_v, wA_h, wB_h, qscale;   // D5-AD4 constants (LigDev; unused by D5)
 };
@@ -696,6 +697,10 @@ __device__ __forceinline__ void tiles_packed(const LigSm &L, const Scratch &S, i
     __syncwarp(mask);   // the scratch rows are reused (H-bond side list, back-projection)
 }
 
+#ifndef DK_HB_FULL
+#define DK_HB_FULL 0   // 1: all five scan levels regardless of the longest segment (A/B)
+#endif
+
 __device__ __forceinline__ float lean_total(const EAcc2 &a) {
     const float v = f2_lo(a.v) + f2_hi(a.v), el = f2_lo(a.el) + f2_hi(a.el), ds = f2_lo(a.ds) + f2_hi(a.ds);
     return fmaf(-3.0f, el, fmaf(kDsUnscale, ds, -v));
@@ -739,6 +744,7 @@ __device__ __forceinline__ void hb_side(const LigSm &L, const Scratch &S, int su
         const int first = (ent >> 9) & 31;
 #pragma unroll
         for (int d = 1; d < W; d <<= 1) {
+            if (!DK_HB_FULL && d >= L.hbspan) break;   // levels up to the longest segment (uniform)
             const float ox = __shfl_up_sync(mask, fx, d), oy = __shfl_up_sync(mask, fy, d), oz = __shfl_up_sync(mask, fz, d);
             if (sub - d >= first) { fx += ox; fy += oy; fz += oz; }
         }
