@@ -557,16 +557,18 @@ __device__ __forceinline__ void slot_pair(float rxi, float ryi, float rzi, float
 constexpr float kDsUnscale = -3.0f * 2.0f * 3.6f * 3.6f;   // -3/k
 
 // ---- Packed FP32x2 lean slots (sm_100 fma/mul/add/sub.rn.f32x2: one instruction, two
-// independent IEEE FP32 operations) for the two-full-chunk shape (W = 32, Bf = 2: 64 <= N
-// <= 96 with a hybrid tail; LigDev::packed, prep.cpp).  Every lane evaluates TWO slots per
-// instruction stream, so the 24 FP32 operations of a lean slot cost 12 issue slots:
+// independent IEEE FP32 operations) for two-chunk ligands (W = 32; LigDev::packed, prep.cpp:
+// 49 <= N <= 64 with the second chunk padded and rotated, 65 <= N <= ~82 with a hybrid
+// tail).  Every lane evaluates TWO slots per instruction stream, so the 24 FP32 operations
+// of a lean slot cost 12 issue slots:
 //   (a) diagonal pair: tiles (0,0) and (1,1) together, step s = 1..16 (own atoms sub and
 //       32 + sub, partners (sub + s) of chunk 0 and of chunk 1);
 //   (b) split tile (0,1): steps u and u + 16 together, u = 0..15 (own atom sub twice);
 //   (c) hybrid tail: tail atom k against chunks 0 and 1 together.
 // The partner poses of (a) and (b) are re-laid out per evaluation as {x_a, x_b, y_a, y_b}
 // + {z_a, z_b} rows (one LDS.128 + one LDS.64 per packed step), in the group's gradient
-// scratch (dead until the back-projection).  The slot constants of packed step q are two
+// scratch (free until the H-bond side list and the back-projection reuse it).  The slot
+// constants of packed step q are two
 // float4 rows [q][0..W) = {-A'_a, -A'_b, B'_a, B'_b} and [q][W..2W) = {SV_a, SV_b, Q_a, Q_b}
 // (the lean constants of slots a and b).  The same D5 terms as the folded slot_pair in
 // another algebraic form (held to the oracle at NS tolerance: test_packed_tiles_parity).
@@ -632,7 +634,8 @@ constexpr int kPackUnroll = DK_PACK_UNROLL;
 #define DK_HYB_PAIR 1   // packed hybrid tail: two tail atoms per transposed butterfly (A/B: 0)
 #endif
 
-// (a) + (b): the full-chunk tiles of the Bf = 2 shape.  Own-atom forces go to hx[0..1] etc.
+// (a) + (b): the tiles of the two chunks (the second one full or padded).  Own-atom forces
+// go to hx[0..1] etc.
 template <int W, int MAXC>
 __device__ __forceinline__ void tiles_packed(const LigSm &L, const Scratch &S, int sub, unsigned mask,
                                              const float (&rx)[MAXC], const float (&ry)[MAXC], const float (&rz)[MAXC],
