@@ -633,6 +633,9 @@ constexpr int kPackUnroll = DK_PACK_UNROLL;
 #ifndef DK_HYB_PAIR
 #define DK_HYB_PAIR 1   // packed hybrid tail: two tail atoms per transposed butterfly (A/B: 0)
 #endif
+#ifndef DK_HYB_PAIR_UNROLL
+#define DK_HYB_PAIR_UNROLL 1   // iterations (atom pairs) of that loop unrolled (A/B)
+#endif
 
 // (a) + (b): the tiles of the two chunks (the second one full or padded).  Own-atom forces
 // go to hx[0..1] etc.
@@ -887,6 +890,8 @@ __device__ __forceinline__ void intra_tiles_slots(const LigSm &L, const Scratch 
                 // and one exchange hands each owner its atom's total (18 shuffles per two atoms
                 // instead of 30, and one dependent chain instead of two)
                 const bool up = sub >= 16;
+                constexpr int kPairUnroll = DK_HYB_PAIR_UNROLL;
+#pragma unroll kPairUnroll
                 for (int k = 0; k < t; k += 2) {
                     const bool two = k + 1 < t;                 // uniform
                     const float4 ra = trow[k], rb = trow[two ? k + 1 : k];
