@@ -627,7 +627,7 @@ __device__ __forceinline__ void slot_pair2(f2_t ox, f2_t oy, f2_t oz, f2_t px, f
 }
 
 #ifndef DK_PACK_UNROLL
-#define DK_PACK_UNROLL 4   // packed steps unrolled (A/B: 1 0.99x, 2 0.997x, 4 kept; scripts/variants.py)
+#define DK_PACK_UNROLL 4   // packed steps unrolled (A/B: 1 0.98x, 2 0.996x, 8 0.96x; scripts/variants.py)
 #endif
 constexpr int kPackUnroll = DK_PACK_UNROLL;
 #ifndef DK_HYB_PAIR
